@@ -1,0 +1,1214 @@
+// oracle/gmpea_oracle.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// A plain-loop, f64 CPU restatement of the reference GMPEA hot path
+// (/root/reference/proj, "the reference"), written from the reference's
+// semantics, not copied.  It exists to check the CUDA engine: only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / reference arm may load
+// it.  The product library (paper_2509_19821_b200/libgmpea_b200.so) never
+// links or calls it.
+//
+// Pinning: everything the reference also has
+// (LIRCMOP1-14, C/DC-DTLZ, WTA, CV, PBI, FPR, OP1/OP2/OP3, lattice, KNN, IGD,
+// HV, metric_front) is checked bit-for-bit against the reference compiled from
+// its own sources (oracle/_ref, built by oracle/Makefile) and against the
+// committed golden fixtures in tests/golden/.  Two parts have no reference
+// counterpart and are "parity unpinned" in the sense of the task statement:
+//   * MW1-MW14 (absent from the reference) — restated from the
+//     MW test-suite definitions (Ma & Wang, IEEE TEVC 2019, as distributed
+//     with PlatEMO);
+//   * reproduce() drawing from the Philox key schema (oracle/philox.h) instead
+//     of the reference's sequential mt19937_64 — it follows
+//     proj/src/gmpea.cpp:113-206 draw for draw (b==a redraw, jrand
+//     short-circuit, PM skip, rejection sampling) but the draws themselves
+//     differ, so only its structure is pinned (identity cases of
+//     tests/test_gmpea.cpp:141-188).
+//
+// All entry points are extern "C" (orc_*), plain pointers, row-major f64.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "philox.h"
+
+namespace {
+
+constexpr double kPi = 3.141592653589793;  // == std::numbers::pi (problems.cpp:16)
+thread_local std::string g_err;
+
+// ---------------------------------------------------------------------------
+// problems (reference: proj/src/problems.cpp, proj/src/wta.cpp)
+
+enum Family { FAM_LIR = 1, FAM_DTLZ = 2, FAM_WTA = 3, FAM_MW = 4 };
+enum DtlzKind {
+    C1_DTLZ1 = 1, C1_DTLZ3, C2_DTLZ2, C3_DTLZ4, DC1_DTLZ1, DC1_DTLZ3,
+    DC2_DTLZ1, DC2_DTLZ3, DC3_DTLZ1, DC3_DTLZ3
+};
+
+struct Wta {
+    int targets = 0, vehicles = 0;
+    std::vector<int> strikes, cap;
+    std::vector<std::vector<double>> p;
+};
+
+struct Problem {
+    std::string name;
+    int fam = 0, id = 0;
+    int d = 0, m = 0, nin = 0, neq = 0;
+    std::vector<double> lo, hi;
+    Wta w;
+};
+
+// mt19937_64-backed draws of the reference Rng (include/gmpea/rng.hpp:18-30),
+// needed only to regenerate the WTA scenarios (wta.cpp:37-47).
+struct MtRng {
+    std::mt19937_64 e;
+    explicit MtRng(uint64_t s) : e(s) {}
+    double uniform() { return static_cast<double>(e() >> 11) * 0x1.0p-53; }
+    uint64_t index(uint64_t n) {
+        uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+        uint64_t v;
+        do { v = e(); } while (v >= limit);
+        return v % n;
+    }
+};
+
+// wta.cpp:23-49
+Wta wta_scenario(int num) {
+    Wta w;
+    w.targets = 4 + 2 * (num - 1);
+    w.vehicles = 3 + (num - 1) / 2;
+    MtRng r(0x57A0000ull + static_cast<uint64_t>(num));
+    w.strikes.resize(w.targets);
+    w.cap.resize(w.vehicles);
+    for (int i = 0; i < w.targets; ++i) w.strikes[i] = 1 + static_cast<int>(r.index(3));
+    for (int v = 0; v < w.vehicles; ++v) w.cap[v] = 2 + static_cast<int>(r.index(3));
+    w.p.resize(w.targets);
+    for (int i = 0; i < w.targets; ++i) {
+        w.p[i].resize(w.strikes[i]);
+        for (int k = 0; k < w.strikes[i]; ++k) w.p[i][k] = 0.35 + 0.6 * r.uniform();
+    }
+    return w;
+}
+
+// problems.cpp:22-35 (LIRCMOP1-4 distance terms)
+void lir_fixed(const double* x, int n, double& g1, double& g2) {
+    double s = std::sin(0.5 * kPi * x[0]);
+    double c = std::cos(0.5 * kPi * x[0]);
+    g1 = 0.0;
+    g2 = 0.0;
+    for (int j = 2; j < n; j += 2) { double t = x[j] - s; g1 += t * t; }
+    for (int j = 1; j < n; j += 2) { double t = x[j] - c; g2 += t * t; }
+}
+
+// problems.cpp:39-51 (LIRCMOP5-12 distance terms)
+void lir_shifted(const double* x, int n, double& g1, double& g2) {
+    const double dn = static_cast<double>(n);
+    g1 = 0.0;
+    g2 = 0.0;
+    for (int j = 2; j < n; j += 2) {
+        double t = x[j] - std::sin(0.5 * static_cast<double>(j + 1) * kPi * x[0] / dn);
+        g1 += t * t;
+    }
+    for (int j = 1; j < n; j += 2) {
+        double t = x[j] - std::cos(0.5 * static_cast<double>(j + 1) * kPi * x[0] / dn);
+        g2 += t * t;
+    }
+}
+
+// problems.cpp:54-59
+double ellipse(double f1, double f2, double p, double q, double a, double b, double r,
+               double th) {
+    double u = (f1 - p) * std::cos(th) - (f2 - q) * std::sin(th);
+    double v = (f1 - p) * std::sin(th) + (f2 - q) * std::cos(th);
+    return r - u * u / (a * a) - v * v / (b * b);
+}
+
+// problems.cpp:66-137
+void eval_lircmop(int id, const double* x, int n, double* f, double* g) {
+    const double x1 = x[0];
+    if (id <= 4) {
+        double g1, g2;
+        lir_fixed(x, n, g1, g2);
+        f[0] = x1 + g1;
+        f[1] = (id == 1 || id == 3) ? 1.0 - x1 * x1 + g2 : 1.0 - std::sqrt(x1) + g2;
+        g[0] = -((0.51 - g1) * (g1 - 0.5));
+        g[1] = -((0.51 - g2) * (g2 - 0.5));
+        if (id >= 3) g[2] = 0.5 - std::sin(20.0 * kPi * x1);
+        return;
+    }
+    if (id <= 8) {
+        double g1, g2;
+        lir_shifted(x, n, g1, g2);
+        f[0] = x1 + 10.0 * g1 + 0.7057;
+        bool sq = (id == 5 || id == 7);
+        f[1] = (sq ? 1.0 - std::sqrt(x1) : 1.0 - x1 * x1) + 10.0 * g2 + 0.7057;
+        const double th = -0.25 * kPi;
+        if (id <= 6) {
+            const double p[2] = {id == 5 ? 1.6 : 1.8, id == 5 ? 2.5 : 2.8};
+            const double a[2] = {2.0, 2.0};
+            const double b[2] = {id == 5 ? 4.0 : 8.0, 8.0};
+            for (int k = 0; k < 2; ++k) g[k] = ellipse(f[0], f[1], p[k], p[k], a[k], b[k], 0.1, th);
+        } else {
+            const double p[3] = {1.2, 2.25, 3.5};
+            const double a[3] = {2.0, 2.5, 2.5};
+            const double b[3] = {6.0, 12.0, 10.0};
+            for (int k = 0; k < 3; ++k) g[k] = ellipse(f[0], f[1], p[k], p[k], a[k], b[k], 0.1, th);
+        }
+        return;
+    }
+    if (id <= 12) {
+        double g1, g2;
+        lir_shifted(x, n, g1, g2);
+        f[0] = 1.7057 * x1 * (10.0 * g1 + 1.0);
+        bool sq = (id == 10 || id == 11);
+        f[1] = 1.7057 * (sq ? 1.0 - std::sqrt(x1) : 1.0 - x1 * x1) * (10.0 * g2 + 1.0);
+        const double th = -0.25 * kPi, al = 0.25 * kPi;
+        double p, q, a, b, lv;
+        switch (id) {
+            case 9: p = 1.4; q = 1.4; a = 1.5; b = 6.0; lv = 2.0; break;
+            case 10: p = 1.1; q = 1.2; a = 2.0; b = 4.0; lv = 1.0; break;
+            case 11: p = 1.2; q = 1.2; a = 1.5; b = 5.0; lv = 2.1; break;
+            default: p = 1.6; q = 1.6; a = 1.5; b = 6.0; lv = 2.5; break;
+        }
+        g[0] = ellipse(f[0], f[1], p, q, a, b, 0.1, th);
+        g[1] = lv - (f[0] * std::sin(al) + f[1] * std::cos(al) -
+                     std::sin(4.0 * kPi * (f[0] * std::cos(al) - f[1] * std::sin(al))));
+        return;
+    }
+    double gs = 0.0;
+    for (int j = 2; j < n; ++j) { double t = x[j] - 0.5; gs += 10.0 * t * t; }
+    double rad = 1.7057 + gs;
+    f[0] = rad * std::cos(0.5 * kPi * x[0]) * std::cos(0.5 * kPi * x[1]);
+    f[1] = rad * std::cos(0.5 * kPi * x[0]) * std::sin(0.5 * kPi * x[1]);
+    f[2] = rad * std::sin(0.5 * kPi * x[0]);
+    double r2 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+    g[0] = -((r2 - 9.0) * (r2 - 4.0));
+    g[1] = -((r2 - 3.61) * (r2 - 3.24));
+    if (id == 14) g[2] = -((r2 - 3.0625) * (r2 - 2.56));
+}
+
+// problems.cpp:141-158
+double dtlz_g_rast(const double* x, int n, int m) {
+    double s = 0.0;
+    int k = n - m + 1;
+    for (int i = m - 1; i < n; ++i) {
+        double t = x[i] - 0.5;
+        s += t * t - std::cos(20.0 * kPi * t);
+    }
+    return 100.0 * (static_cast<double>(k) + s);
+}
+double dtlz_g_sph(const double* x, int n, int m) {
+    double s = 0.0;
+    for (int i = m - 1; i < n; ++i) { double t = x[i] - 0.5; s += t * t; }
+    return s;
+}
+// problems.cpp:160-178
+void shape_linear(const double* pos, double g, int m, double* f) {
+    for (int j = 0; j < m; ++j) {
+        double v = 0.5;
+        for (int i = 0; i + j + 1 < m; ++i) v *= pos[i];
+        if (j > 0) v *= 1.0 - pos[m - 1 - j];
+        f[j] = v * (1.0 + g);
+    }
+}
+void shape_sphere(const double* pos, double g, int m, double* f) {
+    for (int j = 0; j < m; ++j) {
+        double v = 1.0 + g;
+        for (int i = 0; i + j + 1 < m; ++i) v *= std::cos(0.5 * kPi * pos[i]);
+        if (j > 0) v *= std::sin(0.5 * kPi * pos[m - 1 - j]);
+        f[j] = v;
+    }
+}
+// problems.cpp:182-201 (base: 1 linear/rastrigin, 2 sphere/sphere, 3 sphere/rastrigin, 4 DTLZ4)
+void dtlz_base(int base, const double* x, int n, int m, double* f) {
+    double pos[8];
+    for (int i = 0; i < m - 1; ++i) pos[i] = x[i];
+    if (base == 1) shape_linear(pos, dtlz_g_rast(x, n, m), m, f);
+    else if (base == 2) shape_sphere(pos, dtlz_g_sph(x, n, m), m, f);
+    else if (base == 3) shape_sphere(pos, dtlz_g_rast(x, n, m), m, f);
+    else {
+        for (int i = 0; i < m - 1; ++i) pos[i] = std::pow(pos[i], 100.0);
+        shape_sphere(pos, dtlz_g_sph(x, n, m), m, f);
+    }
+}
+
+// problems.cpp:426-525
+void eval_dtlz(int kind, const double* x, int n, int m, double* f, double* g) {
+    switch (kind) {
+        case C1_DTLZ1: {
+            dtlz_base(1, x, n, m, f);
+            double s = 0.0;
+            for (int i = 0; i + 1 < m; ++i) s += f[i] / 0.5;
+            s += f[m - 1] / 0.6;
+            g[0] = s - 1.0;
+            return;
+        }
+        case C1_DTLZ3: {
+            dtlz_base(3, x, n, m, f);
+            double r2 = 0.0;
+            for (int i = 0; i < m; ++i) r2 += f[i] * f[i];
+            const double r = 9.0;
+            g[0] = -((r2 - 16.0) * (r2 - r * r));
+            return;
+        }
+        case C2_DTLZ2: {
+            dtlz_base(2, x, n, m, f);
+            const double r = 0.4;
+            double v1 = std::numeric_limits<double>::infinity();
+            for (int i = 0; i < m; ++i) {
+                double t = (f[i] - 1.0) * (f[i] - 1.0) - r * r;
+                for (int j = 0; j < m; ++j)
+                    if (j != i) t += f[j] * f[j];
+                v1 = std::min(v1, t);
+            }
+            double v2 = 0.0;
+            const double c = 1.0 / std::sqrt(static_cast<double>(m));
+            for (int i = 0; i < m; ++i) v2 += (f[i] - c) * (f[i] - c);
+            v2 -= r * r;
+            g[0] = std::min(v1, v2);
+            return;
+        }
+        case C3_DTLZ4: {
+            dtlz_base(4, x, n, m, f);
+            for (int j = 0; j < m; ++j) {
+                double s = f[j] * f[j] / 4.0;
+                for (int i = 0; i < m; ++i)
+                    if (i != j) s += f[i] * f[i];
+                g[j] = 1.0 - s;
+            }
+            return;
+        }
+        default: break;
+    }
+    bool linear = (kind == DC1_DTLZ1 || kind == DC2_DTLZ1 || kind == DC3_DTLZ1);
+    int base = linear ? 1 : 3;
+    dtlz_base(base, x, n, m, f);
+    if (kind == DC1_DTLZ1 || kind == DC1_DTLZ3) {
+        g[0] = -(std::cos(3.0 * kPi * x[0]) + 0.5);
+    } else if (kind == DC2_DTLZ1 || kind == DC2_DTLZ3) {
+        double gd = dtlz_g_rast(x, n, m);
+        g[0] = 0.9 - std::cos(3.0 * kPi * gd);
+        g[1] = 0.9 - std::exp(-gd);
+    } else {
+        const double a = 3.0;
+        for (int j = 0; j + 1 < m; ++j) g[j] = -(std::cos(a * kPi * x[j]) + 0.5);
+        double gd = dtlz_g_rast(x, n, m);
+        g[m - 1] = -(std::cos(a * kPi * gd) + 0.5);
+    }
+}
+
+// wta.cpp:51-129 (decode: threshold, stable sort by value desc, capacity cap)
+void eval_wta(const Wta& w, const double* x, int n, double* f, double* g) {
+    std::vector<int> cand;
+    for (int i = 0; i < n; ++i)
+        if (x[i] >= 0.5) cand.push_back(i);
+    std::stable_sort(cand.begin(), cand.end(), [&](int a, int b) { return x[a] > x[b]; });
+    std::vector<uint8_t> a(n, 0);
+    std::vector<int> load(w.vehicles, 0);
+    for (int gi : cand) {
+        int v = gi % w.vehicles;
+        if (load[v] < w.cap[v]) { a[gi] = 1; ++load[v]; }
+    }
+    double f1 = 0.0, f2 = 0.0;
+    std::vector<double> lf(w.vehicles, 0.0);
+    int base = 0;
+    for (int i = 0; i < w.targets; ++i) {
+        double surv = 1.0;
+        for (int k = 0; k < w.strikes[i]; ++k) {
+            double hits = 0.0;
+            for (int v = 0; v < w.vehicles; ++v) {
+                double xv = a[(base + k) * w.vehicles + v];
+                hits += xv;
+                lf[v] += xv;
+            }
+            surv *= 1.0 - w.p[i][k] * hits;
+            f2 += hits;
+        }
+        f1 += 1.0 - surv;
+        base += w.strikes[i];
+    }
+    f[0] = -f1;
+    f[1] = f2;
+    for (int v = 0; v < w.vehicles; ++v) g[v] = lf[v] - static_cast<double>(w.cap[v]);
+    base = 0;
+    for (int i = 0; i < w.targets; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < w.strikes[i]; ++k)
+            for (int v = 0; v < w.vehicles; ++v) s += a[(base + k) * w.vehicles + v];
+        g[w.vehicles + i] = s - static_cast<double>(w.strikes[i]);
+        base += w.strikes[i];
+    }
+}
+
+// --- MW1-MW14 (NOT in the reference; parity unpinned). Restated from the MW
+// suite definitions (Ma & Wang, TEVC 2019; PlatEMO conventions: D = 15,
+// M = 2 except MW4/MW8/MW14 with M = 3, x in [0,1]^D except MW14 in
+// [0,1.5]^D).  Index j below is 0-based; the paper's index is j+1.
+double mw_g_exp(const double* x, int n, int m) {  // MW1/4/5/9/12 distance
+    double s = 0.0;
+    for (int j = m - 1; j < n; ++j) {
+        double t = std::pow(x[j], static_cast<double>(n - m)) - 0.5 -
+                   static_cast<double>(j) / (2.0 * n);
+        s += 1.0 - std::exp(-10.0 * t * t);
+    }
+    return s;
+}
+double mw_g_cos(const double* x, int n, int m) {  // MW2/6/8/10/13 distance
+    double s = 0.0;
+    for (int j = m - 1; j < n; ++j) {
+        double t = x[j] - static_cast<double>(j) / n;
+        double z = 1.0 - std::exp(-10.0 * t * t);
+        s += 1.5 + (0.1 / n) * z * z - 1.5 * std::cos(2.0 * kPi * z);
+    }
+    return s;
+}
+double mw_g_lin(const double* x, int n, int m) {  // MW3/7/11/14 distance
+    double s = 0.0;
+    for (int j = m - 1; j < n; ++j) {
+        double p = x[j - 1] - 0.5;
+        double t = x[j] + p * p - 1.0;
+        s += 2.0 * t * t;
+    }
+    return s;
+}
+
+void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
+    switch (id) {
+        case 1: {
+            double gg = 1.0 + mw_g_exp(x, n, m);
+            f[0] = x[0];
+            f[1] = gg * (1.0 - 0.85 * f[0] / gg);
+            double l = std::sqrt(2.0) * f[1] - std::sqrt(2.0) * f[0];
+            g[0] = f[0] + f[1] - 1.0 - 0.5 * std::pow(std::sin(2.0 * kPi * l), 8.0);
+            return;
+        }
+        case 2: {
+            double gg = 1.0 + mw_g_cos(x, n, m);
+            f[0] = x[0];
+            f[1] = gg * (1.0 - f[0] / gg);
+            double l = std::sqrt(2.0) * f[1] - std::sqrt(2.0) * f[0];
+            g[0] = f[0] + f[1] - 1.0 - 0.5 * std::pow(std::sin(3.0 * kPi * l), 8.0);
+            return;
+        }
+        case 3: {
+            double gg = 1.0 + mw_g_lin(x, n, m);
+            f[0] = x[0];
+            f[1] = gg * (1.0 - f[0] / gg);
+            double l = std::sqrt(2.0) * f[1] - std::sqrt(2.0) * f[0];
+            double s = f[0] + f[1];
+            g[0] = s - 1.05 - 0.45 * std::pow(std::sin(0.75 * kPi * l), 6.0);
+            g[1] = 0.85 - s + 0.3 * std::pow(std::sin(0.75 * kPi * l), 2.0);
+            return;
+        }
+        case 4:
+        case 8: {
+            double gg = id == 4 ? mw_g_exp(x, n, m) : mw_g_cos(x, n, m);
+            // f_k = (1+g) * prod_{i < m-1-k} c(x_i) * (k > 0 ? s(x_{m-1-k}) : 1)
+            for (int k = 0; k < m; ++k) {
+                double v = 1.0 + gg;
+                for (int i = 0; i + k + 1 < m; ++i)
+                    v *= id == 4 ? x[i] : std::cos(0.5 * kPi * x[i]);
+                if (k > 0) v *= id == 4 ? 1.0 - x[m - 1 - k] : std::sin(0.5 * kPi * x[m - 1 - k]);
+                f[k] = v;
+            }
+            if (id == 4) {
+                double l = f[m - 1];
+                for (int k = 0; k + 1 < m; ++k) l -= f[k];
+                double s = 0.0;
+                for (int k = 0; k < m; ++k) s += f[k];
+                g[0] = s - (1.0 + 0.4 * std::pow(std::sin(2.5 * kPi * l), 8.0));
+            } else {
+                double s2 = 0.0;
+                for (int k = 0; k < m; ++k) s2 += f[k] * f[k];
+                double l = std::asin(f[m - 1] / std::sqrt(s2));
+                double t = 1.25 - 0.5 * std::pow(std::sin(6.0 * l), 2.0);
+                g[0] = s2 - t * t;
+            }
+            return;
+        }
+        case 5: {
+            double gg = 1.0 + mw_g_exp(x, n, m);
+            f[0] = gg * x[0];
+            double r = f[0] / gg;
+            f[1] = gg * std::sqrt(1.0 - r * r);
+            double l1 = std::atan(f[1] / f[0]);
+            double l2 = 0.5 * kPi - 2.0 * std::fabs(l1 - 0.25 * kPi);
+            double q = f[0] * f[0] + f[1] * f[1];
+            double a = 1.7 - 0.2 * std::sin(2.0 * l1);
+            double b = 1.0 + 0.5 * std::sin(6.0 * l2 * l2 * l2);
+            double c = 1.0 - 0.45 * std::sin(6.0 * l2 * l2 * l2);
+            g[0] = q - a * a;
+            g[1] = b * b - q;
+            g[2] = c * c - q;
+            return;
+        }
+        case 6: {
+            double gg = 1.0 + mw_g_cos(x, n, m);
+            f[0] = gg * x[0] * 1.0999;
+            double r = f[0] / gg;
+            f[1] = gg * std::sqrt(1.1 * 1.1 - r * r);
+            double l = std::pow(std::cos(6.0 * std::pow(std::atan(f[1] / f[0]), 4.0)), 10.0);
+            double a = f[0] / (1.0 + 0.15 * l), b = f[1] / (1.0 + 0.75 * l);
+            g[0] = a * a + b * b - 1.0;
+            return;
+        }
+        case 7: {
+            double gg = 1.0 + mw_g_lin(x, n, m);
+            f[0] = gg * x[0];
+            double r = f[0] / gg;
+            f[1] = gg * std::sqrt(1.0 - r * r);
+            double l = std::atan(f[1] / f[0]);
+            double q = f[0] * f[0] + f[1] * f[1];
+            double a = 1.2 + 0.4 * std::pow(std::sin(4.0 * l), 16.0);
+            double b = 1.15 - 0.2 * std::pow(std::sin(4.0 * l), 8.0);
+            g[0] = q - a * a;
+            g[1] = b * b - q;
+            return;
+        }
+        case 9: {
+            double gg = 1.0 + mw_g_exp(x, n, m);
+            f[0] = gg * x[0];
+            f[1] = gg * (1.0 - std::pow(f[0] / gg, 0.6));
+            double f1s = f[0] * f[0];
+            double t1 = (1.0 - 0.64 * f1s - f[1]) * (1.0 - 0.36 * f1s - f[1]);
+            double a = f[0] + 0.35, b = f[0] + 0.15;
+            double t2 = 1.35 * 1.35 - a * a - f[1];
+            double t3 = 1.15 * 1.15 - b * b - f[1];
+            g[0] = std::min(t1, t2 * t3);
+            return;
+        }
+        case 10: {
+            double gg = 1.0 + mw_g_cos(x, n, m);
+            f[0] = gg * std::pow(x[0], static_cast<double>(n));
+            double r = f[0] / gg;
+            f[1] = gg * (1.0 - r * r);
+            double s = f[0] * f[0];
+            g[0] = -(2.0 - 4.0 * s - f[1]) * (2.0 - 8.0 * s - f[1]);
+            g[1] = (2.0 - 2.0 * s - f[1]) * (2.0 - 16.0 * s - f[1]);
+            g[2] = (1.0 - s - f[1]) * (1.2 - 1.2 * s - f[1]);
+            return;
+        }
+        case 11: {
+            double gg = 1.0 + mw_g_lin(x, n, m);
+            f[0] = gg * x[0] * std::sqrt(1.9999);
+            double r = f[0] / gg;
+            f[1] = gg * std::sqrt(2.0 - r * r);
+            double s = f[0] * f[0];
+            g[0] = -(3.0 - s - f[1]) * (3.0 - 4.0 * s - f[1]);
+            g[1] = (3.0 - 0.625 * s - f[1]) * (3.0 - 7.0 * s - f[1]);
+            g[2] = -(1.62 - 0.18 * s - f[1]) * (1.125 - 0.125 * s - f[1]);
+            g[3] = (2.07 - 0.23 * s - f[1]) * (0.63 - 0.07 * s - f[1]);
+            return;
+        }
+        case 12: {
+            double gg = 1.0 + mw_g_exp(x, n, m);
+            f[0] = gg * x[0];
+            double r = f[0] / gg;
+            f[1] = gg * (0.85 - 0.8 * r - 0.08 * std::fabs(std::sin(3.2 * kPi * r)));
+            double a = 1.0 - 0.8 * f[0] - f[1] + 0.08 * std::sin(2.0 * kPi * (f[1] - f[0] / 1.5));
+            double b = 1.8 - 1.125 * f[0] - f[1] +
+                       0.08 * std::sin(2.0 * kPi * (f[1] / 1.8 - f[0] / 1.6));
+            double c = 1.0 - 0.625 * f[0] - f[1] +
+                       0.08 * std::sin(2.0 * kPi * (f[1] - f[0] / 1.6));
+            double e = 1.4 - 0.875 * f[0] - f[1] +
+                       0.08 * std::sin(2.0 * kPi * (f[1] / 1.4 - f[0] / 1.6));
+            g[0] = a * b;
+            g[1] = -(c * e);
+            return;
+        }
+        case 13: {
+            double gg = 1.0 + mw_g_cos(x, n, m);
+            f[0] = gg * x[0] * 1.5;
+            double r = f[0] / gg;
+            f[1] = gg * (5.0 - std::exp(r) - std::fabs(0.5 * std::sin(3.0 * kPi * r)));
+            double s3 = 0.5 * std::sin(3.0 * kPi * f[0]);
+            double a = 5.0 - std::exp(f[0]) - s3 - f[1];
+            double b = 5.0 - (1.0 + 0.4 * f[0]) - s3 - f[1];
+            double c = 5.0 - (1.0 + f[0] + 0.5 * f[0] * f[0]) - s3 - f[1];
+            double e = 5.0 - (1.0 + 0.7 * f[0]) - s3 - f[1];
+            g[0] = a * b;
+            g[1] = -(c * e);
+            return;
+        }
+        case 14: {
+            double gg = mw_g_lin(x, n, m);
+            double s = 0.0, sa = 0.0;
+            for (int k = 0; k + 1 < m; ++k) {
+                f[k] = x[k];
+                double q = f[k] * f[k];
+                s += 6.0 - std::exp(f[k]) - 1.5 * std::sin(1.1 * kPi * q);
+                sa += 6.1 - (1.0 + f[k] + 0.5 * q + 1.5 * std::sin(1.1 * kPi * q));
+            }
+            f[m - 1] = (1.0 + gg) / (m - 1) * s;
+            g[0] = f[m - 1] - 1.0 / (m - 1) * sa;
+            return;
+        }
+        default: break;
+    }
+}
+
+int mw_ncon(int id) {
+    switch (id) {
+        case 3: case 7: case 12: case 13: return 2;
+        case 5: case 10: return 3;
+        case 11: return 4;
+        default: return 1;
+    }
+}
+
+Problem make_problem(const std::string& name) {
+    Problem p;
+    p.name = name;
+    if (name.rfind("LIRCMOP", 0) == 0) {
+        int id = std::stoi(name.substr(7));
+        if (id < 1 || id > 14) throw std::invalid_argument("unknown problem: " + name);
+        p.fam = FAM_LIR;
+        p.id = id;
+        p.d = 30;
+        p.m = id >= 13 ? 3 : 2;
+        p.nin = (id == 3 || id == 4 || id == 7 || id == 8 || id == 14) ? 3 : 2;
+        p.lo.assign(p.d, 0.0);
+        p.hi.assign(p.d, 1.0);
+        return p;
+    }
+    if (name.rfind("MW", 0) == 0) {
+        int id = std::stoi(name.substr(2));
+        if (id < 1 || id > 14) throw std::invalid_argument("unknown problem: " + name);
+        p.fam = FAM_MW;
+        p.id = id;
+        p.d = 15;
+        p.m = (id == 4 || id == 8 || id == 14) ? 3 : 2;
+        p.nin = mw_ncon(id);
+        p.lo.assign(p.d, 0.0);
+        p.hi.assign(p.d, id == 14 ? 1.5 : 1.0);
+        return p;
+    }
+    if (name.rfind("WTA-P", 0) == 0) {
+        int num = std::stoi(name.substr(5));
+        if (num < 1 || num > 10) throw std::invalid_argument("unknown WTA scenario: " + name.substr(4));
+        p.fam = FAM_WTA;
+        p.id = num;
+        p.w = wta_scenario(num);
+        int slots = 0;
+        for (int s : p.w.strikes) slots += s;
+        p.d = slots * p.w.vehicles;
+        p.m = 2;
+        p.nin = p.w.vehicles + p.w.targets;
+        p.lo.assign(p.d, 0.0);
+        p.hi.assign(p.d, 1.0);
+        return p;
+    }
+    static const char* kDtlz[] = {"C1-DTLZ1", "C1-DTLZ3", "C2-DTLZ2", "C3-DTLZ4", "DC1-DTLZ1",
+                                  "DC1-DTLZ3", "DC2-DTLZ1", "DC2-DTLZ3", "DC3-DTLZ1", "DC3-DTLZ3"};
+    for (int k = 0; k < 10; ++k)
+        if (name == kDtlz[k]) {
+            p.fam = FAM_DTLZ;
+            p.id = k + 1;
+            p.m = 3;
+            bool d7 = (p.id == C1_DTLZ1 || p.id == DC1_DTLZ1 || p.id == DC2_DTLZ1 || p.id == DC3_DTLZ1);
+            p.d = d7 ? 7 : 12;
+            if (p.id == C3_DTLZ4) p.nin = 3;
+            else if (p.id == DC2_DTLZ1 || p.id == DC2_DTLZ3) p.nin = 2;
+            else if (p.id == DC3_DTLZ1 || p.id == DC3_DTLZ3) p.nin = p.m;
+            else p.nin = 1;
+            p.lo.assign(p.d, 0.0);
+            p.hi.assign(p.d, 1.0);
+            return p;
+        }
+    throw std::invalid_argument("unknown problem: " + name);
+}
+
+void eval_row(const Problem& p, const double* x, double* f, double* g) {
+    switch (p.fam) {
+        case FAM_LIR: eval_lircmop(p.id, x, p.d, f, g); break;
+        case FAM_DTLZ: eval_dtlz(p.id, x, p.d, p.m, f, g); break;
+        case FAM_WTA: eval_wta(p.w, x, p.d, f, g); break;
+        case FAM_MW: eval_mw(p.id, x, p.d, p.m, f, g); break;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// scalarization (reference: proj/src/scalarize.cpp, proj/src/kernels.cpp)
+
+// kernels.cpp:56-67: four lane accumulators over the blocked prefix, lanes
+// combined left to right, tail in order
+double relu_sum(const double* a, int n) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    int blocked = n / 4 * 4;
+    for (int i = 0; i < blocked; ++i) acc[i % 4] += a[i] > 0.0 ? a[i] : 0.0;
+    double s = ((acc[0] + acc[1]) + acc[2]) + acc[3];
+    for (int i = blocked; i < n; ++i) s += a[i] > 0.0 ? a[i] : 0.0;
+    return s;
+}
+
+// scalarize.cpp:39-49
+double cv_raw(const double* raw, int nin, int neq) {
+    if (neq == 0) return relu_sum(raw, nin);
+    double s = relu_sum(raw, nin);
+    for (int j = nin; j < nin + neq; ++j) {
+        double v = std::fabs(raw[j]) - 1e-6;
+        s += v > 0.0 ? v : 0.0;
+    }
+    return s;
+}
+
+// scalarize.cpp:72-89
+double pbi(const double* f, const double* w, const double* z, int m, double theta) {
+    double wn2 = 0.0;
+    for (int i = 0; i < m; ++i) wn2 += w[i] * w[i];
+    if (wn2 == 0.0) throw std::invalid_argument("pbi: zero-norm reference vector");
+    double wn = std::sqrt(wn2);
+    double proj = 0.0;
+    for (int i = 0; i < m; ++i) proj += (f[i] - z[i]) * w[i];
+    double d1 = std::fabs(proj) / wn;
+    double d2sq = 0.0;
+    for (int i = 0; i < m; ++i) {
+        double r = (f[i] - z[i]) - d1 * (w[i] / wn);
+        d2sq += r * r;
+    }
+    return d1 + theta * std::sqrt(d2sq);
+}
+
+// scalarize.cpp:91-96
+bool fpr_better(double ga, double cva, double gb, double cvb) {
+    if (cva < 0.0 || cvb < 0.0)
+        throw std::invalid_argument("fpr_better: negative constraint violation");
+    if (cva == cvb) return ga < gb;
+    return cva < cvb;
+}
+
+// ---------------------------------------------------------------------------
+// lattice + neighbourhoods (reference: proj/src/gmpea.cpp:27-100)
+
+size_t lattice_size(size_t m, size_t H) {
+    size_t n = 1;
+    for (size_t i = 1; i < m; ++i) n = n * (H + i) / i;
+    return n;
+}
+
+void compositions(size_t m, size_t H, std::vector<size_t>& cur, std::vector<double>& out) {
+    size_t used = 0;
+    for (size_t v : cur) used += v;
+    if (cur.size() + 1 == m) {
+        for (size_t v : cur) out.push_back(static_cast<double>(v) / H);
+        out.push_back(static_cast<double>(H - used) / H);
+        return;
+    }
+    for (size_t v = 0; v + used <= H; ++v) {
+        cur.push_back(v);
+        compositions(m, H, cur, out);
+        cur.pop_back();
+    }
+}
+
+std::vector<double> reference_vectors(size_t m, size_t n) {
+    size_t H = 1;
+    while (lattice_size(m, H) < n) ++H;
+    std::vector<double> flat;
+    std::vector<size_t> cur;
+    compositions(m, H, cur, flat);
+    flat.resize(n * m);
+    return flat;
+}
+
+// brute-force t-NN with the (d2, j) sort order of gmpea.cpp:84-97
+void knn(const double* W, size_t n, size_t m, size_t t, uint32_t* out) {
+    std::vector<std::pair<double, uint32_t>> d(n);
+    for (size_t i = 0; i < n; ++i) {
+        for (size_t j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (size_t c = 0; c < m; ++c) {
+                double v = W[i * m + c] - W[j * m + c];
+                s += v * v;
+            }
+            d[j] = {s, static_cast<uint32_t>(j)};
+        }
+        std::partial_sort(d.begin(), d.begin() + static_cast<std::ptrdiff_t>(t), d.end());
+        for (size_t k = 0; k < t; ++k) out[i * t + k] = d[k].second;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// environmental selection (reference: proj/src/gmpea.cpp:248-399)
+//
+// Works on (F, cv) only: X and C ride along with the winning row, so the
+// outcome is fully described by a source code per parent slot:
+//   -1 = parent kept, c in [0,N) = off1 row c, N + c = off2 row c.
+// OP1 is represented without a physical swap: eff_k[i] names the row stream k
+// holds after cooperation.
+
+struct SelIn {
+    int n, m;
+    const double *F1, *cv1, *F2, *cv2;     // parents
+    const double *Fo1, *cvo1, *Fo2, *cvo2; // offspring
+    const double *W, *z;
+    double theta;
+    int t1, t2;
+    const uint32_t *B1, *B2;
+};
+
+void selection(const SelIn& s, int32_t* src1, int32_t* src2, uint8_t* marks1, uint8_t* marks2) {
+    const int n = s.n, m = s.m;
+    // OP1 (gmpea.cpp:248-279)
+    std::vector<int32_t> eff1(n), eff2(n);
+    for (int i = 0; i < n; ++i) {
+        double g1 = pbi(s.Fo1 + i * m, s.W + i * m, s.z, m, s.theta);
+        double g2 = pbi(s.Fo2 + i * m, s.W + i * m, s.z, m, s.theta);
+        double c1 = s.cvo1[i], c2 = s.cvo2[i];
+        // the reference builds these through Heaviside masks on differences,
+        // which reject non-finite values (batch.cpp:10-16)
+        if (!std::isfinite(c1 - c2) || !std::isfinite(g1 - g2))
+            throw std::invalid_argument("non-finite mask source");
+        bool s1 = c2 < c1 || (c1 == c2 && g1 > g2);
+        bool s2 = g2 > g1;
+        eff1[i] = s1 ? n + i : i;
+        eff2[i] = s2 ? i : n + i;
+    }
+    auto Fof = [&](int32_t code) { return code < n ? s.Fo1 + code * m : s.Fo2 + (code - n) * m; };
+    auto cvof = [&](int32_t code) { return code < n ? s.cvo1[code] : s.cvo2[code - n]; };
+    for (int pop = 1; pop <= 2; ++pop) {
+        const int t = pop == 1 ? s.t1 : s.t2;
+        const uint32_t* B = pop == 1 ? s.B1 : s.B2;
+        const double* Fp = pop == 1 ? s.F1 : s.F2;
+        const double* cvp = pop == 1 ? s.cv1 : s.cv2;
+        const std::vector<int32_t>& eff = pop == 1 ? eff1 : eff2;
+        int32_t* src = pop == 1 ? src1 : src2;
+        uint8_t* marks = pop == 1 ? marks1 : marks2;
+        // OP2 (gmpea.cpp:283-303): marks; claims bucketed in ascending i (:318-327)
+        std::vector<std::vector<int>> claims(n);
+        for (int i = 0; i < n; ++i)
+            for (int l = 0; l < t; ++l) {
+                int j = static_cast<int>(B[i * t + l]);
+                double go = pbi(Fof(eff[i]), s.W + j * m, s.z, m, s.theta);
+                double gp = pbi(Fp + j * m, s.W + j * m, s.z, m, s.theta);
+                bool rep = pop == 1 ? fpr_better(go, cvof(eff[i]), gp, cvp[j]) : go < gp;
+                if (marks) marks[i * t + l] = rep ? 1 : 0;
+                if (rep) claims[j].push_back(i);
+            }
+        // OP3 (gmpea.cpp:333-380)
+        for (int j = 0; j < n; ++j) {
+            src[j] = -1;
+            const auto& cl = claims[j];
+            if (cl.empty()) continue;
+            int u = 0;
+            for (int c : cl) {
+                if (c != u) break;
+                ++u;
+            }
+            double bcv = cvp[j];
+            double bg = pbi(Fp + j * m, s.W + j * m, s.z, m, s.theta);
+            int bidx = u;
+            int best = -1;
+            for (int c : cl) {
+                double g = pbi(Fof(eff[c]), s.W + j * m, s.z, m, s.theta);
+                double cv = cvof(eff[c]);
+                bool wins;
+                if (pop == 1)
+                    wins = cv < bcv || (cv == bcv && g < bg) || (cv == bcv && g == bg && c < bidx);
+                else
+                    wins = g < bg || (g == bg && c < bidx);
+                if (wins) { bcv = cv; bg = g; bidx = c; best = c; }
+            }
+            if (best >= 0) src[j] = eff[best];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// variation with Philox draws (structure of proj/src/gmpea.cpp:113-206)
+
+struct Keyed {
+    uint32_t key[2];
+    uint32_t slot, gen, pop;
+    // PICK stream: sequence of 64-bit draws
+    uint32_t q = 0;
+    uint64_t next_pick() {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_PICK), q / 2};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        uint64_t v = (q % 2 == 0) ? ((uint64_t)o[1] << 32 | o[0]) : ((uint64_t)o[3] << 32 | o[2]);
+        ++q;
+        return v;
+    }
+    // rng.hpp:23-30 rejection semantics on the PICK stream
+    uint64_t index(uint64_t n) {
+        uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+        uint64_t v;
+        do { v = next_pick(); } while (v >= limit);
+        return v % n;
+    }
+    double child_coin() {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_CHILD), 0};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        uint64_t v = (uint64_t)o[1] << 32 | o[0];
+        return static_cast<double>(v >> 11) * 0x1.0p-53;
+    }
+    void gene(uint32_t j, double u[4]) {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_GENE), j};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        for (int k = 0; k < 4; ++k) u[k] = static_cast<double>(o[k]) * 0x1.0p-32;
+    }
+};
+
+struct OpParams {
+    double sbx_prob, sbx_eta, pm_eta, de_cr, de_f, pm_prob;  // pm_prob < 0: 1/d
+};
+
+// gmpea.cpp:135-160 (one gene), draws u2 (skip coin), u3 (direction)
+void pm_gene(double& x, double lo, double hi, double pm, double eta, double u2, double u3) {
+    if (u2 > pm) return;
+    double span = hi - lo;
+    if (span <= 0.0) return;
+    double u = u3, dq;
+    if (u < 0.5) {
+        double d1 = (x - lo) / span;
+        dq = std::pow(2.0 * u + (1.0 - 2.0 * u) * std::pow(1.0 - d1, eta + 1.0), 1.0 / (eta + 1.0)) - 1.0;
+    } else {
+        double d2 = (hi - x) / span;
+        dq = 1.0 - std::pow(2.0 * (1.0 - u) + 2.0 * (u - 0.5) * std::pow(1.0 - d2, eta + 1.0),
+                            1.0 / (eta + 1.0));
+    }
+    x += dq * span;
+}
+
+// std::clamp semantics: NaN passes through (gmpea.cpp:162-165)
+double clamp_ref(double v, double lo, double hi) { return v < lo ? lo : (hi < v ? hi : v); }
+
+void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, size_t t, int op,
+               const OpParams& prm, uint64_t seed, uint32_t gen, uint32_t pop, double* off,
+               int32_t* picks) {
+    const int d = p.d;
+    const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / static_cast<double>(d);
+    for (size_t i = 0; i < n; ++i) {
+        Keyed k;
+        k.key[0] = static_cast<uint32_t>(seed);
+        k.key[1] = static_cast<uint32_t>(seed >> 32);
+        k.slot = static_cast<uint32_t>(i);
+        k.gen = gen;
+        k.pop = pop;
+        size_t a = k.index(t);
+        size_t b = k.index(t);
+        while (t > 1 && b == a) b = k.index(t);
+        const double* xa = X + static_cast<size_t>(nb[i * t + a]) * d;
+        const double* xb = X + static_cast<size_t>(nb[i * t + b]) * d;
+        double* child = off + i * d;
+        size_t jrand = 0;
+        bool cross = true;
+        if (op == 0) {
+            cross = k.child_coin() <= prm.sbx_prob;
+        } else {
+            jrand = k.index(static_cast<uint64_t>(d));
+        }
+        if (picks) {
+            picks[i * 3 + 0] = static_cast<int32_t>(a);
+            picks[i * 3 + 1] = static_cast<int32_t>(b);
+            picks[i * 3 + 2] = op == 0 ? (cross ? 1 : 0) : static_cast<int32_t>(jrand);
+        }
+        const double* base = X + i * d;
+        for (int j = 0; j < d; ++j) {
+            double u[4];
+            k.gene(static_cast<uint32_t>(j), u);
+            double c;
+            if (op == 0) {
+                if (!cross) {
+                    c = xa[j];
+                } else if (u[0] <= 0.5) {
+                    double beta = u[1] <= 0.5 ? std::pow(2.0 * u[1], 1.0 / (prm.sbx_eta + 1.0))
+                                              : std::pow(1.0 / (2.0 * (1.0 - u[1])), 1.0 / (prm.sbx_eta + 1.0));
+                    c = 0.5 * ((1.0 + beta) * xa[j] + (1.0 - beta) * xb[j]);
+                } else {
+                    c = xa[j];
+                }
+            } else {
+                if (static_cast<size_t>(j) == jrand || u[0] < prm.de_cr)
+                    c = base[j] + prm.de_f * (xa[j] - xb[j]);
+                else
+                    c = base[j];
+            }
+            pm_gene(c, p.lo[j], p.hi[j], pm, prm.pm_eta, u[2], u[3]);
+            child[j] = clamp_ref(c, p.lo[j], p.hi[j]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// metrics (reference: proj/src/metrics.cpp)
+
+bool dominates(const double* a, const double* b, int m) {
+    bool strict = false;
+    for (int i = 0; i < m; ++i) {
+        if (a[i] > b[i]) return false;
+        if (a[i] < b[i]) strict = true;
+    }
+    return strict;
+}
+
+// metrics.cpp:15-37
+double igd(const double* A, size_t na, const double* R, size_t nr, int m) {
+    if (nr == 0) throw std::invalid_argument("igd: empty reference front");
+    if (na == 0) return std::numeric_limits<double>::infinity();
+    double total = 0.0;
+    for (size_t r = 0; r < nr; ++r) {
+        double best = std::numeric_limits<double>::infinity();
+        for (size_t a = 0; a < na; ++a) {
+            double s = 0.0;
+            for (int c = 0; c < m; ++c) {
+                double d = A[a * m + c] - R[r * m + c];
+                s += d * d;
+            }
+            best = std::min(best, s);
+        }
+        total += std::sqrt(best);
+    }
+    return total / static_cast<double>(nr);
+}
+
+// metrics.cpp:155-175 — feasible, dedup (first kept), nondominated rows
+std::vector<size_t> metric_front(const double* F, const double* cv, size_t n, int m) {
+    std::vector<size_t> feas;
+    for (size_t i = 0; i < n; ++i)
+        if (cv[i] == 0.0) feas.push_back(i);
+    std::vector<size_t> keep;
+    for (size_t a = 0; a < feas.size(); ++a) {
+        const double* fa = F + feas[a] * m;
+        bool skip = false;
+        for (size_t b = 0; b < feas.size() && !skip; ++b) {
+            if (a == b) continue;
+            const double* fb = F + feas[b] * m;
+            if (dominates(fb, fa, m)) skip = true;
+            if (b < a && std::equal(fa, fa + m, fb)) skip = true;
+        }
+        if (!skip) keep.push_back(feas[a]);
+    }
+    return keep;
+}
+
+// metrics.cpp:42-121
+std::vector<size_t> hv_relevant(const double* P, size_t n, int m, const double* ref) {
+    std::vector<size_t> keep;
+    for (size_t i = 0; i < n; ++i) {
+        const double* pi = P + i * m;
+        bool inside = true;
+        for (int c = 0; c < m; ++c)
+            if (!(pi[c] < ref[c])) inside = false;
+        if (!inside) continue;
+        bool skip = false;
+        for (size_t j = 0; j < n && !skip; ++j) {
+            if (j == i) continue;
+            if (dominates(P + j * m, pi, m)) skip = true;
+            if (j < i && std::equal(pi, pi + m, P + j * m)) skip = true;
+        }
+        if (!skip) keep.push_back(i);
+    }
+    return keep;
+}
+double hv2(std::vector<std::pair<double, double>> pts, double r0, double r1) {
+    if (pts.empty()) return 0.0;
+    std::sort(pts.begin(), pts.end());
+    double vol = 0.0, prev = r1;
+    for (auto [x, y] : pts)
+        if (y < prev) { vol += (r0 - x) * (prev - y); prev = y; }
+    return vol;
+}
+double hypervolume(const double* P, size_t n, int m, const double* ref) {
+    std::vector<size_t> keep = hv_relevant(P, n, m, ref);
+    if (keep.empty()) return 0.0;
+    if (m == 2) {
+        std::vector<std::pair<double, double>> pts;
+        for (size_t i : keep) pts.emplace_back(P[i * 2], P[i * 2 + 1]);
+        return hv2(std::move(pts), ref[0], ref[1]);
+    }
+    if (m == 3) {
+        std::vector<size_t> order = keep;
+        std::sort(order.begin(), order.end(), [&](size_t a, size_t b) { return P[a * 3 + 2] < P[b * 3 + 2]; });
+        double vol = 0.0;
+        for (size_t k = 0; k < order.size(); ++k) {
+            double z0 = P[order[k] * 3 + 2];
+            double z1 = k + 1 < order.size() ? P[order[k + 1] * 3 + 2] : ref[2];
+            if (z1 <= z0) continue;
+            std::vector<std::pair<double, double>> slab;
+            for (size_t t = 0; t <= k; ++t) slab.emplace_back(P[order[t] * 3], P[order[t] * 3 + 1]);
+            vol += (z1 - z0) * hv2(std::move(slab), ref[0], ref[1]);
+        }
+        return vol;
+    }
+    throw std::invalid_argument("hypervolume: oracle covers m = 2, 3 only");
+}
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+void orc_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    orc_philox4x32_10(ctr, key, out);
+}
+
+int orc_problem_info(const char* name, int32_t* d, int32_t* m, int32_t* nin, int32_t* neq,
+                     double* lo, double* hi) {
+    return guarded([&] {
+        Problem p = make_problem(name);
+        *d = p.d; *m = p.m; *nin = p.nin; *neq = p.neq;
+        if (lo) std::copy(p.lo.begin(), p.lo.end(), lo);
+        if (hi) std::copy(p.hi.begin(), p.hi.end(), hi);
+    });
+}
+
+// problems.cpp:552-573 + gmpea.cpp:15-23 (evaluate + cv)
+int orc_evaluate(const char* name, const double* X, int64_t n, double* F, double* G, double* cv) {
+    return guarded([&] {
+        Problem p = make_problem(name);
+        std::string bad;
+        for (int64_t r = 0; r < n; ++r)
+            for (int c = 0; c < p.d; ++c)
+                if (!(X[r * p.d + c] >= p.lo[c] && X[r * p.d + c] <= p.hi[c])) {
+                    bad += " " + std::to_string(r);
+                    break;
+                }
+        if (!bad.empty()) throw std::invalid_argument("evaluate: out-of-bounds rows:" + bad);
+        int nc = p.nin + p.neq;
+        for (int64_t r = 0; r < n; ++r) {
+            eval_row(p, X + r * p.d, F + r * p.m, G + r * nc);
+            if (cv) cv[r] = cv_raw(G + r * nc, p.nin, p.neq);
+        }
+    });
+}
+
+// opaque problem handle for hot loops (used by the reference-loop baseline to
+// wrap the restated MW evaluators as reference ProblemDefs)
+void* orc_problem_new(const char* name) {
+    try {
+        return new Problem(make_problem(name));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void orc_problem_free(void* h) { delete static_cast<Problem*>(h); }
+void orc_problem_eval_row(const void* h, const double* x, double* f, double* g) {
+    eval_row(*static_cast<const Problem*>(h), x, f, g);
+}
+
+int orc_wta_scenario(int32_t num, int32_t* targets, int32_t* vehicles, int32_t* strikes,
+                     int32_t* cap, double* p) {
+    return guarded([&] {
+        if (num < 1 || num > 10) throw std::invalid_argument("unknown WTA scenario");
+        Wta w = wta_scenario(num);
+        *targets = w.targets;
+        *vehicles = w.vehicles;
+        size_t o = 0;
+        for (int i = 0; i < w.targets; ++i) {
+            if (strikes) strikes[i] = w.strikes[i];
+            for (int k = 0; k < w.strikes[i]; ++k, ++o)
+                if (p) p[o] = w.p[i][k];
+        }
+        if (cap)
+            for (int v = 0; v < w.vehicles; ++v) cap[v] = w.cap[v];
+    });
+}
+
+double orc_pbi(const double* f, const double* w, const double* z, int32_t m, double theta) {
+    return pbi(f, w, z, m, theta);
+}
+
+double orc_cv(const double* raw, int32_t nin, int32_t neq) { return cv_raw(raw, nin, neq); }
+
+int orc_reference_vectors(int32_t m, int64_t n, double* W) {
+    return guarded([&] {
+        if (n <= 0) throw std::invalid_argument("reference_vectors: target_n must be positive");
+        auto v = reference_vectors(static_cast<size_t>(m), static_cast<size_t>(n));
+        std::copy(v.begin(), v.end(), W);
+    });
+}
+
+int orc_knn(const double* W, int64_t n, int32_t m, int32_t t, uint32_t* out) {
+    return guarded([&] {
+        if (t > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
+        knn(W, static_cast<size_t>(n), static_cast<size_t>(m), static_cast<size_t>(t), out);
+    });
+}
+
+int orc_selection(int32_t n, int32_t m, const double* F1, const double* cv1, const double* F2,
+                  const double* cv2, const double* Fo1, const double* cvo1, const double* Fo2,
+                  const double* cvo2, const double* W, const double* z, double theta, int32_t t1,
+                  const uint32_t* B1, int32_t t2, const uint32_t* B2, int32_t* src1, int32_t* src2,
+                  uint8_t* marks1, uint8_t* marks2) {
+    return guarded([&] {
+        SelIn s{n, m, F1, cv1, F2, cv2, Fo1, cvo1, Fo2, cvo2, W, z, theta, t1, t2, B1, B2};
+        selection(s, src1, src2, marks1, marks2);
+    });
+}
+
+int orc_reproduce(const char* name, const double* X, int64_t n, const uint32_t* nb, int32_t t,
+                  int32_t op, const double* params5, double pm_prob, uint64_t seed, uint32_t gen,
+                  uint32_t pop, double* off, int32_t* picks) {
+    return guarded([&] {
+        Problem p = make_problem(name);
+        OpParams prm{params5[0], params5[1], params5[2], params5[3], params5[4], pm_prob};
+        reproduce(p, X, static_cast<size_t>(n), nb, static_cast<size_t>(t), op, prm, seed, gen, pop,
+                  off, picks);
+    });
+}
+
+// initial population draws (INIT stream): X[r][c] = lo + (hi - lo) * u53
+int orc_init_population(const char* name, int64_t n, uint64_t seed, uint32_t pop, double* X) {
+    return guarded([&] {
+        Problem p = make_problem(name);
+        uint32_t key[2] = {static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)};
+        for (int64_t r = 0; r < n; ++r)
+            for (int c = 0; c < p.d; ++c) {
+                uint32_t ctr[4] = {static_cast<uint32_t>(r), 0u, orc_tag(pop, ORC_STREAM_INIT),
+                                   static_cast<uint32_t>(c / 2)};
+                uint32_t o[4];
+                orc_philox4x32_10(ctr, key, o);
+                uint64_t v = (c % 2 == 0) ? ((uint64_t)o[1] << 32 | o[0]) : ((uint64_t)o[3] << 32 | o[2]);
+                double u = static_cast<double>(v >> 11) * 0x1.0p-53;
+                X[r * p.d + c] = p.lo[c] + (p.hi[c] - p.lo[c]) * u;
+            }
+    });
+}
+
+int orc_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t m, double* out) {
+    return guarded([&] { *out = igd(A, static_cast<size_t>(na), R, static_cast<size_t>(nr), m); });
+}
+
+int orc_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx,
+                     int64_t* count) {
+    return guarded([&] {
+        auto k = metric_front(F, cv, static_cast<size_t>(n), m);
+        for (size_t i = 0; i < k.size(); ++i) idx[i] = static_cast<int64_t>(k[i]);
+        *count = static_cast<int64_t>(k.size());
+    });
+}
+
+int orc_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, double* out) {
+    return guarded([&] { *out = hypervolume(P, static_cast<size_t>(n), m, ref); });
+}
+
+}  // extern "C"
