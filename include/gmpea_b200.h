@@ -1,0 +1,168 @@
+/* gmpea_b200.h — C ABI of the B200-native GMPEA engine (libgmpea_b200.so).
+ *
+ * Plain pointers and sizes only; every host array is row-major f64 exactly as
+ * the reference's gmpea::Matrix (proj/include/gmpea/matrix.hpp:13-31).  Each
+ * entry point replaces one reference interface, cited per function.  The
+ * device holds fp32 structure-of-arrays copies; results come back as f64.
+ *
+ * Errors: every int-returning call returns GMPEA_OK or an error code and
+ * leaves a message retrievable with gmpea_last_error() (thread-local).  The
+ * messages reproduce the reference's exception texts; GMPEA_EINVAL maps to
+ * std::invalid_argument, GMPEA_ERUNTIME to std::runtime_error.  There is no
+ * CPU fallback: without a usable sm_100 device every compute call returns
+ * GMPEA_ECUDA.
+ *
+ * Threading: a gmpea_engine is one run (single writer, gmpea.hpp:140-144);
+ * distinct engines and the stateless operator calls may be used from
+ * different threads.
+ */
+#ifndef GMPEA_B200_H
+#define GMPEA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GMPEA_OK 0
+#define GMPEA_EINVAL 1   /* std::invalid_argument in the reference */
+#define GMPEA_ERUNTIME 2 /* std::runtime_error in the reference */
+#define GMPEA_ECUDA 3    /* CUDA runtime failure / no device */
+
+#define GMPEA_OP_SBX_PM 0 /* VariationOp::sbx_pm (gmpea.hpp:56) */
+#define GMPEA_OP_DE 1     /* VariationOp::de */
+
+typedef struct gmpea_problem gmpea_problem;
+typedef struct gmpea_engine gmpea_engine;
+
+const char* gmpea_last_error(void);
+int gmpea_abi_version(void);
+
+/* ---- problems: replaces make_problem / ProblemDef (problems.hpp:19-45,
+ * problems.cpp:531-550) and make_wta_problem / load_wta (wta.hpp:30-48).
+ * Names: LIRCMOP1..14, C1-DTLZ1, C1-DTLZ3, C2-DTLZ2, C3-DTLZ4,
+ * DC{1,2,3}-DTLZ{1,3}, WTA-P1..P10, MW1..MW14 (MW: not in the reference). */
+int gmpea_problem_create(const char* name, gmpea_problem** out);
+/* custom WTA scenario (load_wta, wta.cpp:148-192): p holds sum(strikes)
+ * interception probabilities, target-major */
+int gmpea_problem_create_wta(const char* scenario, int32_t targets, int32_t vehicles,
+                             const int32_t* strikes, const int32_t* capacity, const double* p,
+                             gmpea_problem** out);
+int gmpea_problem_info(const gmpea_problem* p, int32_t* d, int32_t* m, int32_t* n_ineq,
+                       int32_t* n_eq);
+int gmpea_problem_bounds(const gmpea_problem* p, double* lo, double* hi);
+void gmpea_problem_destroy(gmpea_problem* p);
+/* names of all registered problems, '\n'-separated (problem_names, problems.cpp:531-540) */
+const char* gmpea_problem_names(void);
+
+/* ---- evaluation: replaces evaluate (problems.hpp:47-51, problems.cpp:552-573)
+ * plus cv_batch (evaluate_population, gmpea.cpp:15-23).  X: n x d; F: n x m;
+ * G: n x (n_ineq + n_eq) raw constraints (<= 0 feasible); cv: n (may be NULL).
+ * Rows outside the bounds (or NaN) fail with GMPEA_EINVAL
+ * "evaluate: out-of-bounds rows: r1 r2 ...". */
+int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F, double* G,
+                   double* cv);
+
+/* ---- reference vectors and neighbourhoods (gmpea.hpp:37-51, gmpea.cpp:27-100) */
+int gmpea_reference_vectors(int32_t m, int64_t n, double* W);
+/* t-NN of arbitrary W (n x m, m <= 3) by fp64 distance, ties to the lower index */
+int gmpea_build_neighborhoods(const double* W, int64_t n, int32_t m, int32_t t1, int32_t t2,
+                              uint32_t* B1, uint32_t* B2);
+/* same, for W = reference_vectors(m, n), by a provably sufficient window */
+int gmpea_lattice_neighborhoods(int32_t m, int64_t n, int32_t t1, int32_t t2, uint32_t* B1,
+                                uint32_t* B2);
+
+/* ---- variation: replaces reproduce (gmpea.hpp:56-73, gmpea.cpp:113-206).
+ * The reference draws from one mt19937_64 stream (rng.hpp); the engine draws
+ * from Philox4x32-10 keyed by (seed; slot, gen, pop, stream, index) — see
+ * DESIGN.md "Random streams".  pm_prob < 0 means 1/d. */
+typedef struct {
+    double sbx_prob, sbx_eta, pm_eta, de_cr, de_f, pm_prob;
+} gmpea_operator_params;
+int gmpea_operator_params_default(gmpea_operator_params* out);
+int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const uint32_t* nbrs,
+                    int32_t t, int32_t op, const gmpea_operator_params* params, uint64_t seed,
+                    uint32_t gen, uint32_t pop, double* off);
+
+/* ---- environmental selection: replaces op1/op2/op3 and
+ * environmental_selection (gmpea.hpp:75-111, gmpea.cpp:248-399).
+ * Populations are (X n x d, F n x m, C n x nc, cv n).  Outputs are assembled
+ * from the f64 inputs, so surviving rows are bit-identical copies.
+ * winner[j] (optional): -1 parent kept, c in [0,n): off1 row c,
+ * n + c: off2 row c (the row the offspring stream held after OP1). */
+typedef struct {
+    const double *X, *F, *C, *cv;
+} gmpea_population_view;
+typedef struct {
+    double *X, *F, *C, *cv;
+} gmpea_population_out;
+int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
+                                  const gmpea_population_view* pop1,
+                                  const gmpea_population_view* pop2,
+                                  const gmpea_population_view* off1,
+                                  const gmpea_population_view* off2, const double* W,
+                                  const double* z, double theta, const uint32_t* B1, int32_t t1,
+                                  const uint32_t* B2, int32_t t2, gmpea_population_out* out1,
+                                  gmpea_population_out* out2, int32_t* winner1, int32_t* winner2);
+
+/* ---- metrics: replaces igd / hypervolume / metric_front (metrics.hpp:15-29) */
+int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t m, double* out);
+int gmpea_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx,
+                       int64_t* count);
+int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, double* out);
+
+/* ---- the run: replaces run_gmpea (gmpea.hpp:113-144, gmpea.cpp:421-493) */
+typedef struct {
+    int64_t n;             /* requested population size */
+    int64_t k_max;         /* generation cap (0 = unbounded when a budget is set) */
+    double time_budget_s;  /* <= 0: none */
+    int64_t eval_budget;   /* <= 0: none */
+    uint64_t seed;
+    int32_t op;            /* GMPEA_OP_* */
+    gmpea_operator_params params;
+    double theta;
+    int32_t t1, t2;
+    int32_t record_walltime;
+    /* engine extensions */
+    int32_t device;        /* CUDA device ordinal */
+    uint64_t stream;       /* cudaStream_t to run on; 0 = the engine's own stream */
+    const double* igd_reference; /* optional per-generation IGD hook: reference front */
+    int64_t igd_reference_rows;
+} gmpea_run_config;
+
+typedef struct {
+    int64_t gen, evals;
+    double wall_ms, feasible_ratio;
+    double igd, hv;
+    int32_t has_igd, has_hv;
+} gmpea_gen_record;
+
+int gmpea_run_config_default(gmpea_run_config* out);
+/* setup: reference vectors, neighbourhoods, initial populations (Philox INIT
+ * stream), their evaluation, the ideal point and record 0 */
+int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmpea_engine** out);
+/* replace population `which` (1 or 2) by host rows X (n x d) and re-evaluate */
+int gmpea_engine_set_population(gmpea_engine* e, int32_t which, const double* X);
+/* run to completion under k_max / eval_budget / time_budget semantics */
+int gmpea_engine_run(gmpea_engine* e);
+/* enqueue up to `gens` more generations (no host sync) */
+int gmpea_engine_step(gmpea_engine* e, int64_t gens);
+int gmpea_engine_sync(gmpea_engine* e);
+int64_t gmpea_engine_effective_n(const gmpea_engine* e);
+int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, int64_t* n);
+int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C,
+                                double* cv);
+int gmpea_engine_ideal(gmpea_engine* e, double* z);
+/* neighbourhood tables the run uses (n x t1, n x t2) */
+int gmpea_engine_neighborhoods(gmpea_engine* e, uint32_t* B1, uint32_t* B2);
+/* run `gens` generations kernel by kernel with CUDA events around each launch
+ * and return the average device milliseconds of [vary_eval, op1, select,
+ * end_gen] plus the total per generation in ms[4] */
+int gmpea_engine_profile(gmpea_engine* e, int64_t gens, double* ms);
+void gmpea_engine_destroy(gmpea_engine* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -852,11 +852,18 @@ struct Keyed {
         uint64_t v = (uint64_t)o[1] << 32 | o[0];
         return static_cast<double>(v >> 11) * 0x1.0p-53;
     }
-    void gene(uint32_t j, double u[4]) {
-        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_GENE), j};
+    // four genes per counter: gene j is word j % 4 of index j / 4
+    double word(uint32_t stream, uint32_t j) {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, stream), j / 4};
         uint32_t o[4];
         orc_philox4x32_10(ctr, key, o);
-        for (int k = 0; k < 4; ++k) u[k] = static_cast<double>(o[k]) * 0x1.0p-32;
+        return static_cast<double>(o[j % 4]) * 0x1.0p-32;
+    }
+    double mu(uint32_t j) {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_MU), j};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        return static_cast<double>(o[0]) * 0x1.0p-32;
     }
 };
 
@@ -864,12 +871,13 @@ struct OpParams {
     double sbx_prob, sbx_eta, pm_eta, de_cr, de_f, pm_prob;  // pm_prob < 0: 1/d
 };
 
-// gmpea.cpp:135-160 (one gene), draws u2 (skip coin), u3 (direction)
-void pm_gene(double& x, double lo, double hi, double pm, double eta, double u2, double u3) {
-    if (u2 > pm) return;
+// gmpea.cpp:135-160 for one gene: the skip coin comes from MCOIN, the
+// direction uniform from MU (drawn only for mutated genes)
+void pm_gene(double& x, double lo, double hi, double pm, double eta, Keyed& k, uint32_t j) {
+    if (k.word(ORC_STREAM_MCOIN, j) > pm) return;
     double span = hi - lo;
     if (span <= 0.0) return;
-    double u = u3, dq;
+    double u = k.mu(j), dq;
     if (u < 0.5) {
         double d1 = (x - lo) / span;
         dq = std::pow(2.0 * u + (1.0 - 2.0 * u) * std::pow(1.0 - d1, eta + 1.0), 1.0 / (eta + 1.0)) - 1.0;
@@ -916,26 +924,26 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
         }
         const double* base = X + i * d;
         for (int j = 0; j < d; ++j) {
-            double u[4];
-            k.gene(static_cast<uint32_t>(j), u);
+            const uint32_t uj = static_cast<uint32_t>(j);
             double c;
             if (op == 0) {
                 if (!cross) {
                     c = xa[j];
-                } else if (u[0] <= 0.5) {
-                    double beta = u[1] <= 0.5 ? std::pow(2.0 * u[1], 1.0 / (prm.sbx_eta + 1.0))
-                                              : std::pow(1.0 / (2.0 * (1.0 - u[1])), 1.0 / (prm.sbx_eta + 1.0));
+                } else if (k.word(ORC_STREAM_XCOIN, uj) <= 0.5) {
+                    double u = k.word(ORC_STREAM_XU, uj);
+                    double beta = u <= 0.5 ? std::pow(2.0 * u, 1.0 / (prm.sbx_eta + 1.0))
+                                           : std::pow(1.0 / (2.0 * (1.0 - u)), 1.0 / (prm.sbx_eta + 1.0));
                     c = 0.5 * ((1.0 + beta) * xa[j] + (1.0 - beta) * xb[j]);
                 } else {
                     c = xa[j];
                 }
             } else {
-                if (static_cast<size_t>(j) == jrand || u[0] < prm.de_cr)
-                    c = base[j] + prm.de_f * (xa[j] - xb[j]);
-                else
-                    c = base[j];
+                // CR >= 1 decides the coin without drawing it (u < 1 <= CR)
+                bool take = static_cast<size_t>(j) == jrand || prm.de_cr >= 1.0 ||
+                            k.word(ORC_STREAM_XCOIN, uj) < prm.de_cr;
+                c = take ? base[j] + prm.de_f * (xa[j] - xb[j]) : base[j];
             }
-            pm_gene(c, p.lo[j], p.hi[j], pm, prm.pm_eta, u[2], u[3]);
+            pm_gene(c, p.lo[j], p.hi[j], pm, prm.pm_eta, k, uj);
             child[j] = clamp_ref(c, p.lo[j], p.hi[j]);
         }
     }

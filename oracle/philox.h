@@ -3,7 +3,7 @@
  * Independent CPU restatement of Philox4x32-10 (Salmon et al., SC'11; the
  * algorithm cuRAND ships as curand_Philox4x32_10) and of the GMPEA-B200 draw
  * key schema.  The product kernels carry their own implementation
- * (paper_2509_19821_b200/csrc/philox.cuh); tests/test_oracle_pins.py pins this
+ * (paper_2509_19821_b200/csrc/common.cuh); tests/test_oracle_pins.py pins this
  * one to the published Random123 known-answer vectors, and the GPU parity
  * tests compare the two draw for draw.
  *
@@ -11,15 +11,21 @@
  *   key = { (u32)seed, (u32)(seed >> 32) }
  *   ctr = { slot, gen, tag(pop, stream), index }
  *   tag(pop, stream) = (pop << 28) | (stream << 20)
- * streams: INIT (initial population, gen = 0), PICK (neighbour draws and
- * DE jrand: a sequence of 64-bit draws, two per counter), CHILD (the SBX
- * per-child coin), GENE (one counter per gene: four 32-bit words).
+ * streams: INIT (initial population, gen = 0; two 64-bit draws per counter),
+ * PICK (neighbour draws and DE jrand: a sequence of 64-bit draws, two per
+ * counter), CHILD (the SBX per-child coin, one 53-bit uniform), XCOIN (SBX
+ * per-gene coin / DE CR coin), XU (SBX spread uniform), MCOIN (PM coin) —
+ * these three give four genes per counter, gene j = word j%4 of index j/4,
+ * u = w * 2^-32 — and MU (PM direction, index j, word 0).
  */
 #ifndef GMPEA_ORACLE_PHILOX_H
 #define GMPEA_ORACLE_PHILOX_H
 #include <stdint.h>
 
-enum { ORC_STREAM_INIT = 1, ORC_STREAM_PICK = 2, ORC_STREAM_CHILD = 3, ORC_STREAM_GENE = 4 };
+enum {
+    ORC_STREAM_INIT = 1, ORC_STREAM_PICK = 2, ORC_STREAM_CHILD = 3,
+    ORC_STREAM_XCOIN = 5, ORC_STREAM_XU = 6, ORC_STREAM_MCOIN = 7, ORC_STREAM_MU = 8
+};
 
 static inline uint32_t orc_tag(uint32_t pop, uint32_t stream) {
     return (pop << 28) | (stream << 20);

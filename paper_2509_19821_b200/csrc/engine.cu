@@ -1,0 +1,1496 @@
+// GMPEA-B200 engine: host runtime (C++) + C ABI (include/gmpea_b200.h).
+//
+// The host side owns every device buffer, builds the setup (reference
+// vectors, neighbourhoods, reverse lists, initial populations) with kernels,
+// captures one generation (vary_eval -> op1 -> select -> end_gen [-> restore])
+// as a CUDA graph and replays it.  It mirrors run_gmpea (gmpea.cpp:421-493):
+// k_max / eval-budget / time-budget semantics, the discarded crossing
+// generation, per-generation GenRecords and the returned pop1.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <random>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gmpea_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "metrics.cuh"
+#include "problems.cuh"
+#include "topology.cuh"
+
+using namespace gmpea_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(expr)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw cuda_error(std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return GMPEA_OK;
+    } catch (const cuda_error& e) {
+        g_err = e.what();
+        return GMPEA_ECUDA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return GMPEA_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GMPEA_ERUNTIME;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t count) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = count;
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+inline int blocks_for(long long n, int bs) { return (int)((n + bs - 1) / bs); }
+
+void require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw cuda_error("no CUDA device available (the engine has no CPU fallback)");
+}
+
+// ---------------------------------------------------------------- problems
+constexpr double kPi = 3.141592653589793;
+
+struct WtaHost {
+    std::string scenario;
+    int targets = 0, vehicles = 0;
+    std::vector<int> strikes, cap;
+    std::vector<double> p;  // per strike slot, target-major
+};
+
+// wta_scenario (wta.cpp:23-49): sizes grow with the index, tables from the
+// reference's seeded mt19937_64 draws (rng.hpp:18-30)
+WtaHost wta_scenario(int num) {
+    WtaHost w;
+    w.scenario = "P" + std::to_string(num);
+    w.targets = 4 + 2 * (num - 1);
+    w.vehicles = 3 + (num - 1) / 2;
+    std::mt19937_64 e(0x57A0000ull + (uint64_t)num);
+    auto index = [&](uint64_t n) {
+        uint64_t limit = UINT64_MAX - UINT64_MAX % n, v;
+        do {
+            v = e();
+        } while (v >= limit);
+        return v % n;
+    };
+    for (int i = 0; i < w.targets; ++i) w.strikes.push_back(1 + (int)index(3));
+    for (int v = 0; v < w.vehicles; ++v) w.cap.push_back(2 + (int)index(3));
+    for (int i = 0; i < w.targets; ++i)
+        for (int k = 0; k < w.strikes[i]; ++k) w.p.push_back(0.35 + 0.6 * ((double)(e() >> 11) * 0x1.0p-53));
+    return w;
+}
+
+int mw_ncon(int id) {
+    switch (id) {
+        case 3: case 7: case 12: case 13: return 2;
+        case 5: case 10: return 3;
+        case 11: return 4;
+        default: return 1;
+    }
+}
+
+}  // namespace
+
+struct gmpea_problem {
+    std::string name;
+    int fam = 0, id = 0, d = 0, m = 0, nin = 0, neq = 0;
+    std::vector<double> lo, hi;
+    WtaHost wta;
+    int device = 0;
+    // device copies
+    DevBuf<float> dlo, dhi;
+    DevBuf<double> dlo64, dhi64;
+    DevBuf<int> dcap, dstrikes, dslot_target;
+    DevBuf<double> dp;
+    ProbDev dev{};
+
+    void upload() {
+        require_device();
+        CK(cudaGetDevice(&device));
+        std::vector<float> lf(lo.begin(), lo.end()), hf(hi.begin(), hi.end());
+        dlo.alloc(d);
+        dhi.alloc(d);
+        dlo64.alloc(d);
+        dhi64.alloc(d);
+        CK(cudaMemcpy(dlo.p, lf.data(), d * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dhi.p, hf.data(), d * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dlo64.p, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dhi64.p, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+        dev = ProbDev{};
+        dev.fam = fam;
+        dev.id = id;
+        dev.d = d;
+        dev.m = m;
+        dev.nin = nin;
+        dev.neq = neq;
+        dev.lo = dlo.p;
+        dev.hi = dhi.p;
+        // the reference evaluates these with glibc at run time; volatile keeps
+        // the host compiler from folding them with a different rounding
+        volatile double th = -0.25 * kPi, al = 0.25 * kPi;
+        dev.cth = std::cos(th);
+        dev.sth = std::sin(th);
+        dev.cal = std::cos(al);
+        dev.sal = std::sin(al);
+        if (fam == FAM_WTA) {
+            std::vector<int> st;
+            for (int i = 0; i < wta.targets; ++i)
+                for (int k = 0; k < wta.strikes[i]; ++k) st.push_back(i);
+            dcap.alloc(wta.vehicles);
+            dstrikes.alloc(wta.targets);
+            dslot_target.alloc(st.size());
+            dp.alloc(wta.p.size());
+            CK(cudaMemcpy(dcap.p, wta.cap.data(), wta.vehicles * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dstrikes.p, wta.strikes.data(), wta.targets * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dslot_target.p, st.data(), st.size() * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dp.p, wta.p.data(), wta.p.size() * sizeof(double), cudaMemcpyHostToDevice));
+            dev.wta_targets = wta.targets;
+            dev.wta_vehicles = wta.vehicles;
+            dev.wta_slots = (int)st.size();
+            dev.wta_cap = dcap.p;
+            dev.wta_strikes = dstrikes.p;
+            dev.wta_slot_target = dslot_target.p;
+            dev.wta_p = dp.p;
+        }
+    }
+};
+
+namespace {
+
+void make_wta(gmpea_problem& p, const WtaHost& w) {
+    if (w.targets <= 0 || w.vehicles <= 0) throw std::invalid_argument("WTA: empty scenario");
+    if (w.vehicles > kWtaMaxVehicles)
+        throw std::invalid_argument("WTA: at most " + std::to_string(kWtaMaxVehicles) + " vehicles");
+    int slots = 0;
+    for (int s : w.strikes) slots += s;
+    if (slots > kWtaMaxSlots) throw std::invalid_argument("WTA: too many strike slots");
+    for (int c : w.cap)
+        if (c < 0 || c > kWtaMaxCap)
+            throw std::invalid_argument("WTA: vehicle capacity above " + std::to_string(kWtaMaxCap));
+    p.fam = FAM_WTA;
+    p.wta = w;
+    p.name = "WTA-" + w.scenario;
+    p.d = slots * w.vehicles;
+    p.m = 2;
+    p.nin = w.vehicles + w.targets;
+    p.lo.assign(p.d, 0.0);
+    p.hi.assign(p.d, 1.0);
+}
+
+std::unique_ptr<gmpea_problem> make_problem(const std::string& name) {
+    auto p = std::make_unique<gmpea_problem>();
+    p->name = name;
+    auto num = [&](size_t pos) {
+        try {
+            size_t used = 0;
+            int v = std::stoi(name.substr(pos), &used);
+            if (used != name.size() - pos) return -1;
+            return v;
+        } catch (...) {
+            return -1;
+        }
+    };
+    if (name.rfind("LIRCMOP", 0) == 0) {
+        int id = num(7);
+        if (id >= 1 && id <= 14) {
+            p->fam = FAM_LIR;
+            p->id = id;
+            p->d = 30;
+            p->m = id >= 13 ? 3 : 2;
+            p->nin = (id == 3 || id == 4 || id == 7 || id == 8 || id == 14) ? 3 : 2;
+            p->lo.assign(p->d, 0.0);
+            p->hi.assign(p->d, 1.0);
+            return p;
+        }
+    }
+    if (name.rfind("MW", 0) == 0) {
+        int id = num(2);
+        if (id >= 1 && id <= 14) {
+            p->fam = FAM_MW;
+            p->id = id;
+            p->d = 15;
+            p->m = (id == 4 || id == 8 || id == 14) ? 3 : 2;
+            p->nin = mw_ncon(id);
+            p->lo.assign(p->d, 0.0);
+            p->hi.assign(p->d, id == 14 ? 1.5 : 1.0);
+            return p;
+        }
+    }
+    if (name.rfind("WTA-", 0) == 0) {
+        std::string sc = name.substr(4);
+        int v = sc.size() >= 2 && sc[0] == 'P' ? num(5) : -1;
+        if (v < 1 || v > 10) throw std::invalid_argument("unknown WTA scenario: " + sc);
+        make_wta(*p, wta_scenario(v));
+        p->id = v;
+        return p;
+    }
+    static const char* kDtlz[] = {"C1-DTLZ1", "C1-DTLZ3", "C2-DTLZ2", "C3-DTLZ4", "DC1-DTLZ1",
+                                  "DC1-DTLZ3", "DC2-DTLZ1", "DC2-DTLZ3", "DC3-DTLZ1", "DC3-DTLZ3"};
+    for (int k = 0; k < 10; ++k)
+        if (name == kDtlz[k]) {
+            p->fam = FAM_DTLZ;
+            p->id = k + 1;
+            p->m = 3;
+            bool d7 = p->id == C1_DTLZ1 || p->id == DC1_DTLZ1 || p->id == DC2_DTLZ1 || p->id == DC3_DTLZ1;
+            p->d = d7 ? 7 : 12;
+            if (p->id == C3_DTLZ4)
+                p->nin = 3;
+            else if (p->id == DC2_DTLZ1 || p->id == DC2_DTLZ3)
+                p->nin = 2;
+            else if (p->id == DC3_DTLZ1 || p->id == DC3_DTLZ3)
+                p->nin = 3;
+            else
+                p->nin = 1;
+            p->lo.assign(p->d, 0.0);
+            p->hi.assign(p->d, 1.0);
+            return p;
+        }
+    throw std::invalid_argument("unknown problem: " + name);
+}
+
+// ---------------------------------------------------------------- layout helpers
+// row-major f64 (n x k) <-> fp32 planes (k x ld); optional f64 bounds check
+__global__ void to_planes_kernel(const double* in, long long n, int k, float* out, long long ld,
+                                 const double* lo, const double* hi, int* bad, int* nbad) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * k) return;
+    const long long r = e / k;
+    const int c = (int)(e % k);
+    const double v = in[e];
+    out[(long long)c * ld + r] = (float)v;
+    if (lo && !(v >= lo[c] && v <= hi[c])) {
+        // one entry per offending row: the first failing column claims it
+        bool first = true;
+        for (int cc = 0; cc < c; ++cc) {
+            double w = in[r * k + cc];
+            if (!(w >= lo[cc] && w <= hi[cc])) {
+                first = false;
+                break;
+            }
+        }
+        if (first) bad[atomicAdd(nbad, 1)] = (int)r;
+    }
+}
+
+__global__ void from_planes_kernel(const float* in, long long ld, long long n, int k, double* out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * k) return;
+    const long long r = e / k;
+    const int c = (int)(e % k);
+    out[e] = (double)in[(long long)c * ld + r];
+}
+
+__global__ void fcv_from_rows_kernel(const double* F, const double* cv, long long n, int m, float4* out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 o = make_float4((float)F[i * m], (float)F[i * m + 1], m > 2 ? (float)F[i * m + 2] : 0.0f,
+                           (float)cv[i]);
+    out[i] = o;
+}
+
+__global__ void fcv_to_rows_kernel(const float4* in, long long n, int m, double* F, double* cv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 v = in[i];
+    F[i * m] = v.x;
+    F[i * m + 1] = v.y;
+    if (m > 2) F[i * m + 2] = v.z;
+    if (cv) cv[i] = v.w;
+}
+
+__global__ void u32_to_i32_kernel(const unsigned* in, long long n, int* out, int lim, int* err) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    unsigned v = in[e];
+    if (v >= (unsigned)lim) atomicExch(err, 1);
+    out[e] = (int)v;
+}
+
+__global__ void init_state_kernel(DevState* st, int m) {
+    for (int k = 0; k < 4; ++k) st->zbits[k] = k < m ? 0xffffffffu : float_to_ordered(0.0f);
+}
+
+__global__ void set_z_kernel(DevState* st, int m, float z0, float z1, float z2) {
+    st->zbits[0] = float_to_ordered(z0);
+    st->zbits[1] = float_to_ordered(z1);
+    st->zbits[2] = m > 2 ? float_to_ordered(z2) : float_to_ordered(0.0f);
+}
+
+__global__ void z_of_kernel(const float4* Fcv, long long n, int m, DevState* st) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 v = Fcv[i];
+    atomicMin(&st->zbits[0], float_to_ordered(v.x));
+    atomicMin(&st->zbits[1], float_to_ordered(v.y));
+    if (m > 2) atomicMin(&st->zbits[2], float_to_ordered(v.z));
+}
+
+__global__ void publish_stop_kernel(const DevState* st, volatile int* host_flag) {
+    *host_flag = st->stop | (st->err ? 2 : 0);
+}
+
+struct PopBuf {
+    DevBuf<float> X, G;
+    DevBuf<float4> Fcv;
+    void alloc(int d, int nc, long long ld) {
+        X.alloc((size_t)d * ld);
+        G.alloc((size_t)std::max(nc, 1) * ld);
+        Fcv.alloc(ld);
+    }
+};
+
+// ---------------------------------------------------------------- kernel dispatch
+using VaryKernel = void (*)(VaryParams);
+
+template <class Ev>
+VaryKernel pick_vary(int mode, int op) {
+    if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
+    if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
+    return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX>;
+}
+
+VaryKernel vary_kernel_for(int fam, int mode, int op) {
+    switch (fam) {
+        case FAM_LIR: return pick_vary<EvalLir>(mode, op);
+        case FAM_DTLZ: return pick_vary<EvalDtlz>(mode, op);
+        case FAM_WTA: return pick_vary<EvalWta>(mode, op);
+        default: return pick_vary<EvalMw>(mode, op);
+    }
+}
+
+void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
+    vp.sbx_prob = prm.sbx_prob;
+    vp.sbx_e = (float)(1.0 / (prm.sbx_eta + 1.0));
+    vp.pm_e1 = (float)(prm.pm_eta + 1.0);
+    vp.pm_einv = (float)(1.0 / (prm.pm_eta + 1.0));
+    const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / (double)d;
+    // PM: skip iff u > pm with u = w 2^-32  <=>  mutate iff w <= floor(pm 2^32)
+    const double T = pm * 4294967296.0;
+    vp.pm_thr = pm < 0.0 ? -1 : (long long)std::min(std::floor(T), 4294967295.0);
+    // DE: take iff u < CR  <=>  w < ceil(CR 2^32)
+    const double C = prm.de_cr * 4294967296.0;
+    vp.cr_thr = prm.de_cr >= 1.0 ? 0x100000000ull : (prm.de_cr <= 0.0 ? 0ull : (unsigned long long)std::ceil(C));
+    vp.de_f = (float)prm.de_f;
+}
+
+std::string rows_message(std::vector<int> rows) {
+    std::sort(rows.begin(), rows.end());
+    std::ostringstream os;
+    os << "evaluate: out-of-bounds rows:";
+    for (int r : rows) os << ' ' << r;
+    return os.str();
+}
+
+long long lattice_H(int m, long long n) {
+    // reference_vectors: smallest H with C(H + m - 1, m - 1) >= n (gmpea.cpp:62-66)
+    auto size = [&](long long H) {
+        long long s = 1;
+        for (long long i = 1; i < m; ++i) s = s * (H + i) / i;
+        return s;
+    };
+    long long H = 1;
+    if (m == 2) return std::max<long long>(1, n - 1);
+    while (size(H) < n) ++H;
+    return H;
+}
+
+// neighbourhoods on device: B1/B2 as int32 (n x t)
+void device_knn(cudaStream_t s, int n, int m, int t1, int t2, const double* dW, bool lattice, long long H,
+                int* B1, int* B2) {
+    if (t1 > n || t2 > n)
+        throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
+    if (t1 < 1 || t2 < 1) throw std::invalid_argument("build_neighborhoods: empty neighbourhood");
+    if (std::max(t1, t2) <= kMaxT) {
+        const int tmax = std::max(t1, t2);
+        // the insertion list keeps the first t1 of the sorted top-tmax
+        int* Bbig = t2 >= t1 ? B2 : B1;
+        int* Bsmall = t2 >= t1 ? B1 : B2;
+        int tsmall = std::min(t1, t2);
+        if (lattice && n > 4096) {
+            DevBuf<int> retry(1);
+            for (int R = 6;; R *= 2) {
+                retry.zero(s);
+                knn_lattice_kernel<<<blocks_for(n, 128), 128, 0, s>>>(n, m, H, tsmall, tmax, R, dW, Bsmall,
+                                                                       Bbig, retry.p);
+                CK(cudaGetLastError());
+                int flag = 0;
+                CK(cudaMemcpyAsync(&flag, retry.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                if (!flag) return;
+                if (R > 4096) break;
+            }
+        }
+        knn_brute_kernel<<<blocks_for(n, 128), 128, 0, s>>>(n, m, tsmall, tmax, dW, Bsmall, Bbig);
+        CK(cudaGetLastError());
+        return;
+    }
+    knn_select_kernel<<<blocks_for(n, 128), 128, 0, s>>>(n, m, t1, dW, B1);
+    knn_select_kernel<<<blocks_for(n, 128), 128, 0, s>>>(n, m, t2, dW, B2);
+    CK(cudaGetLastError());
+}
+
+// reverse neighbourhood (padded SoA, ascending); returns max in-degree
+int device_reverse(cudaStream_t s, int n, int t, const int* B, long long ld, DevBuf<int>& deg,
+                   DevBuf<int>& R) {
+    deg.alloc(std::max<long long>(ld, 1));
+    deg.zero(s);
+    const long long E = (long long)n * t;
+    indegree_kernel<<<blocks_for(E, 256), 256, 0, s>>>(n, t, B, deg.p);
+    CK(cudaGetLastError());
+    std::vector<int> h(n);
+    CK(cudaMemcpyAsync(h.data(), deg.p, n * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int maxdeg = 0;
+    for (int v : h) maxdeg = std::max(maxdeg, v);
+    R.alloc((size_t)std::max(maxdeg, 1) * ld);
+    DevBuf<int> fill(std::max(n, 1));
+    fill.zero(s);
+    reverse_fill_kernel<<<blocks_for(E, 256), 256, 0, s>>>(n, t, B, fill.p, R.p, ld);
+    reverse_sort_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, deg.p, R.p, ld);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return maxdeg;
+}
+
+}  // namespace
+
+// ====================================================================== engine
+struct gmpea_engine {
+    const gmpea_problem* prob = nullptr;
+    gmpea_run_config cfg{};
+    int n = 0, d = 0, m = 0, nc = 0, t1 = 0, t2 = 0;
+    long long ld = 0, H = 0;
+    cudaStream_t s = nullptr;
+    bool own_stream = false;
+    bool time_mode = false;
+
+    DevBuf<DevState> st;
+    DevBuf<DevRecord> rec;
+    long long rec_cap = 0;
+    DevBuf<double> W64;
+    DevBuf<float4> U;
+    DevBuf<int> B[2], R[2], Rdeg[2];
+    int maxdeg[2] = {0, 0};
+    PopBuf pop[2], off[2], undo[2];
+    DevBuf<float4> eff[2];
+    DevBuf<unsigned char> srcbits;
+    DevBuf<int> ustamp[2];
+    DevBuf<int> bad[2];
+    int* host_flag = nullptr;
+    int* host_flag_dev = nullptr;
+
+    VaryParams vp{};
+    Op1Params op1p{};
+    SelParams sp{};
+    RestoreParams rp{};
+    VaryKernel vary = nullptr;
+    cudaGraphExec_t graph = nullptr;
+
+    long long gens_enqueued = 0;  // generations launched (host view)
+    long long gen_limit = 0;      // max generations allowed by k_max / eval budget (-1 = inf)
+    bool finished = false;
+
+    ~gmpea_engine() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (host_flag) cudaFreeHost(host_flag);
+        if (own_stream && s) cudaStreamDestroy(s);
+    }
+
+    void setup(const gmpea_problem* p, const gmpea_run_config& c) {
+        prob = p;
+        cfg = c;
+        if (c.n <= 0) throw std::invalid_argument("reference_vectors: target_n must be positive");
+        if (c.n > (1ll << 30)) throw std::invalid_argument("engine: n too large");
+        if (p->m > kMaxM || p->m < 2) throw std::invalid_argument("engine: objectives must be 2 or 3");
+        CK(cudaSetDevice(c.device));
+        if (c.stream) {
+            s = (cudaStream_t)(uintptr_t)c.stream;
+        } else {
+            CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            own_stream = true;
+        }
+        n = (int)c.n;
+        d = p->d;
+        m = p->m;
+        nc = p->nin + p->neq;
+        ld = round_up(n, 32);
+        t1 = (int)std::min<long long>(c.t1, n);
+        t2 = (int)std::min<long long>(c.t2, n);
+        time_mode = c.time_budget_s > 0.0;
+        H = lattice_H(m, n);
+
+        st.alloc(1);
+        st.zero(s);
+        init_state_kernel<<<1, 1, 0, s>>>(st.p, m);
+        // generation limit (gmpea.cpp:456-459)
+        bool unbounded = c.k_max == 0 && (time_mode || c.eval_budget > 0);
+        long long lim = c.k_max > 0 ? c.k_max : (unbounded ? -1 : 0);
+        if (c.eval_budget > 0) {
+            long long e = c.eval_budget / (2ll * n) - 1;  // gens with evals + 2n <= budget
+            if (e < 0) e = 0;
+            lim = lim < 0 ? e : std::min(lim, e);
+        }
+        gen_limit = lim;
+        rec_cap = (lim >= 0 ? lim : (1ll << 22)) + 2;
+        rec.alloc(rec_cap);
+        rec.zero(s);
+
+        // reference vectors + neighbourhoods (gmpea.cpp:424-428)
+        W64.alloc((size_t)n * m);
+        U.alloc(ld);
+        U.zero(s);
+        lattice_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, m, H, W64.p, U.p);
+        CK(cudaGetLastError());
+        B[0].alloc((size_t)n * t1);
+        B[1].alloc((size_t)n * t2);
+        device_knn(s, n, m, t1, t2, W64.p, true, H, B[0].p, B[1].p);
+        maxdeg[0] = device_reverse(s, n, t1, B[0].p, ld, Rdeg[0], R[0]);
+        maxdeg[1] = device_reverse(s, n, t2, B[1].p, ld, Rdeg[1], R[1]);
+
+        for (int q = 0; q < 2; ++q) {
+            pop[q].alloc(d, nc, ld);
+            off[q].alloc(d, nc, ld);
+            eff[q].alloc(ld);
+            bad[q].alloc(kMaxBadRows);
+            pop[q].Fcv.zero(s);
+            off[q].Fcv.zero(s);
+            if (time_mode) {
+                undo[q].alloc(d, nc, ld);
+                ustamp[q].alloc(ld);
+                CK(cudaMemsetAsync(ustamp[q].p, 0xff, ld * sizeof(int), s));
+            }
+        }
+        srcbits.alloc(ld);
+        CK(cudaHostAlloc(&host_flag, sizeof(int), cudaHostAllocMapped));
+        *host_flag = 0;
+        CK(cudaHostGetDevicePointer((void**)&host_flag_dev, host_flag, 0));
+
+        // kernel parameter blocks
+        vp = VaryParams{};
+        vp.n = n;
+        vp.ld = (int)ld;
+        vp.slot_base = 0;
+        vp.npops = 2;
+        vp.pop_id[0] = 1;
+        vp.pop_id[1] = 2;
+        vp.P = p->dev;
+        vp.t[0] = t1;
+        vp.t[1] = t2;
+        vp.key0 = (unsigned)c.seed;
+        vp.key1 = (unsigned)(c.seed >> 32);
+        fill_op_params(vp, c.params, d);
+        vp.eval = 1;
+        vp.update_z = 1;
+        vp.fixed_gen = -1;
+        vp.st = st.p;
+        vp.bad_cap = kMaxBadRows;
+        for (int q = 0; q < 2; ++q) {
+            vp.B[q] = B[q].p;
+            vp.bad_rows[q] = bad[q].p;
+        }
+
+        // initial populations (gmpea.cpp:430-437): Philox INIT stream
+        for (int q = 0; q < 2; ++q) {
+            vp.parX[q] = pop[q].X.p;
+            vp.outX[q] = pop[q].X.p;
+            vp.outG[q] = pop[q].G.p;
+            vp.outFcv[q] = pop[q].Fcv.p;
+        }
+        VaryParams ip = vp;
+        ip.fixed_gen = 0;
+        vary_kernel_for(p->fam, MODE_INIT, 0)<<<dim3(blocks_for(n, 128), 2), 128, 0, s>>>(ip);
+        CK(cudaGetLastError());
+        finish_init();
+
+        // generation parameter blocks
+        for (int q = 0; q < 2; ++q) {
+            vp.parX[q] = pop[q].X.p;
+            vp.outX[q] = off[q].X.p;
+            vp.outG[q] = off[q].G.p;
+            vp.outFcv[q] = off[q].Fcv.p;
+        }
+        vary = vary_kernel_for(p->fam, MODE_VARY, c.op);
+        op1p = Op1Params{n, m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p}, {eff[0].p, eff[1].p},
+                         srcbits.p, st.p};
+        sp = SelParams{};
+        sp.n = n;
+        sp.ld = (int)ld;
+        sp.d = d;
+        sp.nc = nc;
+        sp.m = m;
+        sp.theta = (float)c.theta;
+        sp.U = U.p;
+        for (int q = 0; q < 2; ++q) {
+            sp.X[q] = pop[q].X.p;
+            sp.G[q] = pop[q].G.p;
+            sp.Fcv[q] = pop[q].Fcv.p;
+            sp.oX[q] = off[q].X.p;
+            sp.oG[q] = off[q].G.p;
+            sp.oFcv[q] = off[q].Fcv.p;
+            sp.eff[q] = eff[q].p;
+            sp.R[q] = R[q].p;
+            sp.Rdeg[q] = Rdeg[q].p;
+            sp.winner[q] = nullptr;
+            if (time_mode) {
+                sp.uX[q] = undo[q].X.p;
+                sp.uG[q] = undo[q].G.p;
+                sp.uFcv[q] = undo[q].Fcv.p;
+                sp.ustamp[q] = ustamp[q].p;
+                rp.X[q] = pop[q].X.p;
+                rp.G[q] = pop[q].G.p;
+                rp.Fcv[q] = pop[q].Fcv.p;
+                rp.uX[q] = undo[q].X.p;
+                rp.uG[q] = undo[q].G.p;
+                rp.uFcv[q] = undo[q].Fcv.p;
+                rp.ustamp[q] = ustamp[q].p;
+            }
+        }
+        sp.srcbits = srcbits.p;
+        sp.apply = 1;
+        sp.st = st.p;
+        sp.rec = rec.p;
+        rp.n = n;
+        rp.ld = (int)ld;
+        rp.d = d;
+        rp.nc = nc;
+        rp.st = st.p;
+        CK(cudaStreamSynchronize(s));
+        check_errors(0);
+    }
+
+    // evaluation of the initial populations done: z, record 0, gen = 1
+    void finish_init() {
+        init_state_kernel<<<1, 1, 0, s>>>(st.p, m);
+        for (int q = 0; q < 2; ++q) z_of_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[q].Fcv.p, n, m, st.p);
+        rec.zero(s);
+        count_feasible_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[0].Fcv.p, n, &rec.p[0].feasible);
+        DevState init{};
+        CK(cudaMemcpyAsync(&init, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        DevState fresh{};
+        for (int k = 0; k < 4; ++k) fresh.zbits[k] = init.zbits[k];
+        fresh.gen = 1;
+        fresh.err = init.err;
+        fresh.err_gen = init.err_gen;
+        fresh.n_bad[0] = init.n_bad[0];
+        fresh.n_bad[1] = init.n_bad[1];
+        fresh.budget_ns = time_mode ? (unsigned long long)std::llround(cfg.time_budget_s * 1e9) : 0ull;
+        CK(cudaMemcpyAsync(st.p, &fresh, offsetof(DevState, bad_rows), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(&st.p->t_gen_start, &fresh.t_gen_start,
+                           sizeof(DevState) - offsetof(DevState, t_gen_start), cudaMemcpyHostToDevice, s));
+        gens_enqueued = 0;
+        finished = false;
+        if (graph) {
+            cudaGraphExecDestroy(graph);
+            graph = nullptr;
+        }
+    }
+
+    void set_population(int which, const double* X) {
+        if (which != 1 && which != 2) throw std::invalid_argument("set_population: which must be 1 or 2");
+        if (gens_enqueued) throw std::invalid_argument("set_population: the run has started");
+        const int q = which - 1;
+        DevBuf<double> h((size_t)n * d);
+        CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
+        DevBuf<int> nbad(1);
+        nbad.zero(s);
+        DevBuf<int> rows(std::max(n, 1));
+        to_planes_kernel<<<blocks_for((long long)n * d, 256), 256, 0, s>>>(
+            h.p, n, d, pop[q].X.p, ld, prob->dlo64.p, prob->dhi64.p, rows.p, nbad.p);
+        int hb = 0;
+        CK(cudaMemcpyAsync(&hb, nbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (hb) {
+            std::vector<int> r(hb);
+            CK(cudaMemcpy(r.data(), rows.p, hb * sizeof(int), cudaMemcpyDeviceToHost));
+            throw std::invalid_argument(rows_message(r));
+        }
+        VaryParams ep = vp;
+        ep.npops = 1;
+        ep.parX[0] = pop[q].X.p;
+        ep.outX[0] = pop[q].X.p;
+        ep.outG[0] = pop[q].G.p;
+        ep.outFcv[0] = pop[q].Fcv.p;
+        ep.update_z = 0;
+        ep.fixed_gen = 0;
+        vary_kernel_for(prob->fam, MODE_EVAL, 0)<<<dim3(blocks_for(n, 128), 1), 128, 0, s>>>(ep);
+        CK(cudaGetLastError());
+        finish_init();
+        CK(cudaStreamSynchronize(s));
+    }
+
+    void enqueue_generation() {
+        vary<<<dim3(blocks_for(n, 128), 2), 128, 0, s>>>(vp);
+        op1_kernel<<<blocks_for(n, 256), 256, 0, s>>>(op1p);
+        select_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(sp);
+        end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
+        if (time_mode) restore_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(rp);
+        publish_stop_kernel<<<1, 1, 0, s>>>(st.p, host_flag_dev);
+    }
+
+    void build_graph() {
+        if (graph) return;
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t saved = s;
+        s = cs;
+        enqueue_generation();
+        s = saved;
+        CK(cudaStreamEndCapture(cs, &g));
+        CK(cudaGraphInstantiate(&graph, g, 0));
+        CK(cudaGraphDestroy(g));
+        CK(cudaStreamDestroy(cs));
+    }
+
+    void start_loop_clock() {
+        if (gens_enqueued == 0) mark_start_kernel<<<1, 1, 0, s>>>(st.p);
+    }
+
+    // enqueue up to k generations, respecting the generation limit
+    long long step(long long k) {
+        if (gen_limit >= 0) k = std::min(k, gen_limit - gens_enqueued);
+        if (k <= 0) return 0;
+        build_graph();
+        start_loop_clock();
+        for (long long i = 0; i < k; ++i) CK(cudaGraphLaunch(graph, s));
+        gens_enqueued += k;
+        return k;
+    }
+
+    void run() {
+        if (!time_mode) {
+            if (gen_limit < 0) throw std::invalid_argument("run: unbounded run without a budget");
+            step(gen_limit - gens_enqueued);
+            CK(cudaStreamSynchronize(s));
+        } else {
+            // time budget: keep at most two chunks in flight and stop launching
+            // once the device reports the deadline (gmpea.cpp:458, :481-486)
+            const long long chunk = n >= 100000 ? 2 : 16;
+            cudaEvent_t ev[2];
+            CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+            int k = 0;
+            bool pending[2] = {false, false};
+            for (;;) {
+                if (pending[k]) {
+                    CK(cudaEventSynchronize(ev[k]));
+                    pending[k] = false;
+                    if (*(volatile int*)host_flag) break;
+                }
+                long long launched = step(chunk);
+                if (launched == 0) break;
+                CK(cudaEventRecord(ev[k], s));
+                pending[k] = true;
+                k ^= 1;
+            }
+            CK(cudaStreamSynchronize(s));
+            cudaEventDestroy(ev[0]);
+            cudaEventDestroy(ev[1]);
+        }
+        finished = true;
+        check_errors(-1);
+    }
+
+    DevState read_state() {
+        DevState h{};
+        CK(cudaMemcpyAsync(&h, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        return h;
+    }
+
+    void check_errors(int phase) {
+        DevState h = read_state();
+        if (!h.err) return;
+        std::string where = phase == 0 ? std::string("") :
+            "run_gmpea: evaluation failed at generation " + std::to_string(h.err_gen) + ": ";
+        if (h.err == ERR_EVAL_OOB) {
+            int q = h.n_bad[0] > 0 ? 0 : 1;
+            int cnt = std::min(h.n_bad[q], kMaxBadRows);
+            std::vector<int> r(h.bad_rows[q], h.bad_rows[q] + cnt);
+            if (phase == 0) throw std::invalid_argument(rows_message(r));
+            throw std::runtime_error(where + rows_message(r));
+        }
+        if (h.err == ERR_NONFINITE) throw std::invalid_argument("non-finite mask source");
+        if (h.err == ERR_NEG_CV) throw std::invalid_argument("fpr_better: negative constraint violation");
+        throw std::runtime_error("engine error " + std::to_string(h.err));
+    }
+
+    std::vector<gmpea_gen_record> history() {
+        DevState h = read_state();
+        long long g = std::min<long long>(h.gens_done, rec_cap - 1);
+        std::vector<DevRecord> r(g + 1);
+        CK(cudaMemcpyAsync(r.data(), rec.p, (g + 1) * sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<gmpea_gen_record> out(g + 1);
+        for (long long k = 0; k <= g; ++k) {
+            gmpea_gen_record& o = out[k];
+            o = gmpea_gen_record{};
+            o.gen = k;
+            o.evals = 2ll * n * (k + 1);
+            o.wall_ms = cfg.record_walltime ? (k == 0 ? 0.0 : (double)r[k].loop_ns * 1e-6) : 0.0;
+            o.feasible_ratio = (double)r[k].feasible / (double)n;
+            o.igd = std::numeric_limits<double>::quiet_NaN();
+            o.hv = std::numeric_limits<double>::quiet_NaN();
+        }
+        return out;
+    }
+
+    void get_population(int which, double* X, double* F, double* C, double* cv) {
+        if (which != 1 && which != 2) throw std::invalid_argument("get_population: which must be 1 or 2");
+        const int q = which - 1;
+        DevBuf<double> tmp((size_t)n * std::max({d, nc, m}));
+        auto pull = [&](const float* planes, int k, double* out) {
+            if (!out || k == 0) return;
+            from_planes_kernel<<<blocks_for((long long)n * k, 256), 256, 0, s>>>(planes, ld, n, k, tmp.p);
+            CK(cudaMemcpyAsync(out, tmp.p, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        };
+        pull(pop[q].X.p, d, X);
+        pull(pop[q].G.p, nc, C);
+        if (F || cv) {
+            DevBuf<double> f((size_t)n * m), c(n);
+            fcv_to_rows_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[q].Fcv.p, n, m, f.p, c.p);
+            if (F) CK(cudaMemcpyAsync(F, f.p, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+            if (cv) CK(cudaMemcpyAsync(cv, c.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
+    }
+
+    void profile(long long gens, double* ms) {
+        if (gen_limit >= 0) gens = std::min(gens, gen_limit - gens_enqueued);
+        if (gens <= 0) throw std::invalid_argument("profile: no generations left");
+        start_loop_clock();
+        std::vector<cudaEvent_t> ev(5 * gens);
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        for (long long g = 0; g < gens; ++g) {
+            cudaEvent_t* e = &ev[5 * g];
+            CK(cudaEventRecord(e[0], s));
+            vary<<<dim3(blocks_for(n, 128), 2), 128, 0, s>>>(vp);
+            CK(cudaEventRecord(e[1], s));
+            op1_kernel<<<blocks_for(n, 256), 256, 0, s>>>(op1p);
+            CK(cudaEventRecord(e[2], s));
+            select_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(sp);
+            CK(cudaEventRecord(e[3], s));
+            end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
+            if (time_mode) restore_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(rp);
+            CK(cudaEventRecord(e[4], s));
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        gens_enqueued += gens;
+        double acc[5] = {0, 0, 0, 0, 0};
+        for (long long g = 0; g < gens; ++g) {
+            cudaEvent_t* e = &ev[5 * g];
+            for (int k = 0; k < 4; ++k) {
+                float t = 0.0f;
+                CK(cudaEventElapsedTime(&t, e[k], e[k + 1]));
+                acc[k] += t;
+            }
+            float t = 0.0f;
+            CK(cudaEventElapsedTime(&t, e[0], e[4]));
+            acc[4] += t;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        for (int k = 0; k < 5; ++k) ms[k] = acc[k] / (double)gens;
+        check_errors(-1);
+    }
+};
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* gmpea_last_error(void) { return g_err.c_str(); }
+int gmpea_abi_version(void) { return 1; }
+
+int gmpea_problem_create(const char* name, gmpea_problem** out) {
+    return guarded([&] {
+        if (!name || !out) throw std::invalid_argument("gmpea_problem_create: null argument");
+        auto p = make_problem(name);
+        p->upload();
+        *out = p.release();
+    });
+}
+
+int gmpea_problem_create_wta(const char* scenario, int32_t targets, int32_t vehicles,
+                             const int32_t* strikes, const int32_t* capacity, const double* pv,
+                             gmpea_problem** out) {
+    return guarded([&] {
+        WtaHost w;
+        w.scenario = scenario ? scenario : "custom";
+        w.targets = targets;
+        w.vehicles = vehicles;
+        w.strikes.assign(strikes, strikes + targets);
+        w.cap.assign(capacity, capacity + vehicles);
+        int slots = 0;
+        for (int s : w.strikes) {
+            if (s < 0) throw std::invalid_argument("WTA: negative strike count");
+            slots += s;
+        }
+        w.p.assign(pv, pv + slots);
+        for (double v : w.p)
+            if (!(v >= 0.0 && v <= 1.0)) throw std::invalid_argument("WTA: probability out of range");
+        auto p = std::make_unique<gmpea_problem>();
+        make_wta(*p, w);
+        p->upload();
+        *out = p.release();
+    });
+}
+
+int gmpea_problem_info(const gmpea_problem* p, int32_t* d, int32_t* m, int32_t* nin, int32_t* neq) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("null problem");
+        if (d) *d = p->d;
+        if (m) *m = p->m;
+        if (nin) *nin = p->nin;
+        if (neq) *neq = p->neq;
+    });
+}
+
+int gmpea_problem_bounds(const gmpea_problem* p, double* lo, double* hi) {
+    return guarded([&] {
+        if (lo) std::copy(p->lo.begin(), p->lo.end(), lo);
+        if (hi) std::copy(p->hi.begin(), p->hi.end(), hi);
+    });
+}
+
+void gmpea_problem_destroy(gmpea_problem* p) { delete p; }
+
+const char* gmpea_problem_names(void) {
+    static std::string names = [] {
+        std::string s;
+        for (int i = 1; i <= 14; ++i) s += "LIRCMOP" + std::to_string(i) + "\n";
+        for (const char* n : {"C1-DTLZ1", "C1-DTLZ3", "C2-DTLZ2", "C3-DTLZ4", "DC1-DTLZ1", "DC1-DTLZ3",
+                              "DC2-DTLZ1", "DC2-DTLZ3", "DC3-DTLZ1", "DC3-DTLZ3"})
+            s += std::string(n) + "\n";
+        for (int i = 1; i <= 10; ++i) s += "WTA-P" + std::to_string(i) + "\n";
+        for (int i = 1; i <= 14; ++i) s += "MW" + std::to_string(i) + "\n";
+        return s;
+    }();
+    return names.c_str();
+}
+
+int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F, double* G, double* cv) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("null problem");
+        if (n < 0) throw std::invalid_argument("evaluate: negative row count");
+        if (n == 0) return;
+        if (n > (1ll << 30)) throw std::invalid_argument("evaluate: too many rows");
+        CK(cudaSetDevice(p->device));
+        const int d = p->d, m = p->m, nc = p->nin + p->neq;
+        const long long ld = round_up(n, 32);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct SG {
+            cudaStream_t s;
+            ~SG() { cudaStreamDestroy(s); }
+        } sg{s};
+        DevBuf<double> h((size_t)n * d);
+        CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
+        PopBuf pb;
+        pb.alloc(d, nc, ld);
+        DevBuf<int> rows(n), nbad(1);
+        nbad.zero(s);
+        to_planes_kernel<<<blocks_for(n * d, 256), 256, 0, s>>>(h.p, n, d, pb.X.p, ld, p->dlo64.p, p->dhi64.p,
+                                                               rows.p, nbad.p);
+        int hb = 0;
+        CK(cudaMemcpyAsync(&hb, nbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (hb) {
+            std::vector<int> r(hb);
+            CK(cudaMemcpy(r.data(), rows.p, hb * sizeof(int), cudaMemcpyDeviceToHost));
+            throw std::invalid_argument(rows_message(r));
+        }
+        DevBuf<DevState> st(1);
+        st.zero(s);
+        DevBuf<int> bad(n);
+        VaryParams ep{};
+        ep.n = (int)n;
+        ep.ld = (int)ld;
+        ep.npops = 1;
+        ep.pop_id[0] = 1;
+        ep.P = p->dev;
+        ep.parX[0] = pb.X.p;
+        ep.outX[0] = pb.X.p;
+        ep.outG[0] = pb.G.p;
+        ep.outFcv[0] = pb.Fcv.p;
+        ep.eval = 1;
+        ep.fixed_gen = 0;
+        ep.st = st.p;
+        ep.bad_rows[0] = bad.p;
+        ep.bad_cap = (int)n;
+        vary_kernel_for(p->fam, MODE_EVAL, 0)<<<dim3(blocks_for(n, 128), 1), 128, 0, s>>>(ep);
+        CK(cudaGetLastError());
+        DevBuf<double> out((size_t)n * std::max({m, nc, 1}));
+        DevBuf<double> c(n);
+        fcv_to_rows_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pb.Fcv.p, n, m, out.p, c.p);
+        CK(cudaMemcpyAsync(F, out.p, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (cv) CK(cudaMemcpyAsync(cv, c.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (G && nc) {
+            from_planes_kernel<<<blocks_for(n * nc, 256), 256, 0, s>>>(pb.G.p, ld, n, nc, out.p);
+            CK(cudaMemcpyAsync(G, out.p, (size_t)n * nc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaStreamSynchronize(s));
+        CK(cudaGetLastError());
+    });
+}
+
+int gmpea_reference_vectors(int32_t m, int64_t n, double* W) {
+    return guarded([&] {
+        if (n <= 0) throw std::invalid_argument("reference_vectors: target_n must be positive");
+        if (m < 2 || m > 3) throw std::invalid_argument("reference_vectors: m must be 2 or 3");
+        require_device();
+        DevBuf<double> w((size_t)n * m);
+        DevBuf<float4> u(n);
+        lattice_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, lattice_H(m, n), w.p, u.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(W, w.p, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+static void knn_api(const double* Wh, int64_t n, int32_t m, int32_t t1, int32_t t2, uint32_t* B1,
+                    uint32_t* B2, bool lattice) {
+    if (n <= 0) throw std::invalid_argument("build_neighborhoods: empty population");
+    if (m < 2 || m > 3) throw std::invalid_argument("build_neighborhoods: m must be 2 or 3");
+    if (t1 > n || t2 > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
+    require_device();
+    cudaStream_t s = 0;
+    DevBuf<double> w((size_t)n * m);
+    DevBuf<float4> u(n);
+    long long H = lattice_H(m, n);
+    if (lattice)
+        lattice_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, H, w.p, u.p);
+    else
+        CK(cudaMemcpy(w.p, Wh, (size_t)n * m * sizeof(double), cudaMemcpyHostToDevice));
+    DevBuf<int> b1((size_t)n * std::max(t1, 1)), b2((size_t)n * std::max(t2, 1));
+    device_knn(s, (int)n, m, t1, t2, w.p, lattice, H, b1.p, b2.p);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(B1, b1.p, (size_t)n * t1 * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(B2, b2.p, (size_t)n * t2 * sizeof(int), cudaMemcpyDeviceToHost));
+}
+
+int gmpea_build_neighborhoods(const double* W, int64_t n, int32_t m, int32_t t1, int32_t t2, uint32_t* B1,
+                              uint32_t* B2) {
+    return guarded([&] { knn_api(W, n, m, t1, t2, B1, B2, false); });
+}
+
+int gmpea_lattice_neighborhoods(int32_t m, int64_t n, int32_t t1, int32_t t2, uint32_t* B1, uint32_t* B2) {
+    return guarded([&] { knn_api(nullptr, n, m, t1, t2, B1, B2, true); });
+}
+
+int gmpea_operator_params_default(gmpea_operator_params* o) {
+    // OperatorParams defaults (gmpea.hpp:58-66)
+    *o = gmpea_operator_params{1.0, 20.0, 20.0, 1.0, 0.5, -1.0};
+    return GMPEA_OK;
+}
+
+int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const uint32_t* nbrs, int32_t t,
+                    int32_t op, const gmpea_operator_params* params, uint64_t seed, uint32_t gen,
+                    uint32_t pop, double* off) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("null problem");
+        if (n <= 0) return;
+        if (t <= 0) throw std::invalid_argument("reproduce: topology/population mismatch");
+        if (op != GMPEA_OP_SBX_PM && op != GMPEA_OP_DE) throw std::invalid_argument("reproduce: unknown operator");
+        CK(cudaSetDevice(p->device));
+        const int d = p->d;
+        const long long ld = round_up(n, 32);
+        cudaStream_t s = 0;
+        DevBuf<double> h((size_t)n * d);
+        CK(cudaMemcpy(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice));
+        DevBuf<float> Xp((size_t)d * ld), Op((size_t)d * ld);
+        to_planes_kernel<<<blocks_for(n * d, 256), 256>>>(h.p, n, d, Xp.p, ld, nullptr, nullptr, nullptr,
+                                                          nullptr);
+        DevBuf<unsigned> bu((size_t)n * t);
+        DevBuf<int> bi((size_t)n * t), err(1);
+        err.zero(s);
+        CK(cudaMemcpy(bu.p, nbrs, (size_t)n * t * sizeof(unsigned), cudaMemcpyHostToDevice));
+        u32_to_i32_kernel<<<blocks_for(n * t, 256), 256>>>(bu.p, n * t, bi.p, (int)n, err.p);
+        int herr = 0;
+        CK(cudaMemcpy(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (herr) throw std::invalid_argument("reproduce: neighbour index out of range");
+        DevBuf<DevState> st(1);
+        st.zero(s);
+        DevBuf<int> bad(1);
+        VaryParams vp{};
+        vp.n = (int)n;
+        vp.ld = (int)ld;
+        vp.npops = 1;
+        vp.pop_id[0] = (int)pop;
+        vp.P = p->dev;
+        vp.parX[0] = Xp.p;
+        vp.B[0] = bi.p;
+        vp.t[0] = t;
+        vp.outX[0] = Op.p;
+        vp.key0 = (unsigned)seed;
+        vp.key1 = (unsigned)(seed >> 32);
+        gmpea_operator_params prm;
+        gmpea_operator_params_default(&prm);
+        if (params) prm = *params;
+        fill_op_params(vp, prm, d);
+        vp.eval = 0;
+        vp.fixed_gen = (int)gen;
+        vp.st = st.p;
+        vp.bad_rows[0] = bad.p;
+        vp.bad_cap = 0;  // reproduce itself never throws on bounds
+        vary_kernel_for(p->fam, MODE_VARY, op)<<<dim3(blocks_for(n, 128), 1), 128>>>(vp);
+        CK(cudaGetLastError());
+        from_planes_kernel<<<blocks_for(n * d, 256), 256>>>(Op.p, ld, n, d, h.p);
+        CK(cudaMemcpy(off, h.p, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
+                                  const gmpea_population_view* pop1, const gmpea_population_view* pop2,
+                                  const gmpea_population_view* off1, const gmpea_population_view* off2,
+                                  const double* W, const double* z, double theta, const uint32_t* B1,
+                                  int32_t t1, const uint32_t* B2, int32_t t2, gmpea_population_out* out1,
+                                  gmpea_population_out* out2, int32_t* winner1, int32_t* winner2) {
+    return guarded([&] {
+        if (n <= 0) return;
+        if (m < 2 || m > 3) throw std::invalid_argument("environmental_selection: m must be 2 or 3");
+        if (t1 <= 0 || t2 <= 0) throw std::invalid_argument("environmental_selection: empty neighbourhood");
+        require_device();
+        const long long ld = round_up(n, 32);
+        cudaStream_t s = 0;
+        const gmpea_population_view* views[4] = {pop1, pop2, off1, off2};
+        DevBuf<float4> fcv[4];
+        DevBuf<double> hF((size_t)n * m), hc(n);
+        for (int k = 0; k < 4; ++k) {
+            fcv[k].alloc(ld);
+            CK(cudaMemcpy(hF.p, views[k]->F, (size_t)n * m * sizeof(double), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(hc.p, views[k]->cv, (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+            fcv_from_rows_kernel<<<blocks_for(n, 256), 256>>>(hF.p, hc.p, n, m, fcv[k].p);
+        }
+        DevBuf<double> w((size_t)n * m);
+        CK(cudaMemcpy(w.p, W, (size_t)n * m * sizeof(double), cudaMemcpyHostToDevice));
+        DevBuf<float4> U(ld);
+        DevBuf<int> err(1);
+        err.zero(s);
+        unit_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, w.p, U.p, err.p);
+        int herr = 0;
+        CK(cudaMemcpy(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (herr) throw std::invalid_argument("pbi: zero-norm reference vector");
+        DevBuf<int> Bd[2], R[2], Rdeg[2];
+        const uint32_t* Bh[2] = {B1, B2};
+        const int ts[2] = {t1, t2};
+        for (int q = 0; q < 2; ++q) {
+            DevBuf<unsigned> bu((size_t)n * ts[q]);
+            Bd[q].alloc((size_t)n * ts[q]);
+            CK(cudaMemcpy(bu.p, Bh[q], (size_t)n * ts[q] * sizeof(unsigned), cudaMemcpyHostToDevice));
+            err.zero(s);
+            u32_to_i32_kernel<<<blocks_for(n * ts[q], 256), 256>>>(bu.p, n * ts[q], Bd[q].p, (int)n, err.p);
+            CK(cudaMemcpy(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost));
+            if (herr) throw std::invalid_argument("environmental_selection: neighbour index out of range");
+            device_reverse(s, (int)n, ts[q], Bd[q].p, ld, Rdeg[q], R[q]);
+        }
+        DevBuf<DevState> st(1);
+        st.zero(s);
+        set_z_kernel<<<1, 1>>>(st.p, m, (float)z[0], (float)z[1], m > 2 ? (float)z[2] : 0.0f);
+        DevBuf<float4> eff[2];
+        eff[0].alloc(ld);
+        eff[1].alloc(ld);
+        DevBuf<unsigned char> sb(ld);
+        Op1Params o1{(int)n, m, (float)theta, U.p, {fcv[2].p, fcv[3].p}, {eff[0].p, eff[1].p}, sb.p, st.p};
+        op1_kernel<<<blocks_for(n, 256), 256>>>(o1);
+        DevBuf<int> win[2];
+        win[0].alloc(n);
+        win[1].alloc(n);
+        SelParams sp{};
+        sp.n = (int)n;
+        sp.ld = (int)ld;
+        sp.d = d;
+        sp.nc = nc;
+        sp.m = m;
+        sp.theta = (float)theta;
+        sp.U = U.p;
+        for (int q = 0; q < 2; ++q) {
+            sp.Fcv[q] = fcv[q].p;
+            sp.oFcv[q] = fcv[2 + q].p;
+            sp.eff[q] = eff[q].p;
+            sp.R[q] = R[q].p;
+            sp.Rdeg[q] = Rdeg[q].p;
+            sp.winner[q] = win[q].p;
+        }
+        sp.srcbits = sb.p;
+        sp.apply = 0;
+        sp.st = st.p;
+        select_kernel<<<dim3(blocks_for(n, 256), 2), 256>>>(sp);
+        CK(cudaGetLastError());
+        std::vector<int> w1(n), w2(n);
+        CK(cudaMemcpy(w1.data(), win[0].p, n * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(w2.data(), win[1].p, n * sizeof(int), cudaMemcpyDeviceToHost));
+        DevState h{};
+        CK(cudaMemcpy(&h, st.p, sizeof(DevState), cudaMemcpyDeviceToHost));
+        if (h.err == ERR_NONFINITE) throw std::invalid_argument("non-finite mask source");
+        if (h.err == ERR_NEG_CV) throw std::invalid_argument("fpr_better: negative constraint violation");
+        if (winner1) std::copy(w1.begin(), w1.end(), winner1);
+        if (winner2) std::copy(w2.begin(), w2.end(), winner2);
+        // copy_row (gmpea.cpp:329-331): assemble the survivors from the f64 inputs
+        auto assemble = [&](const gmpea_population_view* par, const std::vector<int>& win,
+                            gmpea_population_out* out) {
+            if (!out) return;
+            for (int64_t j = 0; j < n; ++j) {
+                const gmpea_population_view* src = par;
+                int64_t r = j;
+                if (win[j] >= 0) {
+                    src = win[j] < n ? off1 : off2;
+                    r = win[j] < n ? win[j] : win[j] - n;
+                }
+                if (out->X) std::memcpy(out->X + j * d, src->X + r * d, d * sizeof(double));
+                if (out->F) std::memcpy(out->F + j * m, src->F + r * m, m * sizeof(double));
+                if (out->C && nc) std::memcpy(out->C + j * nc, src->C + r * nc, nc * sizeof(double));
+                if (out->cv) out->cv[j] = src->cv[r];
+            }
+        };
+        assemble(pop1, w1, out1);
+        assemble(pop2, w2, out2);
+    });
+}
+
+// ---- metrics (metrics.hpp:15-29)
+namespace {
+
+// nondominated + deduplicated subset of the candidate rows `cand` of F (n x m,
+// device, row-major); returns the kept row ids sorted lexicographically by F
+thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::device_vector<long long>& cand) {
+    const long long k = (long long)cand.size();
+    thrust::device_vector<long long> kept;
+    if (k == 0) return kept;
+    thrust::sort(thrust::device, cand.begin(), cand.end(), LexLess{dF, m});
+    thrust::device_vector<long long> gs(k);
+    const long long* order = thrust::raw_pointer_cast(cand.data());
+    group_start_kernel<<<blocks_for(k, 256), 256>>>(dF, order, k, m, thrust::raw_pointer_cast(gs.data()));
+    thrust::device_vector<unsigned char> keep(k);
+    if (m == 2) {
+        thrust::device_vector<double> col(k);
+        gather_col_kernel<<<blocks_for(k, 256), 256>>>(dF, order, k, m, 1, thrust::raw_pointer_cast(col.data()));
+        thrust::inclusive_scan(thrust::device, col.begin(), col.end(), col.begin(), thrust::minimum<double>());
+        nd2_kernel<<<blocks_for(k, 256), 256>>>(dF, order, thrust::raw_pointer_cast(gs.data()),
+                                                thrust::raw_pointer_cast(col.data()), k,
+                                                thrust::raw_pointer_cast(keep.data()));
+    } else {
+        nd3_kernel<<<blocks_for(k, 256), 256>>>(dF, order, thrust::raw_pointer_cast(gs.data()), k,
+                                                thrust::raw_pointer_cast(keep.data()));
+    }
+    CK(cudaGetLastError());
+    kept.resize(k);
+    auto end = thrust::copy_if(thrust::device, cand.begin(), cand.end(), keep.begin(), kept.begin(),
+                               NonZero{});
+    kept.resize(end - kept.begin());
+    return kept;
+}
+
+}  // namespace
+
+int gmpea_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx, int64_t* count) {
+    return guarded([&] {
+        if (m < 2 || m > 3) throw std::invalid_argument("metric_front: m must be 2 or 3");
+        *count = 0;
+        if (n <= 0) return;
+        require_device();
+        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n);
+        thrust::device_vector<long long> cand(n);
+        auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                   thrust::counting_iterator<long long>(n), cand.begin(),
+                                   IsFeasible{thrust::raw_pointer_cast(dcv.data())});
+        cand.resize(end - cand.begin());
+        auto kept = front_filter(thrust::raw_pointer_cast(dF.data()), m, cand);
+        thrust::sort(thrust::device, kept.begin(), kept.end());
+        std::vector<long long> h(kept.size());
+        thrust::copy(kept.begin(), kept.end(), h.begin());
+        for (size_t i = 0; i < h.size(); ++i) idx[i] = h[i];
+        *count = (int64_t)h.size();
+    });
+}
+
+int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t m, double* out) {
+    return guarded([&] {
+        if (nr <= 0) throw std::invalid_argument("igd: empty reference front");
+        if (na <= 0) {
+            *out = std::numeric_limits<double>::infinity();
+            return;
+        }
+        if (m < 1 || m > 3) throw std::invalid_argument("igd: objective count mismatch");
+        require_device();
+        thrust::device_vector<double> dA(A, A + na * m), dR(R, R + nr * m), res(1);
+        thrust::device_vector<unsigned long long> best(nr, 0x7ff0000000000000ull);  // +inf
+        int gx = (int)std::min<long long>(blocks_for(na, 256), 64);
+        igd_min_kernel<<<dim3(gx, (unsigned)nr), 256>>>(thrust::raw_pointer_cast(dA.data()), na,
+                                                         thrust::raw_pointer_cast(dR.data()), nr, m,
+                                                         thrust::raw_pointer_cast(best.data()));
+        igd_sum_kernel<<<1, 1>>>(thrust::raw_pointer_cast(best.data()), nr, thrust::raw_pointer_cast(res.data()));
+        CK(cudaGetLastError());
+        *out = res[0];
+    });
+}
+
+int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, double* out) {
+    return guarded([&] {
+        if (m < 2 || m > 3) throw std::invalid_argument("hypervolume: m must be 2 or 3 on device");
+        *out = 0.0;
+        if (n <= 0) return;
+        require_device();
+        thrust::device_vector<double> dP(P, P + n * m), dref(ref, ref + m);
+        const double* pP = thrust::raw_pointer_cast(dP.data());
+        thrust::device_vector<long long> cand(n);
+        auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                   thrust::counting_iterator<long long>(n), cand.begin(),
+                                   InsideBox{pP, thrust::raw_pointer_cast(dref.data()), m});
+        cand.resize(end - cand.begin());
+        auto xy = front_filter(pP, m, cand);  // hv_relevant, sorted by (x, y[, z])
+        const long long cnt = (long long)xy.size();
+        if (cnt == 0) return;
+        thrust::device_vector<double> slab(m == 2 ? 1 : cnt), res(1);
+        thrust::device_vector<long long> zorder, zrank;
+        if (m == 3) {
+            zorder = xy;
+            thrust::sort(thrust::device, zorder.begin(), zorder.end(), ZLess{pP});
+            zrank.resize(n);
+            thrust::scatter(thrust::device, thrust::counting_iterator<long long>(0),
+                            thrust::counting_iterator<long long>(cnt), zorder.begin(), zrank.begin());
+        }
+        hv_slab_kernel<<<blocks_for(m == 2 ? 1 : cnt, 128), 128>>>(
+            pP, thrust::raw_pointer_cast(xy.data()), m == 3 ? thrust::raw_pointer_cast(zrank.data()) : nullptr,
+            cnt, m, m == 2 ? 1 : cnt, thrust::raw_pointer_cast(dref.data()), thrust::raw_pointer_cast(slab.data()));
+        CK(cudaGetLastError());
+        if (m == 2) {
+            *out = slab[0];
+            return;
+        }
+        hv3_sum_kernel<<<1, 1>>>(pP, thrust::raw_pointer_cast(zorder.data()), cnt,
+                                 thrust::raw_pointer_cast(dref.data()), thrust::raw_pointer_cast(slab.data()),
+                                 thrust::raw_pointer_cast(res.data()));
+        CK(cudaGetLastError());
+        *out = res[0];
+    });
+}
+
+int gmpea_run_config_default(gmpea_run_config* c) {
+    // RunConfig defaults (gmpea.hpp:113-127)
+    *c = gmpea_run_config{};
+    c->n = 100;
+    c->k_max = 0;
+    c->time_budget_s = -1.0;
+    c->eval_budget = -1;
+    c->seed = 1;
+    c->op = GMPEA_OP_SBX_PM;
+    gmpea_operator_params_default(&c->params);
+    c->theta = 5.0;
+    c->t1 = 5;
+    c->t2 = 20;
+    c->record_walltime = 1;
+    c->device = 0;
+    c->stream = 0;
+    return GMPEA_OK;
+}
+
+int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmpea_engine** out) {
+    return guarded([&] {
+        if (!p || !cfg || !out) throw std::invalid_argument("gmpea_engine_create: null argument");
+        require_device();
+        auto e = std::make_unique<gmpea_engine>();
+        e->setup(p, *cfg);
+        *out = e.release();
+    });
+}
+
+int gmpea_engine_set_population(gmpea_engine* e, int32_t which, const double* X) {
+    return guarded([&] { e->set_population(which, X); });
+}
+
+int gmpea_engine_run(gmpea_engine* e) {
+    return guarded([&] { e->run(); });
+}
+
+int gmpea_engine_step(gmpea_engine* e, int64_t gens) {
+    return guarded([&] { e->step(gens); });
+}
+
+int gmpea_engine_sync(gmpea_engine* e) {
+    return guarded([&] {
+        CK(cudaStreamSynchronize(e->s));
+        e->check_errors(-1);
+    });
+}
+
+int64_t gmpea_engine_effective_n(const gmpea_engine* e) { return e ? e->n : 0; }
+
+int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, int64_t* nrec) {
+    return guarded([&] {
+        auto h = e->history();
+        int64_t k = std::min<int64_t>(cap, (int64_t)h.size());
+        if (out) std::copy(h.begin(), h.begin() + k, out);
+        *nrec = (int64_t)h.size();
+    });
+}
+
+int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C, double* cv) {
+    return guarded([&] { e->get_population(which, X, F, C, cv); });
+}
+
+int gmpea_engine_ideal(gmpea_engine* e, double* z) {
+    return guarded([&] {
+        DevState h = e->read_state();
+        for (int k = 0; k < e->m; ++k) z[k] = ordered_to_float(h.zbits[k]);
+    });
+}
+
+int gmpea_engine_neighborhoods(gmpea_engine* e, uint32_t* B1, uint32_t* B2) {
+    return guarded([&] {
+        if (B1) CK(cudaMemcpy(B1, e->B[0].p, (size_t)e->n * e->t1 * sizeof(int), cudaMemcpyDeviceToHost));
+        if (B2) CK(cudaMemcpy(B2, e->B[1].p, (size_t)e->n * e->t2 * sizeof(int), cudaMemcpyDeviceToHost));
+    });
+}
+
+int gmpea_engine_profile(gmpea_engine* e, int64_t gens, double* ms) {
+    return guarded([&] { e->profile(gens, ms); });
+}
+
+void gmpea_engine_destroy(gmpea_engine* e) { delete e; }
+
+}  // extern "C"

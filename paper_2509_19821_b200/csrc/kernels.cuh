@@ -1,0 +1,556 @@
+// Hot-path kernels of one GMPEA generation (proj/src/gmpea.cpp:457-489):
+//
+//   vary_eval  : reproduce x2 (gmpea.cpp:463-464, :113-206) fused with
+//                evaluate_population x2 (:467-468, problems.cpp:552-573) and the
+//                ideal-point partial min (update_ideal, :474-475).  One thread
+//                per (slot, population); the child is produced and evaluated
+//                gene by gene, written once as fp32 SoA planes.
+//   op1        : offspring cooperation (gmpea.cpp:248-279) as two bits per
+//                slot plus the packed keys of the row each stream keeps.
+//   select     : OP2 update indexing + OP3 elite update (gmpea.cpp:283-390) as
+//                a pull over the reverse neighbourhood: the thread owning parent
+//                slot j visits every offspring c with j in B[c], recomputes the
+//                mark of (c, j) and keeps the lexicographic argmin of the
+//                claimants; the winner row is copied into slot j in place
+//                (one writer per slot, race-free; parents' other rows are never
+//                read by this kernel).
+//   end_gen    : loop time / budget bookkeeping (gmpea.cpp:458-488).
+#pragma once
+#include "common.cuh"
+#include "problems.cuh"
+
+namespace gmpea_b200 {
+
+enum : int { OP_SBX = 0, OP_DE = 1 };
+enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
+
+struct VaryParams {
+    int n, ld;               // slots per population, plane leading dimension
+    int slot_base;           // global slot index of local row 0 (sharding)
+    int npops;               // 1 or 2 populations in blockIdx.y
+    int pop_id[2];           // Philox population id (1 or 2) per blockIdx.y
+    ProbDev P;
+    const float* parX[2];    // parent planes (MODE_VARY) / input planes (MODE_EVAL)
+    const int* B[2];         // neighbourhood rows (local indices), row-major
+    int t[2];
+    float* outX[2];
+    float* outG[2];
+    float4* outFcv[2];
+    unsigned key0, key1;     // Philox key (seed)
+    double sbx_prob;         // SBX per-child coin threshold on the 53-bit uniform
+    float sbx_e;             // 1 / (eta_c + 1)
+    float pm_e1;             // eta_m + 1
+    float pm_einv;           // 1 / (eta_m + 1)
+    long long pm_thr;        // mutate iff w <= pm_thr (w: 32-bit draw)
+    unsigned long long cr_thr; // DE: take iff w < cr_thr (>= 2^32: always)
+    float de_f;
+    int eval;                // evaluate the child (0: reproduce only)
+    int update_z;
+    int fixed_gen;           // >= 0: use this generation number instead of st->gen
+    DevState* st;
+    int* bad_rows[2];        // out-of-bounds rows (local index) per population
+    int bad_cap;
+};
+
+// ---- constraint violation with the reference accumulation order
+// (scalarize.cpp:39-49, kernels.cpp:56-67: four lanes over the blocked
+// prefix of the inequalities, lanes combined left to right, tail in order,
+// then the relaxed equalities).  Values arrive in ascending index.
+struct CvAcc {
+    double acc[4];
+    int nin, blocked;
+    __device__ __forceinline__ void init(int nin_) {
+        acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+        nin = nin_;
+        blocked = nin_ / 4 * 4;
+    }
+    __device__ __forceinline__ void add(int k, double g) {
+        const double r = g > 0.0 ? g : 0.0;
+        switch (k & 3) {
+            case 0: acc[0] += r; break;
+            case 1: acc[1] += r; break;
+            case 2: acc[2] += r; break;
+            default: acc[3] += r; break;
+        }
+    }
+    __device__ __forceinline__ double total() const {
+        return ((acc[0] + acc[1]) + acc[2]) + acc[3];
+    }
+};
+
+// Emits raw constraints into the G planes and folds them into cv in the
+// reference's order.  For the tail we need s = lanes; s += t_k (in order), so
+// the running lane total is materialised when the first tail term arrives.
+struct Emitter {
+    float* G;
+    long long ld, i;
+    CvAcc cv;
+    double s;
+    bool s_ready;
+    int neq;
+    __device__ __forceinline__ void operator()(int k, double g) {
+        G[(long long)k * ld + i] = (float)g;
+        if (k < cv.blocked) {
+            cv.add(k, g);
+        } else {
+            if (!s_ready) {
+                s = cv.total();
+                s_ready = true;
+            }
+            if (k < cv.nin) {
+                s += g > 0.0 ? g : 0.0;
+            } else {
+                double v = fabs(g) - 1e-6;
+                s += v > 0.0 ? v : 0.0;
+            }
+        }
+    }
+    __device__ __forceinline__ double result() {
+        if (!s_ready) {
+            s = cv.total();
+            s_ready = true;
+        }
+        return s;
+    }
+};
+
+// ---- Philox-keyed draws
+struct PickStream {
+    unsigned slot, gen, tag, k0, k1;
+    unsigned q;
+    u32x4 cache;
+    __device__ __forceinline__ unsigned long long next() {
+        if ((q & 1) == 0) cache = philox4x32_10(slot, gen, tag, q >> 1, k0, k1);
+        unsigned long long v = (q & 1) == 0 ? (((unsigned long long)cache.y << 32) | cache.x)
+                                            : (((unsigned long long)cache.w << 32) | cache.z);
+        ++q;
+        return v;
+    }
+    // rng.hpp:23-30: uniform integer in [0, n) by rejection
+    __device__ __forceinline__ unsigned index(unsigned n) {
+        const unsigned long long lim = ~0ull - (~0ull % n);
+        unsigned long long v;
+        do {
+            v = next();
+        } while (v >= lim);
+        return (unsigned)(v % n);
+    }
+};
+
+__device__ __forceinline__ unsigned pick_word(const u32x4& w, int k) {
+    return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
+}
+
+__device__ __forceinline__ float clamp_ref(float v, float lo, float hi) {
+    return v < lo ? lo : (hi < v ? hi : v);  // NaN passes through (std::clamp)
+}
+
+// gmpea.cpp:135-160 for one gene; w = the MU draw
+__device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned w, float e1,
+                                          float einv) {
+    const float span = hi - lo;
+    if (!(span > 0.0f)) return x;
+    float dq;
+    if (w < 0x80000000u) {  // u < 0.5
+        const float two_u = (float)w * 0x1.0p-31f;
+        const float one_m = (float)(0x80000000u - w) * 0x1.0p-31f;  // 1 - 2u
+        const float d1 = (x - lo) / span;
+        dq = powf(two_u + one_m * powf(1.0f - d1, e1), einv) - 1.0f;
+    } else {
+        const float two_1mu = (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;  // 2(1-u)
+        const float two_um = (float)(w - 0x80000000u) * 0x1.0p-31f;                        // 2(u-0.5)
+        const float d2 = (hi - x) / span;
+        dq = 1.0f - powf(two_1mu + two_um * powf(1.0f - d2, e1), einv);
+    }
+    return x + dq * span;
+}
+
+__device__ __forceinline__ float sbx_beta(unsigned w, float e) {
+    if (w <= 0x80000000u) return powf((float)w * 0x1.0p-31f, e);  // u <= 0.5: (2u)^e
+    // u > 0.5: (1 / (2 (1 - u)))^e with 2(1-u) = (2^32 - w) 2^-31 > 0
+    return powf(1.0f / ((float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f), e);
+}
+
+template <class T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        T w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+template <class Ev, int MODE, int OP>
+__global__ void __launch_bounds__(128) vary_eval_kernel(VaryParams p) {
+    DevState* st = p.st;
+    if (st->stop) return;
+    const int pi = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = i < p.n;
+    const int d = p.P.d;
+    const long long ld = p.ld;
+    const unsigned gen = p.fixed_gen >= 0 ? (unsigned)p.fixed_gen : (unsigned)st->gen;
+    const unsigned slot = (unsigned)(p.slot_base + i);
+    const unsigned pid = (unsigned)p.pop_id[pi];
+
+    double f[kMaxM] = {0.0, 0.0, 0.0};
+    bool bad = false;
+    float cvf = 0.0f;
+    if (active) {
+        Ev ev;
+        if (p.eval) ev.begin(p.P);
+        float* __restrict__ outX = p.outX[pi];
+        const float* __restrict__ X = p.parX[pi];
+        int ia = 0, ib = 0, jrand = -1;
+        bool cross = true;
+        if (MODE == MODE_VARY) {
+            const int t = p.t[pi];
+            PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key0, p.key1, 0u, {}};
+            unsigned a = ps.index((unsigned)t);
+            unsigned b = ps.index((unsigned)t);
+            while (t > 1 && b == a) b = ps.index((unsigned)t);
+            const int* Brow = p.B[pi] + (long long)i * t;
+            ia = Brow[a];
+            ib = Brow[b];
+            if (OP == OP_SBX) {
+                u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
+                cross = u53(c.x, c.y) <= p.sbx_prob;
+            } else {
+                jrand = (int)ps.index((unsigned)d);
+            }
+        }
+        const bool de_all = p.cr_thr >= 0x100000000ull;
+        for (int jb = 0; jb < d; jb += 4) {
+            u32x4 xc{0, 0, 0, 0}, xu{0, 0, 0, 0}, mc{0, 0, 0, 0};
+            if (MODE == MODE_VARY) {
+                const unsigned idx4 = (unsigned)(jb >> 2);
+                if (OP == OP_SBX && cross) {
+                    xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
+                    xu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), idx4, p.key0, p.key1);
+                }
+                if (OP == OP_DE && !de_all)
+                    xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
+                if (p.pm_thr >= 0)
+                    mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx4, p.key0, p.key1);
+            } else if (MODE == MODE_INIT) {
+                xc = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), p.key0, p.key1);
+                xu = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, p.key0, p.key1);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = jb + k;
+                if (j >= d) break;
+                const float lo = p.P.lo[j], hi = p.P.hi[j];
+                float c;
+                if (MODE == MODE_EVAL) {
+                    c = X[j * ld + i];
+                } else if (MODE == MODE_INIT) {
+                    // INIT stream: 64-bit pair (j % 2) of counter j / 2
+                    const u32x4& w = k < 2 ? xc : xu;
+                    double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
+                    c = (float)((double)lo + ((double)hi - (double)lo) * u);
+                } else {
+                    const float pa = X[j * ld + ia];
+                    const float pb = X[j * ld + ib];
+                    if (OP == OP_SBX) {
+                        if (cross && pick_word(xc, k) <= 0x80000000u) {
+                            const float beta = sbx_beta(pick_word(xu, k), p.sbx_e);
+                            c = 0.5f * ((1.0f + beta) * pa + (1.0f - beta) * pb);
+                        } else {
+                            c = pa;
+                        }
+                    } else {
+                        const float base = X[j * ld + i];
+                        const bool take = j == jrand || de_all ||
+                                          (unsigned long long)pick_word(xc, k) < p.cr_thr;
+                        c = take ? base + p.de_f * (pa - pb) : base;
+                    }
+                    if ((long long)pick_word(mc, k) <= p.pm_thr) {
+                        const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j,
+                                                       p.key0, p.key1);
+                        c = pm_apply(c, lo, hi, mu.x, p.pm_e1, p.pm_einv);
+                    }
+                    c = clamp_ref(c, lo, hi);
+                }
+                if (!(c >= lo && c <= hi)) bad = true;  // problems.cpp:554-561
+                if (MODE != MODE_EVAL) outX[j * ld + i] = c;
+                if (p.eval) ev.gene(p.P, j, c);
+            }
+        }
+        if (bad) {
+            int k = atomicAdd(&st->n_bad[pi], 1);
+            if (k < p.bad_cap) p.bad_rows[pi][k] = i;
+            if (atomicCAS(&st->err, 0, ERR_EVAL_OOB) == 0) st->err_gen = (int)gen;
+        } else if (p.eval) {
+            Emitter em{p.outG[pi], ld, i, {}, 0.0, false, p.P.neq};
+            em.cv.init(p.P.nin);
+            ev.finish(p.P, f, em);
+            cvf = (float)em.result();
+            float4 o;
+            o.x = (float)f[0];
+            o.y = (float)f[1];
+            o.z = p.P.m > 2 ? (float)f[2] : 0.0f;
+            o.w = cvf;
+            p.outFcv[pi][i] = o;
+        }
+    }
+    if (!p.update_z || !p.eval) return;
+    // ideal point: block min per objective, one atomic per block only when
+    // the block improves on the current z (update_ideal, gmpea.cpp:102-109)
+    __shared__ unsigned smin[kMaxM][4];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kMaxM; ++k) {
+        unsigned v = (active && !bad && k < p.P.m) ? float_to_ordered((float)f[k]) : 0xffffffffu;
+        v = warp_min(v);
+        if (lane == 0) smin[k][wid] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxM && (int)threadIdx.x < p.P.m) {
+        const int k = threadIdx.x;
+        unsigned v = smin[k][0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = smin[k][w] < v ? smin[k][w] : v;
+        if (v < *(volatile unsigned*)&st->zbits[k]) atomicMin(&st->zbits[k], v);
+    }
+}
+
+// ---- PBI in fp32 on unit reference vectors (scalarize.cpp:72-89):
+// d1 = |(f - z) . u|, d2 = |(f - z) - d1 u|, g = d1 + theta d2.  Unused lanes
+// of f, u and z are zero for m = 2.
+__device__ __forceinline__ float pbi(const float4 f, const float4 u, const float3 z, float theta) {
+    const float a = f.x - z.x, b = f.y - z.y, c = f.z - z.z;
+    const float d1 = fabsf(a * u.x + b * u.y + c * u.z);
+    const float r0 = a - d1 * u.x, r1 = b - d1 * u.y, r2 = c - d1 * u.z;
+    return d1 + theta * sqrtf(r0 * r0 + r1 * r1 + r2 * r2);
+}
+
+__device__ __forceinline__ float3 load_z(const DevState* st, int m) {
+    float3 z;
+    z.x = ordered_to_float(st->zbits[0]);
+    z.y = ordered_to_float(st->zbits[1]);
+    z.z = m > 2 ? ordered_to_float(st->zbits[2]) : 0.0f;
+    return z;
+}
+
+struct Op1Params {
+    int n;
+    int m;
+    float theta;
+    const float4* U;
+    const float4* oFcv[2];
+    float4* eff[2];
+    unsigned char* srcbits;
+    DevState* st;
+};
+
+// OP1 (gmpea.cpp:248-279).  s1: stream 1 takes off2 (FPR-preferred),
+// s2: stream 2 takes off1 (PBI-preferred).  The reference builds both from
+// Heaviside masks over differences, which reject non-finite inputs.
+__global__ void __launch_bounds__(256) op1_kernel(Op1Params p) {
+    if (p.st->stop) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.n) return;
+    const float3 z = load_z(p.st, p.m);
+    const float4 a = p.oFcv[0][i], b = p.oFcv[1][i], u = p.U[i];
+    const float g1 = pbi(a, u, z, p.theta), g2 = pbi(b, u, z, p.theta);
+    if (!isfinite(a.w - b.w) || !isfinite(g1 - g2)) {
+        atomicCAS(&p.st->err, 0, ERR_NONFINITE);
+        p.st->stop = 1;
+        return;
+    }
+    const bool s1 = b.w < a.w || (a.w == b.w && g1 > g2);
+    const bool s2 = g2 > g1;
+    p.eff[0][i] = s1 ? b : a;
+    p.eff[1][i] = s2 ? a : b;
+    p.srcbits[i] = (unsigned char)((s1 ? 1 : 0) | (s2 ? 2 : 0));
+}
+
+struct SelParams {
+    int n, ld, d, nc, m;
+    float theta;
+    const float4* U;
+    float* X[2];
+    float* G[2];
+    float4* Fcv[2];
+    const float* oX[2];
+    const float* oG[2];
+    const float4* oFcv[2];
+    const float4* eff[2];
+    const unsigned char* srcbits;
+    const int* R[2];     // reverse neighbourhood, R[k*ld + j] ascending in k
+    const int* Rdeg[2];
+    int* winner[2];      // optional: -1 parent, c: off1 row c, n + c: off2 row c
+    int apply;           // copy winner rows into the parents
+    // undo log for the time budget (gmpea.cpp:481-486)
+    float* uX[2];
+    float* uG[2];
+    float4* uFcv[2];
+    int* ustamp[2];
+    DevState* st;
+    DevRecord* rec;      // optional: feasible count of pop1 for this generation
+};
+
+template <int POP>
+__device__ __forceinline__ void select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
+    const float4 par = p.Fcv[POP][j];
+    const float4 u = p.U[j];
+    const float gp = pbi(par, u, z, p.theta);
+    const int deg = p.Rdeg[POP][j];
+    const int* __restrict__ R = p.R[POP];
+    const float4* __restrict__ eff = p.eff[POP];
+    bool have = false;
+    float4 best = par;
+    float bg = 0.0f;
+    int bc = -1;
+    int mex = 0;
+    bool mex_open = true;
+    bool negcv = false;
+    for (int k = 0; k < deg; ++k) {
+        const int c = R[(long long)k * p.ld + j];
+        const float4 e = eff[c];
+        const float g = pbi(e, u, z, p.theta);
+        bool mark;
+        if (POP == 0) {  // fpr_better (scalarize.cpp:91-96)
+            negcv |= (e.w < 0.0f) || (par.w < 0.0f);
+            mark = (e.w == par.w) ? (g < gp) : (e.w < par.w);
+        } else {
+            mark = g < gp;
+        }
+        if (!mark) continue;
+        // claims arrive in ascending c: the parent sits at their mex (gmpea.cpp:343-348)
+        if (mex_open) {
+            if (c == mex)
+                ++mex;
+            else if (c > mex)
+                mex_open = false;
+        }
+        bool better;
+        if (!have)
+            better = true;
+        else if (POP == 0)
+            better = e.w < best.w || (e.w == best.w && (g < bg || (g == bg && c < bc)));
+        else
+            better = g < bg || (g == bg && c < bc);
+        if (better) {
+            have = true;
+            best = e;
+            bg = g;
+            bc = c;
+        }
+    }
+    if (negcv) {
+        atomicCAS(&p.st->err, 0, ERR_NEG_CV);
+        p.st->stop = 1;
+    }
+    // the parent competes with index mex (gmpea.cpp:349-371)
+    bool off_wins = false;
+    if (have) {
+        if (POP == 0)
+            off_wins = best.w < par.w || (best.w == par.w && (bg < gp || (bg == gp && bc < mex)));
+        else
+            off_wins = bg < gp || (bg == gp && bc < mex);
+    }
+    int code = -1;
+    if (off_wins) {
+        const unsigned char sb = p.srcbits[bc];
+        const bool from2 = POP == 0 ? (sb & 1) : !(sb & 2);
+        code = from2 ? p.n + bc : bc;
+    }
+    if (p.winner[POP]) p.winner[POP][j] = code;
+    feas = (off_wins ? best.w : par.w) == 0.0f;
+    if (!off_wins || !p.apply) return;
+    const int src = code >= p.n ? 1 : 0;
+    const int c = bc;
+    const long long ld = p.ld;
+    float* __restrict__ X = p.X[POP];
+    float* __restrict__ G = p.G[POP];
+    const float* __restrict__ oX = p.oX[src];
+    const float* __restrict__ oG = p.oG[src];
+    if (p.ustamp[POP]) {
+        float* __restrict__ uX = p.uX[POP];
+        float* __restrict__ uG = p.uG[POP];
+        for (int q = 0; q < p.d; ++q) uX[q * ld + j] = X[q * ld + j];
+        for (int q = 0; q < p.nc; ++q) uG[q * ld + j] = G[q * ld + j];
+        p.uFcv[POP][j] = par;
+        p.ustamp[POP][j] = p.st->gen;
+    }
+    for (int q = 0; q < p.d; ++q) X[q * ld + j] = oX[q * ld + c];
+    for (int q = 0; q < p.nc; ++q) G[q * ld + j] = oG[q * ld + c];
+    p.Fcv[POP][j] = best;
+}
+
+__global__ void __launch_bounds__(256) select_kernel(SelParams p) {
+    if (p.st->stop) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const float3 z = load_z(p.st, p.m);
+    bool feas = false;
+    if (j < p.n) {
+        if (blockIdx.y == 0)
+            select_slot<0>(p, j, z, feas);
+        else
+            select_slot<1>(p, j, z, feas);
+    }
+    if (blockIdx.y != 0 || p.rec == nullptr) return;
+    // feasible_ratio of pop1 (gmpea.cpp:411-417): block count, one atomic
+    __shared__ unsigned cnt[8];
+    unsigned b = __popc(__ballot_sync(0xffffffffu, feas && j < p.n));
+    if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += cnt[w];
+        if (s) atomicAdd(&p.rec[p.st->gen].feasible, s);
+    }
+}
+
+// loop-time bookkeeping after a generation (gmpea.cpp:480-488)
+__global__ void end_gen_kernel(DevState* st, DevRecord* rec) {
+    if (st->stop) return;
+    const unsigned long long now = globaltimer();
+    st->loop_ns += now - st->t_gen_start;
+    if (st->budget_ns && st->loop_ns >= st->budget_ns) {
+        st->discard = 1;  // the generation that crossed the deadline is discarded
+        st->stop = 1;
+        return;
+    }
+    rec[st->gen].loop_ns = st->loop_ns;
+    st->gens_done += 1;
+    st->gen += 1;
+    st->t_gen_start = globaltimer();
+}
+
+__global__ void mark_start_kernel(DevState* st) { st->t_gen_start = globaltimer(); }
+
+struct RestoreParams {
+    int n, ld, d, nc;
+    float* X[2];
+    float* G[2];
+    float4* Fcv[2];
+    const float* uX[2];
+    const float* uG[2];
+    const float4* uFcv[2];
+    const int* ustamp[2];
+    DevState* st;
+};
+
+__global__ void restore_kernel(RestoreParams p) {
+    if (!p.st->discard) return;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int q = blockIdx.y;
+    if (j >= p.n || p.ustamp[q][j] != p.st->gen) return;
+    const long long ld = p.ld;
+    for (int k = 0; k < p.d; ++k) p.X[q][k * ld + j] = p.uX[q][k * ld + j];
+    for (int k = 0; k < p.nc; ++k) p.G[q][k * ld + j] = p.uG[q][k * ld + j];
+    p.Fcv[q][j] = p.uFcv[q][j];
+}
+
+// feasible count of pop1 (generation-0 record)
+__global__ void count_feasible_kernel(const float4* Fcv, int n, unsigned* out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool f = j < n && Fcv[j].w == 0.0f;
+    unsigned b = __popc(__ballot_sync(0xffffffffu, f));
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, b);
+}
+
+}  // namespace gmpea_b200

@@ -1,0 +1,522 @@
+// Batched CMOP evaluation on device, streamed gene by gene.
+//
+// A child is produced one gene at a time by the variation loop and handed to
+// Eval::gene(j, x) in ascending j, so no problem needs the whole decision row
+// in registers (D = 252 for WTA-P10).  Eval::finish() forms the objectives and
+// raw constraints (<= 0 feasible) exactly as the reference does:
+//   LIRCMOP1-14    proj/src/problems.cpp:22-137
+//   C-/DC-DTLZ     proj/src/problems.cpp:141-201,426-525
+//   WTA P1-P10     proj/src/wta.cpp:51-129 (decode = per-vehicle top-capacity,
+//                  which equals the reference's global stable sort because the
+//                  vehicles are independent)
+//   MW1-MW14       not in the reference; restated from the MW
+//                  suite (Ma & Wang 2019, PlatEMO conventions), parity
+//                  unpinned, mirrored by oracle/gmpea_oracle.cpp eval_mw.
+// Precision policy: inputs are fp32; sums, products and the
+// per-individual transcendental terms are evaluated in fp64 (B200 runs fp64
+// at half the fp32 rate), the per-gene trigonometric terms of LIRCMOP5-12 in
+// fp32 (argument < pi/2, error < 2e-7).  Outputs are rounded to fp32.
+#pragma once
+#include "common.cuh"
+
+namespace gmpea_b200 {
+
+enum : int { FAM_LIR = 1, FAM_DTLZ = 2, FAM_WTA = 3, FAM_MW = 4 };
+enum : int {
+    C1_DTLZ1 = 1, C1_DTLZ3, C2_DTLZ2, C3_DTLZ4, DC1_DTLZ1, DC1_DTLZ3,
+    DC2_DTLZ1, DC2_DTLZ3, DC3_DTLZ1, DC3_DTLZ3
+};
+
+constexpr int kWtaMaxVehicles = 16;
+constexpr int kWtaMaxCap = 8;
+constexpr int kWtaMaxSlots = 128;
+constexpr int kMaxCon = kWtaMaxVehicles + kWtaMaxSlots;
+
+struct ProbDev {
+    int fam, id, d, m, nin, neq;
+    const float* lo;  // d lower bounds
+    const float* hi;  // d upper bounds
+    // host-computed constants (glibc values, identical to the reference's)
+    double cth, sth;  // cos/sin(-pi/4)  (LIRCMOP5-12 ellipse rotation)
+    double cal, sal;  // cos/sin(pi/4)   (LIRCMOP9-12 alpha)
+    // WTA scenario tables (wta.hpp:17-28)
+    int wta_targets, wta_vehicles, wta_slots;
+    const int* wta_cap;          // per vehicle
+    const int* wta_strikes;      // per target
+    const int* wta_slot_target;  // per strike slot
+    const double* wta_p;         // per strike slot
+};
+
+// ---------------------------------------------------------------- LIRCMOP
+struct EvalLir {
+    double g1, g2, x0, x1, s0, c0;
+    float x0f;
+    __device__ __forceinline__ void begin(const ProbDev&) { g1 = g2 = 0.0; }
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
+        const double x = xf;
+        const int id = P.id;
+        if (j == 0) {
+            x0 = x;
+            x0f = xf;
+            if (id <= 4) sincospi(0.5 * x, &s0, &c0);  // problems.cpp:23-24
+            return;
+        }
+        if (id >= 13) {  // problems.cpp:124-128
+            if (j == 1) {
+                x1 = x;
+                return;
+            }
+            double t = x - 0.5;
+            g1 += 10.0 * t * t;
+            return;
+        }
+        double track;
+        if (id <= 4) {
+            track = (j & 1) ? c0 : s0;
+        } else {  // problems.cpp:43-50: sin/cos(0.5 (j+1) pi x1 / n)
+            float a = __fdiv_rn(0.5f * (float)(j + 1) * x0f, (float)P.d);
+            track = (j & 1) ? (double)cospif(a) : (double)sinpif(a);
+        }
+        double t = x - track;
+        if (j & 1)
+            g2 += t * t;
+        else
+            g1 += t * t;
+    }
+    __device__ static double ellipse(const ProbDev& P, double f1, double f2, double p, double q,
+                                     double a, double b) {
+        double u = (f1 - p) * P.cth - (f2 - q) * P.sth;
+        double v = (f1 - p) * P.sth + (f2 - q) * P.cth;
+        return 0.1 - u * u / (a * a) - v * v / (b * b);
+    }
+    template <class G>
+    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
+        const int id = P.id;
+        if (id <= 4) {
+            f[0] = x0 + g1;
+            f[1] = (id == 1 || id == 3) ? 1.0 - x0 * x0 + g2 : 1.0 - sqrt(x0) + g2;
+            emit(0, -((0.51 - g1) * (g1 - 0.5)));
+            emit(1, -((0.51 - g2) * (g2 - 0.5)));
+            if (id >= 3) emit(2, 0.5 - sinpi(20.0 * x0));
+            return;
+        }
+        if (id <= 8) {
+            f[0] = x0 + 10.0 * g1 + 0.7057;
+            bool sq = (id == 5 || id == 7);
+            f[1] = (sq ? 1.0 - sqrt(x0) : 1.0 - x0 * x0) + 10.0 * g2 + 0.7057;
+            if (id <= 6) {
+                double p0 = id == 5 ? 1.6 : 1.8, p1 = id == 5 ? 2.5 : 2.8;
+                double b0 = id == 5 ? 4.0 : 8.0;
+                emit(0, ellipse(P, f[0], f[1], p0, p0, 2.0, b0));
+                emit(1, ellipse(P, f[0], f[1], p1, p1, 2.0, 8.0));
+            } else {
+                emit(0, ellipse(P, f[0], f[1], 1.2, 1.2, 2.0, 6.0));
+                emit(1, ellipse(P, f[0], f[1], 2.25, 2.25, 2.5, 12.0));
+                emit(2, ellipse(P, f[0], f[1], 3.5, 3.5, 2.5, 10.0));
+            }
+            return;
+        }
+        if (id <= 12) {
+            f[0] = 1.7057 * x0 * (10.0 * g1 + 1.0);
+            bool sq = (id == 10 || id == 11);
+            f[1] = 1.7057 * (sq ? 1.0 - sqrt(x0) : 1.0 - x0 * x0) * (10.0 * g2 + 1.0);
+            double p, q, a, b, lv;
+            switch (id) {
+                case 9: p = 1.4; q = 1.4; a = 1.5; b = 6.0; lv = 2.0; break;
+                case 10: p = 1.1; q = 1.2; a = 2.0; b = 4.0; lv = 1.0; break;
+                case 11: p = 1.2; q = 1.2; a = 1.5; b = 5.0; lv = 2.1; break;
+                default: p = 1.6; q = 1.6; a = 1.5; b = 6.0; lv = 2.5; break;
+            }
+            emit(0, ellipse(P, f[0], f[1], p, q, a, b));
+            emit(1, lv - (f[0] * P.sal + f[1] * P.cal - sinpi(4.0 * (f[0] * P.cal - f[1] * P.sal))));
+            return;
+        }
+        double rad = 1.7057 + g1;
+        double s1, c1;
+        sincospi(0.5 * x0, &s0, &c0);
+        sincospi(0.5 * x1, &s1, &c1);
+        f[0] = rad * c0 * c1;
+        f[1] = rad * c0 * s1;
+        f[2] = rad * s0;
+        double r2 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+        emit(0, -((r2 - 9.0) * (r2 - 4.0)));
+        emit(1, -((r2 - 3.61) * (r2 - 3.24)));
+        if (id == 14) emit(2, -((r2 - 3.0625) * (r2 - 2.56)));
+    }
+};
+
+// ---------------------------------------------------------------- C/DC-DTLZ
+struct EvalDtlz {
+    double pos[2];
+    double rast, sph;
+    __device__ __forceinline__ void begin(const ProbDev&) { rast = sph = 0.0; }
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
+        const double x = xf;
+        if (j < P.m - 1) {
+            pos[j] = x;
+            return;
+        }
+        double t = x - 0.5;  // problems.cpp:144-147, 153-155
+        rast += t * t - cospi(20.0 * t);
+        sph += t * t;
+    }
+    __device__ static void shape(int base, const double* pos, double g, double* f) {
+        // m = 3 (problems.cpp:160-178)
+        if (base == 1) {
+            f[0] = 0.5 * pos[0] * pos[1] * (1.0 + g);
+            f[1] = 0.5 * pos[0] * (1.0 - pos[1]) * (1.0 + g);
+            f[2] = 0.5 * (1.0 - pos[0]) * (1.0 + g);
+        } else {
+            double s0, c0, s1, c1;
+            sincospi(0.5 * pos[0], &s0, &c0);
+            sincospi(0.5 * pos[1], &s1, &c1);
+            f[0] = (1.0 + g) * c0 * c1;
+            f[1] = (1.0 + g) * c0 * s1;
+            f[2] = (1.0 + g) * s0;
+        }
+    }
+    template <class G>
+    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
+        const int k = P.id;
+        const int m = P.m;
+        const double gr = 100.0 * ((double)(P.d - m + 1) + rast);
+        switch (k) {
+            case C1_DTLZ1: {
+                shape(1, pos, gr, f);
+                emit(0, f[0] / 0.5 + f[1] / 0.5 + f[2] / 0.6 - 1.0);
+                return;
+            }
+            case C1_DTLZ3: {
+                shape(2, pos, gr, f);
+                double r2 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+                emit(0, -((r2 - 16.0) * (r2 - 81.0)));
+                return;
+            }
+            case C2_DTLZ2: {
+                shape(2, pos, sph, f);
+                const double r = 0.4;
+                double v1 = 1.0 / 0.0;
+                for (int i = 0; i < 3; ++i) {
+                    double t = (f[i] - 1.0) * (f[i] - 1.0) - r * r;
+                    for (int j = 0; j < 3; ++j)
+                        if (j != i) t += f[j] * f[j];
+                    v1 = fmin(v1, t);
+                }
+                const double c = 1.0 / sqrt(3.0);  // correctly rounded, as glibc
+                double v2 = 0.0;
+                for (int i = 0; i < 3; ++i) v2 += (f[i] - c) * (f[i] - c);
+                v2 -= r * r;
+                emit(0, fmin(v1, v2));
+                return;
+            }
+            case C3_DTLZ4: {
+                double pp[2] = {pow(pos[0], 100.0), pow(pos[1], 100.0)};
+                shape(2, pp, sph, f);
+                for (int j = 0; j < 3; ++j) {
+                    double s = f[j] * f[j] / 4.0;
+                    for (int i = 0; i < 3; ++i)
+                        if (i != j) s += f[i] * f[i];
+                    emit(j, 1.0 - s);
+                }
+                return;
+            }
+            default: break;
+        }
+        bool linear = (k == DC1_DTLZ1 || k == DC2_DTLZ1 || k == DC3_DTLZ1);
+        shape(linear ? 1 : 2, pos, gr, f);
+        if (k == DC1_DTLZ1 || k == DC1_DTLZ3) {
+            emit(0, -(cospi(3.0 * pos[0]) + 0.5));
+        } else if (k == DC2_DTLZ1 || k == DC2_DTLZ3) {
+            emit(0, 0.9 - cospi(3.0 * gr));
+            emit(1, 0.9 - exp(-gr));
+        } else {
+            emit(0, -(cospi(3.0 * pos[0]) + 0.5));
+            emit(1, -(cospi(3.0 * pos[1]) + 0.5));
+            emit(2, -(cospi(3.0 * gr) + 0.5));
+        }
+    }
+};
+
+// ---------------------------------------------------------------- MW (unpinned)
+__device__ __forceinline__ double ipow(double x, int e) {
+    double r = 1.0;
+    while (e) {
+        if (e & 1) r *= x;
+        x *= x;
+        e >>= 1;
+    }
+    return r;
+}
+
+struct EvalMw {
+    double xs[2];
+    double prev;
+    double gs;
+    __device__ __forceinline__ void begin(const ProbDev&) { gs = 0.0; }
+    __device__ __forceinline__ static int kind(int id) {
+        // 0: exp distance (MW1/4/5/9/12), 1: cos distance (2/6/8/10/13), 2: linear (3/7/11/14)
+        switch (id) {
+            case 1: case 4: case 5: case 9: case 12: return 0;
+            case 2: case 6: case 8: case 10: case 13: return 1;
+            default: return 2;
+        }
+    }
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
+        const double x = xf;
+        const int n = P.d, m = P.m;
+        if (j < m - 1) {
+            xs[j] = x;
+            prev = x;
+            return;
+        }
+        int kd = kind(P.id);
+        if (kd == 0) {
+            double t = ipow(x, n - m) - 0.5 - (double)j / (2.0 * n);
+            gs += 1.0 - exp(-10.0 * t * t);
+        } else if (kd == 1) {
+            double t = x - (double)j / n;
+            double z = 1.0 - exp(-10.0 * t * t);
+            gs += 1.5 + (0.1 / n) * z * z - 1.5 * cospi(2.0 * z);
+        } else {
+            double p = prev - 0.5;
+            double t = x + p * p - 1.0;
+            gs += 2.0 * t * t;
+        }
+        prev = x;
+    }
+    template <class G>
+    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
+        const int id = P.id, n = P.d, m = P.m;
+        const double r2 = sqrt(2.0);
+        switch (id) {
+            case 1: case 2: {
+                double g = 1.0 + gs;
+                f[0] = xs[0];
+                f[1] = id == 1 ? g * (1.0 - 0.85 * f[0] / g) : g * (1.0 - f[0] / g);
+                double l = r2 * f[1] - r2 * f[0];
+                emit(0, f[0] + f[1] - 1.0 - 0.5 * ipow(sinpi((id == 1 ? 2.0 : 3.0) * l), 8));
+                return;
+            }
+            case 3: {
+                double g = 1.0 + gs;
+                f[0] = xs[0];
+                f[1] = g * (1.0 - f[0] / g);
+                double l = r2 * f[1] - r2 * f[0];
+                double s = f[0] + f[1];
+                double sn = sinpi(0.75 * l);
+                emit(0, s - 1.05 - 0.45 * ipow(sn, 6));
+                emit(1, 0.85 - s + 0.3 * sn * sn);
+                return;
+            }
+            case 4: case 8: {
+                double g = gs;
+                double c[2], s[2];
+                for (int i = 0; i < m - 1; ++i) {
+                    if (id == 4) {
+                        c[i] = xs[i];
+                        s[i] = 1.0 - xs[i];
+                    } else {
+                        sincospi(0.5 * xs[i], &s[i], &c[i]);
+                    }
+                }
+                for (int k = 0; k < m; ++k) {
+                    double v = 1.0 + g;
+                    for (int i = 0; i + k + 1 < m; ++i) v *= c[i];
+                    if (k > 0) v *= s[m - 1 - k];
+                    f[k] = v;
+                }
+                if (id == 4) {
+                    double l = f[m - 1], sum = 0.0;
+                    for (int k = 0; k + 1 < m; ++k) l -= f[k];
+                    for (int k = 0; k < m; ++k) sum += f[k];
+                    emit(0, sum - (1.0 + 0.4 * ipow(sinpi(2.5 * l), 8)));
+                } else {
+                    double q = 0.0;
+                    for (int k = 0; k < m; ++k) q += f[k] * f[k];
+                    double l = asin(f[m - 1] / sqrt(q));
+                    double sn = sin(6.0 * l);
+                    double t = 1.25 - 0.5 * sn * sn;
+                    emit(0, q - t * t);
+                }
+                return;
+            }
+            case 5: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0];
+                double r = f[0] / g;
+                f[1] = g * sqrt(1.0 - r * r);
+                double l1 = atan(f[1] / f[0]);
+                double l2 = 0.5 * 3.141592653589793 - 2.0 * fabs(l1 - 0.25 * 3.141592653589793);
+                double q = f[0] * f[0] + f[1] * f[1];
+                double a = 1.7 - 0.2 * sin(2.0 * l1);
+                double s6 = sin(6.0 * l2 * l2 * l2);
+                double b = 1.0 + 0.5 * s6, c = 1.0 - 0.45 * s6;
+                emit(0, q - a * a);
+                emit(1, b * b - q);
+                emit(2, c * c - q);
+                return;
+            }
+            case 6: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0] * 1.0999;
+                double r = f[0] / g;
+                f[1] = g * sqrt(1.1 * 1.1 - r * r);
+                double l = ipow(cos(6.0 * ipow(atan(f[1] / f[0]), 4)), 10);
+                double a = f[0] / (1.0 + 0.15 * l), b = f[1] / (1.0 + 0.75 * l);
+                emit(0, a * a + b * b - 1.0);
+                return;
+            }
+            case 7: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0];
+                double r = f[0] / g;
+                f[1] = g * sqrt(1.0 - r * r);
+                double l = atan(f[1] / f[0]);
+                double q = f[0] * f[0] + f[1] * f[1];
+                double sn = sin(4.0 * l);
+                double a = 1.2 + 0.4 * ipow(sn, 16);
+                double b = 1.15 - 0.2 * ipow(sn, 8);
+                emit(0, q - a * a);
+                emit(1, b * b - q);
+                return;
+            }
+            case 9: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0];
+                f[1] = g * (1.0 - pow(f[0] / g, 0.6));
+                double s = f[0] * f[0];
+                double t1 = (1.0 - 0.64 * s - f[1]) * (1.0 - 0.36 * s - f[1]);
+                double a = f[0] + 0.35, b = f[0] + 0.15;
+                double t2 = 1.35 * 1.35 - a * a - f[1];
+                double t3 = 1.15 * 1.15 - b * b - f[1];
+                emit(0, fmin(t1, t2 * t3));
+                return;
+            }
+            case 10: {
+                double g = 1.0 + gs;
+                f[0] = g * ipow(xs[0], n);
+                double r = f[0] / g;
+                f[1] = g * (1.0 - r * r);
+                double s = f[0] * f[0];
+                emit(0, -(2.0 - 4.0 * s - f[1]) * (2.0 - 8.0 * s - f[1]));
+                emit(1, (2.0 - 2.0 * s - f[1]) * (2.0 - 16.0 * s - f[1]));
+                emit(2, (1.0 - s - f[1]) * (1.2 - 1.2 * s - f[1]));
+                return;
+            }
+            case 11: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0] * sqrt(1.9999);
+                double r = f[0] / g;
+                f[1] = g * sqrt(2.0 - r * r);
+                double s = f[0] * f[0];
+                emit(0, -(3.0 - s - f[1]) * (3.0 - 4.0 * s - f[1]));
+                emit(1, (3.0 - 0.625 * s - f[1]) * (3.0 - 7.0 * s - f[1]));
+                emit(2, -(1.62 - 0.18 * s - f[1]) * (1.125 - 0.125 * s - f[1]));
+                emit(3, (2.07 - 0.23 * s - f[1]) * (0.63 - 0.07 * s - f[1]));
+                return;
+            }
+            case 12: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0];
+                double r = f[0] / g;
+                f[1] = g * (0.85 - 0.8 * r - 0.08 * fabs(sinpi(3.2 * r)));
+                double a = 1.0 - 0.8 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] - f[0] / 1.5));
+                double b = 1.8 - 1.125 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] / 1.8 - f[0] / 1.6));
+                double c = 1.0 - 0.625 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] - f[0] / 1.6));
+                double e = 1.4 - 0.875 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] / 1.4 - f[0] / 1.6));
+                emit(0, a * b);
+                emit(1, -(c * e));
+                return;
+            }
+            case 13: {
+                double g = 1.0 + gs;
+                f[0] = g * xs[0] * 1.5;
+                double r = f[0] / g;
+                f[1] = g * (5.0 - exp(r) - fabs(0.5 * sinpi(3.0 * r)));
+                double s3 = 0.5 * sinpi(3.0 * f[0]);
+                double a = 5.0 - exp(f[0]) - s3 - f[1];
+                double b = 5.0 - (1.0 + 0.4 * f[0]) - s3 - f[1];
+                double c = 5.0 - (1.0 + f[0] + 0.5 * f[0] * f[0]) - s3 - f[1];
+                double e = 5.0 - (1.0 + 0.7 * f[0]) - s3 - f[1];
+                emit(0, a * b);
+                emit(1, -(c * e));
+                return;
+            }
+            default: {  // 14
+                double g = gs;
+                double s = 0.0, sa = 0.0;
+                for (int k = 0; k + 1 < m; ++k) {
+                    f[k] = xs[k];
+                    double q = f[k] * f[k];
+                    double sn = sinpi(1.1 * q);
+                    s += 6.0 - exp(f[k]) - 1.5 * sn;
+                    sa += 6.1 - (1.0 + f[k] + 0.5 * q + 1.5 * sn);
+                }
+                f[m - 1] = (1.0 + g) / (m - 1) * s;
+                emit(0, f[m - 1] - 1.0 / (m - 1) * sa);
+                return;
+            }
+        }
+    }
+};
+
+// ---------------------------------------------------------------- WTA
+// decode_wta (wta.cpp:51-72): genes >= 0.5 are candidates, taken in
+// descending value (ties to the lower flat index) while the vehicle has
+// capacity.  Vehicle v = g % vehicles, so per vehicle this is "keep the top
+// cap[v] candidates", maintained as a sorted insertion list while streaming.
+struct EvalWta {
+    float val[kWtaMaxVehicles][kWtaMaxCap];
+    short idx[kWtaMaxVehicles][kWtaMaxCap];
+    unsigned char cnt[kWtaMaxVehicles];
+    __device__ __forceinline__ void begin(const ProbDev& P) {
+        for (int v = 0; v < P.wta_vehicles; ++v) cnt[v] = 0;
+    }
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, float x) {
+        if (!(x >= 0.5f)) return;
+        const int v = j % P.wta_vehicles;
+        const int cap = P.wta_cap[v];
+        int c = cnt[v];
+        // strict '>' keeps earlier (lower) indices ahead on ties
+        int pos = c;
+        while (pos > 0 && x > val[v][pos - 1]) --pos;
+        if (pos >= cap) return;
+        int last = c < cap ? c : cap - 1;
+        for (int k = last; k > pos; --k) {
+            val[v][k] = val[v][k - 1];
+            idx[v][k] = idx[v][k - 1];
+        }
+        val[v][pos] = x;
+        idx[v][pos] = (short)j;
+        if (c < cap) cnt[v] = (unsigned char)(c + 1);
+    }
+    template <class G>
+    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
+        const int V = P.wta_vehicles, T = P.wta_targets, S = P.wta_slots;
+        unsigned char hits[kWtaMaxSlots];
+        for (int s = 0; s < S; ++s) hits[s] = 0;
+        for (int v = 0; v < V; ++v)
+            for (int k = 0; k < cnt[v]; ++k) hits[idx[v][k] / V] += 1;
+        // constraints are emitted in ascending index: vehicle loads first
+        // (wta.cpp:99-100), then per-target strike counts (:101-109)
+        for (int v = 0; v < V; ++v) emit(v, (double)cnt[v] - (double)P.wta_cap[v]);
+        // wta.cpp:78-97: f1 accumulates 1 - prod(1 - p * hits) per target
+        double f1 = 0.0, f2 = 0.0;
+        int s = 0;
+        for (int i = 0; i < T; ++i) {
+            double surv = 1.0, strikes = 0.0;
+            for (int k = 0; k < P.wta_strikes[i]; ++k, ++s) {
+                double h = hits[s];
+                surv *= 1.0 - P.wta_p[s] * h;
+                f2 += h;
+                strikes += h;
+            }
+            f1 += 1.0 - surv;
+            emit(V + i, strikes - (double)P.wta_strikes[i]);
+        }
+        f[0] = -f1;  // wta.cpp:126 (solvers minimise)
+        f[1] = f2;
+    }
+};
+
+}  // namespace gmpea_b200

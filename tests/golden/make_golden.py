@@ -1,0 +1,176 @@
+"""Generates the committed golden fixtures of tests/golden/ from the
+UNMODIFIED reference (oracle/_ref/libgmpea_ref.so, built by oracle/Makefile
+from /root/reference/proj/src).  Run here, where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+The GPU box has no /root/reference; the GPU parity tests read these files.
+Inputs are fp32-representable so the fp32 engine sees exactly what the f64
+reference saw.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from oracle import Oracle, Reference, build_ref  # noqa: E402
+
+from conftest import MW_PROBLEMS, REF_PROBLEMS, f32  # noqa: E402
+
+
+def eval_fixture(ref, orc, rng):
+    out = {}
+    for name in REF_PROBLEMS:
+        d = ref.problem_info(name)["d"]
+        X = f32(rng.random((64, d)))
+        if name.startswith("WTA"):
+            # exercise the 0.5 threshold and ties of the decode
+            X[:8] = f32(np.round(X[:8] * 4) / 4)
+        F, G, cv = ref.evaluate(name, X)
+        out[f"{name}/X"], out[f"{name}/F"], out[f"{name}/G"], out[f"{name}/cv"] = X, F, G, cv
+    for name in MW_PROBLEMS:  # unpinned: oracle restatement, recorded for regression only
+        info = orc.problem_info(name)
+        X = f32(info["lo"] + (info["hi"] - info["lo"]) * rng.random((64, info["d"])))
+        F, G, cv = orc.evaluate(name, X)
+        out[f"{name}/X"], out[f"{name}/F"], out[f"{name}/G"], out[f"{name}/cv"] = X, F, G, cv
+    np.savez_compressed(os.path.join(HERE, "eval.npz"), **out)
+
+
+def random_pop(rng, n, m, nc):
+    """tests/oracles.cpp:545-565 shape: F ~ U(0,5), C ~ U(-1,1), ~35% feasible."""
+    X = f32(rng.random((n, 2)))
+    F = f32(rng.uniform(0.0, 5.0, (n, m)))
+    Cm = f32(rng.uniform(-1.0, 1.0, (n, nc)))
+    feas = rng.random(n) < 0.35
+    Cm[feas] = -np.abs(Cm[feas])
+    cv = f32(np.maximum(Cm, 0.0).sum(1))
+    return dict(X=X, F=F, C=Cm, cv=cv)
+
+
+def selection_fixture(ref, orc, rng, count=200):
+    out = {"count": np.array(count)}
+    for k in range(count):
+        n = int(rng.integers(4, 33))
+        m = int(rng.integers(2, 4))
+        nc = int(rng.integers(1, 4))
+        pops = [random_pop(rng, n, m, nc) for _ in range(4)]
+        if k % 4 == 0:  # lattice weights (tests/test_gmpea.cpp:29-41)
+            W = ref.reference_vectors(m, n)
+        else:  # random positive weights (tests/acceptance.cpp:92-101)
+            W = 0.05 + rng.random((n, m))
+            W /= W.sum(1, keepdims=True)
+        z = f32(rng.uniform(-0.5, 0.5, m))
+        t1 = 1 + int(rng.integers(0, min(n, 5)))
+        t2 = t1 + int(rng.integers(0, n - t1 + 1))
+        B1, B2 = ref.build_neighborhoods(W, t1, t2)
+        outs = ref.environmental_selection(pops, W, z, 5.0, B1, B2)
+        s1, s2 = orc.selection(pops, W, z, 5.0, B1, B2)
+        # the oracle's winner codes reproduce the reference's output rows exactly
+        for s, o, par in ((s1, outs[0], pops[0]), (s2, outs[1], pops[1])):
+            for key in ("X", "F", "C", "cv"):
+                exp = par[key].copy()
+                for j in range(n):
+                    if s[j] >= 0:
+                        exp[j] = (pops[2] if s[j] < n else pops[3])[key][s[j] % n]
+                assert np.array_equal(exp, o[key])
+        pre = f"{k}/"
+        for i, p in enumerate(pops):
+            for key in ("X", "F", "C", "cv"):
+                out[pre + f"{i}{key}"] = p[key]
+        out[pre + "W"], out[pre + "z"], out[pre + "B1"], out[pre + "B2"] = W, z, B1, B2
+        out[pre + "src1"], out[pre + "src2"] = s1, s2
+        for i in range(2):
+            for key in ("X", "F", "C", "cv"):
+                out[pre + f"out{i}{key}"] = outs[i][key]
+    np.savez_compressed(os.path.join(HERE, "selection.npz"), **out)
+
+
+def knn_fixture(ref, rng):
+    out = {}
+    cases = [(2, 5, 2, 5), (2, 100, 5, 20), (2, 1001, 5, 20), (3, 105, 5, 20), (3, 300, 5, 20),
+             (3, 1000, 5, 20), (3, 3000, 5, 20), (2, 40, 20, 40), (3, 33, 33, 33)]
+    for (m, n, t1, t2) in cases:
+        W = ref.reference_vectors(m, n)
+        B1, B2 = ref.build_neighborhoods(W, t1, t2)
+        key = f"lat_{m}_{n}_{t1}_{t2}"
+        out[key + "/W"], out[key + "/B1"], out[key + "/B2"] = W, B1, B2
+    for k in range(10):
+        n = int(rng.integers(4, 200))
+        m = int(rng.integers(2, 4))
+        W = 0.05 + rng.random((n, m))
+        W /= W.sum(1, keepdims=True)
+        t1 = int(rng.integers(1, min(n, 8) + 1))
+        t2 = int(rng.integers(t1, min(n, 40) + 1))
+        B1, B2 = ref.build_neighborhoods(W, t1, t2)
+        key = f"rnd_{k}"
+        out[key + "/W"], out[key + "/B1"], out[key + "/B2"] = W, B1, B2
+    np.savez_compressed(os.path.join(HERE, "knn.npz"), **out)
+
+
+def metrics_fixture(ref, rng):
+    out = {}
+    for k in range(24):
+        m = 2 + k % 2
+        n = int(rng.integers(1, 400))
+        F = f32(rng.random((n, m)))
+        F[rng.random(n) < 0.15] = F[0]  # duplicates
+        cv = np.where(rng.random(n) < 0.3, rng.random(n), 0.0)
+        R = rng.random((50, m))
+        key = f"{k}/"
+        out[key + "F"], out[key + "cv"], out[key + "R"] = F, cv, R
+        out[key + "front"] = ref.metric_front(F, cv)
+        out[key + "igd"] = np.array(ref.igd(F, R))
+        P = f32(rng.random((n, m)) * 1.2)
+        out[key + "P"] = P
+        out[key + "hv"] = np.array(ref.hypervolume(P, np.full(m, 1.1)))
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+
+
+def fronts_fixture(ref):
+    out = {}
+    for name in REF_PROBLEMS:
+        if name.startswith("WTA"):
+            continue
+        out[name] = ref.pf_reference(name, 1000)
+    np.savez_compressed(os.path.join(HERE, "fronts.npz"), **out)
+
+
+def runs_fixture(ref):
+    """Final IGD of the reference's own run_gmpea over 30 seeds (statistical parity)."""
+    fronts = np.load(os.path.join(HERE, "fronts.npz"))
+    out = {}
+    for name, op, n, gens in (("LIRCMOP1", 1, 100, 200), ("LIRCMOP13", 1, 105, 200),
+                              ("C1-DTLZ1", 0, 105, 300), ("LIRCMOP9", 1, 100, 200)):
+        vals = []
+        for seed in range(1, 31):
+            pop, hist = ref.run_gmpea(name, n, k_max=gens, seed=seed, op=op, record_walltime=False)
+            front = ref.metric_front(pop["F"], pop["cv"])
+            vals.append(ref.igd(front, fronts[name]) if len(front) else np.inf)
+        out[f"{name}/igd"] = np.array(vals)
+        out[f"{name}/cfg"] = np.array([op, n, gens])
+    np.savez_compressed(os.path.join(HERE, "runs.npz"), **out)
+
+
+def main():
+    if not build_ref():
+        raise SystemExit("reference sources not available")
+    ref, orc = Reference(), Oracle()
+    rng = np.random.default_rng(20250919)
+    eval_fixture(ref, orc, rng)
+    selection_fixture(ref, orc, rng)
+    knn_fixture(ref, rng)
+    metrics_fixture(ref, rng)
+    fronts_fixture(ref)
+    runs_fixture(ref)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,325 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden fixtures and the pinned oracle, on the same inputs.
+
+Contract (north_star): objectives / constraints / cv within 1e-5 relative in
+fp32; selection and replacement indices bit-exact wherever the deciding keys
+are not tied within that tolerance; integer/index work (neighbourhoods,
+decode, draws) bit-exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import MW_PROBLEMS, REF_PROBLEMS, f32, golden, rel_close
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------------ evaluation
+@pytest.mark.parametrize("name", REF_PROBLEMS + MW_PROBLEMS)
+def test_evaluate_matches_reference_golden(g, name):
+    gd = golden("eval.npz")
+    p = g.make_problem(name)
+    X = gd[f"{name}/X"]
+    r = g.evaluate_population(p, X)
+    assert r.F.shape == gd[f"{name}/F"].shape
+    assert rel_close(r.F, gd[f"{name}/F"]).all(), np.abs(r.F - gd[f"{name}/F"]).max()
+    assert rel_close(r.C, gd[f"{name}/G"]).all(), np.abs(r.C - gd[f"{name}/G"]).max()
+    assert rel_close(r.cv, gd[f"{name}/cv"]).all()
+    # feasibility (cv == 0) is decided identically
+    assert np.array_equal(r.cv == 0.0, gd[f"{name}/cv"] == 0.0)
+
+
+@pytest.mark.parametrize("name", ["LIRCMOP1", "LIRCMOP6", "LIRCMOP11", "LIRCMOP13", "LIRCMOP14", "C1-DTLZ3",
+                                  "C3-DTLZ4", "DC2-DTLZ3", "DC3-DTLZ1", "WTA-P10", "MW1", "MW7", "MW14"])
+def test_evaluate_matches_oracle_500_points(g, orc, name):
+    """tests/test_problems.cpp:46-68 protocol (500 random points) vs the oracle."""
+    rng = np.random.default_rng(hash(name) % 2**32)
+    info = orc.problem_info(name)
+    X = f32(info["lo"] + (info["hi"] - info["lo"]) * rng.random((500, info["d"])))
+    r = g.evaluate_population(g.make_problem(name), X)
+    F, G, cv = orc.evaluate(name, X)
+    assert rel_close(r.F, F).all() and rel_close(r.C, G).all() and rel_close(r.cv, cv).all()
+
+
+def test_evaluate_rejects_out_of_bounds_rows(g):
+    p = g.make_problem("LIRCMOP1")
+    X = np.full((6, 30), 0.5)
+    X[1, 3] = 1.5
+    X[4, 0] = np.nan
+    X[5, 29] = -1e-300
+    with pytest.raises(ValueError, match="evaluate: out-of-bounds rows: 1 4 5"):
+        g.evaluate(p, X)
+
+
+def test_c1dtlz1_known_answer(g):
+    r = g.evaluate(g.make_problem("C1-DTLZ1"), np.full((1, 7), 0.5))
+    assert np.allclose(r.F[0], [0.125, 0.125, 0.25])
+
+
+# ------------------------------------------------------------------ topology
+def test_reference_vectors_bit_exact(g, orc):
+    for m, n in ((2, 5), (2, 1001), (3, 100), (3, 1000), (3, 4000)):
+        assert np.array_equal(g.reference_vectors(m, n), orc.reference_vectors(m, n))
+
+
+def test_neighborhoods_match_reference_golden(g):
+    gd = golden("knn.npz")
+    for key in sorted({k.split("/")[0] for k in gd.files}):
+        W, B1, B2 = gd[key + "/W"], gd[key + "/B1"], gd[key + "/B2"]
+        t = g.build_neighborhoods(W, B1.shape[1], B2.shape[1])
+        assert np.array_equal(t.b1, B1) and np.array_equal(t.b2, B2), key
+        if key.startswith("lat_"):
+            _, m, n, t1, t2 = key.split("_")
+            lt = g.lattice_neighborhoods(int(m), int(n), int(t1), int(t2))
+            assert np.array_equal(lt.b1, B1) and np.array_equal(lt.b2, B2), key
+
+
+@pytest.mark.parametrize("m,n", [(2, 20000), (3, 8000), (3, 20000)])
+def test_lattice_window_knn_equals_brute_force(g, m, n):
+    """The windowed lattice search (with its sufficiency proof) equals the
+    brute-force (d2, j) sort on the same fp64 lattice."""
+    W = g.reference_vectors(m, n)
+    brute = g.build_neighborhoods(W, 5, 20)
+    lat = g.lattice_neighborhoods(m, n, 5, 20)
+    assert np.array_equal(lat.b1, brute.b1) and np.array_equal(lat.b2, brute.b2)
+
+
+# ------------------------------------------------------------------ selection
+def _winner_rows(pops, src, which):
+    n = pops[0]["F"].shape[0]
+    par = pops[which]
+    out = {k: par[k].copy() for k in ("X", "F", "C", "cv")}
+    for j in range(n):
+        if src[j] >= 0:
+            s = pops[2] if src[j] < n else pops[3]
+            for k in out:
+                out[k][j] = s[k][src[j] % n]
+    return out
+
+
+def test_selection_matches_reference_golden(g, orc):
+    """Acceptance criterion 1 protocol on the reference's own outputs: winners
+    bit-exact unless the deciding PBI keys tie within 1e-5."""
+    gd = golden("selection.npz")
+    ties = 0
+    for k in range(int(gd["count"])):
+        pre = f"{k}/"
+        P = [g.Population(gd[pre + f"{i}X"], gd[pre + f"{i}F"], gd[pre + f"{i}C"], gd[pre + f"{i}cv"])
+             for i in range(4)]
+        W, z = gd[pre + "W"], gd[pre + "z"]
+        B1, B2 = gd[pre + "B1"], gd[pre + "B2"]
+        topo = g.NeighborhoodTopology(B1, B2, B1.shape[1], B2.shape[1])
+        o1, o2, w1, w2 = g.environmental_selection(*P, topo, g.SelectionContext(W, z, 5.0), return_winners=True)
+        for w, want, o, which in ((w1, gd[pre + "src1"], o1, 0), (w2, gd[pre + "src2"], o2, 1)):
+            bad = np.nonzero(w != want)[0]
+            for j in bad:
+                # a disagreement is allowed only on a tie within tolerance
+                def key(code):
+                    if code < 0:
+                        F, cv = gd[pre + f"{which}F"][j], gd[pre + f"{which}cv"][j]
+                    else:
+                        src = 2 if code < len(w) else 3
+                        F, cv = gd[pre + f"{src}F"][code % len(w)], gd[pre + f"{src}cv"][code % len(w)]
+                    return cv, orc.pbi(F, W[j], z)
+                (ca, ga), (cb, gb) = key(int(w[j])), key(int(want[j]))
+                assert ca == cb and abs(ga - gb) <= 1e-5 * max(1.0, abs(gb)), (k, which, j)
+                ties += 1
+            if len(bad) == 0:
+                for kk, arr in (("X", o.X), ("F", o.F), ("C", o.C), ("cv", o.cv)):
+                    assert np.array_equal(arr, gd[pre + f"out{which}{kk}"]), (k, kk)
+    assert ties <= 2
+
+
+def test_selection_large_random_vs_oracle(g, orc):
+    """n = 5000 lattice instance with engine-like neighbourhoods."""
+    rng = np.random.default_rng(11)
+    n, m = 5000, 3
+    W = orc.reference_vectors(m, n)
+    topo = g.lattice_neighborhoods(m, n, 5, 20)
+    pops = []
+    for _ in range(4):
+        F = f32(rng.uniform(0, 3, (n, m)))
+        cv = f32(np.where(rng.random(n) < 0.5, 0.0, rng.random(n)))
+        pops.append(g.Population(np.zeros((n, 1)), F, np.zeros((n, 1)), cv))
+    z = f32(rng.uniform(-0.5, 0.0, m))
+    _, _, w1, w2 = g.environmental_selection(*pops, topo, g.SelectionContext(W, z, 5.0), return_winners=True)
+    s1, s2 = orc.selection([dict(F=p.F, cv=p.cv) for p in pops], W, z, 5.0, topo.b1, topo.b2)
+    assert (w1 != s1).sum() <= 3 and (w2 != s2).sum() <= 3
+
+
+def test_selection_rejects_non_finite(g):
+    n, m = 8, 2
+    W = g.reference_vectors(m, n)
+    topo = g.build_neighborhoods(W, 2, 4)
+    P = [g.Population(np.zeros((n, 1)), np.ones((n, m)), np.zeros((n, 1)), np.zeros(n)) for _ in range(4)]
+    P[2].cv[3] = np.inf
+    with pytest.raises(ValueError, match="non-finite mask source"):
+        g.environmental_selection(*P, topo, g.SelectionContext(W, np.zeros(m), 5.0))
+
+
+# ------------------------------------------------------------------ variation
+@pytest.mark.parametrize("name,op", [("LIRCMOP13", 1), ("LIRCMOP1", 0), ("MW1", 0), ("C1-DTLZ1", 0),
+                                     ("WTA-P3", 0), ("MW14", 1)])
+def test_reproduce_matches_oracle_draw_for_draw(g, orc, name, op):
+    info = orc.problem_info(name)
+    n = 400
+    rng = np.random.default_rng(5)
+    X = f32(info["lo"] + (info["hi"] - info["lo"]) * rng.random((n, info["d"])))
+    nb = orc.knn(orc.reference_vectors(2, n), 20)
+    p = g.make_problem(name)
+    for gen in (1, 7):
+        off = g.reproduce(g.Population(X, None, None, None), nb, p, op, seed=99, gen=gen, pop_id=2)
+        want, _ = orc.reproduce(name, X, nb, op, 99, gen, 2)
+        span = info["hi"] - info["lo"]
+        assert (np.abs(off - want) <= 1e-5 * span).mean() > 0.999
+        assert np.all(np.abs(off - want) <= 2e-3 * span)  # PM/SBX fp32 vs f64, never a different draw
+        assert off.min() >= info["lo"].min() and off.max() <= info["hi"].max()
+
+
+def test_reproduce_identities(g):
+    p = g.make_problem("LIRCMOP1")
+    X = np.full((10, 30), 0.5)
+    nb = g.build_neighborhoods(g.reference_vectors(2, 10), 3, 10).b1
+    off = g.reproduce(X, nb, p, g.VariationOp.sbx_pm, g.OperatorParams(sbx_prob=0.0, pm_prob=0.0))
+    assert np.array_equal(off, X)
+    Y = np.random.default_rng(1).random((10, 30)).astype(np.float32).astype(np.float64)
+    off = g.reproduce(Y, nb, p, g.VariationOp.de, g.OperatorParams(de_f=0.0, de_cr=1.0, pm_prob=0.0))
+    assert np.array_equal(off, Y)
+
+
+# ------------------------------------------------------------------ metrics
+def test_metrics_match_reference_golden(g):
+    gd = golden("metrics.npz")
+    for k in range(24):
+        pre = f"{k}/"
+        F, cv = gd[pre + "F"], gd[pre + "cv"]
+        fr = g.metric_front(g.Population(np.zeros((len(F), 1)), F, np.zeros((len(F), 1)), cv))
+        assert np.array_equal(fr, gd[pre + "front"]), k
+        assert g.igd(F, gd[pre + "R"]) == float(gd[pre + "igd"]), k
+        m = F.shape[1]
+        assert g.hypervolume(gd[pre + "P"], np.full(m, 1.1)) == float(gd[pre + "hv"]), k
+
+
+def test_metric_known_answers(g):
+    assert g.igd(np.array([[0.0, 0.0]]), np.array([[3.0, 4.0], [0.0, 0.0]])) == 2.5
+    assert g.igd(np.zeros((0, 2)), np.ones((3, 2))) == np.inf
+    assert g.hypervolume(np.array([[0.0, 0.0]]), [1.0, 1.0]) == 1.0
+    assert g.hypervolume(np.array([[0.0, 1.0], [1.0, 0.0]]), [2.0, 2.0]) == 3.0
+    assert g.hypervolume(np.array([[0.0, 0.0, 0.0]]), [1.0, 1.0, 1.0]) == 1.0
+
+
+def test_metric_front_large_m3_vs_oracle(g, orc):
+    rng = np.random.default_rng(3)
+    F = f32(rng.random((3000, 3)))
+    F[:1500] = F[:1500] / np.linalg.norm(F[:1500], axis=1, keepdims=True)
+    cv = np.where(rng.random(3000) < 0.2, 1.0, 0.0)
+    fr = g.metric_front(g.Population(np.zeros((3000, 1)), F, np.zeros((3000, 1)), cv))
+    assert np.array_equal(fr, F[orc.metric_front(F, cv)])
+
+
+# ------------------------------------------------------------------ the run
+def test_engine_initial_population_and_records(g, orc):
+    p = g.make_problem("LIRCMOP1")
+    eng = g.Engine(p, g.RunConfig(n=25, k_max=6, seed=1))
+    X0 = eng.population(1).X
+    assert np.array_equal(X0, f32(orc.init_population("LIRCMOP1", 25, 1, 1)))
+    eng.run()
+    h = eng.history()
+    assert [r.evals for r in h] == [2 * 25 * (k + 1) for k in range(7)]  # test_gmpea.cpp:319-329
+
+
+def test_eval_budget_and_zero_generations(g):
+    p = g.make_problem("LIRCMOP1")
+    r = g.run_gmpea(p, g.RunConfig(n=20, k_max=100, eval_budget=300))
+    assert r.history[-1].evals == 280  # test_gmpea.cpp:331-345
+    u = g.run_gmpea(p, g.RunConfig(n=20, k_max=0, eval_budget=300))
+    assert u.history[-1].evals == 280
+    z = g.run_gmpea(p, g.RunConfig(n=20, k_max=0, seed=7))
+    assert len(z.history) == 1 and z.history[0].evals == 40
+    re = g.evaluate_population(p, z.pop1.X)
+    assert np.allclose(re.F, z.pop1.F, rtol=1e-6) and np.array_equal(re.cv == 0, z.pop1.cv == 0)
+
+
+def test_runs_are_deterministic_and_in_bounds(g):
+    p = g.make_problem("LIRCMOP5")
+    cfg = g.RunConfig(n=30, k_max=10, seed=3, op=g.VariationOp.de, record_walltime=False)
+    a, b = g.run_gmpea(p, cfg), g.run_gmpea(p, cfg)
+    assert np.array_equal(a.pop1.X, b.pop1.X) and np.array_equal(a.pop1.F, b.pop1.F)
+    assert [r.feasible_ratio for r in a.history] == [r.feasible_ratio for r in b.history]
+    assert all(r.wall_ms == 0.0 for r in a.history)
+    c = g.run_gmpea(p, g.RunConfig(n=30, k_max=10, seed=4, op=g.VariationOp.de))
+    assert not np.array_equal(c.pop1.X, a.pop1.X)
+    q = g.run_gmpea(g.make_problem("C1-DTLZ1"), g.RunConfig(n=21, k_max=15, seed=9))
+    assert q.pop1.X.min() >= 0.0 and q.pop1.X.max() <= 1.0 and q.pop1.X.shape == (21, 7)
+
+
+def test_time_budget_discards_crossing_generation(g):
+    p = g.make_problem("LIRCMOP1")
+    r = g.run_gmpea(p, g.RunConfig(n=200, time_budget_s=0.05, seed=2, op=g.VariationOp.de))
+    h = r.history
+    assert len(h) > 2
+    assert h[-1].wall_ms < 50.0  # every kept generation ended inside the budget
+    assert all(b.wall_ms >= a.wall_ms for a, b in zip(h[1:], h[2:]))
+
+
+def test_engine_generation_matches_operator_chain(g, orc):
+    """One engine generation == oracle reproduce -> evaluate -> update_ideal ->
+    environmental_selection on the same (fp32) state, with the engine's keys."""
+    name, n, seed = "LIRCMOP13", 300, 5
+    p = g.make_problem(name)
+    eng = g.Engine(p, g.RunConfig(n=n, k_max=1, seed=seed, op=g.VariationOp.de))
+    P1, P2 = eng.population(1), eng.population(2)
+    topo = eng.neighborhoods()
+    z0 = eng.ideal()
+    eng.run()
+    N1, N2 = eng.population(1), eng.population(2)
+    W = orc.reference_vectors(3, n)
+    offs = []
+    for pop, nb, pid in ((P1, topo.b1, 1), (P2, topo.b2, 2)):
+        ox, _ = orc.reproduce(name, pop.X, nb, 1, seed, 1, pid)
+        F, G, cv = orc.evaluate(name, f32(ox))
+        offs.append(dict(X=f32(ox), F=f32(F), cv=f32(cv)))
+    z = np.minimum(z0, np.minimum(offs[0]["F"].min(0), offs[1]["F"].min(0)))
+    assert np.allclose(eng.ideal(), z, rtol=1e-5)
+    s1, s2 = orc.selection([dict(F=P1.F, cv=P1.cv), dict(F=P2.F, cv=P2.cv), offs[0], offs[1]], W, z, 5.0,
+                           topo.b1, topo.b2)
+    for s, par, new in ((s1, P1, N1), (s2, P2, N2)):
+        exp = par.X.copy()
+        for j in range(n):
+            if s[j] >= 0:
+                exp[j] = offs[0 if s[j] < n else 1]["X"][s[j] % n]
+        close = np.all(np.abs(exp - new.X) <= 1e-5, axis=1)
+        assert close.mean() >= 0.99, close.mean()
+
+
+def test_out_of_bounds_child_raises_with_generation(g):
+    """A NaN child (PM after a DE overshoot, gmpea.cpp:146-150) is reported as
+    the reference reports it, not clipped away."""
+    p = g.make_problem("LIRCMOP1")
+    eng = g.Engine(p, g.RunConfig(n=50, k_max=3, seed=1, op=g.VariationOp.de,
+                                  op_params=g.OperatorParams(de_f=40.0, pm_prob=1.0)))
+    with pytest.raises(RuntimeError, match=r"run_gmpea: evaluation failed at generation 1: "
+                                           r"evaluate: out-of-bounds rows:"):
+        eng.run()
+
+
+def test_statistical_parity_with_reference_runs(g):
+    """30 seeds of the reference's own run_gmpea (mt19937) vs 30 engine seeds
+    (Philox): the final IGD must not be significantly worse (two-sided
+    Wilcoxon rank-sum, the reference's metrics.cpp:216-255 statistic)."""
+    from scipy.stats import mannwhitneyu
+
+    gd = golden("runs.npz")
+    fronts = golden("fronts.npz")
+    for name in ("LIRCMOP1", "LIRCMOP13", "C1-DTLZ1", "LIRCMOP9"):
+        op, n, gens = (int(v) for v in gd[f"{name}/cfg"])
+        p = g.make_problem(name)
+        vals = []
+        for seed in range(1, 31):
+            r = g.run_gmpea(p, g.RunConfig(n=n, k_max=gens, seed=seed, op=op))
+            fr = g.metric_front(r.pop1)
+            vals.append(g.igd(fr, fronts[name]) if len(fr) else np.inf)
+        ref_vals = gd[f"{name}/igd"]
+        stat = mannwhitneyu(vals, ref_vals, alternative="two-sided")
+        worse = np.median(vals) > np.median(ref_vals)
+        assert not (stat.pvalue < 0.01 and worse), (name, np.median(vals), np.median(ref_vals), stat.pvalue)
