@@ -151,6 +151,8 @@ int gmpea_engine_step(gmpea_engine* e, int64_t gens);
 int gmpea_engine_sync(gmpea_engine* e);
 int64_t gmpea_engine_effective_n(const gmpea_engine* e);
 int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, int64_t* n);
+/* the newest record only (blocks until the enqueued generations finished) */
+int gmpea_engine_last_record(gmpea_engine* e, gmpea_gen_record* out);
 int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C,
                                 double* cv);
 int gmpea_engine_ideal(gmpea_engine* e, double* z);

@@ -10,7 +10,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB = os.path.join(HERE, "libgmpea_b200.so")
+LIB = os.environ.get("GMPEA_LIB") or os.path.join(HERE, "libgmpea_b200.so")
 
 GMPEA_OK, GMPEA_EINVAL, GMPEA_ERUNTIME, GMPEA_ECUDA = 0, 1, 2, 3
 GMPEA_OP_SBX_PM, GMPEA_OP_DE = 0, 1
@@ -432,14 +432,18 @@ class Engine:
         return [GenRecord(r.gen, r.evals, r.wall_ms, r.feasible_ratio,
                           r.igd if r.has_igd else None, r.hv if r.has_hv else None) for r in buf]
 
-    def population(self, which: int = 1) -> Population:
+    def last_record(self) -> GenRecord:
+        r = _GenRecord()
+        _check(_L.gmpea_engine_last_record(self._h, C.byref(r)))
+        return GenRecord(r.gen, r.evals, r.wall_ms, r.feasible_ratio)
+
+    def population(self, which: int = 1, out: Optional[Population] = None) -> Population:
+        """pop `which` as f64 rows; `out` may supply (pinned) destination arrays."""
         n, p = self.n, self.problem
-        X = np.zeros((n, p.d))
-        F = np.zeros((n, p.m))
-        Cm = np.zeros((n, p.n_constraints))
-        cv = np.zeros(n)
-        _check(_L.gmpea_engine_get_population(self._h, which, _p(X), _p(F), _p(Cm), _p(cv)))
-        return Population(X, F, Cm, cv)
+        if out is None:
+            out = Population(np.zeros((n, p.d)), np.zeros((n, p.m)), np.zeros((n, p.n_constraints)), np.zeros(n))
+        _check(_L.gmpea_engine_get_population(self._h, which, _p(out.X), _p(out.F), _p(out.C), _p(out.cv)))
+        return out
 
     def ideal(self) -> np.ndarray:
         z = np.zeros(self.problem.m)

@@ -519,6 +519,8 @@ struct gmpea_engine {
     DevBuf<int> ustamp[2];
     DevBuf<int> bad[2];
     int* host_flag = nullptr;
+    DevBuf<double> staging;  // f64 row-major staging for population transfers
+    DevBuf<int> rowsbuf;
     int* host_flag_dev = nullptr;
 
     VaryParams vp{};
@@ -732,11 +734,13 @@ struct gmpea_engine {
         if (which != 1 && which != 2) throw std::invalid_argument("set_population: which must be 1 or 2");
         if (gens_enqueued) throw std::invalid_argument("set_population: the run has started");
         const int q = which - 1;
-        DevBuf<double> h((size_t)n * d);
+        if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
+        DevBuf<double>& h = staging;
         CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
         DevBuf<int> nbad(1);
         nbad.zero(s);
-        DevBuf<int> rows(std::max(n, 1));
+        if (rowsbuf.n < (size_t)std::max(n, 1)) rowsbuf.alloc(std::max(n, 1));
+        DevBuf<int>& rows = rowsbuf;
         to_planes_kernel<<<blocks_for((long long)n * d, 256), 256, 0, s>>>(
             h.p, n, d, pop[q].X.p, ld, prob->dlo64.p, prob->dhi64.p, rows.p, nbad.p);
         int hb = 0;
@@ -879,10 +883,32 @@ struct gmpea_engine {
         return out;
     }
 
+
+    // the newest generation record only (one small D2H; the per-step result)
+    gmpea_gen_record last_record() {
+        struct {
+            int gens_done;
+        } g{};
+        CK(cudaMemcpyAsync(&g.gens_done, &st.p->gens_done, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        DevRecord r{};
+        long long k = std::min<long long>(g.gens_done, rec_cap - 1);
+        CK(cudaMemcpyAsync(&r, rec.p + k, sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        gmpea_gen_record o{};
+        o.gen = k;
+        o.evals = 2ll * n * (k + 1);
+        o.wall_ms = cfg.record_walltime && k ? (double)r.loop_ns * 1e-6 : 0.0;
+        o.feasible_ratio = (double)r.feasible / (double)n;
+        o.igd = o.hv = std::numeric_limits<double>::quiet_NaN();
+        return o;
+    }
+
     void get_population(int which, double* X, double* F, double* C, double* cv) {
         if (which != 1 && which != 2) throw std::invalid_argument("get_population: which must be 1 or 2");
         const int q = which - 1;
-        DevBuf<double> tmp((size_t)n * std::max({d, nc, m}));
+        if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
+        DevBuf<double>& tmp = staging;
         auto pull = [&](const float* planes, int k, double* out) {
             if (!out || k == 0) return;
             from_planes_kernel<<<blocks_for((long long)n * k, 256), 256, 0, s>>>(planes, ld, n, k, tmp.p);
@@ -892,10 +918,11 @@ struct gmpea_engine {
         pull(pop[q].X.p, d, X);
         pull(pop[q].G.p, nc, C);
         if (F || cv) {
-            DevBuf<double> f((size_t)n * m), c(n);
-            fcv_to_rows_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[q].Fcv.p, n, m, f.p, c.p);
-            if (F) CK(cudaMemcpyAsync(F, f.p, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-            if (cv) CK(cudaMemcpyAsync(cv, c.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+            double* f = tmp.p;
+            double* c = tmp.p + (size_t)n * m;
+            fcv_to_rows_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[q].Fcv.p, n, m, f, c);
+            if (F) CK(cudaMemcpyAsync(F, f, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+            if (cv) CK(cudaMemcpyAsync(cv, c, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         }
     }
@@ -1466,6 +1493,13 @@ int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, in
         int64_t k = std::min<int64_t>(cap, (int64_t)h.size());
         if (out) std::copy(h.begin(), h.begin() + k, out);
         *nrec = (int64_t)h.size();
+    });
+}
+
+int gmpea_engine_last_record(gmpea_engine* e, gmpea_gen_record* out) {
+    return guarded([&] {
+        *out = e->last_record();
+        e->check_errors(-1);
     });
 }
 

@@ -181,8 +181,18 @@ __device__ __forceinline__ T warp_min(T v) {
     return v;
 }
 
+// One thread per (slot, population).  Phase 1 writes the child genes (before
+// mutation) into the offspring planes, 64 genes per window, and records which
+// genes the PM coin selects; phase 2 applies polynomial mutation + clipping
+// to the selected genes only, so a warp pays for the mutation arithmetic once
+// per mutated gene of its busiest lane instead of once per gene that any lane
+// mutates (PM picks ~1 of D genes per child); phase 3 streams the final genes
+// (coalesced re-read, L2-resident) through the problem evaluator.
+#ifndef GMPEA_VARY_MINBLOCKS
+#define GMPEA_VARY_MINBLOCKS 8
+#endif
 template <class Ev, int MODE, int OP>
-__global__ void __launch_bounds__(128) vary_eval_kernel(VaryParams p) {
+__global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
     DevState* st = p.st;
     if (st->stop) return;
     const int pi = blockIdx.y;
@@ -193,106 +203,139 @@ __global__ void __launch_bounds__(128) vary_eval_kernel(VaryParams p) {
     const unsigned gen = p.fixed_gen >= 0 ? (unsigned)p.fixed_gen : (unsigned)st->gen;
     const unsigned slot = (unsigned)(p.slot_base + i);
     const unsigned pid = (unsigned)p.pop_id[pi];
+    const float* __restrict__ lo_ = p.P.lo;
+    const float* __restrict__ hi_ = p.P.hi;
 
     double f[kMaxM] = {0.0, 0.0, 0.0};
     bool bad = false;
-    float cvf = 0.0f;
     if (active) {
-        Ev ev;
-        if (p.eval) ev.begin(p.P);
         float* __restrict__ outX = p.outX[pi];
-        const float* __restrict__ X = p.parX[pi];
-        int ia = 0, ib = 0, jrand = -1;
-        bool cross = true;
-        if (MODE == MODE_VARY) {
-            const int t = p.t[pi];
-            PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key0, p.key1, 0u, {}};
-            unsigned a = ps.index((unsigned)t);
-            unsigned b = ps.index((unsigned)t);
-            while (t > 1 && b == a) b = ps.index((unsigned)t);
-            const int* Brow = p.B[pi] + (long long)i * t;
-            ia = Brow[a];
-            ib = Brow[b];
-            if (OP == OP_SBX) {
-                u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
-                cross = u53(c.x, c.y) <= p.sbx_prob;
-            } else {
-                jrand = (int)ps.index((unsigned)d);
-            }
-        }
-        const bool de_all = p.cr_thr >= 0x100000000ull;
-        for (int jb = 0; jb < d; jb += 4) {
-            u32x4 xc{0, 0, 0, 0}, xu{0, 0, 0, 0}, mc{0, 0, 0, 0};
+        if (MODE != MODE_EVAL) {
+            const float* __restrict__ X = p.parX[pi];
+            int ia = 0, ib = 0, jrand = -1;
+            bool cross = true;
             if (MODE == MODE_VARY) {
-                const unsigned idx4 = (unsigned)(jb >> 2);
-                if (OP == OP_SBX && cross) {
-                    xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
-                    xu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), idx4, p.key0, p.key1);
-                }
-                if (OP == OP_DE && !de_all)
-                    xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
-                if (p.pm_thr >= 0)
-                    mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx4, p.key0, p.key1);
-            } else if (MODE == MODE_INIT) {
-                xc = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), p.key0, p.key1);
-                xu = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, p.key0, p.key1);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int j = jb + k;
-                if (j >= d) break;
-                const float lo = p.P.lo[j], hi = p.P.hi[j];
-                float c;
-                if (MODE == MODE_EVAL) {
-                    c = X[j * ld + i];
-                } else if (MODE == MODE_INIT) {
-                    // INIT stream: 64-bit pair (j % 2) of counter j / 2
-                    const u32x4& w = k < 2 ? xc : xu;
-                    double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
-                    c = (float)((double)lo + ((double)hi - (double)lo) * u);
+                const int t = p.t[pi];
+                PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key0, p.key1, 0u, {}};
+                unsigned a = ps.index((unsigned)t);
+                unsigned b = ps.index((unsigned)t);
+                while (t > 1 && b == a) b = ps.index((unsigned)t);
+                const int* Brow = p.B[pi] + (long long)i * t;
+                ia = Brow[a];
+                ib = Brow[b];
+                if (OP == OP_SBX) {
+                    u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
+                    cross = u53(c.x, c.y) <= p.sbx_prob;
                 } else {
-                    const float pa = X[j * ld + ia];
-                    const float pb = X[j * ld + ib];
-                    if (OP == OP_SBX) {
-                        if (cross && pick_word(xc, k) <= 0x80000000u) {
-                            const float beta = sbx_beta(pick_word(xu, k), p.sbx_e);
-                            c = 0.5f * ((1.0f + beta) * pa + (1.0f - beta) * pb);
-                        } else {
-                            c = pa;
-                        }
-                    } else {
-                        const float base = X[j * ld + i];
-                        const bool take = j == jrand || de_all ||
-                                          (unsigned long long)pick_word(xc, k) < p.cr_thr;
-                        c = take ? base + p.de_f * (pa - pb) : base;
-                    }
-                    if ((long long)pick_word(mc, k) <= p.pm_thr) {
-                        const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j,
-                                                       p.key0, p.key1);
-                        c = pm_apply(c, lo, hi, mu.x, p.pm_e1, p.pm_einv);
-                    }
-                    c = clamp_ref(c, lo, hi);
+                    jrand = (int)ps.index((unsigned)d);
                 }
-                if (!(c >= lo && c <= hi)) bad = true;  // problems.cpp:554-561
-                if (MODE != MODE_EVAL) outX[j * ld + i] = c;
-                if (p.eval) ev.gene(p.P, j, c);
+            }
+            const bool de_all = p.cr_thr >= 0x100000000ull;
+            for (int w0 = 0; w0 < d; w0 += 64) {
+                const int w1 = min(d, w0 + 64);
+                unsigned long long mmask = 0ull;
+                for (int jb = w0; jb < w1; jb += 4) {
+                    u32x4 xc{0, 0, 0, 0}, xu{0, 0, 0, 0}, mc{0, 0, 0, 0};
+                    const unsigned idx4 = (unsigned)(jb >> 2);
+                    if (MODE == MODE_VARY) {
+                        if (OP == OP_SBX && cross) {
+                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
+                            xu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), idx4, p.key0, p.key1);
+                        }
+                        if (OP == OP_DE && !de_all)
+                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
+                        if (p.pm_thr >= 0)
+                            mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx4, p.key0, p.key1);
+                    } else {  // MODE_INIT: 64-bit pair (j % 2) of counter j / 2
+                        xc = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), p.key0, p.key1);
+                        xu = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, p.key0,
+                                           p.key1);
+                    }
+                    float pa[4], pb[4], pc[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {  // issue the gathers of the group together
+                        const int j = jb + k;
+                        if (MODE == MODE_VARY && j < w1) {
+                            pa[k] = X[j * ld + ia];
+                            pb[k] = X[j * ld + ib];
+                            if (OP == OP_DE) pc[k] = X[j * ld + i];
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = jb + k;
+                        if (j >= w1) break;
+                        float c;
+                        if (MODE == MODE_INIT) {
+                            const u32x4& w = k < 2 ? xc : xu;
+                            double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
+                            const double lo = lo_[j], hi = hi_[j];
+                            c = (float)(lo + (hi - lo) * u);
+                        } else {
+                            if (OP == OP_SBX) {
+                                if (cross && pick_word(xc, k) <= 0x80000000u) {
+                                    const float beta = sbx_beta(pick_word(xu, k), p.sbx_e);
+                                    c = 0.5f * ((1.0f + beta) * pa[k] + (1.0f - beta) * pb[k]);
+                                } else {
+                                    c = pa[k];
+                                }
+                            } else {
+                                const bool take = j == jrand || de_all ||
+                                                  (unsigned long long)pick_word(xc, k) < p.cr_thr;
+                                c = take ? pc[k] + p.de_f * (pa[k] - pb[k]) : pc[k];
+                            }
+                            if ((long long)pick_word(mc, k) <= p.pm_thr)
+                                mmask |= 1ull << (j - w0);  // mutated + clipped in phase 2
+                            else
+                                c = clamp_ref(c, lo_[j], hi_[j]);
+                        }
+                        outX[j * ld + i] = c;
+                    }
+                }
+                // phase 2: polynomial mutation then clip (gmpea.cpp:202-203)
+                while (mmask) {
+                    const int j = w0 + __ffsll((long long)mmask) - 1;
+                    mmask &= mmask - 1ull;
+                    const float lo = lo_[j], hi = hi_[j];
+                    const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key0, p.key1);
+                    float c = pm_apply(outX[j * ld + i], lo, hi, mu.x, p.pm_e1, p.pm_einv);
+                    outX[j * ld + i] = clamp_ref(c, lo, hi);
+                }
             }
         }
-        if (bad) {
-            int k = atomicAdd(&st->n_bad[pi], 1);
-            if (k < p.bad_cap) p.bad_rows[pi][k] = i;
-            if (atomicCAS(&st->err, 0, ERR_EVAL_OOB) == 0) st->err_gen = (int)gen;
-        } else if (p.eval) {
-            Emitter em{p.outG[pi], ld, i, {}, 0.0, false, p.P.neq};
-            em.cv.init(p.P.nin);
-            ev.finish(p.P, f, em);
-            cvf = (float)em.result();
-            float4 o;
-            o.x = (float)f[0];
-            o.y = (float)f[1];
-            o.z = p.P.m > 2 ? (float)f[2] : 0.0f;
-            o.w = cvf;
-            p.outFcv[pi][i] = o;
+        if (p.eval) {
+            // phase 3: bounds check (problems.cpp:554-561) + streamed evaluation
+            const float* __restrict__ src = MODE == MODE_EVAL ? p.parX[pi] : outX;
+            Ev ev;
+            ev.begin(p.P);
+            for (int jb = 0; jb < d; jb += 4) {
+                float v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (jb + k < d) v[k] = src[(jb + k) * ld + i];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int j = jb + k;
+                    if (j >= d) break;
+                    if (!(v[k] >= lo_[j] && v[k] <= hi_[j])) bad = true;
+                    ev.gene(p.P, j, v[k]);
+                }
+            }
+            if (bad) {
+                int k = atomicAdd(&st->n_bad[pi], 1);
+                if (k < p.bad_cap) p.bad_rows[pi][k] = i;
+                if (atomicCAS(&st->err, 0, ERR_EVAL_OOB) == 0) st->err_gen = (int)gen;
+            } else {
+                Emitter em{p.outG[pi], ld, i, {}, 0.0, false, p.P.neq};
+                em.cv.init(p.P.nin);
+                ev.finish(p.P, f, em);
+                float4 o;
+                o.x = (float)f[0];
+                o.y = (float)f[1];
+                o.z = p.P.m > 2 ? (float)f[2] : 0.0f;
+                o.w = (float)em.result();
+                p.outFcv[pi][i] = o;
+            }
         }
     }
     if (!p.update_z || !p.eval) return;
@@ -394,8 +437,8 @@ struct SelParams {
 template <int POP>
 __device__ __forceinline__ void select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
     const float4 par = p.Fcv[POP][j];
-    const float4 u = p.U[j];
-    const float gp = pbi(par, u, z, p.theta);
+    const float4 u4 = p.U[j];
+    const float gp = pbi(par, u4, z, p.theta);
     const int deg = p.Rdeg[POP][j];
     const int* __restrict__ R = p.R[POP];
     const float4* __restrict__ eff = p.eff[POP];
@@ -406,37 +449,49 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
     int mex = 0;
     bool mex_open = true;
     bool negcv = false;
-    for (int k = 0; k < deg; ++k) {
-        const int c = R[(long long)k * p.ld + j];
-        const float4 e = eff[c];
-        const float g = pbi(e, u, z, p.theta);
-        bool mark;
-        if (POP == 0) {  // fpr_better (scalarize.cpp:91-96)
-            negcv |= (e.w < 0.0f) || (par.w < 0.0f);
-            mark = (e.w == par.w) ? (g < gp) : (e.w < par.w);
-        } else {
-            mark = g < gp;
-        }
-        if (!mark) continue;
-        // claims arrive in ascending c: the parent sits at their mex (gmpea.cpp:343-348)
-        if (mex_open) {
-            if (c == mex)
-                ++mex;
-            else if (c > mex)
-                mex_open = false;
-        }
-        bool better;
-        if (!have)
-            better = true;
-        else if (POP == 0)
-            better = e.w < best.w || (e.w == best.w && (g < bg || (g == bg && c < bc)));
-        else
-            better = g < bg || (g == bg && c < bc);
-        if (better) {
-            have = true;
-            best = e;
-            bg = g;
-            bc = c;
+    for (int k0 = 0; k0 < deg; k0 += 4) {
+        // batch the index loads and the key gathers of four claimants (ILP)
+        int cc[4];
+        float4 ee[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cc[u] = k0 + u < deg ? R[(long long)(k0 + u) * p.ld + j] : -1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (cc[u] >= 0) ee[u] = eff[cc[u]];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = cc[u];
+            if (c < 0) continue;
+            const float4 e = ee[u];
+            const float g = pbi(e, u4, z, p.theta);
+            bool mark;
+            if (POP == 0) {  // fpr_better (scalarize.cpp:91-96)
+                negcv |= (e.w < 0.0f) || (par.w < 0.0f);
+                mark = (e.w == par.w) ? (g < gp) : (e.w < par.w);
+            } else {
+                mark = g < gp;
+            }
+            if (!mark) continue;
+            // claims arrive in ascending c: the parent sits at their mex (gmpea.cpp:343-348)
+            if (mex_open) {
+                if (c == mex)
+                    ++mex;
+                else if (c > mex)
+                    mex_open = false;
+            }
+            bool better;
+            if (!have)
+                better = true;
+            else if (POP == 0)
+                better = e.w < best.w || (e.w == best.w && (g < bg || (g == bg && c < bc)));
+            else
+                better = g < bg || (g == bg && c < bc);
+            if (better) {
+                have = true;
+                best = e;
+                bg = g;
+                bc = c;
+            }
         }
     }
     if (negcv) {
@@ -475,7 +530,15 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
         p.uFcv[POP][j] = par;
         p.ustamp[POP][j] = p.st->gen;
     }
-    for (int q = 0; q < p.d; ++q) X[q * ld + j] = oX[q * ld + c];
+    for (int q0 = 0; q0 < p.d; q0 += 4) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (q0 + u < p.d) v[u] = oX[(q0 + u) * ld + c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (q0 + u < p.d) X[(q0 + u) * ld + j] = v[u];
+    }
     for (int q = 0; q < p.nc; ++q) G[q * ld + j] = oG[q * ld + c];
     p.Fcv[POP][j] = best;
 }
