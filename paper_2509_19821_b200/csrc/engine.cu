@@ -291,15 +291,16 @@ std::unique_ptr<gmpea_problem> make_problem(const std::string& name) {
 }
 
 // ---------------------------------------------------------------- layout helpers
-// row-major f64 (n x k) <-> fp32 planes (k x ld); optional f64 bounds check
-__global__ void to_planes_kernel(const double* in, long long n, int k, float* out, long long ld,
-                                 const double* lo, const double* hi, int* bad, int* nbad) {
+// row-major f64 (n x k) -> columns [0, k) of fp32 rows (stride rs floats),
+// with the reference's f64 bounds check (problems.cpp:554-568)
+__global__ void to_rows_kernel(const double* in, long long n, int k, float* out, int rs, const double* lo,
+                               const double* hi, int* bad, int* nbad) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n * k) return;
     const long long r = e / k;
     const int c = (int)(e % k);
     const double v = in[e];
-    out[(long long)c * ld + r] = (float)v;
+    out[r * rs + c] = (float)v;
     if (lo && !(v >= lo[c] && v <= hi[c])) {
         // one entry per offending row: the first failing column claims it
         bool first = true;
@@ -314,12 +315,13 @@ __global__ void to_planes_kernel(const double* in, long long n, int k, float* ou
     }
 }
 
-__global__ void from_planes_kernel(const float* in, long long ld, long long n, int k, double* out) {
+// columns [col0, col0 + k) of fp32 rows -> row-major f64 (n x k)
+__global__ void from_rows_kernel(const float* in, int rs, long long n, int col0, int k, double* out) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n * k) return;
     const long long r = e / k;
     const int c = (int)(e % k);
-    out[e] = (double)in[(long long)c * ld + r];
+    out[e] = (double)in[r * rs + col0 + c];
 }
 
 __global__ void fcv_from_rows_kernel(const double* F, const double* cv, long long n, int m, float4* out) {
@@ -371,12 +373,30 @@ __global__ void publish_stop_kernel(const DevState* st, volatile int* host_flag)
     *host_flag = st->stop | (st->err ? 2 : 0);
 }
 
+// individuals as padded fp32 rows [x | g | pad] plus packed keys
+struct RowGeom {
+    int rs4;   // row stride, float4
+    int srs4;  // shared-memory row stride (odd float4 count)
+    int bs;    // vary_eval block size
+    size_t smem;
+};
+
+RowGeom row_geom(int d, int nc) {
+    RowGeom g;
+    g.rs4 = (d + nc + 3) / 4;
+    g.srs4 = g.rs4 | 1;
+    const int per = g.srs4 * 16;
+    g.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
+    g.smem = (size_t)g.bs * per;
+    if (g.smem > 48 * 1024) throw std::invalid_argument("problem rows too wide for the engine");
+    return g;
+}
+
 struct PopBuf {
-    DevBuf<float> X, G;
+    DevBuf<float4> X;  // n rows of rs4 float4
     DevBuf<float4> Fcv;
-    void alloc(int d, int nc, long long ld) {
-        X.alloc((size_t)d * ld);
-        G.alloc((size_t)std::max(nc, 1) * ld);
+    void alloc(long long n, int rs4, long long ld) {
+        X.alloc((size_t)n * rs4);
         Fcv.alloc(ld);
     }
 };
@@ -398,6 +418,19 @@ VaryKernel vary_kernel_for(int fam, int mode, int op) {
         case FAM_WTA: return pick_vary<EvalWta>(mode, op);
         default: return pick_vary<EvalMw>(mode, op);
     }
+}
+
+void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStream_t s) {
+    const RowGeom g = [&] {
+        RowGeom r;
+        r.rs4 = vp.rs4;
+        r.srs4 = vp.srs4;
+        const int per = r.srs4 * 16;
+        r.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
+        r.smem = (size_t)r.bs * per;
+        return r;
+    }();
+    k<<<dim3(blocks_for(vp.n, g.bs), npops), g.bs, g.smem, s>>>(vp);
 }
 
 void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
@@ -502,6 +535,7 @@ struct gmpea_engine {
     gmpea_run_config cfg{};
     int n = 0, d = 0, m = 0, nc = 0, t1 = 0, t2 = 0;
     long long ld = 0, H = 0;
+    RowGeom geo{};
     cudaStream_t s = nullptr;
     bool own_stream = false;
     bool time_mode = false;
@@ -558,6 +592,7 @@ struct gmpea_engine {
         m = p->m;
         nc = p->nin + p->neq;
         ld = round_up(n, 32);
+        geo = row_geom(d, nc);
         t1 = (int)std::min<long long>(c.t1, n);
         t2 = (int)std::min<long long>(c.t2, n);
         time_mode = c.time_budget_s > 0.0;
@@ -592,14 +627,14 @@ struct gmpea_engine {
         maxdeg[1] = device_reverse(s, n, t2, B[1].p, ld, Rdeg[1], R[1]);
 
         for (int q = 0; q < 2; ++q) {
-            pop[q].alloc(d, nc, ld);
-            off[q].alloc(d, nc, ld);
+            pop[q].alloc(n, geo.rs4, ld);
+            off[q].alloc(n, geo.rs4, ld);
             eff[q].alloc(ld);
             bad[q].alloc(kMaxBadRows);
             pop[q].Fcv.zero(s);
             off[q].Fcv.zero(s);
             if (time_mode) {
-                undo[q].alloc(d, nc, ld);
+                undo[q].alloc(n, geo.rs4, ld);
                 ustamp[q].alloc(ld);
                 CK(cudaMemsetAsync(ustamp[q].p, 0xff, ld * sizeof(int), s));
             }
@@ -612,9 +647,9 @@ struct gmpea_engine {
         // kernel parameter blocks
         vp = VaryParams{};
         vp.n = n;
-        vp.ld = (int)ld;
+        vp.rs4 = geo.rs4;
+        vp.srs4 = geo.srs4;
         vp.slot_base = 0;
-        vp.npops = 2;
         vp.pop_id[0] = 1;
         vp.pop_id[1] = 2;
         vp.P = p->dev;
@@ -636,21 +671,19 @@ struct gmpea_engine {
         // initial populations (gmpea.cpp:430-437): Philox INIT stream
         for (int q = 0; q < 2; ++q) {
             vp.parX[q] = pop[q].X.p;
-            vp.outX[q] = pop[q].X.p;
-            vp.outG[q] = pop[q].G.p;
+            vp.out[q] = pop[q].X.p;
             vp.outFcv[q] = pop[q].Fcv.p;
         }
         VaryParams ip = vp;
         ip.fixed_gen = 0;
-        vary_kernel_for(p->fam, MODE_INIT, 0)<<<dim3(blocks_for(n, 128), 2), 128, 0, s>>>(ip);
+        launch_vary(vary_kernel_for(p->fam, MODE_INIT, 0), ip, 2, s);
         CK(cudaGetLastError());
         finish_init();
 
         // generation parameter blocks
         for (int q = 0; q < 2; ++q) {
             vp.parX[q] = pop[q].X.p;
-            vp.outX[q] = off[q].X.p;
-            vp.outG[q] = off[q].G.p;
+            vp.out[q] = off[q].X.p;
             vp.outFcv[q] = off[q].Fcv.p;
         }
         vary = vary_kernel_for(p->fam, MODE_VARY, c.op);
@@ -658,18 +691,15 @@ struct gmpea_engine {
                          srcbits.p, st.p};
         sp = SelParams{};
         sp.n = n;
-        sp.ld = (int)ld;
-        sp.d = d;
-        sp.nc = nc;
+        sp.rs4 = geo.rs4;
+        sp.ldr = ld;
         sp.m = m;
         sp.theta = (float)c.theta;
         sp.U = U.p;
         for (int q = 0; q < 2; ++q) {
             sp.X[q] = pop[q].X.p;
-            sp.G[q] = pop[q].G.p;
             sp.Fcv[q] = pop[q].Fcv.p;
             sp.oX[q] = off[q].X.p;
-            sp.oG[q] = off[q].G.p;
             sp.oFcv[q] = off[q].Fcv.p;
             sp.eff[q] = eff[q].p;
             sp.R[q] = R[q].p;
@@ -677,14 +707,11 @@ struct gmpea_engine {
             sp.winner[q] = nullptr;
             if (time_mode) {
                 sp.uX[q] = undo[q].X.p;
-                sp.uG[q] = undo[q].G.p;
                 sp.uFcv[q] = undo[q].Fcv.p;
                 sp.ustamp[q] = ustamp[q].p;
                 rp.X[q] = pop[q].X.p;
-                rp.G[q] = pop[q].G.p;
                 rp.Fcv[q] = pop[q].Fcv.p;
                 rp.uX[q] = undo[q].X.p;
-                rp.uG[q] = undo[q].G.p;
                 rp.uFcv[q] = undo[q].Fcv.p;
                 rp.ustamp[q] = ustamp[q].p;
             }
@@ -694,9 +721,7 @@ struct gmpea_engine {
         sp.st = st.p;
         sp.rec = rec.p;
         rp.n = n;
-        rp.ld = (int)ld;
-        rp.d = d;
-        rp.nc = nc;
+        rp.rs4 = geo.rs4;
         rp.st = st.p;
         CK(cudaStreamSynchronize(s));
         check_errors(0);
@@ -741,8 +766,8 @@ struct gmpea_engine {
         nbad.zero(s);
         if (rowsbuf.n < (size_t)std::max(n, 1)) rowsbuf.alloc(std::max(n, 1));
         DevBuf<int>& rows = rowsbuf;
-        to_planes_kernel<<<blocks_for((long long)n * d, 256), 256, 0, s>>>(
-            h.p, n, d, pop[q].X.p, ld, prob->dlo64.p, prob->dhi64.p, rows.p, nbad.p);
+        to_rows_kernel<<<blocks_for((long long)n * d, 256), 256, 0, s>>>(
+            h.p, n, d, (float*)pop[q].X.p, geo.rs4 * 4, prob->dlo64.p, prob->dhi64.p, rows.p, nbad.p);
         int hb = 0;
         CK(cudaMemcpyAsync(&hb, nbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -752,21 +777,19 @@ struct gmpea_engine {
             throw std::invalid_argument(rows_message(r));
         }
         VaryParams ep = vp;
-        ep.npops = 1;
         ep.parX[0] = pop[q].X.p;
-        ep.outX[0] = pop[q].X.p;
-        ep.outG[0] = pop[q].G.p;
+        ep.out[0] = pop[q].X.p;
         ep.outFcv[0] = pop[q].Fcv.p;
         ep.update_z = 0;
         ep.fixed_gen = 0;
-        vary_kernel_for(prob->fam, MODE_EVAL, 0)<<<dim3(blocks_for(n, 128), 1), 128, 0, s>>>(ep);
+        launch_vary(vary_kernel_for(prob->fam, MODE_EVAL, 0), ep, 1, s);
         CK(cudaGetLastError());
         finish_init();
         CK(cudaStreamSynchronize(s));
     }
 
     void enqueue_generation() {
-        vary<<<dim3(blocks_for(n, 128), 2), 128, 0, s>>>(vp);
+        launch_vary(vary, vp, 2, s);
         op1_kernel<<<blocks_for(n, 256), 256, 0, s>>>(op1p);
         select_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(sp);
         end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
@@ -909,14 +932,15 @@ struct gmpea_engine {
         const int q = which - 1;
         if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
         DevBuf<double>& tmp = staging;
-        auto pull = [&](const float* planes, int k, double* out) {
+        auto pull = [&](int col0, int k, double* out) {
             if (!out || k == 0) return;
-            from_planes_kernel<<<blocks_for((long long)n * k, 256), 256, 0, s>>>(planes, ld, n, k, tmp.p);
+            from_rows_kernel<<<blocks_for((long long)n * k, 256), 256, 0, s>>>((const float*)pop[q].X.p,
+                                                                              geo.rs4 * 4, n, col0, k, tmp.p);
             CK(cudaMemcpyAsync(out, tmp.p, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         };
-        pull(pop[q].X.p, d, X);
-        pull(pop[q].G.p, nc, C);
+        pull(0, d, X);
+        pull(d, nc, C);
         if (F || cv) {
             double* f = tmp.p;
             double* c = tmp.p + (size_t)n * m;
@@ -936,7 +960,7 @@ struct gmpea_engine {
         for (long long g = 0; g < gens; ++g) {
             cudaEvent_t* e = &ev[5 * g];
             CK(cudaEventRecord(e[0], s));
-            vary<<<dim3(blocks_for(n, 128), 2), 128, 0, s>>>(vp);
+            launch_vary(vary, vp, 2, s);
             CK(cudaEventRecord(e[1], s));
             op1_kernel<<<blocks_for(n, 256), 256, 0, s>>>(op1p);
             CK(cudaEventRecord(e[2], s));
@@ -1057,12 +1081,13 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         } sg{s};
         DevBuf<double> h((size_t)n * d);
         CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
+        const RowGeom geo = row_geom(d, nc);
         PopBuf pb;
-        pb.alloc(d, nc, ld);
+        pb.alloc(n, geo.rs4, ld);
         DevBuf<int> rows(n), nbad(1);
         nbad.zero(s);
-        to_planes_kernel<<<blocks_for(n * d, 256), 256, 0, s>>>(h.p, n, d, pb.X.p, ld, p->dlo64.p, p->dhi64.p,
-                                                               rows.p, nbad.p);
+        to_rows_kernel<<<blocks_for(n * d, 256), 256, 0, s>>>(h.p, n, d, (float*)pb.X.p, geo.rs4 * 4, p->dlo64.p,
+                                                             p->dhi64.p, rows.p, nbad.p);
         int hb = 0;
         CK(cudaMemcpyAsync(&hb, nbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1076,20 +1101,19 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         DevBuf<int> bad(n);
         VaryParams ep{};
         ep.n = (int)n;
-        ep.ld = (int)ld;
-        ep.npops = 1;
+        ep.rs4 = geo.rs4;
+        ep.srs4 = geo.srs4;
         ep.pop_id[0] = 1;
         ep.P = p->dev;
         ep.parX[0] = pb.X.p;
-        ep.outX[0] = pb.X.p;
-        ep.outG[0] = pb.G.p;
+        ep.out[0] = pb.X.p;
         ep.outFcv[0] = pb.Fcv.p;
         ep.eval = 1;
         ep.fixed_gen = 0;
         ep.st = st.p;
         ep.bad_rows[0] = bad.p;
         ep.bad_cap = (int)n;
-        vary_kernel_for(p->fam, MODE_EVAL, 0)<<<dim3(blocks_for(n, 128), 1), 128, 0, s>>>(ep);
+        launch_vary(vary_kernel_for(p->fam, MODE_EVAL, 0), ep, 1, s);
         CK(cudaGetLastError());
         DevBuf<double> out((size_t)n * std::max({m, nc, 1}));
         DevBuf<double> c(n);
@@ -1098,7 +1122,8 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         if (cv) CK(cudaMemcpyAsync(cv, c.p, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (G && nc) {
-            from_planes_kernel<<<blocks_for(n * nc, 256), 256, 0, s>>>(pb.G.p, ld, n, nc, out.p);
+            from_rows_kernel<<<blocks_for(n * nc, 256), 256, 0, s>>>((const float*)pb.X.p, geo.rs4 * 4, n, d, nc,
+                                                                    out.p);
             CK(cudaMemcpyAsync(G, out.p, (size_t)n * nc * sizeof(double), cudaMemcpyDeviceToHost, s));
         }
         CK(cudaStreamSynchronize(s));
@@ -1164,14 +1189,14 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         if (t <= 0) throw std::invalid_argument("reproduce: topology/population mismatch");
         if (op != GMPEA_OP_SBX_PM && op != GMPEA_OP_DE) throw std::invalid_argument("reproduce: unknown operator");
         CK(cudaSetDevice(p->device));
-        const int d = p->d;
-        const long long ld = round_up(n, 32);
+        const int d = p->d, nc = p->nin + p->neq;
+        const RowGeom geo = row_geom(d, nc);
         cudaStream_t s = 0;
         DevBuf<double> h((size_t)n * d);
         CK(cudaMemcpy(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice));
-        DevBuf<float> Xp((size_t)d * ld), Op((size_t)d * ld);
-        to_planes_kernel<<<blocks_for(n * d, 256), 256>>>(h.p, n, d, Xp.p, ld, nullptr, nullptr, nullptr,
-                                                          nullptr);
+        DevBuf<float4> Xp((size_t)n * geo.rs4), Op((size_t)n * geo.rs4);
+        to_rows_kernel<<<blocks_for(n * d, 256), 256>>>(h.p, n, d, (float*)Xp.p, geo.rs4 * 4, nullptr, nullptr,
+                                                        nullptr, nullptr);
         DevBuf<unsigned> bu((size_t)n * t);
         DevBuf<int> bi((size_t)n * t), err(1);
         err.zero(s);
@@ -1185,14 +1210,14 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         DevBuf<int> bad(1);
         VaryParams vp{};
         vp.n = (int)n;
-        vp.ld = (int)ld;
-        vp.npops = 1;
+        vp.rs4 = geo.rs4;
+        vp.srs4 = geo.srs4;
         vp.pop_id[0] = (int)pop;
         vp.P = p->dev;
         vp.parX[0] = Xp.p;
         vp.B[0] = bi.p;
         vp.t[0] = t;
-        vp.outX[0] = Op.p;
+        vp.out[0] = Op.p;
         vp.key0 = (unsigned)seed;
         vp.key1 = (unsigned)(seed >> 32);
         gmpea_operator_params prm;
@@ -1204,9 +1229,9 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.st = st.p;
         vp.bad_rows[0] = bad.p;
         vp.bad_cap = 0;  // reproduce itself never throws on bounds
-        vary_kernel_for(p->fam, MODE_VARY, op)<<<dim3(blocks_for(n, 128), 1), 128>>>(vp);
+        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op), vp, 1, s);
         CK(cudaGetLastError());
-        from_planes_kernel<<<blocks_for(n * d, 256), 256>>>(Op.p, ld, n, d, h.p);
+        from_rows_kernel<<<blocks_for(n * d, 256), 256>>>((const float*)Op.p, geo.rs4 * 4, n, 0, d, h.p);
         CK(cudaMemcpy(off, h.p, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
@@ -1269,9 +1294,7 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
         win[1].alloc(n);
         SelParams sp{};
         sp.n = (int)n;
-        sp.ld = (int)ld;
-        sp.d = d;
-        sp.nc = nc;
+        sp.ldr = ld;
         sp.m = m;
         sp.theta = (float)theta;
         sp.U = U.p;

@@ -3,8 +3,9 @@
 //   vary_eval  : reproduce x2 (gmpea.cpp:463-464, :113-206) fused with
 //                evaluate_population x2 (:467-468, problems.cpp:552-573) and the
 //                ideal-point partial min (update_ideal, :474-475).  One thread
-//                per (slot, population); the child is produced and evaluated
-//                gene by gene, written once as fp32 SoA planes.
+//                per (slot, population); the child row is built in shared
+//                memory, evaluated there, and the block's rows leave as one
+//                contiguous, fully coalesced store.
 //   op1        : offspring cooperation (gmpea.cpp:248-279) as two bits per
 //                slot plus the packed keys of the row each stream keeps.
 //   select     : OP2 update indexing + OP3 elite update (gmpea.cpp:283-390) as
@@ -12,9 +13,13 @@
 //                slot j visits every offspring c with j in B[c], recomputes the
 //                mark of (c, j) and keeps the lexicographic argmin of the
 //                claimants; the winner row is copied into slot j in place
-//                (one writer per slot, race-free; parents' other rows are never
-//                read by this kernel).
+//                (one writer per slot, race-free; no other parent row is read).
 //   end_gen    : loop time / budget bookkeeping (gmpea.cpp:458-488).
+//
+// Individuals are stored as padded rows  [x_0 .. x_{d-1} | g_0 .. g_{nc-1} | pad]
+// of rs4 float4 (LIRCMOP13: 30 + 2 floats = one 128 B line), so a parent or
+// winner row is one cache line instead of d separate sectors; the selection
+// keys live apart as packed float4 {f0, f1, f2, cv} per slot.
 #pragma once
 #include "common.cuh"
 #include "problems.cuh"
@@ -25,16 +30,16 @@ enum : int { OP_SBX = 0, OP_DE = 1 };
 enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
 
 struct VaryParams {
-    int n, ld;               // slots per population, plane leading dimension
+    int n;                   // slots per population
+    int rs4;                 // row stride (float4)
+    int srs4;                // shared-memory row stride (float4, odd: bank-conflict free)
     int slot_base;           // global slot index of local row 0 (sharding)
-    int npops;               // 1 or 2 populations in blockIdx.y
     int pop_id[2];           // Philox population id (1 or 2) per blockIdx.y
     ProbDev P;
-    const float* parX[2];    // parent planes (MODE_VARY) / input planes (MODE_EVAL)
+    const float4* parX[2];   // parent rows (MODE_VARY) / input rows (MODE_EVAL)
     const int* B[2];         // neighbourhood rows (local indices), row-major
     int t[2];
-    float* outX[2];
-    float* outG[2];
+    float4* out[2];          // output rows (x | g)
     float4* outFcv[2];
     unsigned key0, key1;     // Philox key (seed)
     double sbx_prob;         // SBX per-child coin threshold on the 53-bit uniform
@@ -78,18 +83,16 @@ struct CvAcc {
     }
 };
 
-// Emits raw constraints into the G planes and folds them into cv in the
+// Emits raw constraints into the row's g part and folds them into cv in the
 // reference's order.  For the tail we need s = lanes; s += t_k (in order), so
 // the running lane total is materialised when the first tail term arrives.
 struct Emitter {
     float* G;
-    long long ld, i;
     CvAcc cv;
     double s;
     bool s_ready;
-    int neq;
     __device__ __forceinline__ void operator()(int k, double g) {
-        G[(long long)k * ld + i] = (float)g;
+        G[k] = (float)g;
         if (k < cv.blocked) {
             cv.add(k, g);
         } else {
@@ -181,38 +184,48 @@ __device__ __forceinline__ T warp_min(T v) {
     return v;
 }
 
-// One thread per (slot, population).  Phase 1 writes the child genes (before
-// mutation) into the offspring planes, 64 genes per window, and records which
-// genes the PM coin selects; phase 2 applies polynomial mutation + clipping
-// to the selected genes only, so a warp pays for the mutation arithmetic once
-// per mutated gene of its busiest lane instead of once per gene that any lane
-// mutates (PM picks ~1 of D genes per child); phase 3 streams the final genes
-// (coalesced re-read, L2-resident) through the problem evaluator.
+// One thread per (slot, population); block rows are staged in shared memory.
+// Phase 1 writes the child genes (before mutation), 64 genes per window, and
+// records which genes the PM coin selects; phase 2 applies polynomial
+// mutation + clipping to those genes only, so a warp pays for the mutation
+// arithmetic once per mutated gene of its busiest lane instead of once per
+// gene that any lane mutates (PM picks ~1 of d genes per child); phase 3
+// streams the final genes through the problem evaluator; phase 4 stores the
+// block's rows as one contiguous coalesced copy.
 #ifndef GMPEA_VARY_MINBLOCKS
 #define GMPEA_VARY_MINBLOCKS 8
 #endif
 template <class Ev, int MODE, int OP>
 __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
+    extern __shared__ float4 sm4[];
     DevState* st = p.st;
     if (st->stop) return;
     const int pi = blockIdx.y;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int tid = threadIdx.x;
+    const int i0 = blockIdx.x * blockDim.x;
+    const int i = i0 + tid;
     const bool active = i < p.n;
     const int d = p.P.d;
-    const long long ld = p.ld;
+    const int rs4 = p.rs4;
     const unsigned gen = p.fixed_gen >= 0 ? (unsigned)p.fixed_gen : (unsigned)st->gen;
     const unsigned slot = (unsigned)(p.slot_base + i);
     const unsigned pid = (unsigned)p.pop_id[pi];
     const float* __restrict__ lo_ = p.P.lo;
     const float* __restrict__ hi_ = p.P.hi;
+    float4* my4 = sm4 + tid * p.srs4;
+    float* my = reinterpret_cast<float*>(my4);
 
     double f[kMaxM] = {0.0, 0.0, 0.0};
     bool bad = false;
     if (active) {
-        float* __restrict__ outX = p.outX[pi];
-        if (MODE != MODE_EVAL) {
-            const float* __restrict__ X = p.parX[pi];
-            int ia = 0, ib = 0, jrand = -1;
+        if (MODE == MODE_EVAL) {
+            const float4* __restrict__ row = p.parX[pi] + (long long)i * rs4;
+            for (int q = 0; q < rs4; ++q) my4[q] = row[q];
+        } else {
+            const float4* __restrict__ PA = p.parX[pi];
+            const float4* __restrict__ PB = p.parX[pi];
+            const float4* __restrict__ PC = p.parX[pi] + (long long)i * rs4;
+            int jrand = -1;
             bool cross = true;
             if (MODE == MODE_VARY) {
                 const int t = p.t[pi];
@@ -221,8 +234,8 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                 unsigned b = ps.index((unsigned)t);
                 while (t > 1 && b == a) b = ps.index((unsigned)t);
                 const int* Brow = p.B[pi] + (long long)i * t;
-                ia = Brow[a];
-                ib = Brow[b];
+                PA += (long long)Brow[a] * rs4;
+                PB += (long long)Brow[b] * rs4;
                 if (OP == OP_SBX) {
                     u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
                     cross = u53(c.x, c.y) <= p.sbx_prob;
@@ -235,9 +248,29 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                 const int w1 = min(d, w0 + 64);
                 unsigned long long mmask = 0ull;
                 for (int jb = w0; jb < w1; jb += 4) {
+                    const int q = jb >> 2;
                     u32x4 xc{0, 0, 0, 0}, xu{0, 0, 0, 0}, mc{0, 0, 0, 0};
-                    const unsigned idx4 = (unsigned)(jb >> 2);
-                    if (MODE == MODE_VARY) {
+                    float4 out;
+                    if (MODE == MODE_INIT) {  // 64-bit pair (j % 2) of counter j / 2
+                        xc = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), p.key0, p.key1);
+                        xu = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, p.key0,
+                                           p.key1);
+                        float v[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int j = jb + k;
+                            if (j >= w1) {
+                                v[k] = 0.0f;
+                                continue;
+                            }
+                            const u32x4& w = k < 2 ? xc : xu;
+                            const double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
+                            const double lo = lo_[j], hi = hi_[j];
+                            v[k] = (float)(lo + (hi - lo) * u);
+                        }
+                        out = make_float4(v[0], v[1], v[2], v[3]);
+                    } else {
+                        const unsigned idx4 = (unsigned)q;
                         if (OP == OP_SBX && cross) {
                             xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
                             xu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), idx4, p.key0, p.key1);
@@ -246,51 +279,41 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                             xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
                         if (p.pm_thr >= 0)
                             mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx4, p.key0, p.key1);
-                    } else {  // MODE_INIT: 64-bit pair (j % 2) of counter j / 2
-                        xc = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), p.key0, p.key1);
-                        xu = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, p.key0,
-                                           p.key1);
-                    }
-                    float pa[4], pb[4], pc[4];
+                        const float4 a4 = PA[q], b4 = PB[q];
+                        const float4 c4 = OP == OP_DE ? PC[q] : a4;
+                        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+                        const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+                        const float cvv[4] = {c4.x, c4.y, c4.z, c4.w};
+                        float v[4];
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {  // issue the gathers of the group together
-                        const int j = jb + k;
-                        if (MODE == MODE_VARY && j < w1) {
-                            pa[k] = X[j * ld + ia];
-                            pb[k] = X[j * ld + ib];
-                            if (OP == OP_DE) pc[k] = X[j * ld + i];
-                        }
-                    }
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int j = jb + k;
-                        if (j >= w1) break;
-                        float c;
-                        if (MODE == MODE_INIT) {
-                            const u32x4& w = k < 2 ? xc : xu;
-                            double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
-                            const double lo = lo_[j], hi = hi_[j];
-                            c = (float)(lo + (hi - lo) * u);
-                        } else {
+                        for (int k = 0; k < 4; ++k) {
+                            const int j = jb + k;
+                            if (j >= w1) {
+                                v[k] = 0.0f;
+                                continue;
+                            }
+                            float c;
                             if (OP == OP_SBX) {
                                 if (cross && pick_word(xc, k) <= 0x80000000u) {
                                     const float beta = sbx_beta(pick_word(xu, k), p.sbx_e);
-                                    c = 0.5f * ((1.0f + beta) * pa[k] + (1.0f - beta) * pb[k]);
+                                    c = 0.5f * ((1.0f + beta) * av[k] + (1.0f - beta) * bv[k]);
                                 } else {
-                                    c = pa[k];
+                                    c = av[k];
                                 }
                             } else {
                                 const bool take = j == jrand || de_all ||
                                                   (unsigned long long)pick_word(xc, k) < p.cr_thr;
-                                c = take ? pc[k] + p.de_f * (pa[k] - pb[k]) : pc[k];
+                                c = take ? cvv[k] + p.de_f * (av[k] - bv[k]) : cvv[k];
                             }
                             if ((long long)pick_word(mc, k) <= p.pm_thr)
                                 mmask |= 1ull << (j - w0);  // mutated + clipped in phase 2
                             else
                                 c = clamp_ref(c, lo_[j], hi_[j]);
+                            v[k] = c;
                         }
-                        outX[j * ld + i] = c;
+                        out = make_float4(v[0], v[1], v[2], v[3]);
                     }
+                    my4[q] = out;
                 }
                 // phase 2: polynomial mutation then clip (gmpea.cpp:202-203)
                 while (mmask) {
@@ -298,21 +321,17 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                     mmask &= mmask - 1ull;
                     const float lo = lo_[j], hi = hi_[j];
                     const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key0, p.key1);
-                    float c = pm_apply(outX[j * ld + i], lo, hi, mu.x, p.pm_e1, p.pm_einv);
-                    outX[j * ld + i] = clamp_ref(c, lo, hi);
+                    my[j] = clamp_ref(pm_apply(my[j], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
                 }
             }
         }
         if (p.eval) {
             // phase 3: bounds check (problems.cpp:554-561) + streamed evaluation
-            const float* __restrict__ src = MODE == MODE_EVAL ? p.parX[pi] : outX;
             Ev ev;
             ev.begin(p.P);
             for (int jb = 0; jb < d; jb += 4) {
-                float v[4];
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (jb + k < d) v[k] = src[(jb + k) * ld + i];
+                const float4 v4 = my4[jb >> 2];
+                const float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int j = jb + k;
@@ -326,7 +345,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                 if (k < p.bad_cap) p.bad_rows[pi][k] = i;
                 if (atomicCAS(&st->err, 0, ERR_EVAL_OOB) == 0) st->err_gen = (int)gen;
             } else {
-                Emitter em{p.outG[pi], ld, i, {}, 0.0, false, p.P.neq};
+                Emitter em{my + d, {}, 0.0, false};
                 em.cv.init(p.P.nin);
                 ev.finish(p.P, f, em);
                 float4 o;
@@ -336,6 +355,17 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                 o.w = (float)em.result();
                 p.outFcv[pi][i] = o;
             }
+        }
+    }
+    // phase 4: rows [i0, i0 + rows) leave as one contiguous, coalesced copy
+    __syncthreads();
+    {
+        const int rows = min((int)blockDim.x, p.n - i0);
+        const int total = rows * rs4;
+        float4* __restrict__ dst = p.out[pi] + (long long)i0 * rs4;
+        for (int e = tid; e < total; e += blockDim.x) {
+            const int r = e / rs4;
+            dst[e] = sm4[r * p.srs4 + (e - r * rs4)];
         }
     }
     if (!p.update_z || !p.eval) return;
@@ -410,29 +440,39 @@ __global__ void __launch_bounds__(256) op1_kernel(Op1Params p) {
 }
 
 struct SelParams {
-    int n, ld, d, nc, m;
+    int n, rs4, m;
     float theta;
     const float4* U;
-    float* X[2];
-    float* G[2];
+    float4* X[2];        // parent rows, updated in place
     float4* Fcv[2];
-    const float* oX[2];
-    const float* oG[2];
+    const float4* oX[2]; // offspring rows
     const float4* oFcv[2];
     const float4* eff[2];
     const unsigned char* srcbits;
-    const int* R[2];     // reverse neighbourhood, R[k*ld + j] ascending in k
+    const int* R[2];     // reverse neighbourhood, R[k*ldr + j] ascending in k
     const int* Rdeg[2];
+    long long ldr;
     int* winner[2];      // optional: -1 parent, c: off1 row c, n + c: off2 row c
     int apply;           // copy winner rows into the parents
     // undo log for the time budget (gmpea.cpp:481-486)
-    float* uX[2];
-    float* uG[2];
+    float4* uX[2];
     float4* uFcv[2];
     int* ustamp[2];
     DevState* st;
     DevRecord* rec;      // optional: feasible count of pop1 for this generation
 };
+
+__device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4* __restrict__ src, int rs4) {
+    for (int q0 = 0; q0 < rs4; q0 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (q0 + u < rs4) v[u] = src[q0 + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (q0 + u < rs4) dst[q0 + u] = v[u];
+    }
+}
 
 template <int POP>
 __device__ __forceinline__ void select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
@@ -454,7 +494,7 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
         int cc[4];
         float4 ee[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cc[u] = k0 + u < deg ? R[(long long)(k0 + u) * p.ld + j] : -1;
+        for (int u = 0; u < 4; ++u) cc[u] = k0 + u < deg ? R[(long long)(k0 + u) * p.ldr + j] : -1;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (cc[u] >= 0) ee[u] = eff[cc[u]];
@@ -516,30 +556,13 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
     feas = (off_wins ? best.w : par.w) == 0.0f;
     if (!off_wins || !p.apply) return;
     const int src = code >= p.n ? 1 : 0;
-    const int c = bc;
-    const long long ld = p.ld;
-    float* __restrict__ X = p.X[POP];
-    float* __restrict__ G = p.G[POP];
-    const float* __restrict__ oX = p.oX[src];
-    const float* __restrict__ oG = p.oG[src];
+    float4* dst = p.X[POP] + (long long)j * p.rs4;
     if (p.ustamp[POP]) {
-        float* __restrict__ uX = p.uX[POP];
-        float* __restrict__ uG = p.uG[POP];
-        for (int q = 0; q < p.d; ++q) uX[q * ld + j] = X[q * ld + j];
-        for (int q = 0; q < p.nc; ++q) uG[q * ld + j] = G[q * ld + j];
+        copy_row(p.uX[POP] + (long long)j * p.rs4, dst, p.rs4);
         p.uFcv[POP][j] = par;
         p.ustamp[POP][j] = p.st->gen;
     }
-    for (int q0 = 0; q0 < p.d; q0 += 4) {
-        float v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (q0 + u < p.d) v[u] = oX[(q0 + u) * ld + c];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (q0 + u < p.d) X[(q0 + u) * ld + j] = v[u];
-    }
-    for (int q = 0; q < p.nc; ++q) G[q * ld + j] = oG[q * ld + c];
+    copy_row(dst, p.oX[src] + (long long)bc * p.rs4, p.rs4);  // copy_row, gmpea.cpp:372-377
     p.Fcv[POP][j] = best;
 }
 
@@ -586,12 +609,10 @@ __global__ void end_gen_kernel(DevState* st, DevRecord* rec) {
 __global__ void mark_start_kernel(DevState* st) { st->t_gen_start = globaltimer(); }
 
 struct RestoreParams {
-    int n, ld, d, nc;
-    float* X[2];
-    float* G[2];
+    int n, rs4;
+    float4* X[2];
     float4* Fcv[2];
-    const float* uX[2];
-    const float* uG[2];
+    const float4* uX[2];
     const float4* uFcv[2];
     const int* ustamp[2];
     DevState* st;
@@ -602,9 +623,7 @@ __global__ void restore_kernel(RestoreParams p) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int q = blockIdx.y;
     if (j >= p.n || p.ustamp[q][j] != p.st->gen) return;
-    const long long ld = p.ld;
-    for (int k = 0; k < p.d; ++k) p.X[q][k * ld + j] = p.uX[q][k * ld + j];
-    for (int k = 0; k < p.nc; ++k) p.G[q][k * ld + j] = p.uG[q][k * ld + j];
+    copy_row(p.X[q] + (long long)j * p.rs4, p.uX[q] + (long long)j * p.rs4, p.rs4);
     p.Fcv[q][j] = p.uFcv[q][j];
 }
 
