@@ -167,6 +167,11 @@ struct gmpea_problem {
         dev.neq = neq;
         dev.lo = dlo.p;
         dev.hi = dhi.p;
+        dev.uniform = 1;
+        for (int j = 0; j < d; ++j)
+            if (lo[j] != lo[0] || hi[j] != hi[0]) dev.uniform = 0;
+        dev.ulo = d ? (float)lo[0] : 0.0f;
+        dev.uhi = d ? (float)hi[0] : 0.0f;
         // the reference evaluates these with glibc at run time; volatile keeps
         // the host compiler from folding them with a different rounding
         volatile double th = -0.25 * kPi, al = 0.25 * kPi;

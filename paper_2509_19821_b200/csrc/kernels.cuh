@@ -184,6 +184,51 @@ __device__ __forceinline__ T warp_min(T v) {
     return v;
 }
 
+// Warp-cooperative polynomial mutation.  Every lane holds a 64-bit mask of
+// the genes [w0, w0 + 64) its child mutates; the warp numbers all tasks by an
+// exclusive scan of the mask popcounts and, round by round, the owners post
+// 32 tasks to shared memory and lane k runs task k on the owner's staged row
+// with the owner's Philox key.  Must be reached by all lanes of the warp.
+template <class VP>
+__device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, int w0, float4* sm4,
+                                         unsigned gen, unsigned pid, int i0) {
+    __shared__ unsigned task[4][32];  // (owner lane << 16) | gene
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int cnt = __popcll(mmask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    const int excl = incl - cnt;
+    for (int r0 = 0; r0 < total; r0 += 32) {
+        // post my tasks with global index in [r0, r0 + 32)
+        if (excl < r0 + 32 && incl > r0) {
+            unsigned long long mm = mmask;
+            for (int t = excl; t < incl && t < r0 + 32; ++t) {
+                const int b = __ffsll((long long)mm) - 1;
+                mm &= mm - 1ull;
+                if (t >= r0) task[wid][t - r0] = ((unsigned)lane << 16) | (unsigned)(w0 + b);
+            }
+        }
+        __syncwarp();
+        if (r0 + lane < total) {
+            const unsigned tk = task[wid][lane];
+            const int owner = (int)(tk >> 16), j = (int)(tk & 0xffffu);
+            const int row = wid * 32 + owner;
+            float* x = reinterpret_cast<float*>(sm4 + row * p.srs4);
+            const unsigned slot = (unsigned)(p.slot_base + i0 + row);
+            const float lo = p.P.lob(j), hi = p.P.hib(j);
+            const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key0, p.key1);
+            x[j] = clamp_ref(pm_apply(x[j], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
+        }
+        __syncwarp();
+    }
+}
+
 // One thread per (slot, population); block rows are staged in shared memory.
 // Phase 1 writes the child genes (before mutation), 64 genes per window, and
 // records which genes the PM coin selects; phase 2 applies polynomial
@@ -210,24 +255,27 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
     const unsigned gen = p.fixed_gen >= 0 ? (unsigned)p.fixed_gen : (unsigned)st->gen;
     const unsigned slot = (unsigned)(p.slot_base + i);
     const unsigned pid = (unsigned)p.pop_id[pi];
-    const float* __restrict__ lo_ = p.P.lo;
-    const float* __restrict__ hi_ = p.P.hi;
+    const ProbDev& P = p.P;
     float4* my4 = sm4 + tid * p.srs4;
     float* my = reinterpret_cast<float*>(my4);
 
     double f[kMaxM] = {0.0, 0.0, 0.0};
     bool bad = false;
-    if (active) {
+    {
         if (MODE == MODE_EVAL) {
-            const float4* __restrict__ row = p.parX[pi] + (long long)i * rs4;
-            for (int q = 0; q < rs4; ++q) my4[q] = row[q];
+            if (active) {
+                const float4* __restrict__ row = p.parX[pi] + (long long)i * rs4;
+                for (int q = 0; q < rs4; ++q) my4[q] = row[q];
+            }
         } else {
+            // the whole warp stays in this branch (pm_tasks is warp-cooperative);
+            // lanes past the end only skip the per-slot work
             const float4* __restrict__ PA = p.parX[pi];
             const float4* __restrict__ PB = p.parX[pi];
             const float4* __restrict__ PC = p.parX[pi] + (long long)i * rs4;
             int jrand = -1;
             bool cross = true;
-            if (MODE == MODE_VARY) {
+            if (MODE == MODE_VARY && active) {
                 const int t = p.t[pi];
                 PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key0, p.key1, 0u, {}};
                 unsigned a = ps.index((unsigned)t);
@@ -247,7 +295,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
             for (int w0 = 0; w0 < d; w0 += 64) {
                 const int w1 = min(d, w0 + 64);
                 unsigned long long mmask = 0ull;
-                for (int jb = w0; jb < w1; jb += 4) {
+                for (int jb = w0; jb < w1 && active; jb += 4) {
                     const int q = jb >> 2;
                     u32x4 xc{0, 0, 0, 0}, xu{0, 0, 0, 0}, mc{0, 0, 0, 0};
                     float4 out;
@@ -265,7 +313,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                             }
                             const u32x4& w = k < 2 ? xc : xu;
                             const double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
-                            const double lo = lo_[j], hi = hi_[j];
+                            const double lo = P.lob(j), hi = P.hib(j);
                             v[k] = (float)(lo + (hi - lo) * u);
                         }
                         out = make_float4(v[0], v[1], v[2], v[3]);
@@ -308,24 +356,20 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                             if ((long long)pick_word(mc, k) <= p.pm_thr)
                                 mmask |= 1ull << (j - w0);  // mutated + clipped in phase 2
                             else
-                                c = clamp_ref(c, lo_[j], hi_[j]);
+                                c = clamp_ref(c, P.lob(j), P.hib(j));
                             v[k] = c;
                         }
                         out = make_float4(v[0], v[1], v[2], v[3]);
                     }
                     my4[q] = out;
                 }
-                // phase 2: polynomial mutation then clip (gmpea.cpp:202-203)
-                while (mmask) {
-                    const int j = w0 + __ffsll((long long)mmask) - 1;
-                    mmask &= mmask - 1ull;
-                    const float lo = lo_[j], hi = hi_[j];
-                    const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key0, p.key1);
-                    my[j] = clamp_ref(pm_apply(my[j], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
-                }
+                // phase 2: polynomial mutation then clip (gmpea.cpp:202-203).
+                // The warp's mutation tasks (lane, gene) are dealt round-robin
+                // over its lanes, ~1 task per lane per round.
+                if (MODE == MODE_VARY) pm_tasks(p, mmask, w0, sm4, gen, pid, i0);
             }
         }
-        if (p.eval) {
+        if (p.eval && active) {
             // phase 3: bounds check (problems.cpp:554-561) + streamed evaluation
             Ev ev;
             ev.begin(p.P);
@@ -336,7 +380,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                 for (int k = 0; k < 4; ++k) {
                     const int j = jb + k;
                     if (j >= d) break;
-                    if (!(v[k] >= lo_[j] && v[k] <= hi_[j])) bad = true;
+                    if (!(v[k] >= P.lob(j) && v[k] <= P.hib(j))) bad = true;
                     ev.gene(p.P, j, v[k]);
                 }
             }
@@ -363,8 +407,9 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
         const int rows = min((int)blockDim.x, p.n - i0);
         const int total = rows * rs4;
         float4* __restrict__ dst = p.out[pi] + (long long)i0 * rs4;
+        const float inv = 1.0f / (float)rs4;  // exact floor for e < 2^20
         for (int e = tid; e < total; e += blockDim.x) {
-            const int r = e / rs4;
+            const int r = (int)(((float)e + 0.5f) * inv);
             dst[e] = sm4[r * p.srs4 + (e - r * rs4)];
         }
     }

@@ -36,6 +36,10 @@ struct ProbDev {
     int fam, id, d, m, nin, neq;
     const float* lo;  // d lower bounds
     const float* hi;  // d upper bounds
+    int uniform;      // all genes share [ulo, uhi] (every registered suite)
+    float ulo, uhi;
+    __device__ __forceinline__ float lob(int j) const { return uniform ? ulo : lo[j]; }
+    __device__ __forceinline__ float hib(int j) const { return uniform ? uhi : hi[j]; }
     // host-computed constants (glibc values, identical to the reference's)
     double cth, sth;  // cos/sin(-pi/4)  (LIRCMOP5-12 ellipse rotation)
     double cal, sal;  // cos/sin(pi/4)   (LIRCMOP9-12 alpha)
