@@ -148,23 +148,22 @@ __device__ __forceinline__ float clamp_ref(float v, float lo, float hi) {
     return v < lo ? lo : (hi < v ? hi : v);  // NaN passes through (std::clamp)
 }
 
-// gmpea.cpp:135-160 for one gene; w = the MU draw
+// gmpea.cpp:135-160 for one gene; w = the MU draw.  Both branches share one
+// pair of powf: for u < 0.5  dq = (2u + (1-2u)(1-d1)^e1)^einv - 1, otherwise
+// dq = 1 - (2(1-u) + 2(u-0.5)(1-d2)^e1)^einv; the operands are selected first
+// so a warp whose lanes disagree on the branch pays for one evaluation.
 __device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned w, float e1,
                                           float einv) {
     const float span = hi - lo;
     if (!(span > 0.0f)) return x;
-    float dq;
-    if (w < 0x80000000u) {  // u < 0.5
-        const float two_u = (float)w * 0x1.0p-31f;
-        const float one_m = (float)(0x80000000u - w) * 0x1.0p-31f;  // 1 - 2u
-        const float d1 = (x - lo) / span;
-        dq = powf(two_u + one_m * powf(1.0f - d1, e1), einv) - 1.0f;
-    } else {
-        const float two_1mu = (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;  // 2(1-u)
-        const float two_um = (float)(w - 0x80000000u) * 0x1.0p-31f;                        // 2(u-0.5)
-        const float d2 = (hi - x) / span;
-        dq = 1.0f - powf(two_1mu + two_um * powf(1.0f - d2, e1), einv);
-    }
+    const bool low = w < 0x80000000u;  // u < 0.5
+    const float A = low ? (float)w * 0x1.0p-31f                                            // 2u
+                        : (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;   // 2(1-u)
+    const float B = low ? (float)(0x80000000u - w) * 0x1.0p-31f                          // 1 - 2u
+                        : (float)(w - 0x80000000u) * 0x1.0p-31f;                         // 2(u-0.5)
+    const float dd = (low ? (x - lo) : (hi - x)) / span;                                 // d1 / d2
+    const float r = powf(A + B * powf(1.0f - dd, e1), einv);
+    const float dq = low ? r - 1.0f : 1.0f - r;
     return x + dq * span;
 }
 
@@ -611,7 +610,10 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
     p.Fcv[POP][j] = best;
 }
 
-__global__ void __launch_bounds__(256) select_kernel(SelParams p) {
+#ifndef GMPEA_SELECT_MINBLOCKS
+#define GMPEA_SELECT_MINBLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
     if (p.st->stop) return;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const float3 z = load_z(p.st, p.m);
