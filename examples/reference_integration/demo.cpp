@@ -1,0 +1,52 @@
+// Registers the B200 engine next to the reference's own algorithms, exactly
+// as INTEGRATION.md describes, and runs both on one reference ProblemDef.
+// Built by tests/test_integration.py against the UNMODIFIED reference library
+// (oracle/_ref/libgmpea_ref.so) and libgmpea_b200.so.
+#include <cstdio>
+#include <string>
+
+#include "gmpea/gmpea.hpp"
+#include "gmpea/metrics.hpp"
+#include "gmpea/problems.hpp"
+#include "gmpea_b200_adapter.hpp"
+
+using namespace gmpea;
+
+// the maintainer's one-line registration (experiment.cpp:125-138)
+static RunResult run_algorithm_with_b200(const std::string& algorithm, const ProblemDef& problem,
+                                         const RunConfig& cfg) {
+    if (algorithm == "gmpea-b200") return gmpea_b200::run_gmpea(problem, cfg);
+    return run_gmpea(problem, cfg);
+}
+
+int main(int argc, char** argv) {
+    const std::string name = argc > 1 ? argv[1] : "LIRCMOP13";
+    ProblemDef p = make_problem(name);
+    Matrix ref = pf_reference(p, 1000);
+    RunConfig cfg;
+    cfg.n = 300;
+    cfg.k_max = 100;
+    cfg.op = name.rfind("LIRCMOP", 0) == 0 ? VariationOp::de : VariationOp::sbx_pm;
+    cfg.record_walltime = false;
+    RunResult a = run_algorithm_with_b200("gmpea", p, cfg);
+    RunResult b = run_algorithm_with_b200("gmpea-b200", p, cfg);
+    std::printf("problem %s n=%zu gens ref=%zu b200=%zu\n", name.c_str(), cfg.n, a.history.size() - 1,
+                b.history.size() - 1);
+    std::printf("igd ref=%.6g b200=%.6g\n", igd(metric_front(a.pop1), ref), igd(metric_front(b.pop1), ref));
+    std::printf("evals ref=%zu b200=%zu\n", a.history.back().evals, b.history.back().evals);
+    // operator level: the engine's evaluation of the reference's own final rows
+    Population re = gmpea_b200::evaluate_population(p, a.pop1.X);
+    double worst = 0.0;
+    for (std::size_t i = 0; i < re.F.data.size(); ++i) {
+        double d = std::abs(re.F.data[i] - a.pop1.F.data[i]) / std::max(1.0, std::abs(a.pop1.F.data[i]));
+        worst = std::max(worst, d);
+    }
+    std::printf("evaluate max rel diff %.3g\n", worst);
+    // hooks: IGD per generation through the reference's own metric functions
+    RunConfig h = cfg;
+    h.k_max = 5;
+    h.igd_metric = [&](const Population& pop) { return igd(metric_front(pop), ref); };
+    RunResult c = run_algorithm_with_b200("gmpea-b200", p, h);
+    std::printf("hook records %zu last igd %.6g\n", c.history.size(), *c.history.back().igd);
+    return 0;
+}

@@ -818,9 +818,9 @@ struct gmpea_engine {
         CK(cudaStreamDestroy(cs));
     }
 
-    void start_loop_clock() {
-        if (gens_enqueued == 0) mark_start_kernel<<<1, 1, 0, s>>>(st.p);
-    }
+    // the loop clock restarts at every step() so host work between calls
+    // (metric hooks) stays outside the loop time, as in gmpea.cpp:442-453
+    void start_loop_clock() { mark_start_kernel<<<1, 1, 0, s>>>(st.p); }
 
     // enqueue up to k generations, respecting the generation limit
     long long step(long long k) {

@@ -1,0 +1,40 @@
+"""The reference-side integration: the C++ adapter compiles
+against the reference's own headers and, on a GPU, runs next to the unmodified
+reference library."""
+import os
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+DEMO_SRC = os.path.join(ROOT, "examples", "reference_integration", "demo.cpp")
+DEMO_BIN = os.path.join(ROOT, "build", "ref_integration_demo")
+REF_INC = "/root/reference/proj/include"
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libgmpea_ref.so")
+LIB = os.path.join(ROOT, "paper_2509_19821_b200", "libgmpea_b200.so")
+
+
+def build_demo():
+    os.makedirs(os.path.dirname(DEMO_BIN), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-I", REF_INC, "-I", os.path.join(ROOT, "include"), DEMO_SRC, REF_LIB, LIB,
+           f"-Wl,-rpath,{os.path.dirname(REF_LIB)}:{os.path.dirname(LIB)}", "-o", DEMO_BIN]
+    subprocess.run(cmd, check=True)
+
+
+def test_adapter_compiles_against_reference_headers():
+    if not (os.path.isdir(REF_INC) and os.path.exists(REF_LIB) and os.path.exists(LIB)):
+        pytest.skip("reference headers / builds not present")
+    build_demo()
+    assert os.path.exists(DEMO_BIN)
+
+
+@pytest.mark.gpu
+def test_adapter_runs_next_to_reference():
+    if not os.path.exists(DEMO_BIN):
+        pytest.skip("demo not built (needs the reference headers at build time)")
+    out = subprocess.run([DEMO_BIN, "LIRCMOP13"], check=True, capture_output=True, text=True).stdout
+    lines = dict(l.split(" ", 1) for l in out.strip().splitlines())
+    assert "evals ref=20200 b200=20200" in out
+    assert float(lines["evaluate"].split()[-1]) <= 1e-5
+    assert lines["hook"].startswith("records 6")
