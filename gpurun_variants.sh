@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-for lib in libgmpea_b200 libgmpea_b200_s5 libgmpea_b200_s6; do GMPEA_LIB=$PWD/paper_2509_19821_b200/$lib.so timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$lib.log 2>&1; echo "$lib rc=$?"; tail -1 gpurun_out/bench_$lib.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['ms_per_step'], l['value']/1e9, l['roofline']['kernel_ms'])"; done
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --workload mw1-1m > gpurun_out/bench_mw1.log 2>&1; tail -1 gpurun_out/bench_mw1.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print('mw1', l['ms_per_step'], l['value']/1e9, l['roofline']['kernel_ms'])"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench_full.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?; tail -1 gpurun_out/bench_ref.log

@@ -129,6 +129,9 @@ typedef struct {
     uint64_t stream;       /* cudaStream_t to run on; 0 = the engine's own stream */
     const double* igd_reference; /* optional per-generation IGD hook: reference front */
     int64_t igd_reference_rows;
+    /* weight-region sharding: this engine owns the slots
+     * [shard_begin, shard_end) of n; 0, 0 = all of them */
+    int64_t shard_begin, shard_end;
 } gmpea_run_config;
 
 typedef struct {
@@ -163,6 +166,28 @@ int gmpea_engine_neighborhoods(gmpea_engine* e, uint32_t* B1, uint32_t* B2);
  * end_gen] plus the total per generation in ms[4] */
 int gmpea_engine_profile(gmpea_engine* e, int64_t gens, double* ms);
 void gmpea_engine_destroy(gmpea_engine* e);
+
+/* ---- sharded runs (one engine per GPU).  Slot ranges are
+ * global; the engine keeps parent rows for [window_begin, window_end) =
+ * own +- 2*reach, regenerates offspring for [vary_begin, vary_end) = own +-
+ * reach (Philox keys are global, so they equal their owners' offspring) and
+ * selects its own slots. */
+typedef struct {
+    int64_t n_global, window_begin, window_end, vary_begin, vary_end, own_begin, own_end, reach;
+} gmpea_shard_info;
+int gmpea_engine_shard_info(gmpea_engine* e, gmpea_shard_info* out);
+/* one generation in two phases: 1 = variation + evaluation (+ local ideal
+ * point), 2 = OP1 + selection + bookkeeping.  Between them the caller
+ * all-reduces (MIN) the ideal-point words; after phase 2 it exchanges the
+ * boundary rows (own +- 2*reach) with the neighbouring shards. */
+int gmpea_engine_phase(gmpea_engine* e, int32_t phase);
+typedef struct {
+    void* ideal_bits;  /* uint32[4], order-preserving encoding of the ideal point (all-reduce MIN) */
+    void* rows[2];     /* pop1 / pop2 rows; window-local row r at rows + r * row_bytes */
+    void* keys[2];     /* pop1 / pop2 packed keys {f0, f1, f2, cv}, 16 bytes per row */
+    int64_t row_bytes;
+} gmpea_device_buffers;
+int gmpea_engine_device_buffers(gmpea_engine* e, gmpea_device_buffers* out);
 
 #ifdef __cplusplus
 }

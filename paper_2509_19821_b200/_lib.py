@@ -40,7 +40,18 @@ class _RunConfig(C.Structure):
         ("params", _OpParams), ("theta", C.c_double), ("t1", C.c_int32), ("t2", C.c_int32),
         ("record_walltime", C.c_int32), ("device", C.c_int32), ("stream", C.c_uint64),
         ("igd_reference", _dp), ("igd_reference_rows", C.c_int64),
+        ("shard_begin", C.c_int64), ("shard_end", C.c_int64),
     ]
+
+
+class _ShardInfo(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n_global", "window_begin", "window_end", "vary_begin", "vary_end",
+                                         "own_begin", "own_end", "reach")]
+
+
+class _DevBuffers(C.Structure):
+    _fields_ = [("ideal_bits", C.c_void_p), ("rows", C.c_void_p * 2), ("keys", C.c_void_p * 2),
+                ("row_bytes", C.c_int64)]
 
 
 class _GenRecord(C.Structure):
@@ -352,6 +363,7 @@ class RunConfig:
     record_walltime: bool = True
     device: int = 0
     stream: int = 0
+    shard: Optional[tuple] = None  # (begin, end) owned slots of a sharded run
 
     def _c(self) -> _RunConfig:
         c = _RunConfig()
@@ -368,6 +380,8 @@ class RunConfig:
         c.record_walltime = 1 if self.record_walltime else 0
         c.device = self.device
         c.stream = self.stream
+        if self.shard is not None:
+            c.shard_begin, c.shard_end = int(self.shard[0]), int(self.shard[1])
         return c
 
 
@@ -456,6 +470,21 @@ class Engine:
         B2 = np.zeros((self.n, t2), np.uint32)
         _check(_L.gmpea_engine_neighborhoods(self._h, _p(B1, _u32p), _p(B2, _u32p)))
         return NeighborhoodTopology(B1, B2, t1, t2)
+
+    # ---- sharded runs
+    def shard_info(self) -> dict:
+        o = _ShardInfo()
+        _check(_L.gmpea_engine_shard_info(self._h, C.byref(o)))
+        return {k: getattr(o, k) for k, _ in _ShardInfo._fields_}
+
+    def phase(self, ph: int) -> None:
+        _check(_L.gmpea_engine_phase(self._h, ph))
+
+    def device_buffers(self) -> dict:
+        o = _DevBuffers()
+        _check(_L.gmpea_engine_device_buffers(self._h, C.byref(o)))
+        return {"ideal_bits": o.ideal_bits, "rows": [o.rows[0], o.rows[1]], "keys": [o.keys[0], o.keys[1]],
+                "row_bytes": o.row_bytes}
 
     def profile(self, gens: int) -> np.ndarray:
         """Per-kernel average device ms: [vary_eval, op1, select, end_gen, total]."""

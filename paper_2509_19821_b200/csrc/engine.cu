@@ -374,6 +374,25 @@ __global__ void z_of_kernel(const float4* Fcv, long long n, int m, DevState* st)
     if (m > 2) atomicMin(&st->zbits[2], float_to_ordered(v.z));
 }
 
+// max |B[i][l] - i| over all rows (the neighbourhood reach)
+__global__ void reach_kernel(const int* B, long long n, int t, int* out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * t) return;
+    int dlt = B[e] - (int)(e / t);
+    atomicMax(out, dlt < 0 ? -dlt : dlt);
+}
+
+// rows [r0, r1) of the global table, re-indexed to the local window [e0, ...);
+// other local rows point at themselves (never used: variation runs on [r0, r1))
+__global__ void slice_topology_kernel(const int* Bg, int t, long long e0, long long nloc, long long r0,
+                                      long long r1, int* Bl) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nloc * t) return;
+    const long long i = e / t;
+    const long long g = e0 + i;
+    Bl[e] = (g >= r0 && g < r1) ? (int)(Bg[g * t + e % t] - e0) : (int)i;
+}
+
 __global__ void publish_stop_kernel(const DevState* st, volatile int* host_flag) {
     *host_flag = st->stop | (st->err ? 2 : 0);
 }
@@ -435,7 +454,7 @@ void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStream_t s) 
         r.smem = (size_t)r.bs * per;
         return r;
     }();
-    k<<<dim3(blocks_for(vp.n, g.bs), npops), g.bs, g.smem, s>>>(vp);
+    k<<<dim3(blocks_for(vp.row_end - vp.row0, g.bs), npops), g.bs, g.smem, s>>>(vp);
 }
 
 void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
@@ -511,11 +530,14 @@ void device_knn(cudaStream_t s, int n, int m, int t1, int t2, const double* dW, 
 
 // reverse neighbourhood (padded SoA, ascending); returns max in-degree
 int device_reverse(cudaStream_t s, int n, int t, const int* B, long long ld, DevBuf<int>& deg,
-                   DevBuf<int>& R) {
+                   DevBuf<int>& R, int r0 = 0, int r1 = -1) {
+    // claimants are the rows [r0, r1) of B (default: all n)
+    if (r1 < 0) r1 = n;
     deg.alloc(std::max<long long>(ld, 1));
     deg.zero(s);
-    const long long E = (long long)n * t;
-    indegree_kernel<<<blocks_for(E, 256), 256, 0, s>>>(n, t, B, deg.p);
+    const long long E = (long long)(r1 - r0) * t;
+    const int* Bs = B + (long long)r0 * t;
+    indegree_kernel<<<blocks_for(E, 256), 256, 0, s>>>(r1 - r0, t, Bs, deg.p);
     CK(cudaGetLastError());
     std::vector<int> h(n);
     CK(cudaMemcpyAsync(h.data(), deg.p, n * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -525,7 +547,7 @@ int device_reverse(cudaStream_t s, int n, int t, const int* B, long long ld, Dev
     R.alloc((size_t)std::max(maxdeg, 1) * ld);
     DevBuf<int> fill(std::max(n, 1));
     fill.zero(s);
-    reverse_fill_kernel<<<blocks_for(E, 256), 256, 0, s>>>(n, t, B, fill.p, R.p, ld);
+    reverse_fill_kernel<<<blocks_for(E, 256), 256, 0, s>>>(r1 - r0, t, Bs, r0, fill.p, R.p, ld);
     reverse_sort_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, deg.p, R.p, ld);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
@@ -538,7 +560,10 @@ int device_reverse(cudaStream_t s, int n, int t, const int* B, long long ld, Dev
 struct gmpea_engine {
     const gmpea_problem* prob = nullptr;
     gmpea_run_config cfg{};
-    int n = 0, d = 0, m = 0, nc = 0, t1 = 0, t2 = 0;
+    int n = 0, d = 0, m = 0, nc = 0, t1 = 0, t2 = 0;  // n: local rows
+    // shard geometry (global slot indices; unsharded: all equal [0, N))
+    long long N = 0, e0 = 0, e1 = 0, v0 = 0, v1 = 0, own0 = 0, own1 = 0, reach = 0;
+    bool sharded = false;
     long long ld = 0, H = 0;
     RowGeom geo{};
     cudaStream_t s = nullptr;
@@ -548,7 +573,6 @@ struct gmpea_engine {
     DevBuf<DevState> st;
     DevBuf<DevRecord> rec;
     long long rec_cap = 0;
-    DevBuf<double> W64;
     DevBuf<float4> U;
     DevBuf<int> B[2], R[2], Rdeg[2];
     int maxdeg[2] = {0, 0};
@@ -592,16 +616,26 @@ struct gmpea_engine {
             CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
             own_stream = true;
         }
-        n = (int)c.n;
+        N = c.n;
         d = p->d;
         m = p->m;
         nc = p->nin + p->neq;
-        ld = round_up(n, 32);
         geo = row_geom(d, nc);
-        t1 = (int)std::min<long long>(c.t1, n);
-        t2 = (int)std::min<long long>(c.t2, n);
+        t1 = (int)std::min<long long>(c.t1, N);
+        t2 = (int)std::min<long long>(c.t2, N);
         time_mode = c.time_budget_s > 0.0;
-        H = lattice_H(m, n);
+        H = lattice_H(m, N);
+        own0 = 0;
+        own1 = N;
+        if (c.shard_end > c.shard_begin) {
+            if (c.shard_begin < 0 || c.shard_end > N)
+                throw std::invalid_argument("engine: shard range outside [0, n)");
+            own0 = c.shard_begin;
+            own1 = c.shard_end;
+            sharded = own0 > 0 || own1 < N;
+        }
+        if (sharded && time_mode)
+            throw std::invalid_argument("engine: a sharded run takes k_max / eval budgets (the deadline would differ per rank)");
 
         st.alloc(1);
         st.zero(s);
@@ -610,7 +644,7 @@ struct gmpea_engine {
         bool unbounded = c.k_max == 0 && (time_mode || c.eval_budget > 0);
         long long lim = c.k_max > 0 ? c.k_max : (unbounded ? -1 : 0);
         if (c.eval_budget > 0) {
-            long long e = c.eval_budget / (2ll * n) - 1;  // gens with evals + 2n <= budget
+            long long e = c.eval_budget / (2ll * N) - 1;  // gens with evals + 2n <= budget
             if (e < 0) e = 0;
             lim = lim < 0 ? e : std::min(lim, e);
         }
@@ -619,17 +653,51 @@ struct gmpea_engine {
         rec.alloc(rec_cap);
         rec.zero(s);
 
-        // reference vectors + neighbourhoods (gmpea.cpp:424-428)
-        W64.alloc((size_t)n * m);
-        U.alloc(ld);
-        U.zero(s);
-        lattice_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, m, H, W64.p, U.p);
-        CK(cudaGetLastError());
-        B[0].alloc((size_t)n * t1);
-        B[1].alloc((size_t)n * t2);
-        device_knn(s, n, m, t1, t2, W64.p, true, H, B[0].p, B[1].p);
-        maxdeg[0] = device_reverse(s, n, t1, B[0].p, ld, Rdeg[0], R[0]);
-        maxdeg[1] = device_reverse(s, n, t2, B[1].p, ld, Rdeg[1], R[1]);
+        // reference vectors + neighbourhoods (gmpea.cpp:424-428), global
+        {
+            DevBuf<double> Wg((size_t)N * m);
+            DevBuf<float4> Ug(round_up(N, 32));
+            lattice_kernel<<<blocks_for(N, 256), 256, 0, s>>>((int)N, m, H, Wg.p, Ug.p);
+            CK(cudaGetLastError());
+            DevBuf<int> Bg[2];
+            Bg[0].alloc((size_t)N * t1);
+            Bg[1].alloc((size_t)N * t2);
+            device_knn(s, (int)N, m, t1, t2, Wg.p, true, H, Bg[0].p, Bg[1].p);
+            // shard window: own [own0, own1); offspring regenerated on
+            // [own0 - r, own1 + r); parent rows kept on [own0 - 2r, own1 + 2r)
+            if (sharded) {
+                DevBuf<int> r(1);
+                r.zero(s);
+                for (int q = 0; q < 2; ++q)
+                    reach_kernel<<<blocks_for(N * (q ? t2 : t1), 256), 256, 0, s>>>(Bg[q].p, N, q ? t2 : t1, r.p);
+                int hr = 0;
+                CK(cudaMemcpyAsync(&hr, r.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                reach = hr;
+                if (own1 - own0 < 2 * reach)
+                    throw std::invalid_argument("engine: shard narrower than twice the neighbourhood reach (" +
+                                                std::to_string(2 * reach) + " slots)");
+            }
+            e0 = std::max(0ll, own0 - 2 * reach);
+            e1 = std::min(N, own1 + 2 * reach);
+            v0 = std::max(0ll, own0 - reach);
+            v1 = std::min(N, own1 + reach);
+            n = (int)(e1 - e0);
+            ld = round_up(n, 32);
+            U.alloc(ld);
+            U.zero(s);
+            CK(cudaMemcpyAsync(U.p, Ug.p + e0, (size_t)n * sizeof(float4), cudaMemcpyDeviceToDevice, s));
+            for (int q = 0; q < 2; ++q) {
+                const int t = q ? t2 : t1;
+                B[q].alloc((size_t)n * t);
+                slice_topology_kernel<<<blocks_for((long long)n * t, 256), 256, 0, s>>>(Bg[q].p, t, e0, n, v0, v1,
+                                                                                         B[q].p);
+            }
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(s));
+        }
+        maxdeg[0] = device_reverse(s, n, t1, B[0].p, ld, Rdeg[0], R[0], (int)(v0 - e0), (int)(v1 - e0));
+        maxdeg[1] = device_reverse(s, n, t2, B[1].p, ld, Rdeg[1], R[1], (int)(v0 - e0), (int)(v1 - e0));
 
         for (int q = 0; q < 2; ++q) {
             pop[q].alloc(n, geo.rs4, ld);
@@ -652,9 +720,11 @@ struct gmpea_engine {
         // kernel parameter blocks
         vp = VaryParams{};
         vp.n = n;
+        vp.row0 = 0;
+        vp.row_end = n;
         vp.rs4 = geo.rs4;
         vp.srs4 = geo.srs4;
-        vp.slot_base = 0;
+        vp.slot_base = (int)e0;  // Philox keys use global slots
         vp.pop_id[0] = 1;
         vp.pop_id[1] = 2;
         vp.P = p->dev;
@@ -692,10 +762,14 @@ struct gmpea_engine {
             vp.outFcv[q] = off[q].Fcv.p;
         }
         vary = vary_kernel_for(p->fam, MODE_VARY, c.op);
-        op1p = Op1Params{n, m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p}, {eff[0].p, eff[1].p},
-                         srcbits.p, st.p};
+        vp.row0 = (int)(v0 - e0);
+        vp.row_end = (int)(v1 - e0);
+        op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p},
+                         {eff[0].p, eff[1].p}, srcbits.p, st.p};
         sp = SelParams{};
         sp.n = n;
+        sp.row0 = (int)(own0 - e0);
+        sp.row_end = (int)(own1 - e0);
         sp.rs4 = geo.rs4;
         sp.ldr = ld;
         sp.m = m;
@@ -725,7 +799,8 @@ struct gmpea_engine {
         sp.apply = 1;
         sp.st = st.p;
         sp.rec = rec.p;
-        rp.n = n;
+        rp.row0 = (int)(own0 - e0);
+        rp.row_end = (int)(own1 - e0);
         rp.rs4 = geo.rs4;
         rp.st = st.p;
         CK(cudaStreamSynchronize(s));
@@ -735,9 +810,11 @@ struct gmpea_engine {
     // evaluation of the initial populations done: z, record 0, gen = 1
     void finish_init() {
         init_state_kernel<<<1, 1, 0, s>>>(st.p, m);
-        for (int q = 0; q < 2; ++q) z_of_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[q].Fcv.p, n, m, st.p);
+        const int o0 = (int)(own0 - e0), on = (int)(own1 - own0);
+        for (int q = 0; q < 2; ++q)
+            z_of_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[q].Fcv.p + o0, on, m, st.p);
         rec.zero(s);
-        count_feasible_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[0].Fcv.p, n, &rec.p[0].feasible);
+        count_feasible_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[0].Fcv.p, o0, o0 + on, &rec.p[0].feasible);
         DevState init{};
         CK(cudaMemcpyAsync(&init, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -766,7 +843,8 @@ struct gmpea_engine {
         const int q = which - 1;
         if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
         DevBuf<double>& h = staging;
-        CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
+        // X holds all N rows; this engine keeps its window [e0, e1)
+        CK(cudaMemcpyAsync(h.p, X + e0 * d, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
         DevBuf<int> nbad(1);
         nbad.zero(s);
         if (rowsbuf.n < (size_t)std::max(n, 1)) rowsbuf.alloc(std::max(n, 1));
@@ -779,9 +857,12 @@ struct gmpea_engine {
         if (hb) {
             std::vector<int> r(hb);
             CK(cudaMemcpy(r.data(), rows.p, hb * sizeof(int), cudaMemcpyDeviceToHost));
+            for (int& v : r) v += (int)e0;
             throw std::invalid_argument(rows_message(r));
         }
         VaryParams ep = vp;
+        ep.row0 = 0;
+        ep.row_end = n;
         ep.parX[0] = pop[q].X.p;
         ep.out[0] = pop[q].X.p;
         ep.outFcv[0] = pop[q].Fcv.p;
@@ -794,12 +875,19 @@ struct gmpea_engine {
     }
 
     void enqueue_generation() {
-        launch_vary(vary, vp, 2, s);
-        op1_kernel<<<blocks_for(n, 256), 256, 0, s>>>(op1p);
-        select_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(sp);
-        end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
-        if (time_mode) restore_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(rp);
+        enqueue_phase1();
+        enqueue_phase2();
         publish_stop_kernel<<<1, 1, 0, s>>>(st.p, host_flag_dev);
+    }
+
+    // phase 1: variation + evaluation (+ local ideal-point partial)
+    void enqueue_phase1() { launch_vary(vary, vp, 2, s); }
+    // phase 2: OP1, selection, bookkeeping (a sharded run all-reduces z in between)
+    void enqueue_phase2() {
+        op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
+        select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);
+        end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
+        if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
 
     void build_graph() {
@@ -831,6 +919,22 @@ struct gmpea_engine {
         for (long long i = 0; i < k; ++i) CK(cudaGraphLaunch(graph, s));
         gens_enqueued += k;
         return k;
+    }
+
+    // one generation in two phases (sharded runs; no graph, plain launches)
+    void phase(int ph) {
+        if (ph == 1) {
+            if (gen_limit >= 0 && gens_enqueued >= gen_limit)
+                throw std::invalid_argument("phase: generation limit reached");
+            start_loop_clock();
+            enqueue_phase1();
+        } else if (ph == 2) {
+            enqueue_phase2();
+            gens_enqueued += 1;
+        } else {
+            throw std::invalid_argument("phase: must be 1 or 2");
+        }
+        CK(cudaGetLastError());
     }
 
     void run() {
@@ -902,9 +1006,9 @@ struct gmpea_engine {
             gmpea_gen_record& o = out[k];
             o = gmpea_gen_record{};
             o.gen = k;
-            o.evals = 2ll * n * (k + 1);
+            o.evals = 2ll * N * (k + 1);
             o.wall_ms = cfg.record_walltime ? (k == 0 ? 0.0 : (double)r[k].loop_ns * 1e-6) : 0.0;
-            o.feasible_ratio = (double)r[k].feasible / (double)n;
+            o.feasible_ratio = (double)r[k].feasible / (double)(own1 - own0);
             o.igd = std::numeric_limits<double>::quiet_NaN();
             o.hv = std::numeric_limits<double>::quiet_NaN();
         }
@@ -925,33 +1029,35 @@ struct gmpea_engine {
         CK(cudaStreamSynchronize(s));
         gmpea_gen_record o{};
         o.gen = k;
-        o.evals = 2ll * n * (k + 1);
+        o.evals = 2ll * N * (k + 1);
         o.wall_ms = cfg.record_walltime && k ? (double)r.loop_ns * 1e-6 : 0.0;
-        o.feasible_ratio = (double)r.feasible / (double)n;
+        o.feasible_ratio = (double)r.feasible / (double)(own1 - own0);
         o.igd = o.hv = std::numeric_limits<double>::quiet_NaN();
         return o;
     }
 
+    // the owned rows [own0, own1) (all N unsharded)
     void get_population(int which, double* X, double* F, double* C, double* cv) {
         if (which != 1 && which != 2) throw std::invalid_argument("get_population: which must be 1 or 2");
         const int q = which - 1;
+        const long long o0 = own0 - e0, on = own1 - own0;
         if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
         DevBuf<double>& tmp = staging;
+        const float* rows = (const float*)(pop[q].X.p + o0 * geo.rs4);
         auto pull = [&](int col0, int k, double* out) {
             if (!out || k == 0) return;
-            from_rows_kernel<<<blocks_for((long long)n * k, 256), 256, 0, s>>>((const float*)pop[q].X.p,
-                                                                              geo.rs4 * 4, n, col0, k, tmp.p);
-            CK(cudaMemcpyAsync(out, tmp.p, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToHost, s));
+            from_rows_kernel<<<blocks_for(on * k, 256), 256, 0, s>>>(rows, geo.rs4 * 4, on, col0, k, tmp.p);
+            CK(cudaMemcpyAsync(out, tmp.p, (size_t)on * k * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         };
         pull(0, d, X);
         pull(d, nc, C);
         if (F || cv) {
             double* f = tmp.p;
-            double* c = tmp.p + (size_t)n * m;
-            fcv_to_rows_kernel<<<blocks_for(n, 256), 256, 0, s>>>(pop[q].Fcv.p, n, m, f, c);
-            if (F) CK(cudaMemcpyAsync(F, f, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-            if (cv) CK(cudaMemcpyAsync(cv, c, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+            double* c = tmp.p + (size_t)on * m;
+            fcv_to_rows_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[q].Fcv.p + o0, on, m, f, c);
+            if (F) CK(cudaMemcpyAsync(F, f, (size_t)on * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+            if (cv) CK(cudaMemcpyAsync(cv, c, (size_t)on * sizeof(double), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
         }
     }
@@ -967,12 +1073,12 @@ struct gmpea_engine {
             CK(cudaEventRecord(e[0], s));
             launch_vary(vary, vp, 2, s);
             CK(cudaEventRecord(e[1], s));
-            op1_kernel<<<blocks_for(n, 256), 256, 0, s>>>(op1p);
+            op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
             CK(cudaEventRecord(e[2], s));
-            select_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(sp);
+            select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);
             CK(cudaEventRecord(e[3], s));
             end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
-            if (time_mode) restore_kernel<<<dim3(blocks_for(n, 256), 2), 256, 0, s>>>(rp);
+            if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
             CK(cudaEventRecord(e[4], s));
         }
         CK(cudaGetLastError());
@@ -1106,6 +1212,8 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         DevBuf<int> bad(n);
         VaryParams ep{};
         ep.n = (int)n;
+        ep.row0 = 0;
+        ep.row_end = (int)n;
         ep.rs4 = geo.rs4;
         ep.srs4 = geo.srs4;
         ep.pop_id[0] = 1;
@@ -1215,6 +1323,8 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         DevBuf<int> bad(1);
         VaryParams vp{};
         vp.n = (int)n;
+        vp.row0 = 0;
+        vp.row_end = (int)n;
         vp.rs4 = geo.rs4;
         vp.srs4 = geo.srs4;
         vp.pop_id[0] = (int)pop;
@@ -1292,13 +1402,15 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
         eff[0].alloc(ld);
         eff[1].alloc(ld);
         DevBuf<unsigned char> sb(ld);
-        Op1Params o1{(int)n, m, (float)theta, U.p, {fcv[2].p, fcv[3].p}, {eff[0].p, eff[1].p}, sb.p, st.p};
+        Op1Params o1{0, (int)n, m, (float)theta, U.p, {fcv[2].p, fcv[3].p}, {eff[0].p, eff[1].p}, sb.p, st.p};
         op1_kernel<<<blocks_for(n, 256), 256>>>(o1);
         DevBuf<int> win[2];
         win[0].alloc(n);
         win[1].alloc(n);
         SelParams sp{};
         sp.n = (int)n;
+        sp.row0 = 0;
+        sp.row_end = (int)n;
         sp.ldr = ld;
         sp.m = m;
         sp.theta = (float)theta;
@@ -1544,8 +1656,14 @@ int gmpea_engine_ideal(gmpea_engine* e, double* z) {
 
 int gmpea_engine_neighborhoods(gmpea_engine* e, uint32_t* B1, uint32_t* B2) {
     return guarded([&] {
-        if (B1) CK(cudaMemcpy(B1, e->B[0].p, (size_t)e->n * e->t1 * sizeof(int), cudaMemcpyDeviceToHost));
-        if (B2) CK(cudaMemcpy(B2, e->B[1].p, (size_t)e->n * e->t2 * sizeof(int), cudaMemcpyDeviceToHost));
+        const long long o0 = e->own0 - e->e0, on = e->own1 - e->own0;
+        uint32_t* outs[2] = {B1, B2};
+        for (int q = 0; q < 2; ++q) {
+            if (!outs[q]) continue;
+            const int t = q ? e->t2 : e->t1;
+            CK(cudaMemcpy(outs[q], e->B[q].p + o0 * t, (size_t)on * t * sizeof(int), cudaMemcpyDeviceToHost));
+            for (long long k = 0; k < on * t; ++k) outs[q][k] += (uint32_t)e->e0;  // global slots
+        }
     });
 }
 
@@ -1554,5 +1672,26 @@ int gmpea_engine_profile(gmpea_engine* e, int64_t gens, double* ms) {
 }
 
 void gmpea_engine_destroy(gmpea_engine* e) { delete e; }
+
+int gmpea_engine_shard_info(gmpea_engine* e, gmpea_shard_info* o) {
+    return guarded([&] {
+        *o = gmpea_shard_info{e->N, e->e0, e->e1, e->v0, e->v1, e->own0, e->own1, e->reach};
+    });
+}
+
+int gmpea_engine_phase(gmpea_engine* e, int32_t phase) {
+    return guarded([&] { e->phase(phase); });
+}
+
+int gmpea_engine_device_buffers(gmpea_engine* e, gmpea_device_buffers* o) {
+    return guarded([&] {
+        o->ideal_bits = e->st.p->zbits;
+        for (int q = 0; q < 2; ++q) {
+            o->rows[q] = e->pop[q].X.p;
+            o->keys[q] = e->pop[q].Fcv.p;
+        }
+        o->row_bytes = (int64_t)e->geo.rs4 * 16;
+    });
+}
 
 }  // extern "C"

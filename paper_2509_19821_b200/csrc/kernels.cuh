@@ -30,7 +30,8 @@ enum : int { OP_SBX = 0, OP_DE = 1 };
 enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
 
 struct VaryParams {
-    int n;                   // slots per population
+    int n;                   // local rows per population (buffer extent)
+    int row0, row_end;       // rows [row0, row_end) are produced by this launch
     int rs4;                 // row stride (float4)
     int srs4;                // shared-memory row stride (float4, odd: bank-conflict free)
     int slot_base;           // global slot index of local row 0 (sharding)
@@ -246,9 +247,9 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
     if (st->stop) return;
     const int pi = blockIdx.y;
     const int tid = threadIdx.x;
-    const int i0 = blockIdx.x * blockDim.x;
+    const int i0 = p.row0 + blockIdx.x * blockDim.x;
     const int i = i0 + tid;
-    const bool active = i < p.n;
+    const bool active = i < p.row_end;
     const int d = p.P.d;
     const int rs4 = p.rs4;
     const unsigned gen = p.fixed_gen >= 0 ? (unsigned)p.fixed_gen : (unsigned)st->gen;
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
     // phase 4: rows [i0, i0 + rows) leave as one contiguous, coalesced copy
     __syncthreads();
     {
-        const int rows = min((int)blockDim.x, p.n - i0);
+        const int rows = min((int)blockDim.x, p.row_end - i0);
         const int total = rows * rs4;
         float4* __restrict__ dst = p.out[pi] + (long long)i0 * rs4;
         const float inv = 1.0f / (float)rs4;  // exact floor for e < 2^20
@@ -451,7 +452,7 @@ __device__ __forceinline__ float3 load_z(const DevState* st, int m) {
 }
 
 struct Op1Params {
-    int n;
+    int row0, row_end;
     int m;
     float theta;
     const float4* U;
@@ -466,8 +467,8 @@ struct Op1Params {
 // Heaviside masks over differences, which reject non-finite inputs.
 __global__ void __launch_bounds__(256) op1_kernel(Op1Params p) {
     if (p.st->stop) return;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p.n) return;
+    const int i = p.row0 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= p.row_end) return;
     const float3 z = load_z(p.st, p.m);
     const float4 a = p.oFcv[0][i], b = p.oFcv[1][i], u = p.U[i];
     const float g1 = pbi(a, u, z, p.theta), g2 = pbi(b, u, z, p.theta);
@@ -484,7 +485,8 @@ __global__ void __launch_bounds__(256) op1_kernel(Op1Params p) {
 }
 
 struct SelParams {
-    int n, rs4, m;
+    int n, rs4, m;       // n: local rows (winner code c | n + c)
+    int row0, row_end;   // parent slots [row0, row_end) selected by this launch
     float theta;
     const float4* U;
     float4* X[2];        // parent rows, updated in place
@@ -615,10 +617,10 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
 #endif
 __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
     if (p.st->stop) return;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = p.row0 + blockIdx.x * blockDim.x + threadIdx.x;
     const float3 z = load_z(p.st, p.m);
     bool feas = false;
-    if (j < p.n) {
+    if (j < p.row_end) {
         if (blockIdx.y == 0)
             select_slot<0>(p, j, z, feas);
         else
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(Sel
     if (blockIdx.y != 0 || p.rec == nullptr) return;
     // feasible_ratio of pop1 (gmpea.cpp:411-417): block count, one atomic
     __shared__ unsigned cnt[8];
-    unsigned b = __popc(__ballot_sync(0xffffffffu, feas && j < p.n));
+    unsigned b = __popc(__ballot_sync(0xffffffffu, feas && j < p.row_end));
     if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = b;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -656,7 +658,7 @@ __global__ void end_gen_kernel(DevState* st, DevRecord* rec) {
 __global__ void mark_start_kernel(DevState* st) { st->t_gen_start = globaltimer(); }
 
 struct RestoreParams {
-    int n, rs4;
+    int row0, row_end, rs4;
     float4* X[2];
     float4* Fcv[2];
     const float4* uX[2];
@@ -667,17 +669,17 @@ struct RestoreParams {
 
 __global__ void restore_kernel(RestoreParams p) {
     if (!p.st->discard) return;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = p.row0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int q = blockIdx.y;
-    if (j >= p.n || p.ustamp[q][j] != p.st->gen) return;
+    if (j >= p.row_end || p.ustamp[q][j] != p.st->gen) return;
     copy_row(p.X[q] + (long long)j * p.rs4, p.uX[q] + (long long)j * p.rs4, p.rs4);
     p.Fcv[q][j] = p.uFcv[q][j];
 }
 
 // feasible count of pop1 (generation-0 record)
-__global__ void count_feasible_kernel(const float4* Fcv, int n, unsigned* out) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool f = j < n && Fcv[j].w == 0.0f;
+__global__ void count_feasible_kernel(const float4* Fcv, int row0, int row_end, unsigned* out) {
+    const int j = row0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const bool f = j < row_end && Fcv[j].w == 0.0f;
     unsigned b = __popc(__ballot_sync(0xffffffffu, f));
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(out, b);
 }

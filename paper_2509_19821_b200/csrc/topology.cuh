@@ -208,10 +208,10 @@ __global__ void indegree_kernel(int n, int t, const int* B, int* deg) {
     atomicAdd(&deg[B[e]], 1);
 }
 
-__global__ void reverse_fill_kernel(int n, int t, const int* B, int* fill, int* R, long long ld) {
+__global__ void reverse_fill_kernel(int n, int t, const int* B, int c0, int* fill, int* R, long long ld) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (long long)n * t) return;
-    const int c = (int)(e / t);
+    const int c = c0 + (int)(e / t);
     const int j = B[e];
     const int k = atomicAdd(&fill[j], 1);
     R[(long long)k * ld + j] = c;

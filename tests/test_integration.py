@@ -35,6 +35,6 @@ def test_adapter_runs_next_to_reference():
         pytest.skip("demo not built (needs the reference headers at build time)")
     out = subprocess.run([DEMO_BIN, "LIRCMOP13"], check=True, capture_output=True, text=True).stdout
     lines = dict(l.split(" ", 1) for l in out.strip().splitlines())
-    assert "evals ref=20200 b200=20200" in out
+    assert "evals ref=60600 b200=60600" in out  # 2 n (k_max + 1)
     assert float(lines["evaluate"].split()[-1]) <= 1e-5
     assert lines["hook"].startswith("records 6")
