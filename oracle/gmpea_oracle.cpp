@@ -894,14 +894,14 @@ double clamp_ref(double v, double lo, double hi) { return v < lo ? lo : (hi < v 
 
 void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, size_t t, int op,
                const OpParams& prm, uint64_t seed, uint32_t gen, uint32_t pop, double* off,
-               int32_t* picks) {
+               int32_t* picks, uint32_t slot_base = 0) {
     const int d = p.d;
     const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / static_cast<double>(d);
     for (size_t i = 0; i < n; ++i) {
         Keyed k;
         k.key[0] = static_cast<uint32_t>(seed);
         k.key[1] = static_cast<uint32_t>(seed >> 32);
-        k.slot = static_cast<uint32_t>(i);
+        k.slot = slot_base + static_cast<uint32_t>(i);  // Philox keys use global slots
         k.gen = gen;
         k.pop = pop;
         size_t a = k.index(t);
@@ -1175,12 +1175,12 @@ int orc_selection(int32_t n, int32_t m, const double* F1, const double* cv1, con
 
 int orc_reproduce(const char* name, const double* X, int64_t n, const uint32_t* nb, int32_t t,
                   int32_t op, const double* params5, double pm_prob, uint64_t seed, uint32_t gen,
-                  uint32_t pop, double* off, int32_t* picks) {
+                  uint32_t pop, double* off, int32_t* picks, uint32_t slot_base) {
     return guarded([&] {
         Problem p = make_problem(name);
         OpParams prm{params5[0], params5[1], params5[2], params5[3], params5[4], pm_prob};
         reproduce(p, X, static_cast<size_t>(n), nb, static_cast<size_t>(t), op, prm, seed, gen, pop,
-                  off, picks);
+                  off, picks, slot_base);
     });
 }
 

@@ -156,7 +156,7 @@ class Oracle(_Lib):
         return (s1, s2, m1, m2) if want_marks else (s1, s2)
 
     # -- variation --------------------------------------------------------
-    def reproduce(self, name, X, nb, op, seed, gen, pop, params=None, pm_prob=-1.0):
+    def reproduce(self, name, X, nb, op, seed, gen, pop, params=None, pm_prob=-1.0, slot_base=0):
         """op: 0 = sbx_pm, 1 = de.  params = (sbx_prob, sbx_eta, pm_eta, de_cr, de_f)."""
         X = _f64(X)
         nb = np.ascontiguousarray(nb, np.uint32)
@@ -167,7 +167,7 @@ class Oracle(_Lib):
         self._check(self.lib.orc_reproduce(name.encode(), _ptr(X, _dp), C.c_int64(n), _ptr(nb, _u32p),
                                            nb.shape[1], op, _ptr(prm, _dp), C.c_double(pm_prob),
                                            C.c_uint64(seed), C.c_uint32(gen), C.c_uint32(pop),
-                                           _ptr(off, _dp), _ptr(picks, _i32p)))
+                                           _ptr(off, _dp), _ptr(picks, _i32p), C.c_uint32(slot_base)))
         return off, picks
 
     def init_population(self, name, n, seed, pop):

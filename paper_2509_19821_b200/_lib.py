@@ -413,6 +413,8 @@ class Engine:
         _check(_L.gmpea_engine_create(problem._h, C.byref(self._c), C.byref(h)))
         self._h = h
         self.n = int(_L.gmpea_engine_effective_n(h))
+        info = self.shard_info()
+        self.rows_owned = info["own_end"] - info["own_begin"]  # rows population() returns
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -453,7 +455,7 @@ class Engine:
 
     def population(self, which: int = 1, out: Optional[Population] = None) -> Population:
         """pop `which` as f64 rows; `out` may supply (pinned) destination arrays."""
-        n, p = self.n, self.problem
+        n, p = self.rows_owned, self.problem
         if out is None:
             out = Population(np.zeros((n, p.d)), np.zeros((n, p.m)), np.zeros((n, p.n_constraints)), np.zeros(n))
         _check(_L.gmpea_engine_get_population(self._h, which, _p(out.X), _p(out.F), _p(out.C), _p(out.cv)))
@@ -466,8 +468,8 @@ class Engine:
 
     def neighborhoods(self) -> NeighborhoodTopology:
         t1, t2 = min(self.cfg.t1, self.n), min(self.cfg.t2, self.n)
-        B1 = np.zeros((self.n, t1), np.uint32)
-        B2 = np.zeros((self.n, t2), np.uint32)
+        B1 = np.zeros((self.rows_owned, t1), np.uint32)
+        B2 = np.zeros((self.rows_owned, t2), np.uint32)
         _check(_L.gmpea_engine_neighborhoods(self._h, _p(B1, _u32p), _p(B2, _u32p)))
         return NeighborhoodTopology(B1, B2, t1, t2)
 

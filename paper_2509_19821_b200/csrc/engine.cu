@@ -1625,7 +1625,7 @@ int gmpea_engine_sync(gmpea_engine* e) {
     });
 }
 
-int64_t gmpea_engine_effective_n(const gmpea_engine* e) { return e ? e->n : 0; }
+int64_t gmpea_engine_effective_n(const gmpea_engine* e) { return e ? e->N : 0; }
 
 int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, int64_t* nrec) {
     return guarded([&] {
