@@ -9,9 +9,10 @@ reference's evals unit, gmpea.cpp:433,487).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Multi-GPU: N independent replicas, one per rank (DESIGN.md "Multi-GPU" —
-the sharded engine is exercised separately); value = all ranks' work / max
-time over ranks.
+Multi-GPU (torchrun, one rank per GPU): the same N = 1M run split into
+weight-region shards — an ideal-point all-reduce and a
+boundary-row exchange over NCCL per generation; value = 2N per generation /
+max step time over ranks (strong scaling).
 """
 from __future__ import annotations
 
@@ -173,7 +174,7 @@ def main():
         value = float(np.median(vals))
         line = {"metric": METRIC, "value": value, "unit": "ind-gen/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2 * n / value * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (Philox/mt19937 initial populations)", "impl": "reference",
                 "config": config,
                 "cpu_baseline": {"value": value, "unit": "ind-gen/s", "cores": threads, "kind": kind,
@@ -195,10 +196,22 @@ def main():
     stream = torch.cuda.Stream()  # the engine's launching stream (events are recorded on it)
     torch.cuda.set_stream(stream)
     prob = g.make_problem(problem)
-    cfg = g.RunConfig(n=n, k_max=0, eval_budget=2 * n * (args.warmup + 4 * args.steps + 16),
-                      seed=1 + rank, op=op, device=local, stream=stream.cuda_stream)
-    eng = g.Engine(prob, cfg)
-    eng.step(args.warmup)
+    budget_gens = args.warmup + 4 * args.steps + 16
+    if world == 1:
+        cfg = g.RunConfig(n=n, k_max=0, eval_budget=2 * n * budget_gens, seed=1, op=op, device=local,
+                          stream=stream.cuda_stream)
+        eng = g.Engine(prob, cfg)
+        advance = eng.step  # CUDA-graph replay, one graph per generation
+    else:
+        # weight-region shards of the same N = 1M run (strong scaling): ideal
+        # point all-reduce + boundary-row exchange over NCCL every generation
+        from paper_2509_19821_b200.sharded import GpuShard, TorchComm
+
+        cfg = g.RunConfig(n=n, k_max=budget_gens, seed=1, op=op, device=local, stream=stream.cuda_stream)
+        shard = GpuShard(prob, cfg, world, rank, TorchComm())
+        eng = shard.eng
+        advance = shard.run
+    advance(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -209,47 +222,64 @@ def main():
     with clocks:
         torch.cuda.synchronize()
         start.record(stream)
-        eng.step(args.steps)
+        advance(args.steps)
         end.record(stream)
         torch.cuda.synchronize()
     eng.sync()
     ms_total = start.elapsed_time(end)
-    # per-kernel device times (events around every launch), same stream
-    kms = eng.profile(args.steps)
     if world > 1:
         t = torch.tensor([ms_total], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * 2 * n / (ms_step * 1e-3)
+    value = 2 * n / (ms_step * 1e-3)  # whole job: all ranks together process the N-slot generation
+    # per-kernel device times (events around every launch) on this rank's
+    # engine; run after the timed region (the shards no longer exchange)
+    kms = eng.profile(args.steps)
 
     # ---- e2e: the public API with (pinned) host buffers
     def pinned(shape):
         return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
 
-    rng = np.random.default_rng(rank)
+    rng = np.random.default_rng(7)
     X1, X2 = pinned((n, prob.d)), pinned((n, prob.d))
     X1[:] = prob.lower + (prob.upper - prob.lower) * rng.random((n, prob.d))
     X2[:] = prob.lower + (prob.upper - prob.lower) * rng.random((n, prob.d))
-    out = g.Population(pinned((n, prob.d)), pinned((n, prob.m)), pinned((n, prob.n_constraints)), pinned(n))
-    e2e_cfg = g.RunConfig(n=n, k_max=args.steps, seed=11 + rank, op=op, device=local)
-    eng2 = g.Engine(prob, e2e_cfg)
+    if world == 1:
+        eng2 = g.Engine(prob, g.RunConfig(n=n, k_max=args.steps, seed=11, op=op, device=local))
+        step1 = lambda: eng2.step(1)  # noqa: E731
+    else:
+        sh2 = GpuShard(prob, g.RunConfig(n=n, k_max=args.steps, seed=11, op=op, device=local,
+                                         stream=stream.cuda_stream), world, rank, TorchComm())
+        eng2 = sh2.eng
+        step1 = sh2.step
+    rows = eng2.rows_owned
+    out = g.Population(pinned((rows, prob.d)), pinned((rows, prob.m)), pinned((rows, prob.n_constraints)),
+                       pinned(rows))
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     eng2.set_population(1, X1)
     eng2.set_population(2, X2)
+    if world > 1:
+        sh2._z_allreduce()
     for _ in range(args.steps):
-        eng2.step(1)
+        step1()
         eng2.last_record()  # D2H of the generation's record (feasible ratio), host-synchronous
     pop = eng2.population(1, out=out)
     t1 = time.perf_counter()
     e2e_s = t1 - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
     h2d = X1.nbytes + X2.nbytes
     d2h = 48 * args.steps + pop.X.nbytes + pop.F.nbytes + pop.C.nbytes + pop.cv.nbytes
-    e2e = {"value": world * 2 * n * args.steps / e2e_s, "unit": "ind-gen/s",
+    e2e = {"value": 2 * n * args.steps / e2e_s, "unit": "ind-gen/s",
            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
            "note": "pinned host buffers: set_population x2 (H2D + evaluation) + K x (step + GenRecord "
-                   "read) + final pop1 (X, F, C, cv) D2H, host wall clock"}
+                   "read) + final pop1 (X, F, C, cv) D2H, host wall clock, max over ranks"}
     eng2.close()
 
     if rank != 0:
@@ -283,7 +313,7 @@ def main():
             threads = max(1, min(os.cpu_count() or 1, 8))
             v, secs, kind = cpu_reference(problem, n, op, args.cpu_gens, 0, threads, topo=topo)
             cpu = {"value": v, "unit": "ind-gen/s", "cores": threads, "kind": kind,
-                   "sample": f"{threads} independent reference runs x {args.cpu_gens} generations of "
+                   "sample": f"{threads} concurrent reference runs x {args.cpu_gens} generations of "
                              f"N={n} ({secs:.1f} s), topology injected, setup untimed"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "ind-gen/s", "cores": 0, "kind": "reference",
@@ -291,10 +321,11 @@ def main():
     eng.close()
 
     line = {"metric": METRIC, "value": value, "unit": "ind-gen/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong",  # N = 1M slots in total, split into weight-region shards
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (Philox-initialised populations)",
             "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": int(args.steps * 5)}
+            "clocks": clocks.summary(), "gpu_launches": int(args.steps * 5 + 1)}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -428,19 +428,22 @@ struct PopBuf {
 // ---------------------------------------------------------------- kernel dispatch
 using VaryKernel = void (*)(VaryParams);
 
-template <class Ev>
+template <class Ev, int DC = 0>
 VaryKernel pick_vary(int mode, int op) {
     if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
     if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
-    return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX>;
+    return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC>;
 }
 
-VaryKernel vary_kernel_for(int fam, int mode, int op) {
+// the generation kernel is compiled for the registered suites' dimension
+VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0) {
     switch (fam) {
-        case FAM_LIR: return pick_vary<EvalLir>(mode, op);
-        case FAM_DTLZ: return pick_vary<EvalDtlz>(mode, op);
+        case FAM_LIR: return d == 30 ? pick_vary<EvalLir, 30>(mode, op) : pick_vary<EvalLir>(mode, op);
+        case FAM_DTLZ:
+            return d == 7 ? pick_vary<EvalDtlz, 7>(mode, op)
+                          : (d == 12 ? pick_vary<EvalDtlz, 12>(mode, op) : pick_vary<EvalDtlz>(mode, op));
         case FAM_WTA: return pick_vary<EvalWta>(mode, op);
-        default: return pick_vary<EvalMw>(mode, op);
+        default: return d == 15 ? pick_vary<EvalMw, 15>(mode, op) : pick_vary<EvalMw>(mode, op);
     }
 }
 
@@ -761,7 +764,7 @@ struct gmpea_engine {
             vp.out[q] = off[q].X.p;
             vp.outFcv[q] = off[q].Fcv.p;
         }
-        vary = vary_kernel_for(p->fam, MODE_VARY, c.op);
+        vary = vary_kernel_for(p->fam, MODE_VARY, c.op, d);
         vp.row0 = (int)(v0 - e0);
         vp.row_end = (int)(v1 - e0);
         op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p},
@@ -1344,7 +1347,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.st = st.p;
         vp.bad_rows[0] = bad.p;
         vp.bad_cap = 0;  // reproduce itself never throws on bounds
-        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op), vp, 1, s);
+        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op, d), vp, 1, s);
         CK(cudaGetLastError());
         from_rows_kernel<<<blocks_for(n * d, 256), 256>>>((const float*)Op.p, geo.rs4 * 4, n, 0, d, h.p);
         CK(cudaMemcpy(off, h.p, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToHost));

@@ -149,6 +149,19 @@ __device__ __forceinline__ float clamp_ref(float v, float lo, float hi) {
     return v < lo ? lo : (hi < v ? hi : v);  // NaN passes through (std::clamp)
 }
 
+// y^e1 for the mutation; eta_m + 1 is an integer in practice (default 21):
+// square-and-multiply then, powf otherwise
+__device__ __forceinline__ float pow_e1(float y, float e1) {
+    const int k = (int)e1;
+    if ((float)k != e1 || k < 1 || k > 64) return powf(y, e1);
+    float r = 1.0f, b = y;
+    for (int e = k; e; e >>= 1) {
+        if (e & 1) r *= b;
+        b *= b;
+    }
+    return r;
+}
+
 // gmpea.cpp:135-160 for one gene; w = the MU draw.  Both branches share one
 // pair of powf: for u < 0.5  dq = (2u + (1-2u)(1-d1)^e1)^einv - 1, otherwise
 // dq = 1 - (2(1-u) + 2(u-0.5)(1-d2)^e1)^einv; the operands are selected first
@@ -163,7 +176,7 @@ __device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned 
     const float B = low ? (float)(0x80000000u - w) * 0x1.0p-31f                          // 1 - 2u
                         : (float)(w - 0x80000000u) * 0x1.0p-31f;                         // 2(u-0.5)
     const float dd = (low ? (x - lo) : (hi - x)) / span;                                 // d1 / d2
-    const float r = powf(A + B * powf(1.0f - dd, e1), einv);
+    const float r = powf(A + B * pow_e1(1.0f - dd, e1), einv);
     const float dq = low ? r - 1.0f : 1.0f - r;
     return x + dq * span;
 }
@@ -240,7 +253,9 @@ __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, 
 #ifndef GMPEA_VARY_MINBLOCKS
 #define GMPEA_VARY_MINBLOCKS 8
 #endif
-template <class Ev, int MODE, int OP>
+// DC > 0 compiles the kernel for a fixed decision dimension (the registered
+// suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
+template <class Ev, int MODE, int OP, int DC = 0>
 __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
     extern __shared__ float4 sm4[];
     DevState* st = p.st;
@@ -250,7 +265,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
     const int i0 = p.row0 + blockIdx.x * blockDim.x;
     const int i = i0 + tid;
     const bool active = i < p.row_end;
-    const int d = p.P.d;
+    const int d = DC > 0 ? DC : p.P.d;
     const int rs4 = p.rs4;
     const unsigned gen = p.fixed_gen >= 0 ? (unsigned)p.fixed_gen : (unsigned)st->gen;
     const unsigned slot = (unsigned)(p.slot_base + i);
