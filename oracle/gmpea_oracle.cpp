@@ -852,6 +852,19 @@ struct Keyed {
         uint64_t v = (uint64_t)o[1] << 32 | o[0];
         return static_cast<double>(v >> 11) * 0x1.0p-53;
     }
+    // 32-bit coin of gene j: head = 16-bit half j % 8 of index j / 8 of the
+    // coin stream, tail = low 16 bits of index j of the refinement stream
+    double coin(uint32_t stream, uint32_t ref_stream, uint32_t j) {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, stream), j / 8};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        uint32_t word = o[(j % 8) / 2];
+        uint32_t head = (j % 2) ? (word >> 16) : (word & 0xffffu);
+        uint32_t rc[4] = {slot, gen, orc_tag(pop, ref_stream), j};
+        orc_philox4x32_10(rc, key, o);
+        uint32_t tail = o[0] & 0xffffu;
+        return static_cast<double>((head << 16) | tail) * 0x1.0p-32;
+    }
     // four genes per counter: gene j is word j % 4 of index j / 4
     double word(uint32_t stream, uint32_t j) {
         uint32_t ctr[4] = {slot, gen, orc_tag(pop, stream), j / 4};
@@ -874,7 +887,7 @@ struct OpParams {
 // gmpea.cpp:135-160 for one gene: the skip coin comes from MCOIN, the
 // direction uniform from MU (drawn only for mutated genes)
 void pm_gene(double& x, double lo, double hi, double pm, double eta, Keyed& k, uint32_t j) {
-    if (k.word(ORC_STREAM_MCOIN, j) > pm) return;
+    if (k.coin(ORC_STREAM_MCOIN, ORC_STREAM_MREF, j) > pm) return;
     double span = hi - lo;
     if (span <= 0.0) return;
     double u = k.mu(j), dq;
@@ -929,7 +942,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
             if (op == 0) {
                 if (!cross) {
                     c = xa[j];
-                } else if (k.word(ORC_STREAM_XCOIN, uj) <= 0.5) {
+                } else if (k.coin(ORC_STREAM_XCOIN, ORC_STREAM_XREF, uj) <= 0.5) {
                     double u = k.word(ORC_STREAM_XU, uj);
                     double beta = u <= 0.5 ? std::pow(2.0 * u, 1.0 / (prm.sbx_eta + 1.0))
                                            : std::pow(1.0 / (2.0 * (1.0 - u)), 1.0 / (prm.sbx_eta + 1.0));
@@ -940,7 +953,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
             } else {
                 // CR >= 1 decides the coin without drawing it (u < 1 <= CR)
                 bool take = static_cast<size_t>(j) == jrand || prm.de_cr >= 1.0 ||
-                            k.word(ORC_STREAM_XCOIN, uj) < prm.de_cr;
+                            k.coin(ORC_STREAM_XCOIN, ORC_STREAM_XREF, uj) < prm.de_cr;
                 c = take ? base[j] + prm.de_f * (xa[j] - xb[j]) : base[j];
             }
             pm_gene(c, p.lo[j], p.hi[j], pm, prm.pm_eta, k, uj);

@@ -13,10 +13,13 @@
  *   tag(pop, stream) = (pop << 28) | (stream << 20)
  * streams: INIT (initial population, gen = 0; two 64-bit draws per counter),
  * PICK (neighbour draws and DE jrand: a sequence of 64-bit draws, two per
- * counter), CHILD (the SBX per-child coin, one 53-bit uniform), XCOIN (SBX
- * per-gene coin / DE CR coin), XU (SBX spread uniform), MCOIN (PM coin) —
- * these three give four genes per counter, gene j = word j%4 of index j/4,
- * u = w * 2^-32 — and MU (PM direction, index j, word 0).
+ * counter), CHILD (the SBX per-child coin, one 53-bit uniform), XU (SBX
+ * spread uniform: gene j = word j%4 of index j/4, u = w * 2^-32), MU (PM
+ * direction, index j, word 0) and the two coin streams XCOIN (SBX per-gene
+ * coin / DE CR coin) and MCOIN (PM coin).  A coin is the 32-bit value
+ * w = (h << 16) | l: its head h is 16-bit half j%8 of index j/8 of the coin
+ * stream (word (j%8)/2, low half first), its tail l the low 16 bits of word 0
+ * of index j of XREF / MREF; u = w * 2^-32 as for every other draw.
  */
 #ifndef GMPEA_ORACLE_PHILOX_H
 #define GMPEA_ORACLE_PHILOX_H
@@ -24,7 +27,8 @@
 
 enum {
     ORC_STREAM_INIT = 1, ORC_STREAM_PICK = 2, ORC_STREAM_CHILD = 3,
-    ORC_STREAM_XCOIN = 5, ORC_STREAM_XU = 6, ORC_STREAM_MCOIN = 7, ORC_STREAM_MU = 8
+    ORC_STREAM_XCOIN = 5, ORC_STREAM_XU = 6, ORC_STREAM_MCOIN = 7, ORC_STREAM_MU = 8,
+    ORC_STREAM_XREF = 9, ORC_STREAM_MREF = 10
 };
 
 static inline uint32_t orc_tag(uint32_t pop, uint32_t stream) {

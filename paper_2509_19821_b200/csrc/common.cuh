@@ -1,9 +1,8 @@
 // Common device definitions for the GMPEA-B200 engine (sm_100a).
 //
-// Layout conventions:
-//   * populations are structure-of-arrays fp32 planes with leading dimension
-//     `ld` (N rounded up to a multiple of 32): X[j*ld + i] gene j of slot i,
-//     G[k*ld + i] raw constraint k, and the selection keys packed per slot as
+// Layout conventions (DESIGN.md §3 "Data layout in HBM"):
+//   * individuals are padded fp32 rows [x_0..x_{d-1} | g_0..g_{nc-1} | pad] of
+//     rs4 float4, and the selection keys are packed per slot as
 //     Fcv[i] = float4{f0, f1, f2, cv} (m <= 3; unused lanes are 0).
 //   * reference vectors are kept twice: exact fp64 lattice values only during
 //     setup (neighbourhoods are decided by fp64 distances, gmpea.cpp:84-97),
@@ -80,10 +79,12 @@ enum : unsigned {
     STREAM_INIT = 1,   // initial population, pair of 64-bit draws per counter
     STREAM_PICK = 2,   // neighbour picks / DE jrand: 64-bit draw sequence
     STREAM_CHILD = 3,  // SBX per-child crossover coin (53-bit uniform)
-    STREAM_XCOIN = 5,  // per-gene SBX coin / DE CR coin, 4 genes per counter
+    STREAM_XCOIN = 5,  // per-gene SBX coin / DE CR coin: 16-bit heads, 8 genes per counter
     STREAM_XU = 6,     // per-gene SBX spread uniform, 4 genes per counter
-    STREAM_MCOIN = 7,  // per-gene PM coin, 4 genes per counter
+    STREAM_MCOIN = 7,  // per-gene PM coin: 16-bit heads, 8 genes per counter
     STREAM_MU = 8,     // PM direction uniform, one counter per mutated gene
+    STREAM_XREF = 9,   // low 16 bits of an XCOIN coin whose head ties the threshold
+    STREAM_MREF = 10,  // low 16 bits of an MCOIN coin whose head ties the threshold
 };
 
 __host__ __device__ inline unsigned philox_tag(unsigned pop, unsigned stream) {

@@ -428,11 +428,14 @@ struct PopBuf {
 // ---------------------------------------------------------------- kernel dispatch
 using VaryKernel = void (*)(VaryParams);
 
+// the dimension-specialised generation kernels also assume uniform bounds
+// (true of every registered suite; checked by the caller)
 template <class Ev, int DC = 0>
 VaryKernel pick_vary(int mode, int op) {
     if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
     if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
-    return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC>;
+    constexpr bool UB = DC > 0;
+    return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC, UB> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UB>;
 }
 
 // the generation kernel is compiled for the registered suites' dimension
@@ -468,10 +471,11 @@ void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
     const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / (double)d;
     // PM: skip iff u > pm with u = w 2^-32  <=>  mutate iff w <= floor(pm 2^32)
     const double T = pm * 4294967296.0;
-    vp.pm_thr = pm < 0.0 ? -1 : (long long)std::min(std::floor(T), 4294967295.0);
-    // DE: take iff u < CR  <=>  w < ceil(CR 2^32)
+    vp.pm_T = pm < 0.0 ? -1 : (long long)std::min(std::floor(T), 4294967295.0);
+    // DE: take iff u < CR  <=>  w < ceil(CR 2^32)  <=>  w <= ceil(CR 2^32) - 1
     const double C = prm.de_cr * 4294967296.0;
-    vp.cr_thr = prm.de_cr >= 1.0 ? 0x100000000ull : (prm.de_cr <= 0.0 ? 0ull : (unsigned long long)std::ceil(C));
+    vp.de_T = prm.de_cr >= 1.0 ? 0xffffffffll : (prm.de_cr <= 0.0 ? -1ll : (long long)std::ceil(C) - 1);
+    vp.uid = make_uidx((unsigned long long)d);
     vp.de_f = (float)prm.de_f;
 }
 
@@ -733,6 +737,8 @@ struct gmpea_engine {
         vp.P = p->dev;
         vp.t[0] = t1;
         vp.t[1] = t2;
+        vp.ui[0] = make_uidx((unsigned long long)t1);
+        vp.ui[1] = make_uidx((unsigned long long)t2);
         vp.key0 = (unsigned)c.seed;
         vp.key1 = (unsigned)(c.seed >> 32);
         fill_op_params(vp, c.params, d);
@@ -764,7 +770,7 @@ struct gmpea_engine {
             vp.out[q] = off[q].X.p;
             vp.outFcv[q] = off[q].Fcv.p;
         }
-        vary = vary_kernel_for(p->fam, MODE_VARY, c.op, d);
+        vary = vary_kernel_for(p->fam, MODE_VARY, c.op, p->dev.uniform ? d : 0);
         vp.row0 = (int)(v0 - e0);
         vp.row_end = (int)(v1 - e0);
         op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p},
@@ -1335,6 +1341,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.parX[0] = Xp.p;
         vp.B[0] = bi.p;
         vp.t[0] = t;
+        vp.ui[0] = make_uidx((unsigned long long)t);
         vp.out[0] = Op.p;
         vp.key0 = (unsigned)seed;
         vp.key1 = (unsigned)(seed >> 32);
@@ -1347,7 +1354,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.st = st.p;
         vp.bad_rows[0] = bad.p;
         vp.bad_cap = 0;  // reproduce itself never throws on bounds
-        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op, d), vp, 1, s);
+        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op, p->dev.uniform ? d : 0), vp, 1, s);
         CK(cudaGetLastError());
         from_rows_kernel<<<blocks_for(n * d, 256), 256>>>((const float*)Op.p, geo.rs4 * 4, n, 0, d, h.p);
         CK(cudaMemcpy(off, h.p, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToHost));

@@ -29,6 +29,20 @@ namespace gmpea_b200 {
 enum : int { OP_SBX = 0, OP_DE = 1 };
 enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
 
+// a divisor of uniform_index with its rejection limit and 64-bit reciprocal
+struct UIdx {
+    unsigned long long n, lim, mag;
+};
+__host__ inline UIdx make_uidx(unsigned long long n) {
+    UIdx u;
+    u.n = n;
+    u.lim = ~0ull - (~0ull % n);
+    u.mag = ~0ull / n;  // floor((2^64 - 1) / n) == floor(2^64 / n) unless n | 2^64
+    if (n && (n & (n - 1)) == 0) u.mag = n == 1 ? ~0ull : (1ull << 63) / (n >> 1);
+    return u;
+}
+
+
 struct VaryParams {
     int n;                   // local rows per population (buffer extent)
     int row0, row_end;       // rows [row0, row_end) are produced by this launch
@@ -47,8 +61,9 @@ struct VaryParams {
     float sbx_e;             // 1 / (eta_c + 1)
     float pm_e1;             // eta_m + 1
     float pm_einv;           // 1 / (eta_m + 1)
-    long long pm_thr;        // mutate iff w <= pm_thr (w: 32-bit draw)
-    unsigned long long cr_thr; // DE: take iff w < cr_thr (>= 2^32: always)
+    long long pm_T;          // PM: mutate iff w <= pm_T (w: 32-bit coin; -1 never)
+    long long de_T;          // DE: take iff w <= de_T (>= 2^32 - 1: always)
+    UIdx ui[2], uid;         // uniform_index divisors: t per population, d (jrand)
     float de_f;
     int eval;                // evaluate the child (0: reproduce only)
     int update_z;
@@ -119,6 +134,43 @@ struct Emitter {
 };
 
 // ---- Philox-keyed draws
+// 16-bit coin h of a gene, refined to an exact 32-bit comparison w <= thr:
+// with w = h * 2^16 + l,  w <= thr  <=>  h < thr_hi  or  (h == thr_hi and l <= thr_lo),
+// where l (the low half) is drawn from its own counter only in the rare tie.
+__device__ __forceinline__ unsigned half16(const u32x4& w, int k8) {
+    const unsigned word = (k8 >> 1) == 0 ? w.x : ((k8 >> 1) == 1 ? w.y : ((k8 >> 1) == 2 ? w.z : w.w));
+    return (k8 & 1) ? (word >> 16) : (word & 0xffffu);
+}
+
+// Eight exact 32-bit coins "w <= T" (T in [-1, 2^32 - 1]) from the 16-bit
+// heads of one counter: bit k is set when gene j0 + k wins.  A head equal to
+// T's head is refined with the tail drawn from its own counter (probability
+// 2^-16 per gene), so the result equals the full 32-bit comparison.
+__device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngenes, unsigned slot, unsigned gen,
+                                           unsigned tag_ref, unsigned j0, unsigned k0, unsigned k1) {
+    if (T < 0) return 0u;
+    if (T >= 0xffffffffll) return (1u << ngenes) - 1u;
+    const unsigned thi = (unsigned)(T >> 16), tlo = (unsigned)(T & 0xffff);
+    const unsigned words[4] = {w.x, w.y, w.z, w.w};
+    unsigned win = 0u, tie = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const unsigned h = (k & 1) ? (words[k >> 1] >> 16) : (words[k >> 1] & 0xffffu);
+        win |= (unsigned)(h < thi) << k;
+        tie |= (unsigned)(h == thi) << k;
+    }
+    const unsigned valid = (1u << ngenes) - 1u;
+    win &= valid;
+    tie &= valid;
+    while (tie) {  // rare
+        const int k = __ffs(tie) - 1;
+        tie &= tie - 1u;
+        const unsigned l = philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, k0, k1).x & 0xffffu;
+        win |= (unsigned)(l <= tlo) << k;
+    }
+    return win;
+}
+
 struct PickStream {
     unsigned slot, gen, tag, k0, k1;
     unsigned q;
@@ -130,14 +182,18 @@ struct PickStream {
         ++q;
         return v;
     }
-    // rng.hpp:23-30: uniform integer in [0, n) by rejection
-    __device__ __forceinline__ unsigned index(unsigned n) {
-        const unsigned long long lim = ~0ull - (~0ull % n);
+    // rng.hpp:23-30: uniform integer in [0, n) by rejection; the division is
+    // a precomputed reciprocal (UIdx): q = hi64(v * floor(2^64 / n)) is
+    // floor(v / n) or one less, so one correction makes v % n exact
+    __device__ __forceinline__ unsigned index(const UIdx& u) {
         unsigned long long v;
         do {
             v = next();
-        } while (v >= lim);
-        return (unsigned)(v % n);
+        } while (v >= u.lim);
+        const unsigned long long q = __umul64hi(v, u.mag);
+        unsigned long long r = v - q * u.n;
+        if (r >= u.n) r -= u.n;
+        return (unsigned)r;
     }
 };
 
@@ -175,16 +231,25 @@ __device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned 
                         : (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;   // 2(1-u)
     const float B = low ? (float)(0x80000000u - w) * 0x1.0p-31f                          // 1 - 2u
                         : (float)(w - 0x80000000u) * 0x1.0p-31f;                         // 2(u-0.5)
-    const float dd = (low ? (x - lo) : (hi - x)) / span;                                 // d1 / d2
-    const float r = powf(A + B * pow_e1(1.0f - dd, e1), einv);
+    const float dd = (low ? (x - lo) : (hi - x)) * (span == 1.0f ? 1.0f : 1.0f / span);  // d1 / d2
+    // (base)^(1/(eta+1)) with base in [0, 2] (NaN for the reference's negative-base
+    // hazard, which then fails the bounds check as in gmpea.cpp:146-150)
+    const float base = A + B * pow_e1(1.0f - dd, e1);
+    const float r = base == 0.0f ? 0.0f : exp2f(einv * __log2f(base));
     const float dq = low ? r - 1.0f : 1.0f - r;
     return x + dq * span;
 }
 
+// SBX spread factor (gmpea.cpp:121-124): u <= 0.5: (2u)^e, else
+// (1 / (2(1-u)))^e = (2(1-u))^-e with 2(1-u) = (2^32 - w) 2^-31 > 0.  The base
+// lies in (0, 2] and e = 1/(eta+1) is small, so exp2(e log2 b) through the
+// MUFU pair is accurate to ~2 ulp here (the child differs from the f64 oracle
+// by < 1e-6 of the parents' spread) at a fraction of powf's cost.
 __device__ __forceinline__ float sbx_beta(unsigned w, float e) {
-    if (w <= 0x80000000u) return powf((float)w * 0x1.0p-31f, e);  // u <= 0.5: (2u)^e
-    // u > 0.5: (1 / (2 (1 - u)))^e with 2(1-u) = (2^32 - w) 2^-31 > 0
-    return powf(1.0f / ((float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f), e);
+    const bool low = w <= 0x80000000u;
+    const float b = low ? (float)w * 0x1.0p-31f : (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;
+    if (b == 0.0f) return 0.0f;  // u = 0: beta = 0
+    return exp2f((low ? e : -e) * __log2f(b));
 }
 
 template <class T>
@@ -197,17 +262,19 @@ __device__ __forceinline__ T warp_min(T v) {
     return v;
 }
 
-// Warp-cooperative polynomial mutation.  Every lane holds a 64-bit mask of
-// the genes [w0, w0 + 64) its child mutates; the warp numbers all tasks by an
+// Block-cooperative polynomial mutation.  Every thread holds a 64-bit mask of
+// the genes [w0, w0 + 64) its child mutates; the block numbers all tasks by an
 // exclusive scan of the mask popcounts and, round by round, the owners post
-// 32 tasks to shared memory and lane k runs task k on the owner's staged row
-// with the owner's Philox key.  Must be reached by all lanes of the warp.
+// blockDim tasks to shared memory and thread k runs task k on the owner's
+// staged row with the owner's Philox key (~1 round per block: PM picks ~1 of
+// d genes per child).  Must be reached by every thread of the block.
 template <class VP>
 __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, int w0, float4* sm4,
                                          unsigned gen, unsigned pid, int i0) {
-    __shared__ unsigned task[4][32];  // (owner lane << 16) | gene
+    __shared__ unsigned task[128];  // (owner thread << 16) | gene
+    __shared__ int wsum[4];
     const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
     const int cnt = __popcll(mmask);
     int incl = cnt;
 #pragma unroll
@@ -215,30 +282,35 @@ __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, 
         const int v = __shfl_up_sync(FULL, incl, o);
         if (lane >= o) incl += v;
     }
-    const int total = __shfl_sync(FULL, incl, 31);
-    const int excl = incl - cnt;
-    for (int r0 = 0; r0 < total; r0 += 32) {
-        // post my tasks with global index in [r0, r0 + 32)
-        if (excl < r0 + 32 && incl > r0) {
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    int base = 0, total = 0;
+    for (int w = 0; w < nw; ++w) {
+        base += w < wid ? wsum[w] : 0;
+        total += wsum[w];
+    }
+    const int excl = base + incl - cnt, inc = base + incl;
+    const int bs = blockDim.x;
+    for (int r0 = 0; r0 < total; r0 += bs) {
+        if (excl < r0 + bs && inc > r0) {  // post my tasks with index in [r0, r0 + bs)
             unsigned long long mm = mmask;
-            for (int t = excl; t < incl && t < r0 + 32; ++t) {
+            for (int t = excl; t < inc && t < r0 + bs; ++t) {
                 const int b = __ffsll((long long)mm) - 1;
                 mm &= mm - 1ull;
-                if (t >= r0) task[wid][t - r0] = ((unsigned)lane << 16) | (unsigned)(w0 + b);
+                if (t >= r0) task[t - r0] = ((unsigned)tid << 16) | (unsigned)(w0 + b);
             }
         }
-        __syncwarp();
-        if (r0 + lane < total) {
-            const unsigned tk = task[wid][lane];
-            const int owner = (int)(tk >> 16), j = (int)(tk & 0xffffu);
-            const int row = wid * 32 + owner;
+        __syncthreads();
+        if (r0 + tid < total) {
+            const unsigned tk = task[tid];
+            const int row = (int)(tk >> 16), j = (int)(tk & 0xffffu);
             float* x = reinterpret_cast<float*>(sm4 + row * p.srs4);
             const unsigned slot = (unsigned)(p.slot_base + i0 + row);
             const float lo = p.P.lob(j), hi = p.P.hib(j);
             const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key0, p.key1);
             x[j] = clamp_ref(pm_apply(x[j], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
         }
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -255,7 +327,7 @@ __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, 
 #endif
 // DC > 0 compiles the kernel for a fixed decision dimension (the registered
 // suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
-template <class Ev, int MODE, int OP, int DC = 0>
+template <class Ev, int MODE, int OP, int DC = 0, bool UB = false>
 __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
     extern __shared__ float4 sm4[];
     DevState* st = p.st;
@@ -271,6 +343,10 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
     const unsigned slot = (unsigned)(p.slot_base + i);
     const unsigned pid = (unsigned)p.pop_id[pi];
     const ProbDev& P = p.P;
+    // UB: every gene shares [ulo, uhi] (all registered suites), no per-gene loads
+    const float ulo = P.ulo, uhi = P.uhi;
+#define GMPEA_LO(j) (UB ? ulo : P.lob(j))
+#define GMPEA_HI(j) (UB ? uhi : P.hib(j))
     float4* my4 = sm4 + tid * p.srs4;
     float* my = reinterpret_cast<float*>(my4);
 
@@ -293,9 +369,9 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
             if (MODE == MODE_VARY && active) {
                 const int t = p.t[pi];
                 PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key0, p.key1, 0u, {}};
-                unsigned a = ps.index((unsigned)t);
-                unsigned b = ps.index((unsigned)t);
-                while (t > 1 && b == a) b = ps.index((unsigned)t);
+                unsigned a = ps.index(p.ui[pi]);
+                unsigned b = ps.index(p.ui[pi]);
+                while (t > 1 && b == a) b = ps.index(p.ui[pi]);
                 const int* Brow = p.B[pi] + (long long)i * t;
                 PA += (long long)Brow[a] * rs4;
                 PB += (long long)Brow[b] * rs4;
@@ -303,21 +379,19 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                     u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
                     cross = u53(c.x, c.y) <= p.sbx_prob;
                 } else {
-                    jrand = (int)ps.index((unsigned)d);
+                    jrand = (int)ps.index(p.uid);
                 }
             }
-            const bool de_all = p.cr_thr >= 0x100000000ull;
+            const bool de_all = p.de_T >= 0xffffffffll;
+            const unsigned k0 = p.key0, k1 = p.key1;
             for (int w0 = 0; w0 < d; w0 += 64) {
                 const int w1 = min(d, w0 + 64);
                 unsigned long long mmask = 0ull;
-                for (int jb = w0; jb < w1 && active; jb += 4) {
-                    const int q = jb >> 2;
-                    u32x4 xc{0, 0, 0, 0}, xu{0, 0, 0, 0}, mc{0, 0, 0, 0};
-                    float4 out;
-                    if (MODE == MODE_INIT) {  // 64-bit pair (j % 2) of counter j / 2
-                        xc = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), p.key0, p.key1);
-                        xu = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, p.key0,
-                                           p.key1);
+                if (MODE == MODE_INIT) {
+                    for (int jb = w0; jb < (active ? w1 : w0); jb += 4) {  // 64-bit pair (j % 2) of counter j / 2
+                        const u32x4 xa = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), k0, k1);
+                        const u32x4 xb =
+                            philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, k0, k1);
                         float v[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
@@ -326,57 +400,87 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                                 v[k] = 0.0f;
                                 continue;
                             }
-                            const u32x4& w = k < 2 ? xc : xu;
+                            const u32x4& w = k < 2 ? xa : xb;
                             const double u = (k & 1) ? u53(w.z, w.w) : u53(w.x, w.y);
-                            const double lo = P.lob(j), hi = P.hib(j);
+                            const double lo = GMPEA_LO(j), hi = GMPEA_HI(j);
                             v[k] = (float)(lo + (hi - lo) * u);
                         }
-                        out = make_float4(v[0], v[1], v[2], v[3]);
-                    } else {
-                        const unsigned idx4 = (unsigned)q;
+                        my4[jb >> 2] = make_float4(v[0], v[1], v[2], v[3]);
+                    }
+                } else {
+                    // eight genes per group: one XCOIN and one MCOIN counter (16-bit coin
+                    // heads), two XU counters (32-bit spread uniforms)
+                    if (active)
+#pragma unroll 1
+                    for (int jb = w0; jb < w1; jb += 8) {
+                        const int q = jb >> 2;
+                        const bool two = jb + 4 < w1;
+                        u32x4 xc{0, 0, 0, 0}, mc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0};
+                        const unsigned idx8 = (unsigned)(jb >> 3);
                         if (OP == OP_SBX && cross) {
-                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
-                            xu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), idx4, p.key0, p.key1);
+                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, k0, k1);
+                            xu0 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q, k0, k1);
+                            if (two) xu1 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q + 1u, k0, k1);
                         }
-                        if (OP == OP_DE && !de_all)
-                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx4, p.key0, p.key1);
-                        if (p.pm_thr >= 0)
-                            mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx4, p.key0, p.key1);
-                        const float4 a4 = PA[q], b4 = PB[q];
-                        const float4 c4 = OP == OP_DE ? PC[q] : a4;
-                        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
-                        const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
-                        const float cvv[4] = {c4.x, c4.y, c4.z, c4.w};
-                        float v[4];
+                        if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, k0, k1);
+                        if (p.pm_T >= 0) mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, k0, k1);
+                        float4 a4[2], b4[2], c4[2];
+                        a4[0] = PA[q];
+                        b4[0] = PB[q];
+                        c4[0] = OP == OP_DE ? PC[q] : a4[0];
+                        if (two) {
+                            a4[1] = PA[q + 1];
+                            b4[1] = PB[q + 1];
+                            c4[1] = OP == OP_DE ? PC[q + 1] : a4[1];
+                        } else {
+                            a4[1] = b4[1] = c4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                        const int ng = min(8, w1 - jb);
+                        // per-gene SBX coin u <= 0.5 <=> w <= 2^31 (gmpea.cpp:119), DE CR coin, PM coin
+                        const unsigned xbits =
+                            OP == OP_SBX ? (cross ? coins8(xc, 0x80000000ll, ng, slot, gen, philox_tag(pid, STREAM_XREF),
+                                                           (unsigned)jb, k0, k1)
+                                                  : 0u)
+                                         : (de_all ? (1u << ng) - 1u
+                                                   : coins8(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
+                                                            (unsigned)jb, k0, k1));
+                        const unsigned mbits = coins8(mc, p.pm_T, ng, slot, gen, philox_tag(pid, STREAM_MREF),
+                                                      (unsigned)jb, k0, k1);
+                        float v[8];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) {
+                        for (int k = 0; k < 8; ++k) {
                             const int j = jb + k;
                             if (j >= w1) {
                                 v[k] = 0.0f;
                                 continue;
                             }
+                            const float4& A = a4[k >> 2];
+                            const float4& Bv = b4[k >> 2];
+                            const float4& Cv = c4[k >> 2];
+                            const int kk = k & 3;
+                            const float av = kk == 0 ? A.x : (kk == 1 ? A.y : (kk == 2 ? A.z : A.w));
+                            const float bv = kk == 0 ? Bv.x : (kk == 1 ? Bv.y : (kk == 2 ? Bv.z : Bv.w));
+                            const float cvv = kk == 0 ? Cv.x : (kk == 1 ? Cv.y : (kk == 2 ? Cv.z : Cv.w));
+                            const bool xk = (xbits >> k) & 1u;
                             float c;
                             if (OP == OP_SBX) {
-                                if (cross && pick_word(xc, k) <= 0x80000000u) {
-                                    const float beta = sbx_beta(pick_word(xu, k), p.sbx_e);
-                                    c = 0.5f * ((1.0f + beta) * av[k] + (1.0f - beta) * bv[k]);
+                                if (xk) {
+                                    const float beta = sbx_beta(pick_word(k < 4 ? xu0 : xu1, kk), p.sbx_e);
+                                    c = 0.5f * ((1.0f + beta) * av + (1.0f - beta) * bv);
                                 } else {
-                                    c = av[k];
+                                    c = av;
                                 }
                             } else {
-                                const bool take = j == jrand || de_all ||
-                                                  (unsigned long long)pick_word(xc, k) < p.cr_thr;
-                                c = take ? cvv[k] + p.de_f * (av[k] - bv[k]) : cvv[k];
+                                c = (j == jrand || xk) ? cvv + p.de_f * (av - bv) : cvv;
                             }
-                            if ((long long)pick_word(mc, k) <= p.pm_thr)
-                                mmask |= 1ull << (j - w0);  // mutated + clipped in phase 2
-                            else
-                                c = clamp_ref(c, P.lob(j), P.hib(j));
-                            v[k] = c;
+                            // mutated genes are clipped after PM (phase 2)
+                            const float cl = clamp_ref(c, GMPEA_LO(j), GMPEA_HI(j));
+                            v[k] = ((mbits >> k) & 1u) ? c : cl;
                         }
-                        out = make_float4(v[0], v[1], v[2], v[3]);
+                        mmask |= (unsigned long long)mbits << (jb - w0);
+                        my4[q] = make_float4(v[0], v[1], v[2], v[3]);
+                        if (two) my4[q + 1] = make_float4(v[4], v[5], v[6], v[7]);
                     }
-                    my4[q] = out;
                 }
                 // phase 2: polynomial mutation then clip (gmpea.cpp:202-203).
                 // The warp's mutation tasks (lane, gene) are dealt round-robin
@@ -395,7 +499,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                 for (int k = 0; k < 4; ++k) {
                     const int j = jb + k;
                     if (j >= d) break;
-                    if (!(v[k] >= P.lob(j) && v[k] <= P.hib(j))) bad = true;
+                    if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
                     ev.gene(p.P, j, v[k]);
                 }
             }
@@ -447,6 +551,8 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
         if (v < *(volatile unsigned*)&st->zbits[k]) atomicMin(&st->zbits[k], v);
     }
 }
+#undef GMPEA_LO
+#undef GMPEA_HI
 
 // ---- PBI in fp32 on unit reference vectors (scalarize.cpp:72-89):
 // d1 = |(f - z) . u|, d2 = |(f - z) - d1 u|, g = d1 + theta d2.  Unused lanes

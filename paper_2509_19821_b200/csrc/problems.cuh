@@ -156,8 +156,11 @@ struct EvalDtlz {
     __device__ __forceinline__ void begin(const ProbDev&) { rast = sph = 0.0; }
     __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
         const double x = xf;
-        if (j < P.m - 1) {
-            pos[j] = x;
+        if (j < P.m - 1) {  // static indices keep pos[] in registers
+            if (j == 0)
+                pos[0] = x;
+            else
+                pos[1] = x;
             return;
         }
         double t = x - 0.5;  // problems.cpp:144-147, 153-155
@@ -268,19 +271,24 @@ struct EvalMw {
     __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
         const double x = xf;
         const int n = P.d, m = P.m;
-        if (j < m - 1) {
-            xs[j] = x;
+        if (j < m - 1) {  // static indices keep xs[] in registers
+            if (j == 0)
+                xs[0] = x;
+            else
+                xs[1] = x;
             prev = x;
             return;
         }
         int kd = kind(P.id);
+        // per-gene terms: argument in fp64, the exponential / cosine in fp32
+        // (each term < 1e-7 off; the sum accumulates in fp64)
         if (kd == 0) {
-            double t = ipow(x, n - m) - 0.5 - (double)j / (2.0 * n);
-            gs += 1.0 - exp(-10.0 * t * t);
+            double t = ipow(x, n - m) - 0.5 - (double)j * (0.5 / n);
+            gs += 1.0 - (double)expf((float)(-10.0 * t * t));
         } else if (kd == 1) {
-            double t = x - (double)j / n;
-            double z = 1.0 - exp(-10.0 * t * t);
-            gs += 1.5 + (0.1 / n) * z * z - 1.5 * cospi(2.0 * z);
+            double t = x - (double)j * (1.0 / n);
+            double z = 1.0 - (double)expf((float)(-10.0 * t * t));
+            gs += 1.5 + (0.1 / n) * z * z - 1.5 * (double)cospif((float)(2.0 * z));
         } else {
             double p = prev - 0.5;
             double t = x + p * p - 1.0;
@@ -314,8 +322,10 @@ struct EvalMw {
             }
             case 4: case 8: {
                 double g = gs;
+                // registered with m = 3: f = (1+g)(c0 c1, c0 s1, s0)
                 double c[2], s[2];
-                for (int i = 0; i < m - 1; ++i) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
                     if (id == 4) {
                         c[i] = xs[i];
                         s[i] = 1.0 - xs[i];
@@ -323,21 +333,16 @@ struct EvalMw {
                         sincospi(0.5 * xs[i], &s[i], &c[i]);
                     }
                 }
-                for (int k = 0; k < m; ++k) {
-                    double v = 1.0 + g;
-                    for (int i = 0; i + k + 1 < m; ++i) v *= c[i];
-                    if (k > 0) v *= s[m - 1 - k];
-                    f[k] = v;
-                }
+                f[0] = (1.0 + g) * c[0] * c[1];
+                f[1] = (1.0 + g) * c[0] * s[1];
+                f[2] = (1.0 + g) * s[0];
                 if (id == 4) {
-                    double l = f[m - 1], sum = 0.0;
-                    for (int k = 0; k + 1 < m; ++k) l -= f[k];
-                    for (int k = 0; k < m; ++k) sum += f[k];
+                    double l = f[2] - f[0] - f[1];
+                    double sum = f[0] + f[1] + f[2];
                     emit(0, sum - (1.0 + 0.4 * ipow(sinpi(2.5 * l), 8)));
                 } else {
-                    double q = 0.0;
-                    for (int k = 0; k < m; ++k) q += f[k] * f[k];
-                    double l = asin(f[m - 1] / sqrt(q));
+                    double q = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
+                    double l = asin(f[2] / sqrt(q));
                     double sn = sin(6.0 * l);
                     double t = 1.25 - 0.5 * sn * sn;
                     emit(0, q - t * t);
@@ -446,18 +451,19 @@ struct EvalMw {
                 emit(1, -(c * e));
                 return;
             }
-            default: {  // 14
+            default: {  // 14, registered with m = 3
                 double g = gs;
                 double s = 0.0, sa = 0.0;
-                for (int k = 0; k + 1 < m; ++k) {
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
                     f[k] = xs[k];
                     double q = f[k] * f[k];
                     double sn = sinpi(1.1 * q);
                     s += 6.0 - exp(f[k]) - 1.5 * sn;
                     sa += 6.1 - (1.0 + f[k] + 0.5 * q + 1.5 * sn);
                 }
-                f[m - 1] = (1.0 + g) / (m - 1) * s;
-                emit(0, f[m - 1] - 1.0 / (m - 1) * sa);
+                f[2] = (1.0 + g) / 2.0 * s;
+                emit(0, f[2] - 1.0 / 2.0 * sa);
                 return;
             }
         }
