@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for w in lircmop13-1m mw1-1m mw7-1m; do timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --workload $w > gpurun_out/bench_$w.log 2>&1; echo "$w rc=$?"; tail -1 gpurun_out/bench_$w.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['ms_per_step'], l['value']/1e9, l['roofline']['kernel_ms'])"; done
-python bench.py --steps 3 --warmup 2 --no-cpu-baseline --workload mw1-1m > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"vary_eval" -s 2 -c 1 -o gpurun_out/prof9_mw1 python bench.py --steps 3 --warmup 2 --no-cpu-baseline --workload mw1-1m > gpurun_out/ncu9.log 2>&1; echo ncu=$?
-python bench.py --steps 3 --warmup 2 --no-cpu-baseline > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"vary_eval|select" -s 2 -c 2 -o gpurun_out/prof9_lir python bench.py --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/ncu9b.log 2>&1; echo ncu=$?
+timeout 900 python tools/sweep.py > gpurun_out/sweep.log 2>&1; echo sweep=$?; tail -5 gpurun_out/sweep.log | cut -c1-200
+timeout 1200 python tools/quality_budget.py --budget 1.0 --seeds 3 > gpurun_out/quality.log 2>&1; echo q=$?; tail -40 gpurun_out/quality.log
+cp profiles/r01_sweep_mw7.json profiles/r01_quality_1s.json gpurun_out/ 2>/dev/null

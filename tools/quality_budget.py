@@ -1,0 +1,76 @@
+"""Fixed wall-clock quality comparison (BASELINE.json metric, second half:
+"IGD at fixed 1 s budget").
+
+For each problem, the reference's own run_gmpea (oracle/_ref, one host core,
+its time budget semantics gmpea.cpp:458,481-486) and the engine (one B200,
+identical semantics on the device clock) each get the same loop budget; the
+final pop1 is scored with the reference's metric_front + IGD against the
+reference's own 1000-point pf_reference front (tests/golden/fronts.npz).
+
+    python tools/quality_budget.py [--budget 1.0] [--seeds 3] [--out profiles/r01_quality_1s.json]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--budget", type=float, default=1.0)
+    ap.add_argument("--seeds", type=int, default=3)
+    ap.add_argument("--problems", default="LIRCMOP9,LIRCMOP13,C1-DTLZ1,LIRCMOP1,LIRCMOP5")
+    ap.add_argument("--gpu-n", default="1000,100000")
+    ap.add_argument("--ref-n", type=int, default=1000)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_quality_1s.json"))
+    args = ap.parse_args()
+    import paper_2509_19821_b200 as g
+    from oracle import Reference  # the reference arm (checker / baseline only)
+
+    fronts = np.load(os.path.join(ROOT, "tests", "golden", "fronts.npz"))
+    ref = Reference() if Reference.available() else None
+    rows = []
+    for name in args.problems.split(","):
+        op = 1 if name.startswith("LIRCMOP") else 0  # suite default (experiment.cpp:117-123)
+        front = fronts[name]
+        p = g.make_problem(name)
+        for seed in range(1, args.seeds + 1):
+            rec = {"problem": name, "seed": seed, "budget_s": args.budget}
+            if ref is not None:
+                pop, hist = ref.run_gmpea(name, args.ref_n, k_max=0, seed=seed, op=op,
+                                          time_budget_s=args.budget, record_walltime=True)
+                fr = ref.metric_front(pop["F"], pop["cv"])
+                rec["reference"] = {"n": args.ref_n, "generations": int(hist[-1][0]),
+                                    "igd": float(ref.igd(fr, front)) if len(fr) else float("inf")}
+            for n in (int(x) for x in args.gpu_n.split(",")):
+                r = g.run_gmpea(p, g.RunConfig(n=n, time_budget_s=args.budget, seed=seed, op=op))
+                fr = g.metric_front(r.pop1)
+                rec[f"b200_n{n}"] = {"n": n, "generations": r.history[-1].gen,
+                                     "loop_ms": r.history[-1].wall_ms,
+                                     "igd": float(g.igd(fr, front)) if len(fr) else float("inf")}
+            rows.append(rec)
+            print(json.dumps(rec), flush=True)
+    summary = {}
+    for name in args.problems.split(","):
+        rs = [r for r in rows if r["problem"] == name]
+        s = {}
+        for key in rs[0]:
+            if isinstance(rs[0][key], dict):
+                s[key] = {"median_igd": float(np.median([r[key]["igd"] for r in rs])),
+                          "median_generations": float(np.median([r[key]["generations"] for r in rs]))}
+        summary[name] = s
+    with open(args.out, "w") as f:
+        json.dump({"runs": rows, "summary": summary}, f, indent=1)
+    print(json.dumps(summary, indent=1))
+
+
+if __name__ == "__main__":
+    main()
