@@ -405,10 +405,10 @@ struct RowGeom {
     size_t smem;
 };
 
-RowGeom row_geom(int d, int nc) {
+RowGeom row_geom(int d, int nc, int scratch_f4 = 0) {
     RowGeom g;
     g.rs4 = (d + nc + 3) / 4;
-    g.srs4 = g.rs4 | 1;
+    g.srs4 = (g.rs4 + scratch_f4) | 1;  // evaluator scratch after the row
     const int per = g.srs4 * 16;
     g.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
     g.smem = (size_t)g.bs * per;
@@ -627,7 +627,7 @@ struct gmpea_engine {
         d = p->d;
         m = p->m;
         nc = p->nin + p->neq;
-        geo = row_geom(d, nc);
+        geo = row_geom(d, nc, p->fam == FAM_WTA ? EvalWta::kScratchF4 : 0);
         t1 = (int)std::min<long long>(c.t1, N);
         t2 = (int)std::min<long long>(c.t2, N);
         time_mode = c.time_budget_s > 0.0;
@@ -1201,7 +1201,7 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         } sg{s};
         DevBuf<double> h((size_t)n * d);
         CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
-        const RowGeom geo = row_geom(d, nc);
+        const RowGeom geo = row_geom(d, nc, p->fam == FAM_WTA ? EvalWta::kScratchF4 : 0);
         PopBuf pb;
         pb.alloc(n, geo.rs4, ld);
         DevBuf<int> rows(n), nbad(1);
@@ -1312,7 +1312,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         if (op != GMPEA_OP_SBX_PM && op != GMPEA_OP_DE) throw std::invalid_argument("reproduce: unknown operator");
         CK(cudaSetDevice(p->device));
         const int d = p->d, nc = p->nin + p->neq;
-        const RowGeom geo = row_geom(d, nc);
+        const RowGeom geo = row_geom(d, nc, p->fam == FAM_WTA ? EvalWta::kScratchF4 : 0);
         cudaStream_t s = 0;
         DevBuf<double> h((size_t)n * d);
         CK(cudaMemcpy(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice));

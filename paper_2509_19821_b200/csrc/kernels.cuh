@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
                     const int j = jb + k;
                     if (j >= d) break;
                     if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
-                    ev.gene(p.P, j, v[k]);
+                    if (!Ev::kWholeRow) ev.gene(p.P, j, v[k]);
                 }
             }
             if (bad) {
@@ -510,7 +510,10 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
             } else {
                 Emitter em{my + d, {}, 0.0, false};
                 em.cv.init(p.P.nin);
-                ev.finish(p.P, f, em);
+                if (Ev::kWholeRow)
+                    ev.eval_row(p.P, my, my + 4 * rs4, f, em);  // row + scratch staged in shared memory
+                else
+                    ev.finish(p.P, f, em);
                 float4 o;
                 o.x = (float)f[0];
                 o.y = (float)f[1];

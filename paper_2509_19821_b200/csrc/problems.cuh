@@ -53,6 +53,10 @@ struct ProbDev {
 
 // ---------------------------------------------------------------- LIRCMOP
 struct EvalLir {
+    static constexpr bool kWholeRow = false;
+    static constexpr int kScratchF4 = 0;
+    template <class G>
+    __device__ __forceinline__ void eval_row(const ProbDev&, const float*, float*, double*, G&&) {}
     double g1, g2, x0, x1, s0, c0;
     float x0f;
     __device__ __forceinline__ void begin(const ProbDev&) { g1 = g2 = 0.0; }
@@ -151,6 +155,10 @@ struct EvalLir {
 
 // ---------------------------------------------------------------- C/DC-DTLZ
 struct EvalDtlz {
+    static constexpr bool kWholeRow = false;
+    static constexpr int kScratchF4 = 0;
+    template <class G>
+    __device__ __forceinline__ void eval_row(const ProbDev&, const float*, float*, double*, G&&) {}
     double pos[2];
     double rast, sph;
     __device__ __forceinline__ void begin(const ProbDev&) { rast = sph = 0.0; }
@@ -256,6 +264,10 @@ __device__ __forceinline__ double ipow(double x, int e) {
 }
 
 struct EvalMw {
+    static constexpr bool kWholeRow = false;
+    static constexpr int kScratchF4 = 0;
+    template <class G>
+    __device__ __forceinline__ void eval_row(const ProbDev&, const float*, float*, double*, G&&) {}
     double xs[2];
     double prev;
     double gs;
@@ -473,56 +485,74 @@ struct EvalMw {
 // ---------------------------------------------------------------- WTA
 // decode_wta (wta.cpp:51-72): genes >= 0.5 are candidates, taken in
 // descending value (ties to the lower flat index) while the vehicle has
-// capacity.  Vehicle v = g % vehicles, so per vehicle this is "keep the top
-// cap[v] candidates", maintained as a sorted insertion list while streaming.
+// capacity.  Vehicle v = g % vehicles and vehicles are independent, so vehicle
+// v keeps exactly its first cap[v] candidates in that order: it selects every
+// candidate at or above its cap[v]-th one.  The evaluator works on the whole
+// child row (staged in shared memory by the generation kernel): one selection
+// pass per capacity unit finds each vehicle's threshold, then one pass over
+// the strike slots forms hits, objectives and constraints (wta.cpp:74-110)
+// in the reference's order.  No per-thread arrays (no local memory).
 struct EvalWta {
-    float val[kWtaMaxVehicles][kWtaMaxCap];
-    short idx[kWtaMaxVehicles][kWtaMaxCap];
-    unsigned char cnt[kWtaMaxVehicles];
-    __device__ __forceinline__ void begin(const ProbDev& P) {
-        for (int v = 0; v < P.wta_vehicles; ++v) cnt[v] = 0;
-    }
-    __device__ __forceinline__ void gene(const ProbDev& P, int j, float x) {
-        if (!(x >= 0.5f)) return;
-        const int v = j % P.wta_vehicles;
-        const int cap = P.wta_cap[v];
-        int c = cnt[v];
-        // strict '>' keeps earlier (lower) indices ahead on ties
-        int pos = c;
-        while (pos > 0 && x > val[v][pos - 1]) --pos;
-        if (pos >= cap) return;
-        int last = c < cap ? c : cap - 1;
-        for (int k = last; k > pos; --k) {
-            val[v][k] = val[v][k - 1];
-            idx[v][k] = idx[v][k - 1];
-        }
-        val[v][pos] = x;
-        idx[v][pos] = (short)j;
-        if (c < cap) cnt[v] = (unsigned char)(c + 1);
-    }
+    static constexpr bool kWholeRow = true;
+    __device__ __forceinline__ void begin(const ProbDev&) {}
+    __device__ __forceinline__ void gene(const ProbDev&, int, float) {}
     template <class G>
-    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
-        const int V = P.wta_vehicles, T = P.wta_targets, S = P.wta_slots;
-        unsigned char hits[kWtaMaxSlots];
-        for (int s = 0; s < S; ++s) hits[s] = 0;
-        for (int v = 0; v < V; ++v)
-            for (int k = 0; k < cnt[v]; ++k) hits[idx[v][k] / V] += 1;
-        // constraints are emitted in ascending index: vehicle loads first
-        // (wta.cpp:99-100), then per-target strike counts (:101-109)
-        for (int v = 0; v < V; ++v) emit(v, (double)cnt[v] - (double)P.wta_cap[v]);
-        // wta.cpp:78-97: f1 accumulates 1 - prod(1 - p * hits) per target
+    __device__ __forceinline__ void finish(const ProbDev&, double*, G&&) {}
+
+    // shared-memory scratch after the row: kWtaMaxVehicles thresholds + indices
+    static constexpr int kScratchF4 = (kWtaMaxVehicles * 2 + 3) / 4;
+    template <class G>
+    __device__ __forceinline__ void eval_row(const ProbDev& P, const float* x, float* scratch, double* f,
+                                             G&& emit) {
+        float* s_tv = scratch;
+        int* s_ti = reinterpret_cast<int*>(scratch + kWtaMaxVehicles);
+        const int V = P.wta_vehicles, T = P.wta_targets;
+        const int D = P.d;
+        for (int v = 0; v < V; ++v) {
+            const int cap = P.wta_cap[v];
+            float pv = 3.0f;  // above every gene in [0, 1]
+            int pi = -1, c = 0;
+            for (int r = 0; r < cap; ++r) {
+                float bv = -1.0f;
+                int bi = -1;
+                for (int j = v; j < D; j += V) {
+                    const float xv = x[j];
+                    // after (pv, pi) in (value desc, index asc) order and better than (bv, bi)
+                    const bool after = xv < pv || (xv == pv && j > pi);
+                    if (xv >= 0.5f && after && xv > bv) {
+                        bv = xv;
+                        bi = j;
+                    }
+                }
+                if (bi < 0) break;
+                pv = bv;
+                pi = bi;
+                ++c;
+            }
+            s_tv[v] = pv;
+            s_ti[v] = c ? pi : -1;
+            emit(v, (double)c - (double)cap);  // per-vehicle capacity (wta.cpp:99-100)
+        }
         double f1 = 0.0, f2 = 0.0;
         int s = 0;
         for (int i = 0; i < T; ++i) {
             double surv = 1.0, strikes = 0.0;
             for (int k = 0; k < P.wta_strikes[i]; ++k, ++s) {
-                double h = hits[s];
-                surv *= 1.0 - P.wta_p[s] * h;
-                f2 += h;
-                strikes += h;
+                int h = 0;
+                for (int v = 0; v < V; ++v) {
+                    const int j = s * V + v;
+                    const float xv = x[j];
+                    const float tv = s_tv[v];
+                    const int ti = s_ti[v];
+                    h += (ti >= 0 && xv >= 0.5f && (xv > tv || (xv == tv && j <= ti))) ? 1 : 0;
+                }
+                const double hd = (double)h;
+                surv *= 1.0 - P.wta_p[s] * hd;
+                f2 += hd;
+                strikes += hd;
             }
             f1 += 1.0 - surv;
-            emit(V + i, strikes - (double)P.wta_strikes[i]);
+            emit(V + i, strikes - (double)P.wta_strikes[i]);  // per-target strikes (wta.cpp:101-109)
         }
         f[0] = -f1;  // wta.cpp:126 (solvers minimise)
         f[1] = f2;
