@@ -1,0 +1,115 @@
+"""BASELINE.json configs[1]: MW1-MW14, N = 10,000, 30 seeds — final-population
+quality of the engine vs the reference's own run_gmpea on the same problems.
+
+The reference has no MW problems, so its loop runs the oracle's
+restated MW evaluators wrapped as reference ProblemDefs (oracle/ref_shim.cpp,
+problem_for) — "reference loop + restated evaluator".  Neither side has an
+analytic MW front, so the metric is the reference harness's normalised
+hypervolume (experiment.cpp:240-281: ideal/nadir over the runs' fronts,
+reference point 1.1): here the bounds come from the reference runs and are
+applied to both arms.
+
+    python tools/mw_parity.py ref   [--seeds 30 --n 10000 --gens 200 --procs 8]
+        runs the reference here (CPU) -> tests/golden/mw_ref_hv.json
+    python tools/mw_parity.py gpu   -> profiles/r01_mw_parity.json (needs a B200)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+REF_JSON = os.path.join(ROOT, "tests", "golden", "mw_ref_hv.json")
+PROBLEMS = [f"MW{i}" for i in range(1, 15)]
+
+
+def _ref_run(job):
+    name, n, gens, seed = job
+    from oracle import Reference
+
+    r = Reference()
+    pop, _ = r.run_gmpea(name, n, k_max=gens, seed=seed, op=0, record_walltime=False)
+    return name, seed, r.metric_front(pop["F"], pop["cv"])
+
+
+def hv_of(front, lo, hi, hv_fn):
+    if len(front) == 0:
+        return 0.0
+    span = np.where(hi > lo, hi - lo, 1.0)
+    return float(hv_fn((front - lo) / span, np.full(front.shape[1], 1.1)))
+
+
+def cmd_ref(args):
+    from oracle import Reference
+
+    jobs = [(p, args.n, args.gens, s) for p in PROBLEMS for s in range(1, args.seeds + 1)]
+    fronts = {}
+    with ProcessPoolExecutor(args.procs) as ex:
+        for name, seed, fr in ex.map(_ref_run, jobs):
+            fronts.setdefault(name, {})[seed] = fr
+            print(name, seed, len(fr), flush=True)
+    ref = Reference()
+    out = {"n": args.n, "gens": args.gens, "seeds": args.seeds, "problems": {}}
+    for name in PROBLEMS:
+        allf = [f for f in fronts[name].values() if len(f)]
+        if not allf:
+            out["problems"][name] = {"ideal": None, "nadir": None, "hv": [0.0] * args.seeds}
+            continue
+        cat = np.concatenate(allf)
+        lo, hi = cat.min(0), cat.max(0)
+        hvs = [hv_of(fronts[name][s], lo, hi, ref.hypervolume) for s in range(1, args.seeds + 1)]
+        out["problems"][name] = {"ideal": lo.tolist(), "nadir": hi.tolist(), "hv": hvs}
+    with open(REF_JSON, "w") as f:
+        json.dump(out, f, indent=1)
+
+
+def cmd_gpu(args):
+    from scipy.stats import mannwhitneyu
+
+    import paper_2509_19821_b200 as g
+
+    ref = json.load(open(REF_JSON))
+    res = {}
+    for name in PROBLEMS:
+        rp = ref["problems"][name]
+        p = g.make_problem(name)
+        hvs = []
+        for seed in range(1, ref["seeds"] + 1):
+            r = g.run_gmpea(p, g.RunConfig(n=ref["n"], k_max=ref["gens"], seed=seed, op=g.VariationOp.sbx_pm))
+            fr = g.metric_front(r.pop1)
+            if rp["ideal"] is None:
+                hvs.append(0.0)
+            else:
+                hvs.append(hv_of(fr, np.array(rp["ideal"]), np.array(rp["nadir"]), g.hypervolume))
+        a, b = np.array(hvs), np.array(rp["hv"])
+        if np.all(a == a[0]) and np.all(b == a[0]):
+            pval = 1.0
+        else:
+            pval = float(mannwhitneyu(a, b, alternative="two-sided").pvalue)
+        res[name] = {"b200_median_hv": float(np.median(a)), "ref_median_hv": float(np.median(b)), "p_value": pval,
+                     "verdict": "=" if pval >= 0.05 else ("+" if np.median(a) > np.median(b) else "-")}
+        print(name, res[name], flush=True)
+    with open(os.path.join(ROOT, "profiles", "r01_mw_parity.json"), "w") as f:
+        json.dump({"config": {k: ref[k] for k in ("n", "gens", "seeds")}, "results": res}, f, indent=1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cmd", choices=["ref", "gpu"])
+    ap.add_argument("--seeds", type=int, default=30)
+    ap.add_argument("--n", type=int, default=10000)
+    ap.add_argument("--gens", type=int, default=200)
+    ap.add_argument("--procs", type=int, default=6)
+    args = ap.parse_args()
+    cmd_ref(args) if args.cmd == "ref" else cmd_gpu(args)
+
+
+if __name__ == "__main__":
+    main()
