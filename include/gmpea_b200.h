@@ -49,6 +49,10 @@ int gmpea_problem_create(const char* name, gmpea_problem** out);
 int gmpea_problem_create_wta(const char* scenario, int32_t targets, int32_t vehicles,
                              const int32_t* strikes, const int32_t* capacity, const double* p,
                              gmpea_problem** out);
+/* built-in scenario tables P1..P10 (wta_scenario, wta.cpp:23-49); host-only.
+ * strikes: targets entries, capacity: vehicles entries, p: sum(strikes) */
+int gmpea_wta_scenario(int32_t num, int32_t* targets, int32_t* vehicles, int32_t* strikes,
+                       int32_t* capacity, double* p);
 int gmpea_problem_info(const gmpea_problem* p, int32_t* d, int32_t* m, int32_t* n_ineq,
                        int32_t* n_eq);
 int gmpea_problem_bounds(const gmpea_problem* p, double* lo, double* hi);

@@ -318,6 +318,13 @@ class Reference(_Lib):
             _ptr(m1, _u8p), _ptr(m2, _u8p)))
         return m1, m2
 
+    def wilcoxon(self, a, b, alpha=0.05):
+        a, b = _f64(a), _f64(b)
+        p, d = C.c_double(), C.c_int32()
+        self._check(self.lib.ref_wilcoxon(_ptr(a, _dp), C.c_int64(len(a)), _ptr(b, _dp), C.c_int64(len(b)),
+                                          C.c_double(alpha), C.byref(p), C.byref(d)))
+        return p.value, d.value
+
     def igd(self, A, R):
         A, R = _f64(A), _f64(R)
         out = C.c_double()

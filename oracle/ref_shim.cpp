@@ -231,6 +231,15 @@ int ref_op2_marks(int64_t n, int32_t d, int32_t m, int32_t nc, const double* con
     });
 }
 
+int ref_wilcoxon(const double* a, int64_t na, const double* b, int64_t nb, double alpha, double* p,
+                 int32_t* direction) {
+    return guarded([&] {
+        WilcoxonResult w = wilcoxon_rank_sum(std::vector<double>(a, a + na), std::vector<double>(b, b + nb), alpha);
+        *p = w.p_value;
+        *direction = w.direction;
+    });
+}
+
 int ref_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t m, double* out) {
     return guarded([&] { *out = igd(mat(A, na, m), mat(R, nr, m)); });
 }

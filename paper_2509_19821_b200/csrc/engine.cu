@@ -1151,6 +1151,19 @@ int gmpea_problem_create_wta(const char* scenario, int32_t targets, int32_t vehi
     });
 }
 
+int gmpea_wta_scenario(int32_t num, int32_t* targets, int32_t* vehicles, int32_t* strikes, int32_t* capacity,
+                       double* p) {
+    return guarded([&] {
+        if (num < 1 || num > 10) throw std::invalid_argument("unknown WTA scenario: P" + std::to_string(num));
+        WtaHost w = wta_scenario(num);
+        *targets = w.targets;
+        *vehicles = w.vehicles;
+        if (strikes) std::copy(w.strikes.begin(), w.strikes.end(), strikes);
+        if (capacity) std::copy(w.cap.begin(), w.cap.end(), capacity);
+        if (p) std::copy(w.p.begin(), w.p.end(), p);
+    });
+}
+
 int gmpea_problem_info(const gmpea_problem* p, int32_t* d, int32_t* m, int32_t* nin, int32_t* neq) {
     return guarded([&] {
         if (!p) throw std::invalid_argument("null problem");
