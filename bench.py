@@ -85,7 +85,7 @@ class Clocks:
     def __exit__(self, *a):
         self.out = ""
         if self.p is not None:
-            time.sleep(0.15)
+            time.sleep(0.05)
             self.p.terminate()
             try:
                 self.out, _ = self.p.communicate(timeout=5)
@@ -196,7 +196,8 @@ def main():
     stream = torch.cuda.Stream()  # the engine's launching stream (events are recorded on it)
     torch.cuda.set_stream(stream)
     prob = g.make_problem(problem)
-    budget_gens = args.warmup + 4 * args.steps + 16
+    PRE_MAX = 20000  # untimed generations keeping the GPU busy while the clock sampler settles
+    budget_gens = args.warmup + 4 * args.steps + 16 + PRE_MAX
     if world == 1:
         cfg = g.RunConfig(n=n, k_max=0, eval_budget=2 * n * budget_gens, seed=1, op=op, device=local,
                           stream=stream.cuda_stream)
@@ -211,16 +212,26 @@ def main():
         shard = GpuShard(prob, cfg, world, rank, TorchComm())
         eng = shard.eng
         advance = shard.run
+    t0 = time.perf_counter()
     advance(args.warmup)
     torch.cuda.synchronize()
+    t_gen = (time.perf_counter() - t0) / max(1, args.warmup)
+    pre = int(min(PRE_MAX, max(0, 0.6 / max(t_gen, 1e-6))))  # ~0.6 s of load before the timed region
     if world > 1:
+        t = torch.tensor([pre], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        pre = int(t.item())
         torch.distributed.barrier()
 
-    # ---- timed region: K generations, CUDA events on the engine's stream
+    # ---- timed region: K generations, CUDA events on the engine's stream; the
+    # clock sampler runs across the untimed load generations and the region
     clocks = Clocks(local)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clocks:
+        advance(pre)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         start.record(stream)
         advance(args.steps)
         end.record(stream)

@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for w in wta-p10-100k; do timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --workload $w > gpurun_out/bench_$w.log 2>&1; echo "$w rc=$?"; tail -1 gpurun_out/bench_$w.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['ms_per_step'], l['value']/1e9, l['roofline']['kernel_ms'])"; done
-python bench.py --steps 3 --warmup 2 --no-cpu-baseline --workload wta-p10-100k > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"vary_eval" -s 2 -c 1 -o gpurun_out/prof10_wta python bench.py --steps 3 --warmup 2 --no-cpu-baseline --workload wta-p10-100k > gpurun_out/ncu10.log 2>&1; echo ncu=$?
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --workload wta-p10-100k > gpurun_out/bench_wta.log 2>&1; tail -1 gpurun_out/bench_wta.log | python -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['ms_per_step'], l['value']/1e9, l['roofline']['kernel_ms'])"
