@@ -21,6 +21,8 @@
 // winner row is one cache line instead of d separate sectors; the selection
 // keys live apart as packed float4 {f0, f1, f2, cv} per slot.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "problems.cuh"
 
@@ -328,13 +330,13 @@ __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, 
 // DC > 0 compiles the kernel for a fixed decision dimension (the registered
 // suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
 template <class Ev, int MODE, int OP, int DC = 0, bool UB = false>
-__global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
+__device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, const int by) {
     extern __shared__ float4 sm4[];
     DevState* st = p.st;
     if (st->stop) return;
-    const int pi = blockIdx.y;
+    const int pi = by;
     const int tid = threadIdx.x;
-    const int i0 = p.row0 + blockIdx.x * blockDim.x;
+    const int i0 = p.row0 + bx * blockDim.x;
     const int i = i0 + tid;
     const bool active = i < p.row_end;
     const int d = DC > 0 ? DC : p.P.d;
@@ -557,6 +559,11 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
 #undef GMPEA_LO
 #undef GMPEA_HI
 
+template <class Ev, int MODE, int OP, int DC = 0, bool UB = false>
+__global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
+    vary_body<Ev, MODE, OP, DC, UB>(p, blockIdx.x, blockIdx.y);
+}
+
 // ---- PBI in fp32 on unit reference vectors (scalarize.cpp:72-89):
 // d1 = |(f - z) . u|, d2 = |(f - z) - d1 u|, g = d1 + theta d2.  Unused lanes
 // of f, u and z are zero for m = 2.
@@ -589,9 +596,9 @@ struct Op1Params {
 // OP1 (gmpea.cpp:248-279).  s1: stream 1 takes off2 (FPR-preferred),
 // s2: stream 2 takes off1 (PBI-preferred).  The reference builds both from
 // Heaviside masks over differences, which reject non-finite inputs.
-__global__ void __launch_bounds__(256) op1_kernel(Op1Params p) {
+__device__ __forceinline__ void op1_body(const Op1Params& p, const int bx) {
     if (p.st->stop) return;
-    const int i = p.row0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = p.row0 + bx * blockDim.x + threadIdx.x;
     if (i >= p.row_end) return;
     const float3 z = load_z(p.st, p.m);
     const float4 a = p.oFcv[0][i], b = p.oFcv[1][i], u = p.U[i];
@@ -607,6 +614,8 @@ __global__ void __launch_bounds__(256) op1_kernel(Op1Params p) {
     p.eff[1][i] = s2 ? a : b;
     p.srcbits[i] = (unsigned char)((s1 ? 1 : 0) | (s2 ? 2 : 0));
 }
+
+__global__ void __launch_bounds__(256) op1_kernel(Op1Params p) { op1_body(p, blockIdx.x); }
 
 struct SelParams {
     int n, rs4, m;       // n: local rows (winner code c | n + c)
@@ -739,18 +748,18 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
 #ifndef GMPEA_SELECT_MINBLOCKS
 #define GMPEA_SELECT_MINBLOCKS 4
 #endif
-__global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
+__device__ __forceinline__ void select_body(const SelParams& p, const int bx, const int by) {
     if (p.st->stop) return;
-    const int j = p.row0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = p.row0 + bx * blockDim.x + threadIdx.x;
     const float3 z = load_z(p.st, p.m);
     bool feas = false;
     if (j < p.row_end) {
-        if (blockIdx.y == 0)
+        if (by == 0)
             select_slot<0>(p, j, z, feas);
         else
             select_slot<1>(p, j, z, feas);
     }
-    if (blockIdx.y != 0 || p.rec == nullptr) return;
+    if (by != 0 || p.rec == nullptr) return;
     // feasible_ratio of pop1 (gmpea.cpp:411-417): block count, one atomic
     __shared__ unsigned cnt[8];
     unsigned b = __popc(__ballot_sync(0xffffffffu, feas && j < p.row_end));
@@ -763,8 +772,12 @@ __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(Sel
     }
 }
 
+__global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
+    select_body(p, blockIdx.x, blockIdx.y);
+}
+
 // loop-time bookkeeping after a generation (gmpea.cpp:480-488)
-__global__ void end_gen_kernel(DevState* st, DevRecord* rec) {
+__device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     if (st->stop) return;
     const unsigned long long now = globaltimer();
     st->loop_ns += now - st->t_gen_start;
@@ -779,6 +792,8 @@ __global__ void end_gen_kernel(DevState* st, DevRecord* rec) {
     st->t_gen_start = globaltimer();
 }
 
+__global__ void end_gen_kernel(DevState* st, DevRecord* rec) { end_gen_body(st, rec); }
+
 __global__ void mark_start_kernel(DevState* st) { st->t_gen_start = globaltimer(); }
 
 struct RestoreParams {
@@ -791,13 +806,65 @@ struct RestoreParams {
     DevState* st;
 };
 
-__global__ void restore_kernel(RestoreParams p) {
+__device__ __forceinline__ void restore_body(const RestoreParams& p, const int bx, const int by) {
     if (!p.st->discard) return;
-    const int j = p.row0 + blockIdx.x * blockDim.x + threadIdx.x;
-    const int q = blockIdx.y;
+    const int j = p.row0 + bx * blockDim.x + threadIdx.x;
+    const int q = by;
     if (j >= p.row_end || p.ustamp[q][j] != p.st->gen) return;
     copy_row(p.X[q] + (long long)j * p.rs4, p.uX[q] + (long long)j * p.rs4, p.rs4);
     p.Fcv[q][j] = p.uFcv[q][j];
+}
+
+__global__ void restore_kernel(RestoreParams p) { restore_body(p, blockIdx.x, blockIdx.y); }
+
+// ---- many generations in one cooperative launch (small populations, where
+// kernel launches, not bandwidth, bound a generation): the four phases of a
+// generation are separated by grid-wide barriers instead of kernel boundaries;
+// every block walks the phases' tiles with 128 threads.
+struct GenParams {
+    VaryParams vp;
+    Op1Params op1;
+    SelParams sp;
+    RestoreParams rp;
+    DevState* st;
+    DevRecord* rec;
+    int gens;
+    int time_mode;
+    volatile int* host_flag;
+};
+
+template <class Ev, int OP, int DC, bool UB>
+__global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) generation_coop_kernel(GenParams* gptr, int gens) {
+    // the parameter blocks live in global memory; the pointer is deliberately
+    // not __restrict__/const so the compiler re-reads fields per phase instead
+    // of hoisting hundreds of loop-invariant values into (spilled) registers
+    GenParams& g = *gptr;
+    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+    const int vt = (g.vp.row_end - g.vp.row0 + 127) / 128;
+    const int ot = (g.op1.row_end - g.op1.row0 + 127) / 128;
+    const int st_ = (g.sp.row_end - g.sp.row0 + 127) / 128;
+    for (int k = 0; k < gens; ++k) {
+        if (*(volatile int*)&g.st->stop) break;  // uniform: written before the last barrier
+        for (int t = blockIdx.x; t < 2 * vt; t += gridDim.x) {
+            vary_body<Ev, MODE_VARY, OP, DC, UB>(g.vp, t % vt, t / vt);
+            __syncthreads();  // shared staging rows are reused by the next tile
+        }
+        grid.sync();
+        for (int t = blockIdx.x; t < ot; t += gridDim.x) op1_body(g.op1, t);
+        grid.sync();
+        for (int t = blockIdx.x; t < 2 * st_; t += gridDim.x) {
+            select_body(g.sp, t % st_, t / st_);
+            __syncthreads();
+        }
+        grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x == 0) end_gen_body(g.st, g.rec);
+        grid.sync();
+        if (g.time_mode) {
+            for (int t = blockIdx.x; t < 2 * st_; t += gridDim.x) restore_body(g.rp, t % st_, t / st_);
+            grid.sync();
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *g.host_flag = g.st->stop | (g.st->err ? 2 : 0);
 }
 
 // feasible count of pop1 (generation-0 record)
