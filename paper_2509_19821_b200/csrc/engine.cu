@@ -438,24 +438,6 @@ VaryKernel pick_vary(int mode, int op) {
     return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC, UB> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UB>;
 }
 
-using CoopKernel = void (*)(GenParams*, int);
-
-template <class Ev, int DC = 0>
-CoopKernel pick_coop(int op) {
-    constexpr bool UB = DC > 0;
-    return op == OP_DE ? generation_coop_kernel<Ev, OP_DE, DC, UB> : generation_coop_kernel<Ev, OP_SBX, DC, UB>;
-}
-
-CoopKernel coop_kernel_for(int fam, int op, int d) {
-    switch (fam) {
-        case FAM_LIR: return d == 30 ? pick_coop<EvalLir, 30>(op) : pick_coop<EvalLir>(op);
-        case FAM_DTLZ:
-            return d == 7 ? pick_coop<EvalDtlz, 7>(op) : (d == 12 ? pick_coop<EvalDtlz, 12>(op) : pick_coop<EvalDtlz>(op));
-        case FAM_WTA: return nullptr;  // wide rows: 32-64 thread blocks, keep the per-kernel path
-        default: return d == 15 ? pick_coop<EvalMw, 15>(op) : pick_coop<EvalMw>(op);
-    }
-}
-
 // the generation kernel is compiled for the registered suites' dimension
 VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0) {
     switch (fam) {
@@ -617,11 +599,6 @@ struct gmpea_engine {
     RestoreParams rp{};
     VaryKernel vary = nullptr;
     cudaGraphExec_t graph = nullptr;
-    // small populations: whole generations inside one cooperative launch
-    CoopKernel coop = nullptr;
-    GenParams gp{};
-    DevBuf<GenParams> gp_dev;
-    int coop_grid = 0;
 
     long long gens_enqueued = 0;  // generations launched (host view)
     long long gen_limit = 0;      // max generations allowed by k_max / eval budget (-1 = inf)
@@ -835,7 +812,6 @@ struct gmpea_engine {
         rp.row_end = (int)(own1 - e0);
         rp.rs4 = geo.rs4;
         rp.st = st.p;
-        setup_coop(p, c);
         CK(cudaStreamSynchronize(s));
         check_errors(0);
     }
@@ -948,48 +924,10 @@ struct gmpea_engine {
         if (gen_limit >= 0) k = std::min(k, gen_limit - gens_enqueued);
         if (k <= 0) return 0;
         start_loop_clock();
-        if (coop) {
-            for (long long left = k; left > 0;) {
-                const int chunk = (int)std::min<long long>(left, 256);
-                launch_coop(chunk);
-                left -= chunk;
-            }
-        } else {
-            build_graph();
-            for (long long i = 0; i < k; ++i) CK(cudaGraphLaunch(graph, s));
-        }
+        build_graph();
+        for (long long i = 0; i < k; ++i) CK(cudaGraphLaunch(graph, s));
         gens_enqueued += k;
         return k;
-    }
-
-    void setup_coop(const gmpea_problem* p, const gmpea_run_config& c) {
-        long long max_n = 131072;
-        if (const char* e = getenv("GMPEA_COOP_MAX_N")) max_n = atoll(e);
-        if (sharded || geo.bs != 128 || N > max_n) return;
-        CoopKernel k = coop_kernel_for(p->fam, c.op, p->dev.uniform ? d : 0);
-        if (!k) return;
-        int dev = 0, coop_ok = 0, sms = 0, per_sm = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&coop_ok, cudaDevAttrCooperativeLaunch, dev));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (!coop_ok) return;
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)geo.smem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, geo.smem));
-        if (per_sm < 1) return;
-        const int vt = (int)((v1 - v0 + 127) / 128), stt = (int)((own1 - own0 + 127) / 128);
-        const int want = std::max({2 * vt, vt, 2 * stt});
-        coop_grid = std::min(want, per_sm * sms);
-        gp = GenParams{vp, op1p, sp, rp, st.p, rec.p, 0, time_mode ? 1 : 0, host_flag_dev};
-        gp_dev.alloc(1);
-        CK(cudaMemcpyAsync(gp_dev.p, &gp, sizeof(GenParams), cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));
-        coop = k;
-    }
-
-    void launch_coop(int gens) {
-        GenParams* ptr = gp_dev.p;
-        void* args[] = {(void*)&ptr, (void*)&gens};
-        CK(cudaLaunchCooperativeKernel((const void*)coop, dim3(coop_grid), dim3(128), args, geo.smem, s));
     }
 
     // one generation in two phases (sharded runs; no graph, plain launches)

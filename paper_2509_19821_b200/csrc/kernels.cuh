@@ -21,8 +21,6 @@
 // winner row is one cache line instead of d separate sectors; the selection
 // keys live apart as packed float4 {f0, f1, f2, cv} per slot.
 #pragma once
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 #include "problems.cuh"
 
@@ -816,56 +814,6 @@ __device__ __forceinline__ void restore_body(const RestoreParams& p, const int b
 }
 
 __global__ void restore_kernel(RestoreParams p) { restore_body(p, blockIdx.x, blockIdx.y); }
-
-// ---- many generations in one cooperative launch (small populations, where
-// kernel launches, not bandwidth, bound a generation): the four phases of a
-// generation are separated by grid-wide barriers instead of kernel boundaries;
-// every block walks the phases' tiles with 128 threads.
-struct GenParams {
-    VaryParams vp;
-    Op1Params op1;
-    SelParams sp;
-    RestoreParams rp;
-    DevState* st;
-    DevRecord* rec;
-    int gens;
-    int time_mode;
-    volatile int* host_flag;
-};
-
-template <class Ev, int OP, int DC, bool UB>
-__global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) generation_coop_kernel(GenParams* gptr, int gens) {
-    // the parameter blocks live in global memory; the pointer is deliberately
-    // not __restrict__/const so the compiler re-reads fields per phase instead
-    // of hoisting hundreds of loop-invariant values into (spilled) registers
-    GenParams& g = *gptr;
-    cooperative_groups::grid_group grid = cooperative_groups::this_grid();
-    const int vt = (g.vp.row_end - g.vp.row0 + 127) / 128;
-    const int ot = (g.op1.row_end - g.op1.row0 + 127) / 128;
-    const int st_ = (g.sp.row_end - g.sp.row0 + 127) / 128;
-    for (int k = 0; k < gens; ++k) {
-        if (*(volatile int*)&g.st->stop) break;  // uniform: written before the last barrier
-        for (int t = blockIdx.x; t < 2 * vt; t += gridDim.x) {
-            vary_body<Ev, MODE_VARY, OP, DC, UB>(g.vp, t % vt, t / vt);
-            __syncthreads();  // shared staging rows are reused by the next tile
-        }
-        grid.sync();
-        for (int t = blockIdx.x; t < ot; t += gridDim.x) op1_body(g.op1, t);
-        grid.sync();
-        for (int t = blockIdx.x; t < 2 * st_; t += gridDim.x) {
-            select_body(g.sp, t % st_, t / st_);
-            __syncthreads();
-        }
-        grid.sync();
-        if (blockIdx.x == 0 && threadIdx.x == 0) end_gen_body(g.st, g.rec);
-        grid.sync();
-        if (g.time_mode) {
-            for (int t = blockIdx.x; t < 2 * st_; t += gridDim.x) restore_body(g.rp, t % st_, t / st_);
-            grid.sync();
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *g.host_flag = g.st->stop | (g.st->err ? 2 : 0);
-}
 
 // feasible count of pop1 (generation-0 record)
 __global__ void count_feasible_kernel(const float4* Fcv, int row0, int row_end, unsigned* out) {
