@@ -589,6 +589,7 @@ struct gmpea_engine {
     DevBuf<int> ustamp[2];
     DevBuf<int> bad[2];
     int* host_flag = nullptr;
+    DevBuf<unsigned> done_ctr;
     DevBuf<double> staging;  // f64 row-major staging for population transfers
     DevBuf<int> rowsbuf;
     int* host_flag_dev = nullptr;
@@ -808,6 +809,10 @@ struct gmpea_engine {
         sp.apply = 1;
         sp.st = st.p;
         sp.rec = rec.p;
+        done_ctr.alloc(1);
+        done_ctr.zero(s);
+        sp.done = done_ctr.p;
+        sp.host_flag = host_flag_dev;
         rp.row0 = (int)(own0 - e0);
         rp.row_end = (int)(own1 - e0);
         rp.rs4 = geo.rs4;
@@ -885,8 +890,7 @@ struct gmpea_engine {
 
     void enqueue_generation() {
         enqueue_phase1();
-        enqueue_phase2();
-        publish_stop_kernel<<<1, 1, 0, s>>>(st.p, host_flag_dev);
+        enqueue_phase2();  // select's last block also publishes the stop flag
     }
 
     // phase 1: variation + evaluation (+ local ideal-point partial)
@@ -894,8 +898,7 @@ struct gmpea_engine {
     // phase 2: OP1, selection, bookkeeping (a sharded run all-reduces z in between)
     void enqueue_phase2() {
         op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
-        select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);
-        end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
+        select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);  // + end_gen
         if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
 
@@ -1084,9 +1087,8 @@ struct gmpea_engine {
             CK(cudaEventRecord(e[1], s));
             op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
             CK(cudaEventRecord(e[2], s));
-            select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);
+            select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);  // + end_gen
             CK(cudaEventRecord(e[3], s));
-            end_gen_kernel<<<1, 1, 0, s>>>(st.p, rec.p);
             if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
             CK(cudaEventRecord(e[4], s));
         }

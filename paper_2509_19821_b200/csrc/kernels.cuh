@@ -637,6 +637,10 @@ struct SelParams {
     int* ustamp[2];
     DevState* st;
     DevRecord* rec;      // optional: feasible count of pop1 for this generation
+    // the last block to finish runs the generation's bookkeeping (end_gen)
+    // and publishes the stop flag, saving two launches per generation
+    unsigned* done;
+    volatile int* host_flag;
 };
 
 __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4* __restrict__ src, int rs4) {
@@ -770,10 +774,6 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
     }
 }
 
-__global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
-    select_body(p, blockIdx.x, blockIdx.y);
-}
-
 // loop-time bookkeeping after a generation (gmpea.cpp:480-488)
 __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     if (st->stop) return;
@@ -788,6 +788,22 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     st->gens_done += 1;
     st->gen += 1;
     st->t_gen_start = globaltimer();
+}
+
+__global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
+    select_body(p, blockIdx.x, blockIdx.y);
+    if (p.done == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();  // this block's rows, keys and record counts are visible
+        const unsigned nblocks = gridDim.x * gridDim.y;
+        if (atomicAdd(p.done, 1u) == nblocks - 1) {
+            __threadfence();
+            end_gen_body(p.st, p.rec);
+            if (p.host_flag) *p.host_flag = p.st->stop | (p.st->err ? 2 : 0);
+            *p.done = 0u;  // re-armed for the next generation (stream order)
+        }
+    }
 }
 
 __global__ void end_gen_kernel(DevState* st, DevRecord* rec) { end_gen_body(st, rec); }
