@@ -63,49 +63,57 @@ def alg_bytes(d, m, nc, t1, t2):
 
 
 class Clocks:
-    """nvidia-smi samples during the timed region (B200_PROFILING.md)."""
+    """SM clock and throttle-reason samples DURING the timed region
+    (B200_PROFILING.md): an NVML poller thread (~2 ms period), so even a
+    50 ms region is sampled; falls back to nvidia-smi if NVML is missing."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, device):
         self.device = device
-        self.p = None
+        self.samples = []
+        self.max_mhz = None
+        self._stop = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.p = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001
+            return self
+        self._stop = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(mhz), int(r)))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(0.002)
+
+        self._t = threading.Thread(target=poll, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.p is not None:
-            time.sleep(0.05)
-            self.p.terminate()
-            try:
-                self.out, _ = self.p.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.p.kill()
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=1)
 
     def summary(self):
-        rows = []
-        for line in (self.out or "").strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) >= 8:
-                rows.append(f)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(rows[0][2]) if rows[0][2].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        reasons = sorted({k for _, r in self.samples for k, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median([m for m, _ in self.samples])), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 def dist_env():
@@ -125,36 +133,37 @@ def ncu_traffic(kernel):
         return None
 
 
-def cpu_reference(problem, n, op, gens, warmup, threads, seed=1, topo=None):
-    """The reference's own loop (oracle/_ref) on host cores; returns
-    (ind-gen/s, seconds, replicas, kind)."""
+def cpu_reference(problem, n_sub, op, gens, warmup, threads, seed=1):
+    """The reference's own loop (oracle/_ref, gmpea.cpp:457-489) on host
+    cores: `threads` concurrent replicas of an n_sub-slot population, each
+    running warmup + gens generations; topology from the oracle's windowed
+    lattice KNN (identical to build_neighborhoods, tests/test_oracle_pins.py),
+    setup untimed.  Returns (ind-gen/s over all replicas, loop seconds)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import Reference  # checker / baseline only
+    from oracle import Oracle, Reference  # checker / baseline only
 
     if not Reference.available():
         raise RuntimeError("oracle/_ref not built")
     ref = Reference()
-    secs = ref.loop_bench(problem, n, op, topo.b1, topo.b2, warmup, gens, threads, seed)
-    value = threads * 2 * n * gens / float(secs.max())
-    return value, float(secs.max()), "reference"
+    m = ref._info_any(problem)["m"]
+    b1, b2 = Oracle().lattice_knn(m, n_sub, 5, 20, threads)
+    secs = ref.loop_bench(problem, n_sub, op, b1, b2, warmup, gens, threads, seed)
+    return threads * 2 * n_sub * gens / float(secs.max()), float(secs.max())
 
 
-def host_topology(problem, n):
-    import paper_2509_19821_b200 as g
-
-    p = g.make_problem(problem)
-    return g.lattice_neighborhoods(p.m, n, 5, 20)
+def ref_threads():
+    return int(os.environ.get("GMPEA_REF_THREADS", "0")) or max(1, os.cpu_count() or 1)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=100)   # generations 11-110 (SURVEY.md §8d)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="lircmop13-1m", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-gens", type=int, default=2)
+    ap.add_argument("--cpu-gens", type=int, default=20)
     args = ap.parse_args()
     world, rank, local = dist_env()
     problem, n, op = WORKLOADS[args.workload]
@@ -165,21 +174,22 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        threads = int(os.environ.get("GMPEA_REF_THREADS", "0")) or max(1, min(os.cpu_count() or 1, 8))
-        topo = host_topology(problem, n)
-        vals = []
-        for _ in range(args.steps):
-            v, secs, kind = cpu_reference(problem, n, op, 1, 0, threads, topo=topo)
-            vals.append(v)
-        value = float(np.median(vals))
+        # bounded sample of the workload: `threads` concurrent replicas of
+        # N/threads slots (N slot-generations per step in total), one
+        # generation per step, all host threads busy
+        threads = ref_threads()
+        n_sub = int(os.environ.get("GMPEA_REF_SLOTS", "0")) or -(-n // threads)
+        value, secs = cpu_reference(problem, n_sub, op, args.steps, min(args.warmup, 3), threads)
+        sample = (f"{threads} concurrent reference runs (oracle/_ref, unmodified gmpea loop) x N={n_sub} "
+                  f"slots x {args.steps} timed generations ({secs:.1f} s), windowed-lattice topology, "
+                  f"setup untimed")
         line = {"metric": METRIC, "value": value, "unit": "ind-gen/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 2 * n / value * 1e3,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": threads * 2 * n_sub / value * 1e3,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (Philox/mt19937 initial populations)", "impl": "reference",
+                "data": "synthetic (mt19937_64 initial populations)", "impl": "reference",
                 "config": config,
-                "cpu_baseline": {"value": value, "unit": "ind-gen/s", "cores": threads, "kind": kind,
-                                 "sample": f"{threads} independent reference runs x 1 generation of "
-                                           f"N={n} per step (topology injected, setup untimed)"},
+                "cpu_baseline": {"value": value, "unit": "ind-gen/s", "cores": threads, "kind": "reference",
+                                 "sample": sample},
                 "e2e": {"value": value, "unit": "ind-gen/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -196,8 +206,7 @@ def main():
     stream = torch.cuda.Stream()  # the engine's launching stream (events are recorded on it)
     torch.cuda.set_stream(stream)
     prob = g.make_problem(problem)
-    PRE_MAX = 20000  # untimed generations keeping the GPU busy while the clock sampler settles
-    budget_gens = args.warmup + 4 * args.steps + 16 + PRE_MAX
+    budget_gens = args.warmup + 4 * args.steps + 16
     if world == 1:
         cfg = g.RunConfig(n=n, k_max=0, eval_budget=2 * n * budget_gens, seed=1, op=op, device=local,
                           stream=stream.cuda_stream)
@@ -212,26 +221,16 @@ def main():
         shard = GpuShard(prob, cfg, world, rank, TorchComm())
         eng = shard.eng
         advance = shard.run
-    t0 = time.perf_counter()
     advance(args.warmup)
     torch.cuda.synchronize()
-    t_gen = (time.perf_counter() - t0) / max(1, args.warmup)
-    pre = int(min(PRE_MAX, max(0, 0.6 / max(t_gen, 1e-6))))  # ~0.6 s of load before the timed region
     if world > 1:
-        t = torch.tensor([pre], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        pre = int(t.item())
         torch.distributed.barrier()
 
-    # ---- timed region: K generations, CUDA events on the engine's stream; the
-    # clock sampler runs across the untimed load generations and the region
+    # ---- timed region: K generations, CUDA events on the engine's stream,
+    # clocks sampled by NVML while it runs
     clocks = Clocks(local)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with clocks:
-        advance(pre)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
         start.record(stream)
         advance(args.steps)
         end.record(stream)
@@ -320,12 +319,12 @@ def main():
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            topo = eng.neighborhoods()
-            threads = max(1, min(os.cpu_count() or 1, 8))
-            v, secs, kind = cpu_reference(problem, n, op, args.cpu_gens, 0, threads, topo=topo)
-            cpu = {"value": v, "unit": "ind-gen/s", "cores": threads, "kind": kind,
-                   "sample": f"{threads} concurrent reference runs x {args.cpu_gens} generations of "
-                             f"N={n} ({secs:.1f} s), topology injected, setup untimed"}
+            threads = ref_threads()
+            n_sub = -(-n // threads)
+            v, secs = cpu_reference(problem, n_sub, op, args.cpu_gens, 1, threads)
+            cpu = {"value": v, "unit": "ind-gen/s", "cores": threads, "kind": "reference",
+                   "sample": f"{threads} concurrent reference runs x N={n_sub} slots x {args.cpu_gens} "
+                             f"generations ({secs:.1f} s), windowed-lattice topology, setup untimed"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "ind-gen/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}

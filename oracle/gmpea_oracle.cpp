@@ -31,6 +31,7 @@
 #include <cstring>
 #include <limits>
 #include <random>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -736,6 +737,80 @@ void knn(const double* W, size_t n, size_t m, size_t t, uint32_t* out) {
     }
 }
 
+// windowed t-NN on the Das-Dennis lattice, same (d2, j) order as
+// gmpea.cpp:84-97: candidates within +-R lattice steps, accepted only when
+// every point outside the window is provably farther than the t-th one
+// (else the window doubles).  Lets the CPU baseline build topologies at N
+// where the reference's O(N^2 log N) build_neighborhoods is impractical.
+void lattice_knn(size_t m, size_t n, size_t t1, size_t t2, uint32_t* B1, uint32_t* B2, unsigned threads) {
+    size_t H = 1;
+    if (m == 2) H = n > 1 ? n - 1 : 1;
+    else
+        while (lattice_size(m, H) < n) ++H;
+    std::vector<double> W = reference_vectors(m, n);
+    auto start3 = [&](long long a) { return a * (long long)(H + 1) - a * (a - 1) / 2; };
+    auto unrank = [&](long long i, long long& a, long long& b) {
+        if (m == 2) { a = i; b = (long long)H - i; return; }
+        long long lo = 0, hi = (long long)H;
+        while (lo < hi) {
+            long long mid = (lo + hi + 1) / 2;
+            if (start3(mid) <= i) lo = mid; else hi = mid - 1;
+        }
+        a = lo;
+        b = i - start3(lo);
+    };
+    auto work = [&](size_t r0, size_t r1) {
+        std::vector<std::pair<double, uint32_t>> cand;
+        for (size_t i = r0; i < r1; ++i) {
+            long long a, b;
+            unrank((long long)i, a, b);
+            for (long long R = 6;; R *= 2) {
+                cand.clear();
+                auto push = [&](long long j) {
+                    double s2 = 0.0;
+                    for (size_t c = 0; c < m; ++c) {
+                        double d = W[i * m + c] - W[(size_t)j * m + c];
+                        s2 += d * d;
+                    }
+                    cand.emplace_back(s2, (uint32_t)j);
+                };
+                bool all;
+                if (m == 2) {
+                    long long lo = std::max(0ll, (long long)i - R), hi = std::min((long long)n - 1, (long long)i + R);
+                    for (long long j = lo; j <= hi; ++j) push(j);
+                    all = lo == 0 && hi == (long long)n - 1;
+                } else {
+                    for (long long aa = a - R; aa <= a + R; ++aa) {
+                        if (aa < 0 || aa > (long long)H) continue;
+                        for (long long bb = b - R; bb <= b + R; ++bb) {
+                            if (bb < 0 || aa + bb > (long long)H) continue;
+                            long long j = start3(aa) + bb;
+                            if (j < (long long)n) push(j);
+                        }
+                    }
+                    all = (a - R <= 0) && (a + R >= (long long)H) && (b - R <= 0) && (b + R >= (long long)H);
+                }
+                size_t t = std::max(t1, t2);
+                if (cand.size() < t && !all) continue;
+                std::partial_sort(cand.begin(), cand.begin() + (std::ptrdiff_t)t, cand.end());
+                if (!all) {
+                    double step = (double)(R + 1) / (double)H;
+                    double bound = (m == 2 ? 2.0 : 1.0) * step * step * (1.0 - 1e-9);
+                    if (!(cand[t - 1].first < bound)) continue;
+                }
+                for (size_t k = 0; k < t1; ++k) B1[i * t1 + k] = cand[k].second;
+                for (size_t k = 0; k < t2; ++k) B2[i * t2 + k] = cand[k].second;
+                break;
+            }
+        }
+    };
+    threads = std::max(1u, threads);
+    std::vector<std::thread> th;
+    for (unsigned k = 0; k < threads; ++k)
+        th.emplace_back(work, n * k / threads, n * (k + 1) / threads);
+    for (auto& x : th) x.join();
+}
+
 // ---------------------------------------------------------------------------
 // environmental selection (reference: proj/src/gmpea.cpp:248-399)
 //
@@ -1172,6 +1247,13 @@ int orc_knn(const double* W, int64_t n, int32_t m, int32_t t, uint32_t* out) {
     return guarded([&] {
         if (t > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
         knn(W, static_cast<size_t>(n), static_cast<size_t>(m), static_cast<size_t>(t), out);
+    });
+}
+
+int orc_lattice_knn(int32_t m, int64_t n, int32_t t1, int32_t t2, uint32_t* B1, uint32_t* B2, int32_t threads) {
+    return guarded([&] {
+        if (t1 > n || t2 > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
+        lattice_knn((size_t)m, (size_t)n, (size_t)t1, (size_t)t2, B1, B2, (unsigned)threads);
     });
 }
 

@@ -133,6 +133,13 @@ class Oracle(_Lib):
         self._check(self.lib.orc_knn(_ptr(W, _dp), C.c_int64(n), m, t, _ptr(out, _u32p)))
         return out
 
+    def lattice_knn(self, m, n, t1, t2, threads=0):
+        B1 = np.zeros((n, t1), np.uint32)
+        B2 = np.zeros((n, t2), np.uint32)
+        threads = threads or (os.cpu_count() or 1)
+        self._check(self.lib.orc_lattice_knn(m, C.c_int64(n), t1, t2, _ptr(B1, _u32p), _ptr(B2, _u32p), threads))
+        return B1, B2
+
     # -- selection --------------------------------------------------------
     def selection(self, pops, W, z, theta, B1, B2, want_marks=False):
         """pops = [pop1, pop2, off1, off2], each a dict with F (n x m), cv (n).

@@ -53,6 +53,10 @@ def test_lattice_and_knn_match_golden(orc):
         if W.shape[0] <= 1100:
             assert np.array_equal(orc.knn(W, gd[key + "/B1"].shape[1]), gd[key + "/B1"]), key
             assert np.array_equal(orc.knn(W, gd[key + "/B2"].shape[1]), gd[key + "/B2"]), key
+        if key.startswith("lat_"):
+            # the windowed lattice KNN (CPU-baseline topology) == build_neighborhoods
+            B1, B2 = orc.lattice_knn(int(m), int(n), int(t1), int(t2), threads=2)
+            assert np.array_equal(B1, gd[key + "/B1"]) and np.array_equal(B2, gd[key + "/B2"]), key
 
 
 def test_selection_matches_golden(orc):
