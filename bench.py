@@ -335,7 +335,7 @@ def main():
             "scaling": "strong",  # N = 1M slots in total, split into weight-region shards
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (Philox-initialised populations)",
             "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": int(args.steps * 5 + 1)}
+            "clocks": clocks.summary(), "gpu_launches": int(3 * args.steps + 1 if world == 1 else 4 * args.steps)}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -393,10 +393,6 @@ __global__ void slice_topology_kernel(const int* Bg, int t, long long e0, long l
     Bl[e] = (g >= r0 && g < r1) ? (int)(Bg[g * t + e % t] - e0) : (int)i;
 }
 
-__global__ void publish_stop_kernel(const DevState* st, volatile int* host_flag) {
-    *host_flag = st->stop | (st->err ? 2 : 0);
-}
-
 // individuals as padded fp32 rows [x | g | pad] plus packed keys
 struct RowGeom {
     int rs4;   // row stride, float4
@@ -430,18 +426,25 @@ using VaryKernel = void (*)(VaryParams);
 
 // the dimension-specialised generation kernels also assume uniform bounds
 // (true of every registered suite; checked by the caller)
-template <class Ev, int DC = 0>
+template <class Ev, int DC = 0, bool VARY_ONLY = false>
 VaryKernel pick_vary(int mode, int op) {
-    if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
-    if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
+    if (!VARY_ONLY) {
+        if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
+        if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
+    }
     constexpr bool UB = DC > 0;
     return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC, UB> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UB>;
 }
 
 // the generation kernel is compiled for the registered suites' dimension
-VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0) {
+VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0) {
     switch (fam) {
-        case FAM_LIR: return d == 30 ? pick_vary<EvalLir, 30>(mode, op) : pick_vary<EvalLir>(mode, op);
+        case FAM_LIR:
+            if (d != 30 || mode != MODE_VARY) return pick_vary<EvalLir>(mode, op);
+            return id <= 4 ? pick_vary<EvalLirT<1>, 30, true>(mode, op)
+                           : (id <= 8 ? pick_vary<EvalLirT<5>, 30, true>(mode, op)
+                                      : (id <= 12 ? pick_vary<EvalLirT<9>, 30, true>(mode, op)
+                                                  : pick_vary<EvalLirT<13>, 30, true>(mode, op)));
         case FAM_DTLZ:
             return d == 7 ? pick_vary<EvalDtlz, 7>(mode, op)
                           : (d == 12 ? pick_vary<EvalDtlz, 12>(mode, op) : pick_vary<EvalDtlz>(mode, op));
@@ -771,7 +774,7 @@ struct gmpea_engine {
             vp.out[q] = off[q].X.p;
             vp.outFcv[q] = off[q].Fcv.p;
         }
-        vary = vary_kernel_for(p->fam, MODE_VARY, c.op, p->dev.uniform ? d : 0);
+        vary = vary_kernel_for(p->fam, MODE_VARY, c.op, p->dev.uniform ? d : 0, p->dev.id);
         vp.row0 = (int)(v0 - e0);
         vp.row_end = (int)(v1 - e0);
         op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p},
@@ -1369,7 +1372,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.st = st.p;
         vp.bad_rows[0] = bad.p;
         vp.bad_cap = 0;  // reproduce itself never throws on bounds
-        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op, p->dev.uniform ? d : 0), vp, 1, s);
+        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op, p->dev.uniform ? d : 0, p->dev.id), vp, 1, s);
         CK(cudaGetLastError());
         from_rows_kernel<<<blocks_for(n * d, 256), 256>>>((const float*)Op.p, geo.rs4 * 4, n, 0, d, h.p);
         CK(cudaMemcpy(off, h.p, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToHost));

@@ -21,6 +21,8 @@
 // winner row is one cache line instead of d separate sectors; the selection
 // keys live apart as packed float4 {f0, f1, f2, cv} per slot.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "problems.cuh"
 
@@ -196,6 +198,13 @@ struct PickStream {
         return (unsigned)r;
     }
 };
+
+// 256-bit global load (sm_100: LDG.E.256); p must be 32 B aligned
+__device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
+    asm("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+}
 
 __device__ __forceinline__ unsigned pick_word(const u32x4& w, int k) {
     return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
@@ -383,6 +392,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 }
             }
             const bool de_all = p.de_T >= 0xffffffffll;
+            const bool even_rows = (rs4 & 1) == 0;  // rows 32 B aligned
             const unsigned k0 = p.key0, k1 = p.key1;
             for (int w0 = 0; w0 < d; w0 += 64) {
                 const int w1 = min(d, w0 + 64);
@@ -409,12 +419,14 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                     }
                 } else {
                     // eight genes per group: one XCOIN and one MCOIN counter (16-bit coin
-                    // heads), two XU counters (32-bit spread uniforms)
-                    if (active)
-#pragma unroll 1
-                    for (int jb = w0; jb < w1; jb += 8) {
+                    // heads), two XU counters (32-bit spread uniforms).  NGC > 0 makes
+                    // the group's gene count a compile-time constant (DC suites), so
+                    // the per-gene code carries no bounds tests
+                    auto group = [&](const int jb, auto ngc) {
+                        constexpr int NGC = decltype(ngc)::value;
+                        const int ng = NGC > 0 ? NGC : min(8, w1 - jb);
+                        const bool two = NGC > 0 ? (NGC > 4) : (jb + 4 < w1);
                         const int q = jb >> 2;
-                        const bool two = jb + 4 < w1;
                         u32x4 xc{0, 0, 0, 0}, mc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0};
                         const unsigned idx8 = (unsigned)(jb >> 3);
                         if (OP == OP_SBX && cross) {
@@ -425,6 +437,16 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, k0, k1);
                         if (p.pm_T >= 0) mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, k0, k1);
                         float4 a4[2], b4[2], c4[2];
+                        if (two && even_rows) {  // one 32 B sector per parent: 256-bit loads
+                            ldg256(PA + q, a4[0], a4[1]);
+                            ldg256(PB + q, b4[0], b4[1]);
+                            if (OP == OP_DE) {
+                                ldg256(PC + q, c4[0], c4[1]);
+                            } else {
+                                c4[0] = a4[0];
+                                c4[1] = a4[1];
+                            }
+                        } else {
                         a4[0] = PA[q];
                         b4[0] = PB[q];
                         c4[0] = OP == OP_DE ? PC[q] : a4[0];
@@ -435,7 +457,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         } else {
                             a4[1] = b4[1] = c4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
-                        const int ng = min(8, w1 - jb);
+                        }
                         // per-gene SBX coin u <= 0.5 <=> w <= 2^31 (gmpea.cpp:119), DE CR coin, PM coin
                         const unsigned xbits =
                             OP == OP_SBX ? (cross ? coins8(xc, 0x80000000ll, ng, slot, gen, philox_tag(pid, STREAM_XREF),
@@ -450,7 +472,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
                             const int j = jb + k;
-                            if (j >= w1) {
+                            if (k >= ng) {
                                 v[k] = 0.0f;
                                 continue;
                             }
@@ -480,6 +502,16 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         mmask |= (unsigned long long)mbits << (jb - w0);
                         my4[q] = make_float4(v[0], v[1], v[2], v[3]);
                         if (two) my4[q + 1] = make_float4(v[4], v[5], v[6], v[7]);
+                    };
+                    if (active) {
+                        if (DC > 0 && DC <= 64) {  // one window, full groups then the tail
+#pragma unroll 1
+                            for (int jb = 0; jb + 8 <= DC; jb += 8) group(jb, std::integral_constant<int, 8>{});
+                            if (DC % 8) group(DC / 8 * 8, std::integral_constant<int, (DC % 8)>{});
+                        } else {
+#pragma unroll 1
+                            for (int jb = w0; jb < w1; jb += 8) group(jb, std::integral_constant<int, 0>{});
+                        }
                     }
                 }
                 // phase 2: polynomial mutation then clip (gmpea.cpp:202-203).

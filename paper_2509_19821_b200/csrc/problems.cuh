@@ -52,7 +52,10 @@ struct ProbDev {
 };
 
 // ---------------------------------------------------------------- LIRCMOP
-struct EvalLir {
+// SUB > 0 fixes the sub-family at compile time (1: LIRCMOP1-4, 5: 5-8,
+// 9: 9-12, 13: 13-14) so the per-gene code carries no problem dispatch.
+template <int SUB = 0>
+struct EvalLirT {
     static constexpr bool kWholeRow = false;
     static constexpr int kScratchF4 = 0;
     template <class G>
@@ -60,16 +63,19 @@ struct EvalLir {
     double g1, g2, x0, x1, s0, c0;
     float x0f;
     __device__ __forceinline__ void begin(const ProbDev&) { g1 = g2 = 0.0; }
+    __device__ __forceinline__ static int sub_of(int id) {
+        return SUB ? SUB : (id <= 4 ? 1 : (id <= 8 ? 5 : (id <= 12 ? 9 : 13)));
+    }
     __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
         const double x = xf;
-        const int id = P.id;
+        const int sub = sub_of(P.id);
         if (j == 0) {
             x0 = x;
             x0f = xf;
-            if (id <= 4) sincospi(0.5 * x, &s0, &c0);  // problems.cpp:23-24
+            if (sub == 1) sincospi(0.5 * x, &s0, &c0);  // problems.cpp:23-24
             return;
         }
-        if (id >= 13) {  // problems.cpp:124-128
+        if (sub == 13) {  // problems.cpp:124-128
             if (j == 1) {
                 x1 = x;
                 return;
@@ -79,7 +85,7 @@ struct EvalLir {
             return;
         }
         double track;
-        if (id <= 4) {
+        if (sub == 1) {
             track = (j & 1) ? c0 : s0;
         } else {  // problems.cpp:43-50: sin/cos(0.5 (j+1) pi x1 / n)
             float a = __fdiv_rn(0.5f * (float)(j + 1) * x0f, (float)P.d);
@@ -100,7 +106,8 @@ struct EvalLir {
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
         const int id = P.id;
-        if (id <= 4) {
+        const int sub = sub_of(id);
+        if (sub == 1) {
             f[0] = x0 + g1;
             f[1] = (id == 1 || id == 3) ? 1.0 - x0 * x0 + g2 : 1.0 - sqrt(x0) + g2;
             emit(0, -((0.51 - g1) * (g1 - 0.5)));
@@ -108,7 +115,7 @@ struct EvalLir {
             if (id >= 3) emit(2, 0.5 - sinpi(20.0 * x0));
             return;
         }
-        if (id <= 8) {
+        if (sub == 5) {
             f[0] = x0 + 10.0 * g1 + 0.7057;
             bool sq = (id == 5 || id == 7);
             f[1] = (sq ? 1.0 - sqrt(x0) : 1.0 - x0 * x0) + 10.0 * g2 + 0.7057;
@@ -124,7 +131,7 @@ struct EvalLir {
             }
             return;
         }
-        if (id <= 12) {
+        if (sub == 9) {
             f[0] = 1.7057 * x0 * (10.0 * g1 + 1.0);
             bool sq = (id == 10 || id == 11);
             f[1] = 1.7057 * (sq ? 1.0 - sqrt(x0) : 1.0 - x0 * x0) * (10.0 * g2 + 1.0);
@@ -152,6 +159,7 @@ struct EvalLir {
         if (id == 14) emit(2, -((r2 - 3.0625) * (r2 - 2.56)));
     }
 };
+using EvalLir = EvalLirT<0>;
 
 // ---------------------------------------------------------------- C/DC-DTLZ
 struct EvalDtlz {
@@ -310,7 +318,7 @@ struct EvalMw {
     }
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
-        const int id = P.id, n = P.d, m = P.m;
+        const int id = P.id, n = P.d;
         const double r2 = sqrt(2.0);
         switch (id) {
             case 1: case 2: {

@@ -49,7 +49,8 @@ def hv_of(front, lo, hi, hv_fn):
 def cmd_ref(args):
     from oracle import Reference
 
-    jobs = [(p, args.n, args.gens, s) for p in PROBLEMS for s in range(1, args.seeds + 1)]
+    probs = args.problems.split(",") if args.problems else PROBLEMS
+    jobs = [(p, args.n, args.gens, s) for p in probs for s in range(1, args.seeds + 1)]
     fronts = {}
     with ProcessPoolExecutor(args.procs) as ex:
         for name, seed, fr in ex.map(_ref_run, jobs):
@@ -57,7 +58,7 @@ def cmd_ref(args):
             print(name, seed, len(fr), flush=True)
     ref = Reference()
     out = {"n": args.n, "gens": args.gens, "seeds": args.seeds, "problems": {}}
-    for name in PROBLEMS:
+    for name in probs:
         allf = [f for f in fronts[name].values() if len(f)]
         if not allf:
             out["problems"][name] = {"ideal": None, "nadir": None, "hv": [0.0] * args.seeds}
@@ -66,7 +67,7 @@ def cmd_ref(args):
         lo, hi = cat.min(0), cat.max(0)
         hvs = [hv_of(fronts[name][s], lo, hi, ref.hypervolume) for s in range(1, args.seeds + 1)]
         out["problems"][name] = {"ideal": lo.tolist(), "nadir": hi.tolist(), "hv": hvs}
-    with open(REF_JSON, "w") as f:
+    with open(args.ref_json, "w") as f:
         json.dump(out, f, indent=1)
 
 
@@ -75,9 +76,9 @@ def cmd_gpu(args):
 
     import paper_2509_19821_b200 as g
 
-    ref = json.load(open(REF_JSON))
+    ref = json.load(open(args.ref_json))
     res = {}
-    for name in PROBLEMS:
+    for name in ref["problems"]:
         rp = ref["problems"][name]
         p = g.make_problem(name)
         hvs = []
@@ -94,9 +95,11 @@ def cmd_gpu(args):
         else:
             pval = float(mannwhitneyu(a, b, alternative="two-sided").pvalue)
         res[name] = {"b200_median_hv": float(np.median(a)), "ref_median_hv": float(np.median(b)), "p_value": pval,
-                     "verdict": "=" if pval >= 0.05 else ("+" if np.median(a) > np.median(b) else "-")}
+                     "verdict": "=" if pval >= 0.05 else ("+" if np.mean(a) > np.mean(b) else "-"),
+                     "b200_feasible_runs": int((a > 0).sum()), "ref_feasible_runs": int((b > 0).sum()),
+                     "b200_hv": [float(x) for x in a]}
         print(name, res[name], flush=True)
-    with open(os.path.join(ROOT, "profiles", "r01_mw_parity.json"), "w") as f:
+    with open(args.out, "w") as f:
         json.dump({"config": {k: ref[k] for k in ("n", "gens", "seeds")}, "results": res}, f, indent=1)
 
 
@@ -107,6 +110,9 @@ def main():
     ap.add_argument("--n", type=int, default=10000)
     ap.add_argument("--gens", type=int, default=200)
     ap.add_argument("--procs", type=int, default=6)
+    ap.add_argument("--problems", default="")
+    ap.add_argument("--ref-json", default=REF_JSON)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_mw_parity.json"))
     args = ap.parse_args()
     cmd_ref(args) if args.cmd == "ref" else cmd_gpu(args)
 

@@ -43,20 +43,27 @@ def sass_lines(lib, mangled_hint):
     cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".cubin")][0]
     txt = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
     funcs = {}
-    cur, line = None, None
+    # each instruction is preceded by its inlining chain, innermost first
+    # ("line A inlined at B", then "line B" ...); attribute it to the
+    # innermost line in our own sources (CUDA headers are skipped)
+    cur, line, chain, fresh = None, None, [], True
     for ln in txt.splitlines():
-        m = re.match(r"\s*\.text\.(\S+):", ln) or re.match(r"^(\S+):$", ln.strip())
         if ln.strip().startswith(".text.") and ln.strip().endswith(":"):
             cur = ln.strip()[len(".text."):-1]
             funcs[cur] = {}
             continue
         m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
         if m:
-            line = f"{os.path.basename(m.group(1))}:{m.group(2)}"
+            if fresh:
+                chain, fresh = [], False
+            chain.append((m.group(1), f"{os.path.basename(m.group(1))}:{m.group(2)}"))
+            own = [c for f, c in chain if "/cuda" not in f and "targets/" not in f]
+            line = own[0] if own else chain[0][1]
             continue
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and cur is not None:
             funcs[cur][int(m.group(1), 16)] = line
+            fresh = True
     return funcs
 
 
