@@ -236,8 +236,8 @@ __device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned 
     const float span = hi - lo;
     if (!(span > 0.0f)) return x;
     const bool low = w < 0x80000000u;  // u < 0.5
-    const float A = low ? (float)w * 0x1.0p-31f                                            // 2u
-                        : (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;   // 2(1-u)
+    const float A = low ? (float)w * 0x1.0p-31f           // 2u
+                        : (float)(0u - w) * 0x1.0p-31f;   // 2(1-u): 2^32 - w, exact in 32 bits
     const float B = low ? (float)(0x80000000u - w) * 0x1.0p-31f                          // 1 - 2u
                         : (float)(w - 0x80000000u) * 0x1.0p-31f;                         // 2(u-0.5)
     const float dd = (low ? (x - lo) : (hi - x)) * (span == 1.0f ? 1.0f : 1.0f / span);  // d1 / d2
@@ -256,7 +256,7 @@ __device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned 
 // by < 1e-6 of the parents' spread) at a fraction of powf's cost.
 __device__ __forceinline__ float sbx_beta(unsigned w, float e) {
     const bool low = w <= 0x80000000u;
-    const float b = low ? (float)w * 0x1.0p-31f : (float)(0x100000000ull - (unsigned long long)w) * 0x1.0p-31f;
+    const float b = low ? (float)w * 0x1.0p-31f : (float)(0u - w) * 0x1.0p-31f;  // 2^32 - w (w > 2^31)
     if (b == 0.0f) return 0.0f;  // u = 0: beta = 0
     return exp2f((low ? e : -e) * __log2f(b));
 }
@@ -370,9 +370,11 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
         } else {
             // the whole warp stays in this branch (pm_tasks is warp-cooperative);
             // lanes past the end only skip the per-slot work
-            const float4* __restrict__ PA = p.parX[pi];
-            const float4* __restrict__ PB = p.parX[pi];
-            const float4* __restrict__ PC = p.parX[pi] + (long long)i * rs4;
+            // parents as one base pointer plus 32-bit row offsets (float4 units;
+            // n * rs4 < 2^32) to keep the group loop's live set small
+            const float4* __restrict__ PX = p.parX[pi];
+            unsigned oa = 0u, ob = 0u;
+            const unsigned oc = (unsigned)i * (unsigned)rs4;
             int jrand = -1;
             bool cross = true;
             if (MODE == MODE_VARY && active) {
@@ -382,8 +384,8 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 unsigned b = ps.index(p.ui[pi]);
                 while (t > 1 && b == a) b = ps.index(p.ui[pi]);
                 const int* Brow = p.B[pi] + (long long)i * t;
-                PA += (long long)Brow[a] * rs4;
-                PB += (long long)Brow[b] * rs4;
+                oa = (unsigned)Brow[a] * (unsigned)rs4;
+                ob = (unsigned)Brow[b] * (unsigned)rs4;
                 if (OP == OP_SBX) {
                     u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
                     cross = u53(c.x, c.y) <= p.sbx_prob;
@@ -396,7 +398,9 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             const unsigned k0 = p.key0, k1 = p.key1;
             for (int w0 = 0; w0 < d; w0 += 64) {
                 const int w1 = min(d, w0 + 64);
-                unsigned long long mmask = 0ull;
+                // genes of this window PM selects (32 bits suffice for d <= 32)
+                using Mask = typename std::conditional<(DC > 0 && DC <= 32), unsigned, unsigned long long>::type;
+                Mask mmask = 0;
                 if (MODE == MODE_INIT) {
                     for (int jb = w0; jb < (active ? w1 : w0); jb += 4) {  // 64-bit pair (j % 2) of counter j / 2
                         const u32x4 xa = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), k0, k1);
@@ -438,22 +442,22 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         if (p.pm_T >= 0) mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, k0, k1);
                         float4 a4[2], b4[2], c4[2];
                         if (two && even_rows) {  // one 32 B sector per parent: 256-bit loads
-                            ldg256(PA + q, a4[0], a4[1]);
-                            ldg256(PB + q, b4[0], b4[1]);
+                            ldg256(PX + (oa + q), a4[0], a4[1]);
+                            ldg256(PX + (ob + q), b4[0], b4[1]);
                             if (OP == OP_DE) {
-                                ldg256(PC + q, c4[0], c4[1]);
+                                ldg256(PX + (oc + q), c4[0], c4[1]);
                             } else {
                                 c4[0] = a4[0];
                                 c4[1] = a4[1];
                             }
                         } else {
-                        a4[0] = PA[q];
-                        b4[0] = PB[q];
-                        c4[0] = OP == OP_DE ? PC[q] : a4[0];
+                        a4[0] = PX[oa + q];
+                        b4[0] = PX[ob + q];
+                        c4[0] = OP == OP_DE ? PX[oc + q] : a4[0];
                         if (two) {
-                            a4[1] = PA[q + 1];
-                            b4[1] = PB[q + 1];
-                            c4[1] = OP == OP_DE ? PC[q + 1] : a4[1];
+                            a4[1] = PX[oa + q + 1];
+                            b4[1] = PX[ob + q + 1];
+                            c4[1] = OP == OP_DE ? PX[oc + q + 1] : a4[1];
                         } else {
                             a4[1] = b4[1] = c4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
@@ -469,37 +473,48 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         const unsigned mbits = coins8(mc, p.pm_T, ng, slot, gen, philox_tag(pid, STREAM_MREF),
                                                       (unsigned)jb, k0, k1);
                         float v[8];
+                        auto comp = [](const float4& f, int kk) {
+                            return kk == 0 ? f.x : (kk == 1 ? f.y : (kk == 2 ? f.z : f.w));
+                        };
 #pragma unroll
                         for (int k = 0; k < 8; ++k) {
-                            const int j = jb + k;
                             if (k >= ng) {
                                 v[k] = 0.0f;
                                 continue;
                             }
-                            const float4& A = a4[k >> 2];
-                            const float4& Bv = b4[k >> 2];
-                            const float4& Cv = c4[k >> 2];
                             const int kk = k & 3;
-                            const float av = kk == 0 ? A.x : (kk == 1 ? A.y : (kk == 2 ? A.z : A.w));
-                            const float bv = kk == 0 ? Bv.x : (kk == 1 ? Bv.y : (kk == 2 ? Bv.z : Bv.w));
-                            const float cvv = kk == 0 ? Cv.x : (kk == 1 ? Cv.y : (kk == 2 ? Cv.z : Cv.w));
-                            const bool xk = (xbits >> k) & 1u;
-                            float c;
+                            const float av = comp(a4[k >> 2], kk);
+                            const float bv = comp(b4[k >> 2], kk);
                             if (OP == OP_SBX) {
-                                if (xk) {
+                                if ((xbits >> k) & 1u) {
                                     const float beta = sbx_beta(pick_word(k < 4 ? xu0 : xu1, kk), p.sbx_e);
-                                    c = 0.5f * ((1.0f + beta) * av + (1.0f - beta) * bv);
+                                    v[k] = 0.5f * ((1.0f + beta) * av + (1.0f - beta) * bv);
                                 } else {
-                                    c = av;
+                                    v[k] = av;
                                 }
                             } else {
-                                c = (j == jrand || xk) ? cvv + p.de_f * (av - bv) : cvv;
+                                v[k] = comp(c4[k >> 2], kk) + p.de_f * (av - bv);
                             }
-                            // mutated genes are clipped after PM (phase 2)
-                            const float cl = clamp_ref(c, GMPEA_LO(j), GMPEA_HI(j));
-                            v[k] = ((mbits >> k) & 1u) ? c : cl;
                         }
-                        mmask |= (unsigned long long)mbits << (jb - w0);
+                        if (OP == OP_DE) {
+                            // genes that neither win the CR coin nor are jrand keep the
+                            // target's value (gmpea.cpp:196-199); none when CR = 1
+                            unsigned take = xbits;
+                            const int jr = jrand - jb;
+                            if (jr >= 0 && jr < ng) take |= 1u << jr;
+                            if (take != (1u << ng) - 1u) {
+#pragma unroll
+                                for (int k = 0; k < 8; ++k)
+                                    if (k < ng && !((take >> k) & 1u)) v[k] = comp(c4[k >> 2], k & 3);
+                            }
+                        }
+                        // clip (gmpea.cpp:202-203; children are finite here, so min/max
+                        // equals std::clamp); mutated genes are clipped after PM (phase 2)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            if (k < ng && !((mbits >> k) & 1u))
+                                v[k] = fminf(fmaxf(v[k], GMPEA_LO(jb + k)), GMPEA_HI(jb + k));
+                        mmask |= (Mask)mbits << (jb - w0);
                         my4[q] = make_float4(v[0], v[1], v[2], v[3]);
                         if (two) my4[q + 1] = make_float4(v[4], v[5], v[6], v[7]);
                     };
@@ -517,7 +532,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 // phase 2: polynomial mutation then clip (gmpea.cpp:202-203).
                 // The warp's mutation tasks (lane, gene) are dealt round-robin
                 // over its lanes, ~1 task per lane per round.
-                if (MODE == MODE_VARY) pm_tasks(p, mmask, w0, sm4, gen, pid, i0);
+                if (MODE == MODE_VARY) pm_tasks(p, (unsigned long long)mmask, w0, sm4, gen, pid, i0);
             }
         }
         if (p.eval && active) {

@@ -263,6 +263,14 @@ struct EvalDtlz {
 // ---------------------------------------------------------------- MW (unpinned)
 __device__ __forceinline__ double ipow(double x, int e) {
     double r = 1.0;
+    if (e >= 0 && e < 32) {  // square-and-multiply, unrolled (same product order)
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            if (e & (1 << k)) r *= x;
+            x *= x;
+        }
+        return r;
+    }
     while (e) {
         if (e & 1) r *= x;
         x *= x;
@@ -279,7 +287,11 @@ struct EvalMw {
     double xs[2];
     double prev;
     double gs;
-    __device__ __forceinline__ void begin(const ProbDev&) { gs = 0.0; }
+    int kd;
+    __device__ __forceinline__ void begin(const ProbDev& P) {
+        gs = 0.0;
+        kd = kind(P.id);
+    }
     __device__ __forceinline__ static int kind(int id) {
         // 0: exp distance (MW1/4/5/9/12), 1: cos distance (2/6/8/10/13), 2: linear (3/7/11/14)
         switch (id) {
@@ -299,7 +311,6 @@ struct EvalMw {
             prev = x;
             return;
         }
-        int kd = kind(P.id);
         // per-gene terms: argument in fp64, the exponential / cosine in fp32
         // (each term < 1e-7 off; the sum accumulates in fp64)
         if (kd == 0) {
