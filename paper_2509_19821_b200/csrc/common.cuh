@@ -115,6 +115,43 @@ __device__ __forceinline__ u32x4 philox4x32_10(unsigned c0, unsigned c1, unsigne
     return {c0, c1, c2, c3};
 }
 
+// Philox key with the ten round keys precomputed on the host: kept in the
+// kernel's parameter space, every round key is a constant-bank operand of the
+// round's LOP3 instead of a live register (or a per-round add)
+struct PhiloxKey {
+    unsigned k[20];  // (k0, k1) of round r at [2r], [2r + 1]
+};
+
+__host__ inline PhiloxKey make_philox_key(unsigned long long seed) {
+    PhiloxKey K;
+    unsigned k0 = (unsigned)seed, k1 = (unsigned)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        K.k[2 * r] = k0;
+        K.k[2 * r + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return K;
+}
+
+__device__ __forceinline__ u32x4 philox4x32_10(unsigned c0, unsigned c1, unsigned c2, unsigned c3,
+                                               const PhiloxKey& K) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        unsigned lo0 = 0xD2511F53u * c0;
+        unsigned hi0 = __umulhi(0xD2511F53u, c0);
+        unsigned lo1 = 0xCD9E8D57u * c2;
+        unsigned hi1 = __umulhi(0xCD9E8D57u, c2);
+        unsigned n0 = hi1 ^ c1 ^ K.k[2 * r];
+        unsigned n2 = hi0 ^ c3 ^ K.k[2 * r + 1];
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    return {c0, c1, c2, c3};
+}
+
 __device__ __forceinline__ double u53(unsigned lo, unsigned hi) {
     unsigned long long v = ((unsigned long long)hi << 32) | lo;
     return (double)(v >> 11) * 0x1.0p-53;

@@ -743,8 +743,7 @@ struct gmpea_engine {
         vp.t[1] = t2;
         vp.ui[0] = make_uidx((unsigned long long)t1);
         vp.ui[1] = make_uidx((unsigned long long)t2);
-        vp.key0 = (unsigned)c.seed;
-        vp.key1 = (unsigned)(c.seed >> 32);
+        vp.key = make_philox_key(c.seed);
         fill_op_params(vp, c.params, d);
         vp.eval = 1;
         vp.update_z = 1;
@@ -1361,8 +1360,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.t[0] = t;
         vp.ui[0] = make_uidx((unsigned long long)t);
         vp.out[0] = Op.p;
-        vp.key0 = (unsigned)seed;
-        vp.key1 = (unsigned)(seed >> 32);
+        vp.key = make_philox_key(seed);
         gmpea_operator_params prm;
         gmpea_operator_params_default(&prm);
         if (params) prm = *params;

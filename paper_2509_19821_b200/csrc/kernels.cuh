@@ -58,7 +58,7 @@ struct VaryParams {
     int t[2];
     float4* out[2];          // output rows (x | g)
     float4* outFcv[2];
-    unsigned key0, key1;     // Philox key (seed)
+    PhiloxKey key;           // Philox key (seed) with its round keys
     double sbx_prob;         // SBX per-child coin threshold on the 53-bit uniform
     float sbx_e;             // 1 / (eta_c + 1)
     float pm_e1;             // eta_m + 1
@@ -149,7 +149,7 @@ __device__ __forceinline__ unsigned half16(const u32x4& w, int k8) {
 // T's head is refined with the tail drawn from its own counter (probability
 // 2^-16 per gene), so the result equals the full 32-bit comparison.
 __device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngenes, unsigned slot, unsigned gen,
-                                           unsigned tag_ref, unsigned j0, unsigned k0, unsigned k1) {
+                                           unsigned tag_ref, unsigned j0, const PhiloxKey& K) {
     if (T < 0) return 0u;
     if (T >= 0xffffffffll) return (1u << ngenes) - 1u;
     const unsigned thi = (unsigned)(T >> 16), tlo = (unsigned)(T & 0xffff);
@@ -167,18 +167,19 @@ __device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngen
     while (tie) {  // rare
         const int k = __ffs(tie) - 1;
         tie &= tie - 1u;
-        const unsigned l = philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, k0, k1).x & 0xffffu;
+        const unsigned l = philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, K).x & 0xffffu;
         win |= (unsigned)(l <= tlo) << k;
     }
     return win;
 }
 
 struct PickStream {
-    unsigned slot, gen, tag, k0, k1;
+    unsigned slot, gen, tag;
+    const PhiloxKey& K;
     unsigned q;
     u32x4 cache;
     __device__ __forceinline__ unsigned long long next() {
-        if ((q & 1) == 0) cache = philox4x32_10(slot, gen, tag, q >> 1, k0, k1);
+        if ((q & 1) == 0) cache = philox4x32_10(slot, gen, tag, q >> 1, K);
         unsigned long long v = (q & 1) == 0 ? (((unsigned long long)cache.y << 32) | cache.x)
                                             : (((unsigned long long)cache.w << 32) | cache.z);
         ++q;
@@ -316,7 +317,7 @@ __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, 
             float* x = reinterpret_cast<float*>(sm4 + row * p.srs4);
             const unsigned slot = (unsigned)(p.slot_base + i0 + row);
             const float lo = p.P.lob(j), hi = p.P.hib(j);
-            const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key0, p.key1);
+            const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key);
             x[j] = clamp_ref(pm_apply(x[j], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
         }
         __syncthreads();
@@ -379,7 +380,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             bool cross = true;
             if (MODE == MODE_VARY && active) {
                 const int t = p.t[pi];
-                PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key0, p.key1, 0u, {}};
+                PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key, 0u, {}};
                 unsigned a = ps.index(p.ui[pi]);
                 unsigned b = ps.index(p.ui[pi]);
                 while (t > 1 && b == a) b = ps.index(p.ui[pi]);
@@ -387,7 +388,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 oa = (unsigned)Brow[a] * (unsigned)rs4;
                 ob = (unsigned)Brow[b] * (unsigned)rs4;
                 if (OP == OP_SBX) {
-                    u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key0, p.key1);
+                    u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key);
                     cross = u53(c.x, c.y) <= p.sbx_prob;
                 } else {
                     jrand = (int)ps.index(p.uid);
@@ -395,7 +396,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             }
             const bool de_all = p.de_T >= 0xffffffffll;
             const bool even_rows = (rs4 & 1) == 0;  // rows 32 B aligned
-            const unsigned k0 = p.key0, k1 = p.key1;
+            const PhiloxKey& K = p.key;
             for (int w0 = 0; w0 < d; w0 += 64) {
                 const int w1 = min(d, w0 + 64);
                 // genes of this window PM selects (32 bits suffice for d <= 32)
@@ -403,9 +404,9 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 Mask mmask = 0;
                 if (MODE == MODE_INIT) {
                     for (int jb = w0; jb < (active ? w1 : w0); jb += 4) {  // 64-bit pair (j % 2) of counter j / 2
-                        const u32x4 xa = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), k0, k1);
+                        const u32x4 xa = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), K);
                         const u32x4 xb =
-                            philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, k0, k1);
+                            philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1) + 1u, K);
                         float v[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
@@ -434,12 +435,12 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         u32x4 xc{0, 0, 0, 0}, mc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0};
                         const unsigned idx8 = (unsigned)(jb >> 3);
                         if (OP == OP_SBX && cross) {
-                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, k0, k1);
-                            xu0 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q, k0, k1);
-                            if (two) xu1 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q + 1u, k0, k1);
+                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, K);
+                            xu0 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q, K);
+                            if (two) xu1 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q + 1u, K);
                         }
-                        if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, k0, k1);
-                        if (p.pm_T >= 0) mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, k0, k1);
+                        if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, K);
+                        if (p.pm_T >= 0) mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, K);
                         float4 a4[2], b4[2], c4[2];
                         if (two && even_rows) {  // one 32 B sector per parent: 256-bit loads
                             ldg256(PX + (oa + q), a4[0], a4[1]);
@@ -465,13 +466,13 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         // per-gene SBX coin u <= 0.5 <=> w <= 2^31 (gmpea.cpp:119), DE CR coin, PM coin
                         const unsigned xbits =
                             OP == OP_SBX ? (cross ? coins8(xc, 0x80000000ll, ng, slot, gen, philox_tag(pid, STREAM_XREF),
-                                                           (unsigned)jb, k0, k1)
+                                                           (unsigned)jb, K)
                                                   : 0u)
                                          : (de_all ? (1u << ng) - 1u
                                                    : coins8(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
-                                                            (unsigned)jb, k0, k1));
+                                                            (unsigned)jb, K));
                         const unsigned mbits = coins8(mc, p.pm_T, ng, slot, gen, philox_tag(pid, STREAM_MREF),
-                                                      (unsigned)jb, k0, k1);
+                                                      (unsigned)jb, K);
                         float v[8];
                         auto comp = [](const float4& f, int kk) {
                             return kk == 0 ? f.x : (kk == 1 ? f.y : (kk == 2 ? f.z : f.w));
