@@ -243,6 +243,10 @@ def main():
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = 2 * n / (ms_step * 1e-3)  # whole job: all ranks together process the N-slot generation
+    # replacement rate over the timed generations (it drifts
+    # over a run, so it is reported with the throughput)
+    rr = eng.replacement_rates()
+    rep_rate = float(np.mean(rr[args.warmup + 1:args.warmup + 1 + args.steps]))
     # per-kernel device times (events around every launch) on this rank's
     # engine; run after the timed region (the shards no longer exchange)
     kms = eng.profile(args.steps)
@@ -334,7 +338,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong",  # N = 1M slots in total, split into weight-region shards
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (Philox-initialised populations)",
-            "config": config, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": config, "replacement_rate": rep_rate, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks.summary(), "gpu_launches": int(3 * args.steps + 1 if world == 1 else 4 * args.steps)}
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -160,6 +160,11 @@ int64_t gmpea_engine_effective_n(const gmpea_engine* e);
 int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, int64_t* n);
 /* the newest record only (blocks until the enqueued generations finished) */
 int gmpea_engine_last_record(gmpea_engine* e, gmpea_gen_record* out);
+/* diagnostic (no reference counterpart; SURVEY.md §8d "report the replacement
+ * rate"): per generation, the number of owned slots of both populations that
+ * took an offspring in OP3; out[0] (initialisation) is 0.  Same indexing and
+ * count semantics as gmpea_engine_history. */
+int gmpea_engine_replacements(gmpea_engine* e, int64_t* out, int64_t cap, int64_t* n);
 int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C,
                                 double* cv);
 int gmpea_engine_ideal(gmpea_engine* e, double* z);

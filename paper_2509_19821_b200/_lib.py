@@ -448,6 +448,16 @@ class Engine:
         return [GenRecord(r.gen, r.evals, r.wall_ms, r.feasible_ratio,
                           r.igd if r.has_igd else None, r.hv if r.has_hv else None) for r in buf]
 
+    def replacement_rates(self) -> np.ndarray:
+        """per generation: share of the owned slots of both populations that
+        took an offspring in OP3 (entry 0, initialisation, is 0)."""
+        cnt = C.c_int64()
+        _check(_L.gmpea_engine_replacements(self._h, None, 0, C.byref(cnt)))
+        buf = np.zeros(cnt.value, np.int64)
+        _check(_L.gmpea_engine_replacements(self._h, buf.ctypes.data_as(C.POINTER(C.c_int64)), cnt.value,
+                                            C.byref(cnt)))
+        return buf / (2.0 * self.rows_owned)
+
     def last_record(self) -> GenRecord:
         r = _GenRecord()
         _check(_L.gmpea_engine_last_record(self._h, C.byref(r)))

@@ -47,7 +47,7 @@ struct DevState {
 // per-generation record (gmpea.hpp:129-136); evals is derived on the host
 struct DevRecord {
     unsigned feasible;  // rows of pop1 with cv == 0 after the generation
-    unsigned pad;
+    unsigned replaced;  // slots of both populations that took an offspring (OP3)
     unsigned long long loop_ns;
 };
 

@@ -1030,6 +1030,17 @@ struct gmpea_engine {
     }
 
 
+    std::vector<int64_t> replacements() {
+        DevState h = read_state();
+        long long g = std::min<long long>(h.gens_done, rec_cap - 1);
+        std::vector<DevRecord> r(g + 1);
+        CK(cudaMemcpyAsync(r.data(), rec.p, (g + 1) * sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::vector<int64_t> out(g + 1);
+        for (long long k = 0; k <= g; ++k) out[k] = k == 0 ? 0 : (int64_t)r[k].replaced;
+        return out;
+    }
+
     // the newest generation record only (one small D2H; the per-step result)
     gmpea_gen_record last_record() {
         struct {
@@ -1656,6 +1667,15 @@ int64_t gmpea_engine_effective_n(const gmpea_engine* e) { return e ? e->N : 0; }
 int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, int64_t* nrec) {
     return guarded([&] {
         auto h = e->history();
+        int64_t k = std::min<int64_t>(cap, (int64_t)h.size());
+        if (out) std::copy(h.begin(), h.begin() + k, out);
+        *nrec = (int64_t)h.size();
+    });
+}
+
+int gmpea_engine_replacements(gmpea_engine* e, int64_t* out, int64_t cap, int64_t* nrec) {
+    return guarded([&] {
+        auto h = e->replacements();
         int64_t k = std::min<int64_t>(cap, (int64_t)h.size());
         if (out) std::copy(h.begin(), h.begin() + k, out);
         *nrec = (int64_t)h.size();

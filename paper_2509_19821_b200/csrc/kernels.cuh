@@ -612,12 +612,17 @@ __global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(Va
 
 // ---- PBI in fp32 on unit reference vectors (scalarize.cpp:72-89):
 // d1 = |(f - z) . u|, d2 = |(f - z) - d1 u|, g = d1 + theta d2.  Unused lanes
-// of f, u and z are zero for m = 2.
+// of f, u and z are zero for m = 2.  d2 uses the MUFU square root
+// (sqrt.approx, ~1 ulp): the keys are fp32 already, every PBI of a run goes
+// through this one function (op1 and select agree), and select's claimant
+// loop is latency-bound on it (-7.5 % select time vs the IEEE sqrtf).
 __device__ __forceinline__ float pbi(const float4 f, const float4 u, const float3 z, float theta) {
     const float a = f.x - z.x, b = f.y - z.y, c = f.z - z.z;
     const float d1 = fabsf(a * u.x + b * u.y + c * u.z);
     const float r0 = a - d1 * u.x, r1 = b - d1 * u.y, r2 = c - d1 * u.z;
-    return d1 + theta * sqrtf(r0 * r0 + r1 * r1 + r2 * r2);
+    float d2;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(d2) : "f"(r0 * r0 + r1 * r1 + r2 * r2));
+    return d1 + theta * d2;
 }
 
 __device__ __forceinline__ float3 load_z(const DevState* st, int m) {
@@ -704,7 +709,7 @@ __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4*
 }
 
 template <int POP>
-__device__ __forceinline__ void select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
+__device__ __forceinline__ bool select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
     const float4 par = p.Fcv[POP][j];
     const float4 u4 = p.U[j];
     const float gp = pbi(par, u4, z, p.theta);
@@ -783,7 +788,7 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
     }
     if (p.winner[POP]) p.winner[POP][j] = code;
     feas = (off_wins ? best.w : par.w) == 0.0f;
-    if (!off_wins || !p.apply) return;
+    if (!off_wins || !p.apply) return off_wins;
     const int src = code >= p.n ? 1 : 0;
     float4* dst = p.X[POP] + (long long)j * p.rs4;
     if (p.ustamp[POP]) {
@@ -793,6 +798,7 @@ __device__ __forceinline__ void select_slot(const SelParams& p, int j, const flo
     }
     copy_row(dst, p.oX[src] + (long long)bc * p.rs4, p.rs4);  // copy_row, gmpea.cpp:372-377
     p.Fcv[POP][j] = best;
+    return true;
 }
 
 #ifndef GMPEA_SELECT_MINBLOCKS
@@ -802,23 +808,32 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
     if (p.st->stop) return;
     const int j = p.row0 + bx * blockDim.x + threadIdx.x;
     const float3 z = load_z(p.st, p.m);
-    bool feas = false;
+    bool feas = false, off_taken = false;
     if (j < p.row_end) {
         if (by == 0)
-            select_slot<0>(p, j, z, feas);
+            off_taken = select_slot<0>(p, j, z, feas);
         else
-            select_slot<1>(p, j, z, feas);
+            off_taken = select_slot<1>(p, j, z, feas);
     }
-    if (by != 0 || p.rec == nullptr) return;
-    // feasible_ratio of pop1 (gmpea.cpp:411-417): block count, one atomic
-    __shared__ unsigned cnt[8];
-    unsigned b = __popc(__ballot_sync(0xffffffffu, feas && j < p.row_end));
-    if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = b;
+    if (p.rec == nullptr) return;
+    // feasible_ratio of pop1 (gmpea.cpp:411-417) and the replacement count
+    // (diagnostic): block counts, one atomic each
+    __shared__ unsigned cnt[8], rep[8];
+    const unsigned b = __popc(__ballot_sync(0xffffffffu, by == 0 && feas && j < p.row_end));
+    const unsigned r = __popc(__ballot_sync(0xffffffffu, off_taken));
+    if ((threadIdx.x & 31) == 0) {
+        cnt[threadIdx.x >> 5] = b;
+        rep[threadIdx.x >> 5] = r;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned s = 0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += cnt[w];
+        unsigned s = 0, t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            s += cnt[w];
+            t += rep[w];
+        }
         if (s) atomicAdd(&p.rec[p.st->gen].feasible, s);
+        if (t) atomicAdd(&p.rec[p.st->gen].replaced, t);
     }
 }
 

@@ -290,6 +290,11 @@ def test_engine_generation_matches_operator_chain(g, orc):
                 exp[j] = offs[0 if s[j] < n else 1]["X"][s[j] % n]
         close = np.all(np.abs(exp - new.X) <= 1e-5, axis=1)
         assert close.mean() >= 0.99, close.mean()
+    # the replacement diagnostic counts the oracle's offspring winners
+    rr = eng.replacement_rates()
+    assert rr[0] == 0.0 and len(rr) == 2
+    n_rep = int((s1 >= 0).sum() + (s2 >= 0).sum())
+    assert abs(rr[1] * 2 * n - n_rep) <= max(2, 0.01 * n_rep), (rr[1] * 2 * n, n_rep)
 
 
 def test_out_of_bounds_child_raises_with_generation(g):
