@@ -723,15 +723,19 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     int mex = 0;
     bool mex_open = true;
     bool negcv = false;
-    for (int k0 = 0; k0 < deg; k0 += 4) {
-        // batch the index loads and the key gathers of four claimants (ILP)
-        int cc[4];
-        float4 ee[4];
+    // batches of four claimants; the next batch's indices are loaded while
+    // this batch's keys are gathered (one memory round trip per batch)
+    int cc[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cc[u] = k0 + u < deg ? R[(long long)(k0 + u) * p.ldr + j] : -1;
+    for (int u = 0; u < 4; ++u) cc[u] = u < deg ? R[(long long)u * p.ldr + j] : -1;
+    for (int k0 = 0; k0 < deg; k0 += 4) {
+        float4 ee[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (cc[u] >= 0) ee[u] = eff[cc[u]];
+        int cn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cn[u] = k0 + 4 + u < deg ? R[(long long)(k0 + 4 + u) * p.ldr + j] : -1;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = cc[u];
@@ -767,6 +771,8 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
                 bc = c;
             }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cc[u] = cn[u];
     }
     if (negcv) {
         atomicCAS(&p.st->err, 0, ERR_NEG_CV);
