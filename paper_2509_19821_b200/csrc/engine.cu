@@ -198,6 +198,15 @@ struct gmpea_problem {
             dev.wta_strikes = dstrikes.p;
             dev.wta_slot_target = dslot_target.p;
             dev.wta_p = dp.p;
+            if (wta.vehicles > kWtaMaxVehicles) throw std::invalid_argument("wta: too many vehicles");
+            int base = 0;
+            for (int v = 0; v < wta.vehicles; ++v) {
+                dev.wta_capv[v] = wta.cap[v];
+                dev.wta_base[v] = base;
+                base += wta.cap[v];
+            }
+            dev.wta_ncap = base;
+            dev.wta_n8 = base + 2 * wta.vehicles + (d + 63) / 64;  // EvalWta scratch words
         }
     }
 };
@@ -398,14 +407,18 @@ struct RowGeom {
     int rs4;   // row stride, float4
     int srs4;  // shared-memory row stride (odd float4 count)
     int bs;    // vary_eval block size
+    int stream8;
     size_t smem;
 };
 
-RowGeom row_geom(int d, int nc, int scratch_f4 = 0) {
+// stream8 > 0: a streaming evaluator (no staged row) with that many 64-bit
+// shared words per thread
+RowGeom row_geom(int d, int nc, int stream8 = 0) {
     RowGeom g;
     g.rs4 = (d + nc + 3) / 4;
-    g.srs4 = (g.rs4 + scratch_f4) | 1;  // evaluator scratch after the row
-    const int per = g.srs4 * 16;
+    g.srs4 = stream8 > 0 ? 0 : g.rs4 | 1;
+    g.stream8 = stream8;
+    const int per = stream8 > 0 ? stream8 * 8 : g.srs4 * 16;
     g.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
     g.smem = (size_t)g.bs * per;
     if (g.smem > 48 * 1024) throw std::invalid_argument("problem rows too wide for the engine");
@@ -458,7 +471,7 @@ void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStream_t s) 
         RowGeom r;
         r.rs4 = vp.rs4;
         r.srs4 = vp.srs4;
-        const int per = r.srs4 * 16;
+        const int per = vp.scratch8 > 0 ? vp.scratch8 * 8 : r.srs4 * 16;
         r.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
         r.smem = (size_t)r.bs * per;
         return r;
@@ -631,7 +644,7 @@ struct gmpea_engine {
         d = p->d;
         m = p->m;
         nc = p->nin + p->neq;
-        geo = row_geom(d, nc, p->fam == FAM_WTA ? EvalWta::kScratchF4 : 0);
+        geo = row_geom(d, nc, p->fam == FAM_WTA ? p->dev.wta_n8 : 0);
         t1 = (int)std::min<long long>(c.t1, N);
         t2 = (int)std::min<long long>(c.t2, N);
         time_mode = c.time_budget_s > 0.0;
@@ -735,6 +748,7 @@ struct gmpea_engine {
         vp.row_end = n;
         vp.rs4 = geo.rs4;
         vp.srs4 = geo.srs4;
+        vp.scratch8 = geo.stream8;
         vp.slot_base = (int)e0;  // Philox keys use global slots
         vp.pop_id[0] = 1;
         vp.pop_id[1] = 2;
@@ -1229,7 +1243,7 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         } sg{s};
         DevBuf<double> h((size_t)n * d);
         CK(cudaMemcpyAsync(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
-        const RowGeom geo = row_geom(d, nc, p->fam == FAM_WTA ? EvalWta::kScratchF4 : 0);
+        const RowGeom geo = row_geom(d, nc, p->fam == FAM_WTA ? p->dev.wta_n8 : 0);
         PopBuf pb;
         pb.alloc(n, geo.rs4, ld);
         DevBuf<int> rows(n), nbad(1);
@@ -1253,6 +1267,7 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         ep.row_end = (int)n;
         ep.rs4 = geo.rs4;
         ep.srs4 = geo.srs4;
+        ep.scratch8 = geo.stream8;
         ep.pop_id[0] = 1;
         ep.P = p->dev;
         ep.parX[0] = pb.X.p;
@@ -1340,7 +1355,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         if (op != GMPEA_OP_SBX_PM && op != GMPEA_OP_DE) throw std::invalid_argument("reproduce: unknown operator");
         CK(cudaSetDevice(p->device));
         const int d = p->d, nc = p->nin + p->neq;
-        const RowGeom geo = row_geom(d, nc, p->fam == FAM_WTA ? EvalWta::kScratchF4 : 0);
+        const RowGeom geo = row_geom(d, nc, p->fam == FAM_WTA ? p->dev.wta_n8 : 0);
         cudaStream_t s = 0;
         DevBuf<double> h((size_t)n * d);
         CK(cudaMemcpy(h.p, X, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice));
@@ -1364,6 +1379,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.row_end = (int)n;
         vp.rs4 = geo.rs4;
         vp.srs4 = geo.srs4;
+        vp.scratch8 = geo.stream8;
         vp.pop_id[0] = (int)pop;
         vp.P = p->dev;
         vp.parX[0] = Xp.p;

@@ -67,6 +67,7 @@ struct VaryParams {
     long long de_T;          // DE: take iff w <= de_T (>= 2^32 - 1: always)
     UIdx ui[2], uid;         // uniform_index divisors: t per population, d (jrand)
     float de_f;
+    int scratch8;            // streaming evaluators: per-thread shared words (srs4 = 0)
     int eval;                // evaluate the child (0: reproduce only)
     int update_z;
     int fixed_gen;           // >= 0: use this generation number instead of st->gen
@@ -358,13 +359,23 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 #define GMPEA_LO(j) (UB ? ulo : P.lob(j))
 #define GMPEA_HI(j) (UB ? uhi : P.hib(j))
     float4* my4 = sm4 + tid * p.srs4;
-    float* my = reinterpret_cast<float*>(my4);
+    // Ev::kStream: no staged row.  The child's genes go from registers to its
+    // global row and, in the same pass, through the evaluator, which keeps its
+    // per-thread state in shared memory (one column per thread); mutation is
+    // applied inline (PM picks ~1 of d genes and d is large for these).
+    constexpr bool ST = !Ev::kStream;
+    float4* const grow = p.out[pi] + (long long)i * rs4;  // this child's global row
+    float4* const wr4 = ST ? my4 : grow;
+    Ev ev;
+    ev.bind(reinterpret_cast<unsigned long long*>(sm4) + tid, (int)blockDim.x);
+    const bool stream_eval = !ST && MODE == MODE_VARY && p.eval && active;
+    if (stream_eval) ev.begin(p.P);
 
     double f[kMaxM] = {0.0, 0.0, 0.0};
     bool bad = false;
     {
         if (MODE == MODE_EVAL) {
-            if (active) {
+            if (ST && active) {
                 const float4* __restrict__ row = p.parX[pi] + (long long)i * rs4;
                 for (int q = 0; q < rs4; ++q) my4[q] = row[q];
             }
@@ -420,7 +431,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                             const double lo = GMPEA_LO(j), hi = GMPEA_HI(j);
                             v[k] = (float)(lo + (hi - lo) * u);
                         }
-                        my4[jb >> 2] = make_float4(v[0], v[1], v[2], v[3]);
+                        wr4[jb >> 2] = make_float4(v[0], v[1], v[2], v[3]);
                     }
                 } else {
                     // eight genes per group: one XCOIN and one MCOIN counter (16-bit coin
@@ -515,9 +526,32 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         for (int k = 0; k < 8; ++k)
                             if (k < ng && !((mbits >> k) & 1u))
                                 v[k] = fminf(fmaxf(v[k], GMPEA_LO(jb + k)), GMPEA_HI(jb + k));
-                        mmask |= (Mask)mbits << (jb - w0);
-                        my4[q] = make_float4(v[0], v[1], v[2], v[3]);
-                        if (two) my4[q + 1] = make_float4(v[4], v[5], v[6], v[7]);
+                        if (ST) {
+                            mmask |= (Mask)mbits << (jb - w0);
+                        } else {
+                            // inline polynomial mutation + clip, then the evaluator
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                if (k < ng && ((mbits >> k) & 1u)) {
+                                    const int j = jb + k;
+                                    const float lo = GMPEA_LO(j), hi = GMPEA_HI(j);
+                                    const u32x4 mu =
+                                        philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, K);
+                                    v[k] = clamp_ref(pm_apply(v[k], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
+                                }
+                            }
+                            if (stream_eval) {
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    if (k >= ng) continue;
+                                    const int j = jb + k;
+                                    if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
+                                    ev.gene(p.P, j, v[k]);
+                                }
+                            }
+                        }
+                        wr4[q] = make_float4(v[0], v[1], v[2], v[3]);
+                        if (two) wr4[q + 1] = make_float4(v[4], v[5], v[6], v[7]);
                     };
                     if (active) {
                         if (DC > 0 && DC <= 64) {  // one window, full groups then the tail
@@ -533,22 +567,25 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 // phase 2: polynomial mutation then clip (gmpea.cpp:202-203).
                 // The warp's mutation tasks (lane, gene) are dealt round-robin
                 // over its lanes, ~1 task per lane per round.
-                if (MODE == MODE_VARY) pm_tasks(p, (unsigned long long)mmask, w0, sm4, gen, pid, i0);
+                if (ST && MODE == MODE_VARY) pm_tasks(p, (unsigned long long)mmask, w0, sm4, gen, pid, i0);
             }
         }
         if (p.eval && active) {
             // phase 3: bounds check (problems.cpp:554-561) + streamed evaluation
-            Ev ev;
-            ev.begin(p.P);
-            for (int jb = 0; jb < d; jb += 4) {
-                const float4 v4 = my4[jb >> 2];
-                const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+            // (already done in the gene loop for streaming evaluators)
+            if (!stream_eval) {
+                ev.begin(p.P);
+                const float4* rd4 = ST ? my4 : grow;
+                for (int jb = 0; jb < d; jb += 4) {
+                    const float4 v4 = rd4[jb >> 2];
+                    const float v[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int j = jb + k;
-                    if (j >= d) break;
-                    if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
-                    if (!Ev::kWholeRow) ev.gene(p.P, j, v[k]);
+                    for (int k = 0; k < 4; ++k) {
+                        const int j = jb + k;
+                        if (j >= d) break;
+                        if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
+                        ev.gene(p.P, j, v[k]);
+                    }
                 }
             }
             if (bad) {
@@ -556,12 +593,9 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 if (k < p.bad_cap) p.bad_rows[pi][k] = i;
                 if (atomicCAS(&st->err, 0, ERR_EVAL_OOB) == 0) st->err_gen = (int)gen;
             } else {
-                Emitter em{my + d, {}, 0.0, false};
+                Emitter em{reinterpret_cast<float*>(wr4) + d, {}, 0.0, false};
                 em.cv.init(p.P.nin);
-                if (Ev::kWholeRow)
-                    ev.eval_row(p.P, my, my + 4 * rs4, f, em);  // row + scratch staged in shared memory
-                else
-                    ev.finish(p.P, f, em);
+                ev.finish(p.P, f, em);
                 float4 o;
                 o.x = (float)f[0];
                 o.y = (float)f[1];
@@ -572,8 +606,8 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
         }
     }
     // phase 4: rows [i0, i0 + rows) leave as one contiguous, coalesced copy
-    __syncthreads();
-    {
+    if (ST) {
+        __syncthreads();
         const int rows = min((int)blockDim.x, p.row_end - i0);
         const int total = rows * rs4;
         float4* __restrict__ dst = p.out[pi] + (long long)i0 * rs4;

@@ -49,6 +49,11 @@ struct ProbDev {
     const int* wta_strikes;      // per target
     const int* wta_slot_target;  // per strike slot
     const double* wta_p;         // per strike slot
+    // streaming decode state (EvalWta): per-vehicle capacity and the offset
+    // of its candidate list in the per-thread scratch; total scratch words
+    int wta_capv[kWtaMaxVehicles];
+    int wta_base[kWtaMaxVehicles];
+    int wta_ncap, wta_n8;
 };
 
 // ---------------------------------------------------------------- LIRCMOP
@@ -56,10 +61,8 @@ struct ProbDev {
 // 9: 9-12, 13: 13-14) so the per-gene code carries no problem dispatch.
 template <int SUB = 0>
 struct EvalLirT {
-    static constexpr bool kWholeRow = false;
-    static constexpr int kScratchF4 = 0;
-    template <class G>
-    __device__ __forceinline__ void eval_row(const ProbDev&, const float*, float*, double*, G&&) {}
+    static constexpr bool kStream = false;
+    __device__ __forceinline__ void bind(unsigned long long*, int) {}
     double g1, g2, x0, x1, s0, c0;
     float x0f;
     __device__ __forceinline__ void begin(const ProbDev&) { g1 = g2 = 0.0; }
@@ -163,10 +166,8 @@ using EvalLir = EvalLirT<0>;
 
 // ---------------------------------------------------------------- C/DC-DTLZ
 struct EvalDtlz {
-    static constexpr bool kWholeRow = false;
-    static constexpr int kScratchF4 = 0;
-    template <class G>
-    __device__ __forceinline__ void eval_row(const ProbDev&, const float*, float*, double*, G&&) {}
+    static constexpr bool kStream = false;
+    __device__ __forceinline__ void bind(unsigned long long*, int) {}
     double pos[2];
     double rast, sph;
     __device__ __forceinline__ void begin(const ProbDev&) { rast = sph = 0.0; }
@@ -280,10 +281,8 @@ __device__ __forceinline__ double ipow(double x, int e) {
 }
 
 struct EvalMw {
-    static constexpr bool kWholeRow = false;
-    static constexpr int kScratchF4 = 0;
-    template <class G>
-    __device__ __forceinline__ void eval_row(const ProbDev&, const float*, float*, double*, G&&) {}
+    static constexpr bool kStream = false;
+    __device__ __forceinline__ void bind(unsigned long long*, int) {}
     double xs[2];
     double prev;
     double gs;
@@ -515,61 +514,84 @@ struct EvalMw {
 // pass per capacity unit finds each vehicle's threshold, then one pass over
 // the strike slots forms hits, objectives and constraints (wta.cpp:74-110)
 // in the reference's order.  No per-thread arrays (no local memory).
+// WTA (wta.cpp:51-129), streamed gene by gene.  decode_wta keeps, per vehicle
+// v = j mod V, the first cap_v candidates (x_j >= 0.5) in (value desc, index
+// asc) order; only that set matters, so each thread keeps per vehicle the
+// cap_v best keys seen so far (key = value bits << 32 | ~j: larger = earlier
+// in the stable order) and the current minimum, replacing it when a better
+// candidate arrives.  finish() turns the kept sets into a selection bitmask,
+// counts hits per strike slot and forms f and g in the reference's order.
+// The state lives in shared memory as 64-bit words with stride S (one column
+// per thread): [lists | counts (V) | minima (V) | mask (ceil(D / 64))].
 struct EvalWta {
-    static constexpr bool kWholeRow = true;
-    __device__ __forceinline__ void begin(const ProbDev&) {}
-    __device__ __forceinline__ void gene(const ProbDev&, int, float) {}
-    template <class G>
-    __device__ __forceinline__ void finish(const ProbDev&, double*, G&&) {}
-
-    // shared-memory scratch after the row: kWtaMaxVehicles thresholds + indices
-    static constexpr int kScratchF4 = (kWtaMaxVehicles * 2 + 3) / 4;
-    template <class G>
-    __device__ __forceinline__ void eval_row(const ProbDev& P, const float* x, float* scratch, double* f,
-                                             G&& emit) {
-        float* s_tv = scratch;
-        int* s_ti = reinterpret_cast<int*>(scratch + kWtaMaxVehicles);
-        const int V = P.wta_vehicles, T = P.wta_targets;
-        const int D = P.d;
-        for (int v = 0; v < V; ++v) {
-            const int cap = P.wta_cap[v];
-            float pv = 3.0f;  // above every gene in [0, 1]
-            int pi = -1, c = 0;
-            for (int r = 0; r < cap; ++r) {
-                float bv = -1.0f;
-                int bi = -1;
-                for (int j = v; j < D; j += V) {
-                    const float xv = x[j];
-                    // after (pv, pi) in (value desc, index asc) order and better than (bv, bi)
-                    const bool after = xv < pv || (xv == pv && j > pi);
-                    if (xv >= 0.5f && after && xv > bv) {
-                        bv = xv;
-                        bi = j;
-                    }
+    static constexpr bool kStream = true;
+    unsigned long long* L;
+    int S;
+    int v;
+    __device__ __forceinline__ void bind(unsigned long long* base, int stride) {
+        L = base;
+        S = stride;
+    }
+    __device__ __forceinline__ unsigned long long& at(int k) const { return L[(long long)k * S]; }
+    __device__ __forceinline__ void begin(const ProbDev& P) {
+        v = 0;
+        const int V = P.wta_vehicles;
+        for (int k = P.wta_ncap; k < P.wta_n8; ++k) at(k) = 0ull;
+        (void)V;
+    }
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, float x) {
+        const int V = P.wta_vehicles;
+        if (x >= 0.5f) {
+            const unsigned long long key = ((unsigned long long)__float_as_uint(x) << 32) | (0xffffffffu - (unsigned)j);
+            const int cap = P.wta_capv[v], base = P.wta_base[v];
+            const int kc = P.wta_ncap + v, km = P.wta_ncap + V + v;
+            const int c = (int)at(kc);
+            if (c < cap) {
+                at(base + c) = key;
+                at(kc) = (unsigned long long)(c + 1);
+                if (c + 1 == cap) {
+                    unsigned long long mn = key;
+                    for (int e = 0; e < c; ++e) mn = min(mn, at(base + e));
+                    at(km) = mn;
                 }
-                if (bi < 0) break;
-                pv = bv;
-                pi = bi;
-                ++c;
+            } else if (cap > 0 && key > at(km)) {
+                const unsigned long long old = at(km);
+                unsigned long long mn = key;
+                for (int e = 0; e < cap; ++e) {
+                    unsigned long long k2 = at(base + e);
+                    if (k2 == old) {
+                        at(base + e) = key;
+                        k2 = key;
+                    }
+                    mn = min(mn, k2);
+                }
+                at(km) = mn;
             }
-            s_tv[v] = pv;
-            s_ti[v] = c ? pi : -1;
-            emit(v, (double)c - (double)cap);  // per-vehicle capacity (wta.cpp:99-100)
         }
+        v = v + 1 == V ? 0 : v + 1;
+    }
+    template <class G>
+    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
+        const int V = P.wta_vehicles, T = P.wta_targets;
+        const int k0 = P.wta_ncap + 2 * V;  // mask words
+        for (int u = 0; u < V; ++u) {
+            const int c = (int)at(P.wta_ncap + u);
+            for (int e = 0; e < c; ++e) {
+                const unsigned j = 0xffffffffu - (unsigned)(at(P.wta_base[u] + e) & 0xffffffffull);
+                at(k0 + (int)(j >> 6)) |= 1ull << (j & 63);
+            }
+            emit(u, (double)c - (double)P.wta_capv[u]);  // per-vehicle capacity (wta.cpp:99-100)
+        }
+        const unsigned long long vm = V >= 64 ? ~0ull : (1ull << V) - 1ull;
         double f1 = 0.0, f2 = 0.0;
         int s = 0;
         for (int i = 0; i < T; ++i) {
             double surv = 1.0, strikes = 0.0;
             for (int k = 0; k < P.wta_strikes[i]; ++k, ++s) {
-                int h = 0;
-                for (int v = 0; v < V; ++v) {
-                    const int j = s * V + v;
-                    const float xv = x[j];
-                    const float tv = s_tv[v];
-                    const int ti = s_ti[v];
-                    h += (ti >= 0 && xv >= 0.5f && (xv > tv || (xv == tv && j <= ti))) ? 1 : 0;
-                }
-                const double hd = (double)h;
+                const int b = s * V, w = b >> 6, o = b & 63;
+                unsigned long long bits = at(k0 + w) >> o;
+                if (o + V > 64) bits |= at(k0 + w + 1) << (64 - o);
+                const double hd = (double)__popcll(bits & vm);
                 surv *= 1.0 - P.wta_p[s] * hd;
                 f2 += hd;
                 strikes += hd;
