@@ -439,13 +439,13 @@ using VaryKernel = void (*)(VaryParams);
 
 // the dimension-specialised generation kernels also assume uniform bounds
 // (true of every registered suite; checked by the caller)
-template <class Ev, int DC = 0, bool VARY_ONLY = false>
+template <class Ev, int DC = 0, bool VARY_ONLY = false, bool UBF = false>
 VaryKernel pick_vary(int mode, int op) {
     if (!VARY_ONLY) {
         if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
         if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
     }
-    constexpr bool UB = DC > 0;
+    constexpr bool UB = DC > 0 || UBF;  // UBF: uniform bounds at a run-time dimension
     return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC, UB> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UB>;
 }
 
@@ -461,7 +461,9 @@ VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0) {
         case FAM_DTLZ:
             return d == 7 ? pick_vary<EvalDtlz, 7>(mode, op)
                           : (d == 12 ? pick_vary<EvalDtlz, 12>(mode, op) : pick_vary<EvalDtlz>(mode, op));
-        case FAM_WTA: return pick_vary<EvalWta>(mode, op);
+        case FAM_WTA:
+            return d > 0 && mode == MODE_VARY ? pick_vary<EvalWta, 0, true, true>(mode, op)
+                                              : pick_vary<EvalWta>(mode, op);
         default: return d == 15 ? pick_vary<EvalMw, 15>(mode, op) : pick_vary<EvalMw>(mode, op);
     }
 }
