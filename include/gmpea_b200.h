@@ -115,6 +115,13 @@ int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t 
 int gmpea_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx,
                        int64_t* count);
 int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, double* out);
+/* replaces pf_reference (fronts.cpp:54-84, fronts.hpp): the problem's analytic
+ * front candidates built and evaluated in fp64 on the device, feasible rows
+ * only, nondominated-filtered, subsampled to n_points (subsample_front).
+ * Writes *rows (<= n_points unless the front is smaller) rows of m values;
+ * fails (status 2, the reference's runtime_error text) for problems without
+ * an analytic front (MW, WTA).  cap: capacity of out in rows. */
+int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, int64_t cap, int64_t* rows);
 
 /* ---- the run: replaces run_gmpea (gmpea.hpp:113-144, gmpea.cpp:421-493) */
 typedef struct {

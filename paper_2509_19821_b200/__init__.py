@@ -43,6 +43,7 @@ from ._lib import (  # noqa: F401
     make_problem,
     make_wta_problem,
     metric_front,
+    pf_reference,
     problem_names,
     reference_vectors,
     reproduce,

@@ -345,6 +345,24 @@ def hypervolume(points, ref_point) -> float:
     return out.value
 
 
+def pf_reference(problem: "Problem", n_points: int = 1000) -> np.ndarray:
+    """pf_reference (fronts.cpp:54-84): the analytic Pareto front sampled to
+    n_points rows, built and evaluated in fp64 on the device.  RuntimeError
+    for problems without an analytic front (MW, WTA), as the reference."""
+    cap = max(int(n_points), 1)
+    out = np.zeros((cap, problem.m))
+    rows = C.c_int64()
+    rc = _L.gmpea_pf_reference(problem._h, C.c_int64(n_points), _p(out), C.c_int64(cap), C.byref(rows))
+    if rc == GMPEA_EINVAL and "capacity" in _L.gmpea_last_error().decode():
+        # a front smaller than requested never exceeds n_points; only a
+        # retried, unsubsampled front can (fronts.cpp:76)
+        cap = 4 * 50000 + 100000
+        out = np.zeros((cap, problem.m))
+        rc = _L.gmpea_pf_reference(problem._h, C.c_int64(n_points), _p(out), C.c_int64(cap), C.byref(rows))
+    _check(rc)
+    return out[:rows.value].copy()
+
+
 # --------------------------------------------------------------------- the run
 @dataclasses.dataclass
 class RunConfig:

@@ -20,6 +20,7 @@
 
 #include "../../include/gmpea_b200.h"
 #include "common.cuh"
+#include "fronts.cuh"
 #include "kernels.cuh"
 #include "metrics.cuh"
 #include "problems.cuh"
@@ -1517,9 +1518,17 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
 // ---- metrics (metrics.hpp:15-29)
 namespace {
 
+__global__ void gather_rows_kernel(const double* F, const long long* idx, long long k, int m, double* out) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= k) return;
+    for (int c = 0; c < m; ++c) out[r * m + c] = F[idx[r] * m + c];
+}
+
 // nondominated + deduplicated subset of the candidate rows `cand` of F (n x m,
 // device, row-major); returns the kept row ids sorted lexicographically by F
-thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::device_vector<long long>& cand) {
+// dedup = 0 (m = 3 only): equal rows are all kept, as fronts.cpp:34-41 does
+thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::device_vector<long long>& cand,
+                                              int dedup = 1) {
     const long long k = (long long)cand.size();
     thrust::device_vector<long long> kept;
     if (k == 0) return kept;
@@ -1537,7 +1546,7 @@ thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::d
                                                 thrust::raw_pointer_cast(keep.data()));
     } else {
         nd3_kernel<<<blocks_for(k, 256), 256>>>(dF, order, thrust::raw_pointer_cast(gs.data()), k,
-                                                thrust::raw_pointer_cast(keep.data()));
+                                                thrust::raw_pointer_cast(keep.data()), dedup);
     }
     CK(cudaGetLastError());
     kept.resize(k);
@@ -1548,6 +1557,104 @@ thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::d
 }
 
 }  // namespace
+
+int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, int64_t cap, int64_t* rows) {
+    return guarded([&] {
+        if (n_points < 0) throw std::invalid_argument("pf_reference: negative point count");
+        PfParams pp{};
+        if (p->fam == FAM_LIR) {
+            pp.kind = PF_LIR;
+        } else if (p->fam == FAM_DTLZ) {
+            const int id = p->id;
+            if (id == C1_DTLZ1 || id == DC1_DTLZ1 || id == DC2_DTLZ1 || id == DC3_DTLZ1) {
+                pp.kind = PF_DTLZ1;  // problems.cpp:436, 520
+            } else if (id == C3_DTLZ4) {
+                pp.kind = PF_SPHERE;  // problems.cpp:484-486
+                pp.alpha = 100.0;
+                pp.rnum = 0.0;
+                pp.rden = 1.0;
+            } else {
+                pp.kind = PF_SPHERE;  // problems.cpp:447-449, 469-471, 522-524
+                pp.alpha = 1.0;
+                pp.rnum = 1.0;
+                pp.rden = 0.0;
+            }
+        } else {
+            throw std::runtime_error("pf_reference: no analytic front for " + p->name +
+                                     "; use the hypervolume metric instead");
+        }
+        if (p->d > kPfMaxD) throw std::invalid_argument("pf_reference: dimension too large");
+        require_device();
+        const int m = p->m;
+        pp.P = p->dev;
+        // fronts.cpp:60-84
+        long long over = std::max<long long>(8 * n_points, 2000);
+        if (m >= 3) over = std::min<long long>(over, 12000);
+        auto emit = [&](const std::vector<double>& h, long long nrows) {
+            if (nrows > cap) throw std::invalid_argument("pf_reference: output capacity too small");
+            if (out && nrows) std::copy(h.begin(), h.begin() + nrows * m, out);
+            *rows = nrows;
+        };
+        for (int attempt = 0; attempt < 4; ++attempt) {
+            pp.n_samples = over;
+            if (pp.kind == PF_LIR && p->id <= 12) {
+                pp.rows = over;
+            } else {
+                long long h = 1;
+                while ((h + 1) * (h + 2) / 2 < over) ++h;  // simplex_weights (problems.cpp:205-218)
+                pp.h = h;
+                pp.rows = (h + 1) * (h + 2) / 2;
+            }
+            thrust::device_vector<double> dF(pp.rows * m);
+            thrust::device_vector<unsigned char> feas(pp.rows);
+            thrust::device_vector<int> noob(1, 0);
+            pp.F = thrust::raw_pointer_cast(dF.data());
+            pp.feas = thrust::raw_pointer_cast(feas.data());
+            pp.n_oob = thrust::raw_pointer_cast(noob.data());
+            pf_candidates_kernel<<<blocks_for(pp.rows, 128), 128>>>(pp);
+            CK(cudaGetLastError());
+            if ((int)noob[0]) throw std::invalid_argument("evaluate: front candidate rows out of bounds");
+            thrust::device_vector<long long> cand(pp.rows);
+            auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                       thrust::counting_iterator<long long>(pp.rows), feas.begin(), cand.begin(),
+                                       NonZero{});
+            cand.resize(end - cand.begin());
+            if ((long long)cand.size() >= std::max<long long>(n_points, 1)) {
+                // nondominated_rows (fronts.cpp:15-42): m = 2 drops duplicates, m = 3 keeps them
+                auto kept = front_filter(pp.F, m, cand, m == 2 ? 1 : 0);  // lexicographic order
+                const long long nk = (long long)kept.size();
+                const bool enough = nk >= n_points;
+                if (enough || attempt == 3) {
+                    std::vector<double> h;
+                    if (!enough || nk <= n_points || n_points == 0) {
+                        // the filtered rows in their original order (subsample_front returns F)
+                        thrust::sort(thrust::device, kept.begin(), kept.end());
+                        thrust::device_vector<double> o(nk * m);
+                        gather_rows_kernel<<<blocks_for(nk, 256), 256>>>(pp.F, thrust::raw_pointer_cast(kept.data()),
+                                                                        nk, m, thrust::raw_pointer_cast(o.data()));
+                        h.resize(nk * m);
+                        thrust::copy(o.begin(), o.end(), h.begin());
+                        emit(h, nk);
+                    } else {
+                        // subsample_front (fronts.cpp:86-103): stable lexicographic order, even picks
+                        thrust::device_vector<double> o(n_points * m);
+                        pf_pick_kernel<<<blocks_for(n_points, 256), 256>>>(
+                            pp.F, thrust::raw_pointer_cast(kept.data()), nk, n_points, m,
+                            thrust::raw_pointer_cast(o.data()));
+                        h.resize(n_points * m);
+                        thrust::copy(o.begin(), o.end(), h.begin());
+                        emit(h, n_points);
+                    }
+                    CK(cudaGetLastError());
+                    return;
+                }
+            }
+            over *= 4;
+            if (m >= 3) over = std::min<long long>(over, 50000);
+        }
+        throw std::runtime_error("pf_reference: could not build a feasible front for " + p->name);
+    });
+}
 
 int gmpea_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx, int64_t* count) {
     return guarded([&] {

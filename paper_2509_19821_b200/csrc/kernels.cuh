@@ -111,7 +111,7 @@ struct Emitter {
     double s;
     bool s_ready;
     __device__ __forceinline__ void operator()(int k, double g) {
-        G[k] = (float)g;
+        if (G) G[k] = (float)g;
         if (k < cv.blocked) {
             cv.add(k, g);
         } else {

@@ -103,7 +103,7 @@ __global__ void gather_col_kernel(const double* F, const long long* order, long 
 
 // m = 3: does any row before the group weakly dominate in (f2, f3)?
 __global__ void nd3_kernel(const double* F, const long long* order, const long long* gs, long long k,
-                           unsigned char* keep) {
+                           unsigned char* keep, int dedup = 1) {
     __shared__ double s2[256], s3[256];
     const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const bool act = p < k;
@@ -115,7 +115,7 @@ __global__ void nd3_kernel(const double* F, const long long* order, const long l
         a2 = F[a * 3 + 1];
         a3 = F[a * 3 + 2];
         lim = gs[p];
-        alive = lim == p;  // duplicates of an earlier row are dropped
+        alive = !dedup || lim == p;  // dedup: duplicates of an earlier row are dropped
     }
     // block-wide prefix length: the largest group start in the block
     __shared__ long long blim;

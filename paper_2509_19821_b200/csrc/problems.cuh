@@ -17,6 +17,8 @@
 // at half the fp32 rate), the per-gene trigonometric terms of LIRCMOP5-12 in
 // fp32 (argument < pi/2, error < 2e-7).  Outputs are rounded to fp32.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace gmpea_b200 {
@@ -56,6 +58,14 @@ struct ProbDev {
     int wta_ncap, wta_n8;
 };
 
+// c·pi·x trigonometry.  The generation path uses the exact-pi forms
+// (sinpi/cospi).  fp64 front candidates (pf_reference) round c·pi·x first, as
+// problems.cpp does, so that e.g. cos(pi/2) is 6.1e-17 as with glibc:
+// subsample_front orders the front lexicographically by those values.
+constexpr double kPiD = 3.141592653589793;
+__device__ __forceinline__ double trig_sin(bool ref, double c, double x) { return ref ? sin(c * kPiD * x) : sinpi(c * x); }
+__device__ __forceinline__ double trig_cos(bool ref, double c, double x) { return ref ? cos(c * kPiD * x) : cospi(c * x); }
+
 // ---------------------------------------------------------------- LIRCMOP
 // SUB > 0 fixes the sub-family at compile time (1: LIRCMOP1-4, 5: 5-8,
 // 9: 9-12, 13: 13-14) so the per-gene code carries no problem dispatch.
@@ -65,17 +75,32 @@ struct EvalLirT {
     __device__ __forceinline__ void bind(unsigned long long*, int) {}
     double g1, g2, x0, x1, s0, c0;
     float x0f;
-    __device__ __forceinline__ void begin(const ProbDev&) { g1 = g2 = 0.0; }
+    bool ref;  // fp64 candidate rows: reference-rounded trigonometry
+    __device__ __forceinline__ void begin(const ProbDev&) {
+        g1 = g2 = 0.0;
+        ref = false;
+    }
     __device__ __forceinline__ static int sub_of(int id) {
         return SUB ? SUB : (id <= 4 ? 1 : (id <= 8 ? 5 : (id <= 12 ? 9 : 13)));
     }
-    __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
+    // T = float: generation rows (fp32); T = double: reference-front
+    // candidates (pf_reference), evaluated fully in fp64
+    template <class T>
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, T xf) {
         const double x = xf;
         const int sub = sub_of(P.id);
+        ref = std::is_same<T, double>::value;
         if (j == 0) {
             x0 = x;
-            x0f = xf;
-            if (sub == 1) sincospi(0.5 * x, &s0, &c0);  // problems.cpp:23-24
+            x0f = (float)xf;
+            if (sub == 1) {  // problems.cpp:23-24
+                if (ref) {
+                    s0 = trig_sin(true, 0.5, x);
+                    c0 = trig_cos(true, 0.5, x);
+                } else {
+                    sincospi(0.5 * x, &s0, &c0);
+                }
+            }
             return;
         }
         if (sub == 13) {  // problems.cpp:124-128
@@ -90,6 +115,9 @@ struct EvalLirT {
         double track;
         if (sub == 1) {
             track = (j & 1) ? c0 : s0;
+        } else if (std::is_same<T, double>::value) {  // problems.cpp:43-50 in fp64
+            const double a = 0.5 * (double)(j + 1) * kPiD * x0 / (double)P.d;
+            track = (j & 1) ? cos(a) : sin(a);
         } else {  // problems.cpp:43-50: sin/cos(0.5 (j+1) pi x1 / n)
             float a = __fdiv_rn(0.5f * (float)(j + 1) * x0f, (float)P.d);
             track = (j & 1) ? (double)cospif(a) : (double)sinpif(a);
@@ -115,7 +143,7 @@ struct EvalLirT {
             f[1] = (id == 1 || id == 3) ? 1.0 - x0 * x0 + g2 : 1.0 - sqrt(x0) + g2;
             emit(0, -((0.51 - g1) * (g1 - 0.5)));
             emit(1, -((0.51 - g2) * (g2 - 0.5)));
-            if (id >= 3) emit(2, 0.5 - sinpi(20.0 * x0));
+            if (id >= 3) emit(2, 0.5 - trig_sin(ref, 20.0, x0));
             return;
         }
         if (sub == 5) {
@@ -146,13 +174,20 @@ struct EvalLirT {
                 default: p = 1.6; q = 1.6; a = 1.5; b = 6.0; lv = 2.5; break;
             }
             emit(0, ellipse(P, f[0], f[1], p, q, a, b));
-            emit(1, lv - (f[0] * P.sal + f[1] * P.cal - sinpi(4.0 * (f[0] * P.cal - f[1] * P.sal))));
+            emit(1, lv - (f[0] * P.sal + f[1] * P.cal - trig_sin(ref, 4.0, f[0] * P.cal - f[1] * P.sal)));
             return;
         }
         double rad = 1.7057 + g1;
         double s1, c1;
-        sincospi(0.5 * x0, &s0, &c0);
-        sincospi(0.5 * x1, &s1, &c1);
+        if (ref) {
+            s0 = trig_sin(true, 0.5, x0);
+            c0 = trig_cos(true, 0.5, x0);
+            s1 = trig_sin(true, 0.5, x1);
+            c1 = trig_cos(true, 0.5, x1);
+        } else {
+            sincospi(0.5 * x0, &s0, &c0);
+            sincospi(0.5 * x1, &s1, &c1);
+        }
         f[0] = rad * c0 * c1;
         f[1] = rad * c0 * s1;
         f[2] = rad * s0;
@@ -170,9 +205,15 @@ struct EvalDtlz {
     __device__ __forceinline__ void bind(unsigned long long*, int) {}
     double pos[2];
     double rast, sph;
-    __device__ __forceinline__ void begin(const ProbDev&) { rast = sph = 0.0; }
-    __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
+    bool ref;  // fp64 candidate rows: reference-rounded trigonometry
+    __device__ __forceinline__ void begin(const ProbDev&) {
+        rast = sph = 0.0;
+        ref = false;
+    }
+    template <class T>
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, T xf) {
         const double x = xf;
+        ref = std::is_same<T, double>::value;
         if (j < P.m - 1) {  // static indices keep pos[] in registers
             if (j == 0)
                 pos[0] = x;
@@ -181,10 +222,10 @@ struct EvalDtlz {
             return;
         }
         double t = x - 0.5;  // problems.cpp:144-147, 153-155
-        rast += t * t - cospi(20.0 * t);
+        rast += t * t - trig_cos(ref, 20.0, t);
         sph += t * t;
     }
-    __device__ static void shape(int base, const double* pos, double g, double* f) {
+    __device__ static void shape(int base, const double* pos, double g, double* f, bool ref) {
         // m = 3 (problems.cpp:160-178)
         if (base == 1) {
             f[0] = 0.5 * pos[0] * pos[1] * (1.0 + g);
@@ -192,8 +233,15 @@ struct EvalDtlz {
             f[2] = 0.5 * (1.0 - pos[0]) * (1.0 + g);
         } else {
             double s0, c0, s1, c1;
-            sincospi(0.5 * pos[0], &s0, &c0);
-            sincospi(0.5 * pos[1], &s1, &c1);
+            if (ref) {
+                s0 = trig_sin(true, 0.5, pos[0]);
+                c0 = trig_cos(true, 0.5, pos[0]);
+                s1 = trig_sin(true, 0.5, pos[1]);
+                c1 = trig_cos(true, 0.5, pos[1]);
+            } else {
+                sincospi(0.5 * pos[0], &s0, &c0);
+                sincospi(0.5 * pos[1], &s1, &c1);
+            }
             f[0] = (1.0 + g) * c0 * c1;
             f[1] = (1.0 + g) * c0 * s1;
             f[2] = (1.0 + g) * s0;
@@ -206,18 +254,18 @@ struct EvalDtlz {
         const double gr = 100.0 * ((double)(P.d - m + 1) + rast);
         switch (k) {
             case C1_DTLZ1: {
-                shape(1, pos, gr, f);
+                shape(1, pos, gr, f, ref);
                 emit(0, f[0] / 0.5 + f[1] / 0.5 + f[2] / 0.6 - 1.0);
                 return;
             }
             case C1_DTLZ3: {
-                shape(2, pos, gr, f);
+                shape(2, pos, gr, f, ref);
                 double r2 = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
                 emit(0, -((r2 - 16.0) * (r2 - 81.0)));
                 return;
             }
             case C2_DTLZ2: {
-                shape(2, pos, sph, f);
+                shape(2, pos, sph, f, ref);
                 const double r = 0.4;
                 double v1 = 1.0 / 0.0;
                 for (int i = 0; i < 3; ++i) {
@@ -235,7 +283,7 @@ struct EvalDtlz {
             }
             case C3_DTLZ4: {
                 double pp[2] = {pow(pos[0], 100.0), pow(pos[1], 100.0)};
-                shape(2, pp, sph, f);
+                shape(2, pp, sph, f, ref);
                 for (int j = 0; j < 3; ++j) {
                     double s = f[j] * f[j] / 4.0;
                     for (int i = 0; i < 3; ++i)
@@ -247,16 +295,16 @@ struct EvalDtlz {
             default: break;
         }
         bool linear = (k == DC1_DTLZ1 || k == DC2_DTLZ1 || k == DC3_DTLZ1);
-        shape(linear ? 1 : 2, pos, gr, f);
+        shape(linear ? 1 : 2, pos, gr, f, ref);
         if (k == DC1_DTLZ1 || k == DC1_DTLZ3) {
-            emit(0, -(cospi(3.0 * pos[0]) + 0.5));
+            emit(0, -(trig_cos(ref, 3.0, pos[0]) + 0.5));
         } else if (k == DC2_DTLZ1 || k == DC2_DTLZ3) {
-            emit(0, 0.9 - cospi(3.0 * gr));
+            emit(0, 0.9 - trig_cos(ref, 3.0, gr));
             emit(1, 0.9 - exp(-gr));
         } else {
-            emit(0, -(cospi(3.0 * pos[0]) + 0.5));
-            emit(1, -(cospi(3.0 * pos[1]) + 0.5));
-            emit(2, -(cospi(3.0 * gr) + 0.5));
+            emit(0, -(trig_cos(ref, 3.0, pos[0]) + 0.5));
+            emit(1, -(trig_cos(ref, 3.0, pos[1]) + 0.5));
+            emit(2, -(trig_cos(ref, 3.0, gr) + 0.5));
         }
     }
 };

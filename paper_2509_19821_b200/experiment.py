@@ -99,8 +99,8 @@ def validate_config(cfg: ExperimentConfig) -> None:
     for suite, op in cfg.operators.items():
         if op not in ("sbx", "de"):
             errors.append(f"unknown operator '{op}' for suite {suite}")
-    if cfg.igd_reference_points != 1000:
-        errors.append("igd_reference_points: only the committed 1000-point reference fronts are available")
+    if cfg.igd_reference_points < 1:
+        errors.append("igd_reference_points must be positive")
     if errors:
         raise ValueError("invalid experiment config:" + "".join("\n  - " + e for e in errors))
 
@@ -126,12 +126,20 @@ def operator_for(cfg: ExperimentConfig, problem: str) -> g.VariationOp:
 _FRONTS = None
 
 
-def reference_front(problem: str) -> Optional[np.ndarray]:
-    """pf_reference(p, 1000) of the unmodified reference, or None (HV problems)."""
+def reference_front(problem: str, n_points: int = 1000) -> Optional[np.ndarray]:
+    """pf_reference(p, n_points) (experiment.cpp:170-172), or None for the
+    problems without an analytic front (HV problems).  1000 points: the
+    unmodified reference's own front (data/fronts_1000.npz); other sizes are
+    built on the device (gmpea_pf_reference, tests/test_gpu_parity.py)."""
     global _FRONTS
     if _FRONTS is None:
         _FRONTS = dict(np.load(os.path.join(HERE, "data", "fronts_1000.npz")))
-    return _FRONTS.get(problem)
+    if n_points == 1000 or problem not in _FRONTS:
+        return _FRONTS.get(problem)
+    key = f"{problem}/{n_points}"
+    if key not in _FRONTS:
+        _FRONTS[key] = g.pf_reference(g.make_problem(problem), n_points)
+    return _FRONTS[key]
 
 
 def run_algorithm(algorithm: str, problem: g.Problem, cfg: g.RunConfig,
@@ -320,7 +328,7 @@ def run_experiment(cfg: ExperimentConfig) -> ExperimentResult:
     for alg, prob, seed in cells:
         rc = g.RunConfig(n=cfg.n, k_max=cfg.k_max, eval_budget=cfg.eval_budget, time_budget_s=cfg.time_budget_s,
                          seed=seed, op=operator_for(cfg, prob), record_walltime=cfg.record_walltime)
-        res = run_algorithm(alg, problems[prob], rc, reference_front(prob))
+        res = run_algorithm(alg, problems[prob], rc, reference_front(prob, cfg.igd_reference_points))
         outcomes[(alg, prob, seed)] = (res.history, g.metric_front(res.pop1))
     paths = []
     for alg, prob, seed in cells:
@@ -330,7 +338,7 @@ def run_experiment(cfg: ExperimentConfig) -> ExperimentResult:
         paths.append(path)
     summaries = []
     for prob in cfg.problems:
-        front = reference_front(prob)
+        front = reference_front(prob, cfg.igd_reference_points)
         ideal = nadir = None
         if front is None:  # normalised HV over all runs' fronts (experiment.cpp:245-265)
             m = problems[prob].m

@@ -142,6 +142,18 @@ def fronts_fixture(ref):
     np.savez_compressed(os.path.join(HERE, "fronts.npz"), **out)
 
 
+def pf_fixture(ref):
+    """pf_reference at sizes other than 1000 (small, and large enough to need
+    the oversampling retries for some problems)."""
+    out = {}
+    for name in REF_PROBLEMS:
+        if name.startswith("WTA"):
+            continue
+        for npts in (64, 2500):
+            out[f"{name}/{npts}"] = ref.pf_reference(name, npts)
+    np.savez_compressed(os.path.join(HERE, "pf_ref.npz"), **out)
+
+
 def runs_fixture(ref):
     """Final IGD of the reference's own run_gmpea over 30 seeds (statistical parity)."""
     fronts = np.load(os.path.join(HERE, "fronts.npz"))
@@ -168,6 +180,7 @@ def main():
     knn_fixture(ref, rng)
     metrics_fixture(ref, rng)
     fronts_fixture(ref)
+    pf_fixture(ref)
     runs_fixture(ref)
     print("golden fixtures written to", HERE)
 

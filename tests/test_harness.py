@@ -129,3 +129,18 @@ def test_run_experiment_end_to_end(tmp_path, g):
     # byte-identical reruns (record_walltime false)
     again = run_experiment(cfg)
     assert again.csv_text == res.csv_text
+
+
+@pytest.mark.gpu
+def test_run_experiment_custom_reference_points(tmp_path, g):
+    """igd_reference_points != 1000: the IGD front comes from the device
+    pf_reference (experiment.cpp:170-172 semantics)."""
+    from paper_2509_19821_b200.experiment import ExperimentConfig, load_summaries, reference_front, run_experiment
+
+    front = reference_front("LIRCMOP13", 200)
+    assert front.shape == (200, 3)
+    cfg = ExperimentConfig(algorithms=["gmpea"], problems=["LIRCMOP13"], seeds=[1], k_max=5, n=105,
+                           output_dir=str(tmp_path / "exp"), record_walltime=False, igd_reference_points=200)
+    res = run_experiment(cfg)
+    s = load_summaries(res.summary_path)
+    assert len(s) == 1 and s[0]["metric"] == "igd" and s[0]["value"] > 0
