@@ -278,10 +278,15 @@ def main():
     eng2.set_population(2, X2)
     if world > 1:
         sh2._z_allreduce()
-    for _ in range(args.steps):
+    # each step's result (the generation record: pop1 feasible count) is
+    # copied D2H into pinned memory in stream order, without a host stall
+    # between steps; the host reads them after the final population copy
+    recs = torch.zeros((args.steps, 16), dtype=torch.uint8, pin_memory=True).numpy()
+    for k in range(args.steps):
         step1()
-        eng2.last_record()  # D2H of the generation's record (feasible ratio), host-synchronous
-    pop = eng2.population(1, out=out)
+        eng2.record_async(recs[k])
+    pop = eng2.population(1, out=out)  # synchronises the stream
+    feas = recs.view(np.uint32)[:, 0].astype(np.float64) / rows
     t1 = time.perf_counter()
     e2e_s = t1 - t0
     if world > 1:
@@ -289,11 +294,13 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = X1.nbytes + X2.nbytes
-    d2h = 48 * args.steps + pop.X.nbytes + pop.F.nbytes + pop.C.nbytes + pop.cv.nbytes
+    d2h = recs.nbytes + pop.X.nbytes + pop.F.nbytes + pop.C.nbytes + pop.cv.nbytes
     e2e = {"value": 2 * n * args.steps / e2e_s, "unit": "ind-gen/s",
            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
-           "note": "pinned host buffers: set_population x2 (H2D + evaluation) + K x (step + GenRecord "
-                   "read) + final pop1 (X, F, C, cv) D2H, host wall clock, max over ranks"}
+           "note": "pinned host buffers: set_population x2 (H2D + evaluation) + K x (step + async D2H "
+                   "of the step's generation record) + final pop1 (X, F, C, cv) D2H, host wall clock, "
+                   "max over ranks",
+           "feasible_ratio_last": float(feas[-1])}
     eng2.close()
 
     if rank != 0:

@@ -172,6 +172,16 @@ int gmpea_engine_last_record(gmpea_engine* e, gmpea_gen_record* out);
  * took an offspring in OP3; out[0] (initialisation) is 0.  Same indexing and
  * count semantics as gmpea_engine_history. */
 int gmpea_engine_replacements(gmpea_engine* e, int64_t* out, int64_t cap, int64_t* n);
+/* the newest enqueued generation's raw record, copied to host memory dst
+ * (pinned for a true async copy) in stream order WITHOUT waiting: the
+ * per-step result of a pipelined loop, read by the caller after its next
+ * gmpea_engine_sync.  Layout of the 16 bytes: */
+typedef struct {
+    uint32_t feasible; /* rows of pop1 (owned slots) with cv == 0 */
+    uint32_t replaced; /* owned slots of both populations that took an offspring */
+    uint64_t loop_ns;  /* accumulated loop time (device clock) */
+} gmpea_raw_record;
+int gmpea_engine_record_async(gmpea_engine* e, gmpea_raw_record* dst);
 int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C,
                                 double* cv);
 int gmpea_engine_ideal(gmpea_engine* e, double* z);

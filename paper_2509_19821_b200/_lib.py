@@ -476,6 +476,15 @@ class Engine:
                                             C.byref(cnt)))
         return buf / (2.0 * self.rows_owned)
 
+    def record_async(self, dst: np.ndarray) -> None:
+        """Enqueue a copy of the newest generation's raw record (16 bytes:
+        feasible u32, replaced u32, loop_ns u64) into dst without waiting;
+        dst should be pinned (e.g. torch pinned memory viewed as numpy) and
+        is valid after the next sync()."""
+        if dst.nbytes < 16 or not dst.flags["C_CONTIGUOUS"]:
+            raise ValueError("record_async: need 16 contiguous bytes")
+        _check(_L.gmpea_engine_record_async(self._h, C.c_void_p(dst.ctypes.data)))
+
     def last_record(self) -> GenRecord:
         r = _GenRecord()
         _check(_L.gmpea_engine_last_record(self._h, C.byref(r)))

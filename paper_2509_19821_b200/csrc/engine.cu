@@ -1058,6 +1058,12 @@ struct gmpea_engine {
         return out;
     }
 
+    void record_async(void* dst) {
+        static_assert(sizeof(DevRecord) == sizeof(gmpea_raw_record), "raw record layout");
+        const long long k = std::min<long long>(gens_enqueued, rec_cap - 1);
+        CK(cudaMemcpyAsync(dst, rec.p + k, sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+    }
+
     // the newest generation record only (one small D2H; the per-step result)
     gmpea_gen_record last_record() {
         struct {
@@ -1796,6 +1802,10 @@ int gmpea_engine_history(gmpea_engine* e, gmpea_gen_record* out, int64_t cap, in
         if (out) std::copy(h.begin(), h.begin() + k, out);
         *nrec = (int64_t)h.size();
     });
+}
+
+int gmpea_engine_record_async(gmpea_engine* e, gmpea_raw_record* dst) {
+    return guarded([&] { e->record_async(dst); });
 }
 
 int gmpea_engine_replacements(gmpea_engine* e, int64_t* out, int64_t cap, int64_t* nrec) {
