@@ -123,6 +123,19 @@ int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, 
  * an analytic front (MW, WTA).  cap: capacity of out in rows. */
 int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, int64_t cap, int64_t* rows);
 
+/* ---- comparison-algorithm operators: replace baselines.hpp (baselines.cpp:22-190).
+ * fp64 inputs, row-major F (n x m); results equal the reference's exactly.
+ * use_cdp: constrained domination (cdp_better) instead of pareto_dominates;
+ * a negative cv is rejected as cdp_better does. */
+int gmpea_nondominated_sort(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp,
+                            int64_t* rank);
+int gmpea_crowding_distance(const double* F, int64_t n, int32_t m, const int64_t* front, int64_t k,
+                            double* dist);
+int gmpea_spea2_fitness(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, double* fit);
+/* keep: capacity >= min(n, capacity) entries; *count rows kept, ascending */
+int gmpea_spea2_select(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp,
+                       int64_t capacity, int64_t* keep, int64_t* count);
+
 /* ---- the run: replaces run_gmpea (gmpea.hpp:113-144, gmpea.cpp:421-493) */
 typedef struct {
     int64_t n;             /* requested population size */

@@ -381,6 +381,56 @@ class Reference(_Lib):
             _ptr(hist, _dp), C.c_int64(cap), C.byref(rows)))
         return dict(X=X, F=F, C=Cm, cv=cv), hist[:rows.value].copy()
 
+    # -- comparison algorithms (baselines.hpp) --------------------------------
+    def nondominated_sort(self, F, cv, use_cdp):
+        F, cv = _f64(F), _f64(cv)
+        n, m = F.shape
+        rank = np.zeros(n, np.int64)
+        self._check(self.lib.ref_nondominated_sort(_ptr(F, _dp), _ptr(cv, _dp), C.c_int64(n), m,
+                                                   1 if use_cdp else 0, _ptr(rank, _i64p)))
+        return rank
+
+    def crowding_distance(self, F, front):
+        F = _f64(F)
+        n, m = F.shape
+        fr = np.ascontiguousarray(front, np.int64)
+        d = np.zeros(len(fr))
+        self._check(self.lib.ref_crowding_distance(_ptr(F, _dp), C.c_int64(n), m, _ptr(fr, _i64p),
+                                                   C.c_int64(len(fr)), _ptr(d, _dp)))
+        return d
+
+    def spea2_fitness(self, F, cv, use_cdp):
+        F, cv = _f64(F), _f64(cv)
+        n, m = F.shape
+        fit = np.zeros(n)
+        self._check(self.lib.ref_spea2_fitness(_ptr(F, _dp), _ptr(cv, _dp), C.c_int64(n), m,
+                                               1 if use_cdp else 0, _ptr(fit, _dp)))
+        return fit
+
+    def spea2_select(self, F, cv, use_cdp, capacity):
+        F, cv = _f64(F), _f64(cv)
+        n, m = F.shape
+        keep = np.zeros(max(n, 1), np.int64)
+        cnt = C.c_int64()
+        self._check(self.lib.ref_spea2_select(_ptr(F, _dp), _ptr(cv, _dp), C.c_int64(n), m, 1 if use_cdp else 0,
+                                              C.c_int64(capacity), _ptr(keep, _i64p), C.byref(cnt)))
+        return keep[:cnt.value].copy()
+
+    def run_baseline(self, algo, name, n, k_max, seed=1):
+        info = self._info_any(name)
+        X = np.zeros((n, info["d"]))
+        F = np.zeros((n, info["m"]))
+        Cm = np.zeros((n, info["n_ineq"] + info["n_eq"]))
+        cv = np.zeros(n)
+        cap = 100_000
+        hist = np.zeros((cap, 4))
+        rows = C.c_int64()
+        self._check(self.lib.ref_run_baseline({"cnsga2": 0, "ccmo": 1}[algo], name.encode(), C.c_int64(n),
+                                              C.c_int64(k_max), C.c_uint64(seed), _ptr(X, _dp), _ptr(F, _dp),
+                                              _ptr(Cm, _dp), _ptr(cv, _dp), _ptr(hist, _dp), C.c_int64(cap),
+                                              C.byref(rows)))
+        return dict(X=X, F=F, C=Cm, cv=cv), hist[:rows.value].copy()
+
     def _info_any(self, name):
         if name.startswith("MW"):
             return Oracle().problem_info(name)

@@ -24,6 +24,7 @@
 #include <thread>
 #include <vector>
 
+#include "gmpea/baselines.hpp"
 #include "gmpea/gmpea.hpp"
 #include "gmpea/metrics.hpp"
 #include "gmpea/problems.hpp"
@@ -293,6 +294,72 @@ int ref_run_gmpea(const char* name, int64_t n, int64_t k_max, uint64_t seed, int
         cfg.t2 = t2;
         cfg.record_walltime = record_walltime != 0;
         RunResult r = run_gmpea(p, cfg);
+        unpop(r.pop1, X, F, C, cv);
+        int64_t k = 0;
+        for (const GenRecord& g : r.history) {
+            if (k >= hist_cap) break;
+            hist[k * 4 + 0] = static_cast<double>(g.gen);
+            hist[k * 4 + 1] = static_cast<double>(g.evals);
+            hist[k * 4 + 2] = g.wall_ms;
+            hist[k * 4 + 3] = g.feasible_ratio;
+            ++k;
+        }
+        *hist_rows = k;
+    });
+}
+
+// ---- comparison algorithms (baselines.hpp): operators and runs
+int ref_nondominated_sort(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp,
+                          int64_t* rank) {
+    return guarded([&] {
+        Matrix M = mat(F, n, m);
+        std::vector<double> c(cv, cv + n);
+        auto r = nondominated_sort(M, c, use_cdp != 0);
+        for (int64_t i = 0; i < n; ++i) rank[i] = static_cast<int64_t>(r[i]);
+    });
+}
+
+int ref_crowding_distance(const double* F, int64_t n, int32_t m, const int64_t* front, int64_t k,
+                          double* dist) {
+    return guarded([&] {
+        Matrix M = mat(F, n, m);
+        std::vector<std::size_t> fr(front, front + k);
+        auto d = crowding_distance(M, fr);
+        std::copy(d.begin(), d.end(), dist);
+    });
+}
+
+int ref_spea2_fitness(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, double* fit) {
+    return guarded([&] {
+        Matrix M = mat(F, n, m);
+        std::vector<double> c(cv, cv + n);
+        auto f = spea2_fitness(M, c, use_cdp != 0);
+        std::copy(f.begin(), f.end(), fit);
+    });
+}
+
+int ref_spea2_select(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, int64_t capacity,
+                     int64_t* keep, int64_t* count) {
+    return guarded([&] {
+        Matrix M = mat(F, n, m);
+        std::vector<double> c(cv, cv + n);
+        auto k = spea2_select(M, c, use_cdp != 0, capacity);
+        for (size_t i = 0; i < k.size(); ++i) keep[i] = static_cast<int64_t>(k[i]);
+        *count = static_cast<int64_t>(k.size());
+    });
+}
+
+// run_cnsga2 / run_ccmo (baselines.cpp:320-459); algo 0 = cnsga2, 1 = ccmo
+int ref_run_baseline(int32_t algo, const char* name, int64_t n, int64_t k_max, uint64_t seed, double* X, double* F,
+                     double* C, double* cv, double* hist, int64_t hist_cap, int64_t* hist_rows) {
+    return guarded([&] {
+        ProblemDef p = problem_for(name);
+        RunConfig cfg;
+        cfg.n = n;
+        cfg.k_max = k_max;
+        cfg.seed = seed;
+        cfg.record_walltime = false;
+        RunResult r = algo == 0 ? run_cnsga2(p, cfg) : run_ccmo(p, cfg);
         unpop(r.pop1, X, F, C, cv);
         int64_t k = 0;
         for (const GenRecord& g : r.history) {

@@ -33,6 +33,7 @@ from ._lib import (  # noqa: F401
     SelectionContext,
     VariationOp,
     build_neighborhoods,
+    crowding_distance,
     environmental_selection,
     evaluate,
     evaluate_population,
@@ -43,11 +44,14 @@ from ._lib import (  # noqa: F401
     make_problem,
     make_wta_problem,
     metric_front,
+    nondominated_sort,
     pf_reference,
     problem_names,
     reference_vectors,
     reproduce,
     run_gmpea,
+    spea2_fitness,
+    spea2_select,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

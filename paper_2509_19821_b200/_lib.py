@@ -363,6 +363,46 @@ def pf_reference(problem: "Problem", n_points: int = 1000) -> np.ndarray:
     return out[:rows.value].copy()
 
 
+# ------------------------------------------------ comparison-algorithm operators
+def nondominated_sort(F, cv, use_cdp: bool = True) -> np.ndarray:
+    """nondominated_sort (baselines.cpp:22-55): 0-based front rank per row."""
+    F, cv = _f64(F), _f64(cv)
+    n, m = F.shape
+    rank = np.zeros(n, np.int64)
+    _check(_L.gmpea_nondominated_sort(_p(F), _p(cv), C.c_int64(n), m, int(bool(use_cdp)), _p(rank, _i64p)))
+    return rank
+
+
+def crowding_distance(F, front) -> np.ndarray:
+    """crowding_distance (baselines.cpp:56-91) of the rows `front` of F."""
+    F = _f64(F)
+    n, m = F.shape
+    fr = np.ascontiguousarray(front, np.int64)
+    d = np.zeros(len(fr))
+    _check(_L.gmpea_crowding_distance(_p(F), C.c_int64(n), m, _p(fr, _i64p), C.c_int64(len(fr)), _p(d)))
+    return d
+
+
+def spea2_fitness(F, cv, use_cdp: bool = True) -> np.ndarray:
+    """spea2_fitness (baselines.cpp:93-127)."""
+    F, cv = _f64(F), _f64(cv)
+    n, m = F.shape
+    fit = np.zeros(n)
+    _check(_L.gmpea_spea2_fitness(_p(F), _p(cv), C.c_int64(n), m, int(bool(use_cdp)), _p(fit)))
+    return fit
+
+
+def spea2_select(F, cv, use_cdp: bool, capacity: int) -> np.ndarray:
+    """spea2_select (baselines.cpp:129-189): kept row indices, ascending."""
+    F, cv = _f64(F), _f64(cv)
+    n, m = F.shape
+    keep = np.zeros(max(n, 1), np.int64)
+    cnt = C.c_int64()
+    _check(_L.gmpea_spea2_select(_p(F), _p(cv), C.c_int64(n), m, int(bool(use_cdp)), C.c_int64(capacity),
+                                 _p(keep, _i64p), C.byref(cnt)))
+    return keep[:cnt.value].copy()
+
+
 # --------------------------------------------------------------------- the run
 @dataclasses.dataclass
 class RunConfig:

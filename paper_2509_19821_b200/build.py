@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libgmpea_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", "engine.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in
-                  ("common.cuh", "kernels.cuh", "problems.cuh", "topology.cuh", "metrics.cuh", "fronts.cuh")] + [
+                  ("common.cuh", "kernels.cuh", "problems.cuh", "topology.cuh", "metrics.cuh", "fronts.cuh", "baselines.cuh")] + [
     os.path.join(ROOT, "include", "gmpea_b200.h")]
 
 NVCC_FLAGS = [

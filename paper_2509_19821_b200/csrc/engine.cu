@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/gmpea_b200.h"
+#include "baselines.cuh"
 #include "common.cuh"
 #include "fronts.cuh"
 #include "kernels.cuh"
@@ -1876,3 +1877,248 @@ int gmpea_engine_device_buffers(gmpea_engine* e, gmpea_device_buffers* o) {
 }
 
 }  // extern "C"
+
+// ---- comparison-algorithm operators (baselines.hpp; baselines.cu kernels in baselines.cuh)
+namespace {
+
+struct PosLess {  // rows of F at front positions, lexicographic, then position
+    const double* F;
+    const long long* front;
+    int m;
+    __host__ __device__ bool operator()(long long a, long long b) const {
+        for (int c = 0; c < m; ++c) {
+            const double x = F[front[a] * m + c], y = F[front[b] * m + c];
+            if (x < y) return true;
+            if (x > y) return false;
+        }
+        return a < b;
+    }
+};
+
+__global__ void dup_zero_kernel(const double* F, const long long* front, const long long* order, long long k, int m,
+                                double* dist) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q == 0 || q >= k) return;
+    const long long a = front[order[q]], b = front[order[q - 1]];
+    for (int c = 0; c < m; ++c)
+        if (!(F[a * m + c] == F[b * m + c])) return;
+    dist[order[q]] = 0.0;  // an earlier position holds the same row (baselines.cpp:84-90)
+}
+
+__global__ void gather_col_pos_kernel(const double* F, const long long* front, long long k, int m, int c,
+                                      double* out) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < k) out[q] = F[front[q] * m + c];
+}
+
+struct FitBelowOne {
+    const double* fit;
+    __host__ __device__ bool operator()(long long i) const { return fit[i] < 1.0; }
+};
+struct FitAtLeastOne {
+    const double* fit;
+    __host__ __device__ bool operator()(long long i) const { return fit[i] >= 1.0; }
+};
+struct IsInfeasible {
+    const double* cv;
+    __host__ __device__ bool operator()(long long i) const { return cv[i] > 0.0; }
+};
+
+void check_cdp_cv(const double* cv, int64_t n, int32_t use_cdp) {
+    if (!use_cdp || n < 2) return;
+    for (int64_t i = 0; i < n; ++i)
+        if (cv[i] < 0.0) throw std::invalid_argument("cdp_better: negative constraint violation");
+}
+
+// Pareto ranks of the rows `sub` by front peeling; returns the front count
+long long peel_ranks(const DomRel& R, thrust::device_vector<long long>& sub, thrust::device_vector<long long>& rank) {
+    const long long ns = (long long)sub.size();
+    if (ns == 0) return 0;
+    thrust::device_vector<int> cnt(ns), fsz(1, 0), nsz(1, 0);
+    thrust::device_vector<long long> front(ns), next(ns);
+    const long long* ps = thrust::raw_pointer_cast(sub.data());
+    nds_count_kernel<<<blocks_for(ns, 128), 128>>>(R, ps, ns, thrust::raw_pointer_cast(cnt.data()));
+    nds_front0_kernel<<<blocks_for(ns, 256), 256>>>(thrust::raw_pointer_cast(cnt.data()), ns,
+                                                    thrust::raw_pointer_cast(front.data()),
+                                                    thrust::raw_pointer_cast(fsz.data()));
+    CK(cudaGetLastError());
+    long long fsize = (int)fsz[0], r = 0;
+    while (fsize > 0) {
+        // fronts are sets: the order of `next` (atomic) does not affect ranks
+        nds_set_rank_kernel<<<blocks_for(fsize, 256), 256>>>(ps, thrust::raw_pointer_cast(front.data()), fsize, r,
+                                                             thrust::raw_pointer_cast(rank.data()));
+        nsz[0] = 0;
+        nds_peel_kernel<<<blocks_for(fsize * ns, 256), 256>>>(R, ps, ns, thrust::raw_pointer_cast(front.data()), fsize,
+                                                              thrust::raw_pointer_cast(cnt.data()),
+                                                              thrust::raw_pointer_cast(next.data()),
+                                                              thrust::raw_pointer_cast(nsz.data()));
+        CK(cudaGetLastError());
+        fsize = (int)nsz[0];
+        front.swap(next);
+        ++r;
+    }
+    return r;
+}
+
+// spea2_fitness on device arrays (baselines.cpp:93-127)
+void spea2_fitness_dev(const double* dF, const double* dcv, int64_t n, int32_t m, int32_t use_cdp, double* dfit) {
+    if (n == 0) return;
+    DomRel R{dF, dcv, m, use_cdp};
+    thrust::device_vector<double> strength(n), raw(n);
+    spea2_strength_kernel<<<blocks_for(n, 128), 128>>>(R, n, thrust::raw_pointer_cast(strength.data()));
+    spea2_raw_kernel<<<blocks_for(n, 128), 128>>>(R, n, thrust::raw_pointer_cast(strength.data()),
+                                                  thrust::raw_pointer_cast(raw.data()));
+    size_t k = (size_t)std::sqrt((double)n);
+    if (k >= (size_t)n) k = n > 1 ? n - 1 : 0;
+    const long long nd = n - 1;  // distances per row
+    const long long kk = nd > 0 ? (long long)(k < (size_t)nd ? k : nd - 1) : 0;
+    spea2_sigma_kernel<<<(unsigned)n, 256>>>(dF, m, n, kk, thrust::raw_pointer_cast(raw.data()), dfit);
+    CK(cudaGetLastError());
+}
+
+}  // namespace
+
+int gmpea_nondominated_sort(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp,
+                            int64_t* rank) {
+    return guarded([&] {
+        if (m < 1) throw std::invalid_argument("nondominated_sort: no objectives");
+        check_cdp_cv(cv, n, use_cdp);
+        if (n <= 0) return;
+        require_device();
+        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n);
+        thrust::device_vector<long long> drank(n, 0), sub(n);
+        const double* pcv = thrust::raw_pointer_cast(dcv.data());
+        DomRel R{thrust::raw_pointer_cast(dF.data()), pcv, m, 0};
+        if (use_cdp) {
+            auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                       thrust::counting_iterator<long long>(n), sub.begin(), IsFeasible{pcv});
+            sub.resize(end - sub.begin());
+        } else {
+            thrust::sequence(thrust::device, sub.begin(), sub.end());
+        }
+        const long long rf = peel_ranks(R, sub, drank);
+        if (use_cdp) {
+            thrust::device_vector<long long> inf(n);
+            auto e = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                     thrust::counting_iterator<long long>(n), inf.begin(), IsInfeasible{pcv});
+            const long long ni = e - inf.begin();
+            if (ni) {
+                thrust::device_vector<double> u(ni);
+                thrust::gather(thrust::device, inf.begin(), inf.begin() + ni, dcv.begin(), u.begin());
+                thrust::sort(thrust::device, u.begin(), u.end());
+                const long long nu = thrust::unique(thrust::device, u.begin(), u.end()) - u.begin();
+                nds_infeasible_rank_kernel<<<blocks_for(n, 256), 256>>>(pcv, n, thrust::raw_pointer_cast(u.data()), nu,
+                                                                        rf, thrust::raw_pointer_cast(drank.data()));
+                CK(cudaGetLastError());
+            }
+        }
+        std::vector<long long> h(n);
+        thrust::copy(drank.begin(), drank.end(), h.begin());
+        for (int64_t i = 0; i < n; ++i) rank[i] = h[i];
+    });
+}
+
+int gmpea_crowding_distance(const double* F, int64_t n, int32_t m, const int64_t* front, int64_t k, double* dist) {
+    return guarded([&] {
+        if (k <= 0) return;
+        if (k <= 2) {
+            for (int64_t q = 0; q < k; ++q) dist[q] = std::numeric_limits<double>::infinity();
+            return;
+        }
+        for (int64_t q = 0; q < k; ++q)
+            if (front[q] < 0 || front[q] >= n) throw std::invalid_argument("crowding_distance: front index out of range");
+        require_device();
+        thrust::device_vector<double> dF(F, F + n * m), dd(k, 0.0), key(k);
+        thrust::device_vector<long long> fr(front, front + k), order(k);
+        const double* pF = thrust::raw_pointer_cast(dF.data());
+        const long long* pf = thrust::raw_pointer_cast(fr.data());
+        for (int c = 0; c < m; ++c) {
+            thrust::sequence(thrust::device, order.begin(), order.end());
+            gather_col_pos_kernel<<<blocks_for(k, 256), 256>>>(pF, pf, k, m, c, thrust::raw_pointer_cast(key.data()));
+            thrust::stable_sort_by_key(thrust::device, key.begin(), key.end(), order.begin());
+            crowd_axis_kernel<<<blocks_for(k, 256), 256>>>(pF, m, c, pf, thrust::raw_pointer_cast(order.data()), k,
+                                                           thrust::raw_pointer_cast(dd.data()));
+        }
+        thrust::sequence(thrust::device, order.begin(), order.end());
+        thrust::sort(thrust::device, order.begin(), order.end(), PosLess{pF, pf, m});
+        dup_zero_kernel<<<blocks_for(k, 256), 256>>>(pF, pf, thrust::raw_pointer_cast(order.data()), k, m,
+                                                     thrust::raw_pointer_cast(dd.data()));
+        CK(cudaGetLastError());
+        thrust::copy(dd.begin(), dd.end(), dist);
+    });
+}
+
+int gmpea_spea2_fitness(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, double* fit) {
+    return guarded([&] {
+        check_cdp_cv(cv, n, use_cdp);
+        if (n <= 0) return;
+        require_device();
+        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n), dfit(n);
+        spea2_fitness_dev(thrust::raw_pointer_cast(dF.data()), thrust::raw_pointer_cast(dcv.data()), n, m, use_cdp,
+                          thrust::raw_pointer_cast(dfit.data()));
+        thrust::copy(dfit.begin(), dfit.end(), fit);
+    });
+}
+
+int gmpea_spea2_select(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, int64_t capacity,
+                       int64_t* keep, int64_t* count) {
+    return guarded([&] {
+        check_cdp_cv(cv, n, use_cdp);
+        *count = 0;
+        if (n <= 0) return;
+        if (capacity < 0) throw std::invalid_argument("spea2_select: negative capacity");
+        require_device();
+        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n), dfit(n);
+        const double* pF = thrust::raw_pointer_cast(dF.data());
+        double* pfit = thrust::raw_pointer_cast(dfit.data());
+        spea2_fitness_dev(pF, thrust::raw_pointer_cast(dcv.data()), n, m, use_cdp, pfit);
+        thrust::device_vector<long long> kp(n);
+        auto e = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                 thrust::counting_iterator<long long>(n), kp.begin(), FitBelowOne{pfit});
+        long long nk = e - kp.begin();
+        std::vector<long long> out;
+        if (nk < capacity) {
+            // fill with the dominated rows, lowest fitness first (stable)
+            thrust::device_vector<long long> rest(n);
+            auto e2 = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
+                                      thrust::counting_iterator<long long>(n), rest.begin(), FitAtLeastOne{pfit});
+            const long long nr = e2 - rest.begin();
+            thrust::device_vector<double> rf(nr);
+            thrust::gather(thrust::device, rest.begin(), rest.begin() + nr, dfit.begin(), rf.begin());
+            thrust::stable_sort_by_key(thrust::device, rf.begin(), rf.end(), rest.begin());
+            const long long take = std::min<long long>(nr, capacity - nk);
+            std::vector<long long> a(nk), b(take);
+            thrust::copy(kp.begin(), kp.begin() + nk, a.begin());
+            thrust::copy(rest.begin(), rest.begin() + take, b.begin());
+            out = a;
+            out.insert(out.end(), b.begin(), b.end());
+            std::sort(out.begin(), out.end());
+        } else {
+            // serial truncation (baselines.cpp:149-184) in one persistent block
+            thrust::device_vector<unsigned char> alive(n, 0);
+            thrust::device_vector<double> n1(nk), n2(nk), lv(nk);
+            thrust::device_vector<long long> i1(nk), i2(nk), cand(nk);
+            thrust::fill(thrust::device, thrust::make_permutation_iterator(alive.begin(), kp.begin()),
+                         thrust::make_permutation_iterator(alive.begin(), kp.begin() + nk), (unsigned char)1);
+            const long long* pk = thrust::raw_pointer_cast(kp.data());
+            unsigned char* pa = thrust::raw_pointer_cast(alive.data());
+            if (nk > capacity) {
+                trunc_init_kernel<<<blocks_for(nk, 128), 128>>>(pF, m, pk, nk, pa, thrust::raw_pointer_cast(n1.data()),
+                                                                thrust::raw_pointer_cast(i1.data()),
+                                                                thrust::raw_pointer_cast(n2.data()),
+                                                                thrust::raw_pointer_cast(i2.data()));
+                trunc_loop_kernel<<<1, 1024>>>(pF, m, pk, nk, capacity, pa, thrust::raw_pointer_cast(n1.data()),
+                                               thrust::raw_pointer_cast(i1.data()), thrust::raw_pointer_cast(n2.data()),
+                                               thrust::raw_pointer_cast(i2.data()), thrust::raw_pointer_cast(lv.data()),
+                                               thrust::raw_pointer_cast(cand.data()));
+                CK(cudaGetLastError());
+            }
+            std::vector<unsigned char> h(n);
+            thrust::copy(alive.begin(), alive.end(), h.begin());
+            for (int64_t i = 0; i < n; ++i)
+                if (h[i]) out.push_back(i);
+        }
+        for (size_t i = 0; i < out.size(); ++i) keep[i] = out[i];
+        *count = (int64_t)out.size();
+    });
+}
