@@ -168,6 +168,20 @@ typedef struct {
 int gmpea_run_config_default(gmpea_run_config* out);
 /* setup: reference vectors, neighbourhoods, initial populations (Philox INIT
  * stream), their evaluation, the ideal point and record 0 */
+/* comparison algorithms as whole runs: replace run_cnsga2 / run_ccmo
+ * (baselines.cpp:320-459, baselines.hpp:33-34) on the device.  cfg: n, k_max,
+ * time_budget_s, eval_budget, seed, params (SBX + PM, the operator field is
+ * ignored as in the reference), record_walltime, device.  igd_ref (n_ref x m,
+ * optional): the IGD metric hook of experiment.cpp:200-205, evaluated on the
+ * device after every generation outside the loop clock.  Writes the history
+ * (up to hist_cap rows; *n_hist = all) and pop1 (n x d, n x m,
+ * n x (n_ineq + n_eq), n). */
+#define GMPEA_ALGO_CNSGA2 0
+#define GMPEA_ALGO_CCMO 1
+int gmpea_run_baseline(const gmpea_problem* p, int32_t algo, const gmpea_run_config* cfg,
+                       const double* igd_ref, int64_t n_ref, gmpea_gen_record* hist, int64_t hist_cap,
+                       int64_t* n_hist, double* X, double* F, double* C, double* cv);
+
 int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmpea_engine** out);
 /* replace population `which` (1 or 2) by host rows X (n x d) and re-evaluate */
 int gmpea_engine_set_population(gmpea_engine* e, int32_t which, const double* X);

@@ -49,6 +49,7 @@ from ._lib import (  # noqa: F401
     problem_names,
     reference_vectors,
     reproduce,
+    run_baseline,
     run_gmpea,
     spea2_fitness,
     spea2_select,

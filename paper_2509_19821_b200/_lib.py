@@ -572,6 +572,34 @@ class Engine:
         return ms
 
 
+BASELINE_ALGORITHMS = {"cnsga2": 0, "ccmo": 1}
+
+
+def run_baseline(problem: Problem, algorithm: str, cfg: RunConfig,
+                 igd_front: Optional[np.ndarray] = None) -> RunResult:
+    """run_cnsga2 / run_ccmo (baselines.cpp:320-459) on the device; with
+    igd_front the per-generation IGD hook runs on the device too."""
+    if algorithm not in BASELINE_ALGORITHMS:
+        raise ValueError("unknown algorithm: " + algorithm)
+    c = cfg._c()
+    n, p = cfg.n, problem
+    X, F = np.zeros((n, p.d)), np.zeros((n, p.m))
+    Cm, cv = np.zeros((n, p.n_constraints)), np.zeros(n)
+    ref = None if igd_front is None else _f64(igd_front)
+    nref = 0 if ref is None else ref.shape[0]
+    nh = C.c_int64()
+    bounded = not cfg.eval_budget and not cfg.time_budget_s
+    cap = max(cfg.k_max, 0) + 2 if bounded else (cfg.eval_budget // n + 2 if cfg.eval_budget and not cfg.time_budget_s
+                                                 else 1 << 20)
+    buf = (_GenRecord * cap)()
+    _check(_L.gmpea_run_baseline(problem._h, BASELINE_ALGORITHMS[algorithm], C.byref(c),
+                                 _p(ref) if ref is not None else None, C.c_int64(nref), buf, C.c_int64(cap),
+                                 C.byref(nh), _p(X), _p(F), _p(Cm), _p(cv)))
+    hist = [GenRecord(r.gen, r.evals, r.wall_ms, r.feasible_ratio,
+                      r.igd if r.has_igd else None, r.hv if r.has_hv else None) for r in buf[:min(nh.value, cap)]]
+    return RunResult(Population(X, F, Cm, cv), hist, n)
+
+
 def run_gmpea(problem: Problem, cfg: RunConfig) -> RunResult:
     """run_gmpea (gmpea.cpp:421-493) on the device."""
     eng = Engine(problem, cfg)

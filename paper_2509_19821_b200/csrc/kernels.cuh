@@ -66,6 +66,13 @@ struct VaryParams {
     long long pm_T;          // PM: mutate iff w <= pm_T (w: 32-bit coin; -1 never)
     long long de_T;          // DE: take iff w <= de_T (>= 2^32 - 1: always)
     UIdx ui[2], uid;         // uniform_index divisors: t per population, d (jrand)
+    // tournament parents (comparison algorithms, baselines.cpp:347-352, 416-420):
+    // tour 1: binary tournament on (rank asc, crowding desc, else the first);
+    // tour 2: on fitness (fit[a] <= fit[b] ? a : b); 0: neighbourhood picks
+    int tour;
+    UIdx un;                 // uniform_index(n) over the population
+    const long long* trank[2];
+    const double* tkey[2];
     float de_f;
     int scratch8;            // streaming evaluators: per-thread shared words (srs4 = 0)
     int eval;                // evaluate the child (0: reproduce only)
@@ -390,14 +397,32 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             int jrand = -1;
             bool cross = true;
             if (MODE == MODE_VARY && active) {
-                const int t = p.t[pi];
                 PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key, 0u, {}};
-                unsigned a = ps.index(p.ui[pi]);
-                unsigned b = ps.index(p.ui[pi]);
-                while (t > 1 && b == a) b = ps.index(p.ui[pi]);
-                const int* Brow = p.B[pi] + (long long)i * t;
-                oa = (unsigned)Brow[a] * (unsigned)rs4;
-                ob = (unsigned)Brow[b] * (unsigned)rs4;
+                if (p.tour) {
+                    auto tournament = [&]() {
+                        const unsigned a = ps.index(p.un), b = ps.index(p.un);
+                        if (p.tour == 1) {
+                            const long long ra = p.trank[pi][a], rb = p.trank[pi][b];
+                            if (ra != rb) return ra < rb ? a : b;
+                            const double ca = p.tkey[pi][a], cb = p.tkey[pi][b];
+                            if (ca != cb) return ca > cb ? a : b;
+                            return a;
+                        }
+                        return p.tkey[pi][a] <= p.tkey[pi][b] ? a : b;
+                    };
+                    const unsigned a = tournament();
+                    const unsigned b = tournament();
+                    oa = a * (unsigned)rs4;
+                    ob = b * (unsigned)rs4;
+                } else {
+                    const int t = p.t[pi];
+                    unsigned a = ps.index(p.ui[pi]);
+                    unsigned b = ps.index(p.ui[pi]);
+                    while (t > 1 && b == a) b = ps.index(p.ui[pi]);
+                    const int* Brow = p.B[pi] + (long long)i * t;
+                    oa = (unsigned)Brow[a] * (unsigned)rs4;
+                    ob = (unsigned)Brow[b] * (unsigned)rs4;
+                }
                 if (OP == OP_SBX) {
                     u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key);
                     cross = u53(c.x, c.y) <= p.sbx_prob;

@@ -4,9 +4,9 @@ records, summary.jsonl and results.csv (Wilcoxon marks), and scaling_study —
 so an existing experiment matrix switches to the engine by pointing at this
 module.
 
-Algorithms: "gmpea", "gmpea-s" (t1 = t2 = 5), "gmpea-l" (t1 = t2 = 20)
-(experiment.cpp:125-138), all on the engine; the reference's comparison
-baselines (cnsga2, ccmo) are outside this repo's scope and rejected.
+Algorithms: "gmpea", "gmpea-s" (t1 = t2 = 5), "gmpea-l" (t1 = t2 = 20) on the
+engine, and the reference's comparison baselines "cnsga2" and "ccmo"
+(experiment.cpp:125-138) on the device operators of baselines.cuh.
 
 IGD problems use the reference's own 1000-point pf_reference fronts
 (data/fronts_1000.npz, generated from the unmodified reference); per-generation
@@ -26,7 +26,7 @@ import numpy as np
 from . import _lib as g
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-ALGORITHMS = ("gmpea", "gmpea-s", "gmpea-l")
+ALGORITHMS = ("gmpea", "gmpea-s", "gmpea-l", "cnsga2", "ccmo")
 
 
 @dataclasses.dataclass
@@ -148,6 +148,8 @@ def run_algorithm(algorithm: str, problem: g.Problem, cfg: g.RunConfig,
     on pop1 after every generation, outside the loop clock."""
     if algorithm not in ALGORITHMS:
         raise ValueError("unknown algorithm: " + algorithm)
+    if algorithm in g.BASELINE_ALGORITHMS:
+        return g.run_baseline(problem, algorithm, cfg, igd_front)
     c = dataclasses.replace(cfg)
     if algorithm == "gmpea-s":
         c.t1 = c.t2 = 5

@@ -170,6 +170,22 @@ def runs_fixture(ref):
     np.savez_compressed(os.path.join(HERE, "runs.npz"), **out)
 
 
+def baseline_runs_fixture(ref):
+    """Final IGD of the reference's own run_cnsga2 / run_ccmo (statistical parity)."""
+    fronts = np.load(os.path.join(HERE, "fronts.npz"))
+    out = {}
+    for algo, name, n, gens, seeds in (("cnsga2", "LIRCMOP1", 100, 100, 30), ("cnsga2", "C1-DTLZ1", 91, 100, 30),
+                                       ("ccmo", "LIRCMOP1", 60, 40, 30)):
+        vals = []
+        for seed in range(1, seeds + 1):
+            pop, hist = ref.run_baseline(algo, name, n, gens, seed)
+            front = ref.metric_front(pop["F"], pop["cv"])
+            vals.append(ref.igd(front, fronts[name]) if len(front) else np.inf)
+        out[f"{algo}/{name}/igd"] = np.array(vals)
+        out[f"{algo}/{name}/cfg"] = np.array([n, gens])
+    np.savez_compressed(os.path.join(HERE, "baseline_runs.npz"), **out)
+
+
 def main():
     if not build_ref():
         raise SystemExit("reference sources not available")
@@ -182,6 +198,7 @@ def main():
     fronts_fixture(ref)
     pf_fixture(ref)
     runs_fixture(ref)
+    baseline_runs_fixture(ref)
     print("golden fixtures written to", HERE)
 
 

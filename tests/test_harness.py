@@ -12,14 +12,14 @@ import pytest
 def test_validate_config_lists_every_error(g):
     from paper_2509_19821_b200.experiment import ExperimentConfig, validate_config
 
-    cfg = ExperimentConfig(algorithms=["gmpea", "ccmo"], problems=["LIRCMOP1", "NOPE"], seeds=[1],
+    cfg = ExperimentConfig(algorithms=["gmpea", "moead"], problems=["LIRCMOP1", "NOPE"], seeds=[1],
                            eval_budget=100, time_budget_s=1.0, n=0, operators={"lircmop": "ga"})
     with pytest.raises(ValueError) as e:
         validate_config(cfg)
     msg = str(e.value)
     assert msg.startswith("invalid experiment config:")
     for part in ("both evals and seconds budgets set", "population size must be positive",
-                 "unknown algorithm: ccmo", "unknown problem: NOPE", "unknown operator 'ga' for suite lircmop"):
+                 "unknown algorithm: moead", "unknown problem: NOPE", "unknown operator 'ga' for suite lircmop"):
         assert part in msg
 
 
@@ -144,3 +144,20 @@ def test_run_experiment_custom_reference_points(tmp_path, g):
     res = run_experiment(cfg)
     s = load_summaries(res.summary_path)
     assert len(s) == 1 and s[0]["metric"] == "igd" and s[0]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_run_experiment_with_baselines(tmp_path, g):
+    """cnsga2 / ccmo run through the same harness (experiment.cpp:125-128):
+    JSONL records with the IGD hook, Wilcoxon marks against gmpea."""
+    from paper_2509_19821_b200.experiment import ExperimentConfig, load_summaries, run_experiment
+
+    cfg = ExperimentConfig(algorithms=["gmpea", "cnsga2", "ccmo"], problems=["LIRCMOP1"], seeds=[1, 2, 3], k_max=6,
+                           n=30, output_dir=str(tmp_path / "exp"), record_walltime=False)
+    res = run_experiment(cfg)
+    lines = open(os.path.join(cfg.output_dir, "ccmo_LIRCMOP1_s1.jsonl")).read().splitlines()
+    assert len(lines) == 7 and json.loads(lines[-1])["evals"] == 2 * 30 * 7 and "igd" in json.loads(lines[-1])
+    lines = open(os.path.join(cfg.output_dir, "cnsga2_LIRCMOP1_s1.jsonl")).read().splitlines()
+    assert json.loads(lines[-1])["evals"] == 30 * 7
+    assert {x["algorithm"] for x in load_summaries(res.summary_path)} == {"gmpea", "cnsga2", "ccmo"}
+    assert len(res.csv_text.splitlines()) == 4
