@@ -2,9 +2,12 @@
 // as INTEGRATION.md describes, and runs both on one reference ProblemDef.
 // Built by tests/test_integration.py against the UNMODIFIED reference library
 // (oracle/_ref/libgmpea_ref.so) and libgmpea_b200.so.
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <string>
 
+#include "gmpea/baselines.hpp"
 #include "gmpea/gmpea.hpp"
 #include "gmpea/metrics.hpp"
 #include "gmpea/problems.hpp"
@@ -16,6 +19,10 @@ using namespace gmpea;
 static RunResult run_algorithm_with_b200(const std::string& algorithm, const ProblemDef& problem,
                                          const RunConfig& cfg) {
     if (algorithm == "gmpea-b200") return gmpea_b200::run_gmpea(problem, cfg);
+    if (algorithm == "cnsga2-b200") return gmpea_b200::run_cnsga2(problem, cfg);
+    if (algorithm == "ccmo-b200") return gmpea_b200::run_ccmo(problem, cfg);
+    if (algorithm == "cnsga2") return run_cnsga2(problem, cfg);
+    if (algorithm == "ccmo") return run_ccmo(problem, cfg);
     return run_gmpea(problem, cfg);
 }
 
@@ -48,5 +55,26 @@ int main(int argc, char** argv) {
     h.igd_metric = [&](const Population& pop) { return igd(metric_front(pop), ref); };
     RunResult c = run_algorithm_with_b200("gmpea-b200", p, h);
     std::printf("hook records %zu last igd %.6g\n", c.history.size(), *c.history.back().igd);
+    // comparison algorithms through the same registration, with the IGD hook
+    RunConfig bc = cfg;
+    bc.n = 60;
+    bc.k_max = 10;
+    bc.igd_metric = h.igd_metric;
+    RunResult n1 = run_algorithm_with_b200("cnsga2", p, bc), n2 = run_algorithm_with_b200("cnsga2-b200", p, bc);
+    RunResult c1 = run_algorithm_with_b200("ccmo", p, bc), c2 = run_algorithm_with_b200("ccmo-b200", p, bc);
+    std::printf("baselines records cnsga2 %zu/%zu ccmo %zu/%zu evals %zu/%zu %zu/%zu\n", n1.history.size(),
+                n2.history.size(), c1.history.size(), c2.history.size(), n1.history.back().evals,
+                n2.history.back().evals, c1.history.back().evals, c2.history.back().evals);
+    // operator level: the reference's and the engine's operators on the same rows
+    std::vector<std::size_t> r1 = nondominated_sort(c1.pop1.F, c1.pop1.cv, true);
+    std::vector<std::size_t> r2 = gmpea_b200::nondominated_sort(c1.pop1.F, c1.pop1.cv, true);
+    std::vector<double> f1 = spea2_fitness(c1.pop1.F, c1.pop1.cv, false);
+    std::vector<double> f2 = gmpea_b200::spea2_fitness(c1.pop1.F, c1.pop1.cv, false);
+    Matrix fr2 = gmpea_b200::pf_reference(p, 1000);
+    double fd = 0.0;
+    for (std::size_t i = 0; i < fr2.data.size() && fr2.data.size() == ref.data.size(); ++i)
+        fd = std::max(fd, std::abs(fr2.data[i] - ref.data[i]));
+    std::printf("operators ranks_equal %d fitness_equal %d front_rows %zu/%zu\n", (int)(r1 == r2), (int)(f1 == f2),
+                fr2.rows, ref.rows);
     return 0;
 }

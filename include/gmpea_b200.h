@@ -178,9 +178,15 @@ int gmpea_run_config_default(gmpea_run_config* out);
  * n x (n_ineq + n_eq), n). */
 #define GMPEA_ALGO_CNSGA2 0
 #define GMPEA_ALGO_CCMO 1
+/* host metric hook (RunConfig::igd_metric / hv_metric, gmpea.hpp:123-124):
+ * called with pop1 (n rows, host memory) after every generation, outside the
+ * loop clock; sets *igd / *hv and the has_ flags for the values it computed */
+typedef void (*gmpea_pop_hook)(void* user, int64_t n, const double* X, const double* F, const double* C,
+                               const double* cv, double* igd, double* hv, int32_t* has_igd, int32_t* has_hv);
 int gmpea_run_baseline(const gmpea_problem* p, int32_t algo, const gmpea_run_config* cfg,
-                       const double* igd_ref, int64_t n_ref, gmpea_gen_record* hist, int64_t hist_cap,
-                       int64_t* n_hist, double* X, double* F, double* C, double* cv);
+                       const double* igd_ref, int64_t n_ref, gmpea_pop_hook hook, void* hook_user,
+                       gmpea_gen_record* hist, int64_t hist_cap, int64_t* n_hist, double* X, double* F,
+                       double* C, double* cv);
 
 int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmpea_engine** out);
 /* replace population `which` (1 or 2) by host rows X (n x d) and re-evaluate */

@@ -8,11 +8,18 @@
 //        replaces gmpea::evaluate_population (gmpea.hpp:33)
 //   gmpea_b200::environmental_selection(...)                   -> pair<Population>
 //        replaces gmpea::environmental_selection (gmpea.hpp:108-111)
+//   gmpea_b200::run_cnsga2 / run_ccmo(const ProblemDef&, const RunConfig&)
+//        replace gmpea::run_cnsga2 / run_ccmo (baselines.hpp:33-34)
+//   gmpea_b200::nondominated_sort / crowding_distance / spea2_fitness /
+//   spea2_select  replace the baselines.hpp operators (results identical)
+//   gmpea_b200::pf_reference(const ProblemDef&, size_t) -> Matrix
+//        replaces gmpea::pf_reference (fronts.cpp:54-84)
 //
 // Exceptions: GMPEA_EINVAL -> std::invalid_argument, everything else ->
 // std::runtime_error, with the engine's (reference-identical) messages.
 #pragma once
 
+#include <algorithm>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -168,6 +175,122 @@ inline std::pair<gmpea::Population, gmpea::Population> environmental_selection(
                                         ctx.theta, B1.data(), (int32_t)topo.t1, B2.data(), (int32_t)topo.t2, &w1,
                                         &w2, nullptr, nullptr));
     return {std::move(o1), std::move(o2)};
+}
+
+namespace detail {
+inline void pop_hook(void* user, int64_t n, const double* X, const double* F, const double* C, const double* cv,
+                     double* igd, double* hv, int32_t* has_igd, int32_t* has_hv) {
+    const auto& cfg = *static_cast<const std::pair<const gmpea::RunConfig*, const gmpea::ProblemDef*>*>(user);
+    const gmpea::ProblemDef& def = *cfg.second;
+    gmpea::Population p;
+    p.X = gmpea::Matrix((std::size_t)n, def.d);
+    p.F = gmpea::Matrix((std::size_t)n, def.m);
+    p.C = gmpea::Matrix((std::size_t)n, def.n_ineq + def.n_eq);
+    std::copy(X, X + n * def.d, p.X.data.begin());
+    std::copy(F, F + n * def.m, p.F.data.begin());
+    std::copy(C, C + n * (def.n_ineq + def.n_eq), p.C.data.begin());
+    p.cv.assign(cv, cv + n);
+    if (cfg.first->igd_metric) {
+        *igd = cfg.first->igd_metric(p);
+        *has_igd = 1;
+    }
+    if (cfg.first->hv_metric) {
+        *hv = cfg.first->hv_metric(p);
+        *has_hv = 1;
+    }
+}
+
+inline gmpea::RunResult run_baseline(int algo, const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg) {
+    ProblemHandle ph(def);
+    gmpea_run_config c;
+    gmpea_run_config_default(&c);
+    c.n = (int64_t)cfg.n;
+    c.k_max = (int64_t)cfg.k_max;
+    c.time_budget_s = cfg.time_budget_s ? *cfg.time_budget_s : -1.0;
+    c.eval_budget = cfg.eval_budget ? (int64_t)*cfg.eval_budget : -1;
+    c.seed = cfg.seed;
+    c.params = to_c(cfg.op_params);
+    c.record_walltime = cfg.record_walltime ? 1 : 0;
+    std::pair<const gmpea::RunConfig*, const gmpea::ProblemDef*> user{&cfg, &def};
+    const bool hooks = (bool)cfg.igd_metric || (bool)cfg.hv_metric;
+    const std::size_t n = cfg.n;
+    gmpea::RunResult res;
+    res.effective_n = n;
+    res.pop1.X = gmpea::Matrix(n, def.d);
+    res.pop1.F = gmpea::Matrix(n, def.m);
+    res.pop1.C = gmpea::Matrix(n, def.n_ineq + def.n_eq);
+    res.pop1.cv.assign(n, 0.0);
+    int64_t nh = 0;
+    std::vector<gmpea_gen_record> h(1 << 16);
+    for (;;) {
+        check(gmpea_run_baseline(ph.p, algo, &c, nullptr, 0, hooks ? detail::pop_hook : nullptr,
+                                 hooks ? &user : nullptr, h.data(), (int64_t)h.size(), &nh, res.pop1.X.data.data(),
+                                 res.pop1.F.data.data(), res.pop1.C.data.data(), res.pop1.cv.data()));
+        if (nh <= (int64_t)h.size()) break;
+        h.resize((std::size_t)nh);  // deterministic: rerun with room for every record
+    }
+    for (int64_t k = 0; k < nh; ++k) {
+        gmpea::GenRecord g;
+        g.gen = (std::size_t)h[k].gen;
+        g.evals = (std::size_t)h[k].evals;
+        g.wall_ms = h[k].wall_ms;
+        g.feasible_ratio = h[k].feasible_ratio;
+        if (h[k].has_igd) g.igd = h[k].igd;
+        if (h[k].has_hv) g.hv = h[k].hv;
+        res.history.push_back(g);
+    }
+    return res;
+}
+}  // namespace detail
+
+// run_cnsga2 / run_ccmo (baselines.cpp:320-459) on the device; metric hooks are
+// called on pop1 after every generation, outside the loop timer
+inline gmpea::RunResult run_cnsga2(const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg) {
+    return detail::run_baseline(GMPEA_ALGO_CNSGA2, def, cfg);
+}
+inline gmpea::RunResult run_ccmo(const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg) {
+    return detail::run_baseline(GMPEA_ALGO_CCMO, def, cfg);
+}
+
+// baselines.hpp operators on the device
+inline std::vector<std::size_t> nondominated_sort(const gmpea::Matrix& F, const std::vector<double>& cv,
+                                                  bool use_cdp) {
+    std::vector<int64_t> r(F.rows);
+    check(gmpea_nondominated_sort(F.data.data(), cv.data(), (int64_t)F.rows, (int32_t)F.cols, use_cdp ? 1 : 0,
+                                  r.data()));
+    return std::vector<std::size_t>(r.begin(), r.end());
+}
+inline std::vector<double> crowding_distance(const gmpea::Matrix& F, const std::vector<std::size_t>& front) {
+    std::vector<int64_t> fr(front.begin(), front.end());
+    std::vector<double> d(front.size());
+    check(gmpea_crowding_distance(F.data.data(), (int64_t)F.rows, (int32_t)F.cols, fr.data(), (int64_t)fr.size(),
+                                  d.data()));
+    return d;
+}
+inline std::vector<double> spea2_fitness(const gmpea::Matrix& F, const std::vector<double>& cv, bool use_cdp) {
+    std::vector<double> f(F.rows);
+    check(gmpea_spea2_fitness(F.data.data(), cv.data(), (int64_t)F.rows, (int32_t)F.cols, use_cdp ? 1 : 0, f.data()));
+    return f;
+}
+inline std::vector<std::size_t> spea2_select(const gmpea::Matrix& F, const std::vector<double>& cv, bool use_cdp,
+                                             std::size_t capacity) {
+    std::vector<int64_t> k(std::max<std::size_t>(F.rows, 1));
+    int64_t cnt = 0;
+    check(gmpea_spea2_select(F.data.data(), cv.data(), (int64_t)F.rows, (int32_t)F.cols, use_cdp ? 1 : 0,
+                             (int64_t)capacity, k.data(), &cnt));
+    return std::vector<std::size_t>(k.begin(), k.begin() + cnt);
+}
+
+// pf_reference (fronts.cpp:54-84) built on the device
+inline gmpea::Matrix pf_reference(const gmpea::ProblemDef& def, std::size_t n_points) {
+    ProblemHandle ph(def);
+    const std::size_t cap = std::max<std::size_t>(n_points, 1) + 4 * 50000 + 100000;
+    std::vector<double> out(cap * def.m);
+    int64_t rows = 0;
+    check(gmpea_pf_reference(ph.p, (int64_t)n_points, out.data(), (int64_t)cap, &rows));
+    gmpea::Matrix M((std::size_t)rows, def.m);
+    std::copy(out.begin(), out.begin() + rows * def.m, M.data.begin());
+    return M;
 }
 
 }  // namespace gmpea_b200

@@ -593,7 +593,7 @@ def run_baseline(problem: Problem, algorithm: str, cfg: RunConfig,
                                                  else 1 << 20)
     buf = (_GenRecord * cap)()
     _check(_L.gmpea_run_baseline(problem._h, BASELINE_ALGORITHMS[algorithm], C.byref(c),
-                                 _p(ref) if ref is not None else None, C.c_int64(nref), buf, C.c_int64(cap),
+                                 _p(ref) if ref is not None else None, C.c_int64(nref), None, None, buf, C.c_int64(cap),
                                  C.byref(nh), _p(X), _p(F), _p(Cm), _p(cv)))
     hist = [GenRecord(r.gen, r.evals, r.wall_ms, r.feasible_ratio,
                       r.igd if r.has_igd else None, r.hv if r.has_hv else None) for r in buf[:min(nh.value, cap)]]

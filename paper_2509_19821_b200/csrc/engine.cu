@@ -2315,6 +2315,8 @@ struct BaselineRun {
     double loop_s = 0.0;
     thrust::device_vector<double> igd_ref;  // optional IGD hook front (experiment.cpp:200-205)
     long long n_ref = 0;
+    gmpea_pop_hook hook = nullptr;          // optional host metric hook
+    void* hook_user = nullptr;
 
     void setup(const gmpea_problem* prob, int a, const gmpea_run_config& cfg) {
         p = prob;
@@ -2413,6 +2415,11 @@ struct BaselineRun {
             r.igd = igd_dev(thrust::raw_pointer_cast(F.data()), thrust::raw_pointer_cast(cv.data()), n, m,
                             thrust::raw_pointer_cast(igd_ref.data()), n_ref);
             r.has_igd = 1;
+        }
+        if (hook) {
+            std::vector<double> hX((size_t)n * d), hF((size_t)n * m), hC((size_t)n * nc), hcv(n);
+            get_pop1(hX.data(), hF.data(), hC.data(), hcv.data());
+            hook(hook_user, n, hX.data(), hF.data(), hC.data(), hcv.data(), &r.igd, &r.hv, &r.has_igd, &r.has_hv);
         }
         hist.push_back(r);
     }
@@ -2559,13 +2566,15 @@ struct BaselineRun {
 }  // namespace
 
 int gmpea_run_baseline(const gmpea_problem* p, int32_t algo, const gmpea_run_config* cfg, const double* igd_ref,
-                       int64_t n_ref, gmpea_gen_record* hist, int64_t hist_cap, int64_t* n_hist, double* X, double* F,
-                       double* C, double* cv) {
+                       int64_t n_ref, gmpea_pop_hook hook, void* hook_user, gmpea_gen_record* hist, int64_t hist_cap,
+                       int64_t* n_hist, double* X, double* F, double* C, double* cv) {
     return guarded([&] {
         if (!p || !cfg) throw std::invalid_argument("run_baseline: null argument");
         require_device();
         BaselineRun r;
         r.setup(p, algo, *cfg);
+        r.hook = hook;
+        r.hook_user = hook_user;
         if (igd_ref && n_ref > 0) {
             r.igd_ref.assign(igd_ref, igd_ref + n_ref * p->m);
             r.n_ref = n_ref;

@@ -38,3 +38,6 @@ def test_adapter_runs_next_to_reference():
     assert "evals ref=60600 b200=60600" in out  # 2 n (k_max + 1)
     assert float(lines["evaluate"].split()[-1]) <= 1e-5
     assert lines["hook"].startswith("records 6")
+    # comparison algorithms registered the same way: records with the hook, evals per generation
+    assert lines["baselines"] == "records cnsga2 11/11 ccmo 11/11 evals 660/660 1320/1320"
+    assert lines["operators"] == "ranks_equal 1 fitness_equal 1 front_rows 1000/1000"
