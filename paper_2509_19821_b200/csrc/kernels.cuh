@@ -332,6 +332,50 @@ __device__ __forceinline__ void pm_tasks(const VP& p, unsigned long long mmask, 
     }
 }
 
+// Warp-cooperative polynomial mutation for windows of <= 32 genes: the
+// warp's mutation tasks are numbered by an inclusive scan of the lanes' mask
+// popcounts; in each round lane t takes task t, finds its owner lane by a
+// 5-step binary search over the scanned counts and its gene as the k-th set
+// bit of the owner's mask (__fns), then mutates the owner's staged row.  No
+// shared task list and no block barrier.
+template <class VP>
+__device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0, float4* sm4, unsigned gen,
+                                              unsigned pid, int i0) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, wbase = threadIdx.x & ~31;
+    const int cnt = __popc(mask);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    __syncwarp();  // the lanes' staged rows are visible to the warp
+    for (int r0 = 0; r0 < total; r0 += 32) {
+        const int t = r0 + lane;
+        int owner = 0;  // lanes [0, owner) have incl <= t
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int v = __shfl_sync(FULL, incl, owner + step - 1);
+            if (v <= t) owner += step;
+        }
+        owner = min(owner, 31);
+        const int ex = __shfl_sync(FULL, incl - cnt, owner);
+        const unsigned mo = __shfl_sync(FULL, mask, owner);
+        if (t < total) {
+            const int j = w0 + (int)__fns(mo, 0u, t - ex + 1);
+            const int row = wbase + owner;
+            float* x = reinterpret_cast<float*>(sm4 + row * p.srs4);
+            const unsigned slot = (unsigned)(p.slot_base + i0 + row);
+            const float lo = p.P.lob(j), hi = p.P.hib(j);
+            const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, p.key);
+            x[j] = clamp_ref(pm_apply(x[j], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
+        }
+    }
+    __syncwarp();
+}
+
 // One thread per (slot, population); block rows are staged in shared memory.
 // Phase 1 writes the child genes (before mutation), 64 genes per window, and
 // records which genes the PM coin selects; phase 2 applies polynomial
@@ -592,7 +636,12 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 // phase 2: polynomial mutation then clip (gmpea.cpp:202-203).
                 // The warp's mutation tasks (lane, gene) are dealt round-robin
                 // over its lanes, ~1 task per lane per round.
-                if (ST && MODE == MODE_VARY) pm_tasks(p, (unsigned long long)mmask, w0, sm4, gen, pid, i0);
+                if (ST && MODE == MODE_VARY) {
+                    if (DC > 0 && DC <= 32)
+                        pm_tasks_warp(p, (unsigned)mmask, w0, sm4, gen, pid, i0);
+                    else
+                        pm_tasks(p, (unsigned long long)mmask, w0, sm4, gen, pid, i0);
+                }
             }
         }
         if (p.eval && active) {
