@@ -686,9 +686,20 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
         const int total = rows * rs4;
         float4* __restrict__ dst = p.out[pi] + (long long)i0 * rs4;
         const float inv = 1.0f / (float)rs4;  // exact floor for e < 2^20
-        for (int e = tid; e < total; e += blockDim.x) {
-            const int r = (int)(((float)e + 0.5f) * inv);
-            dst[e] = sm4[r * p.srs4 + (e - r * rs4)];
+        if ((rs4 & 1) == 0) {  // float4 pairs: 256-bit stores (rows 32 B aligned)
+            for (int e = 2 * tid; e < total; e += 2 * blockDim.x) {
+                const int r = (int)(((float)e + 0.5f) * inv);
+                const float4* src = sm4 + r * p.srs4 + (e - r * rs4);
+                const float4 a = src[0], b = src[1];
+                asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + e), "f"(a.x), "f"(a.y),
+                             "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                             : "memory");
+            }
+        } else {
+            for (int e = tid; e < total; e += blockDim.x) {
+                const int r = (int)(((float)e + 0.5f) * inv);
+                dst[e] = sm4[r * p.srs4 + (e - r * rs4)];
+            }
         }
     }
     if (!p.update_z || !p.eval) return;
