@@ -816,6 +816,22 @@ struct SelParams {
 };
 
 __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4* __restrict__ src, int rs4) {
+    if ((rs4 & 1) == 0) {  // rows 32 B aligned: 256-bit loads and stores
+        for (int q0 = 0; q0 < rs4; q0 += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u += 2)
+                if (q0 + u < rs4) ldg256(src + q0 + u, v[u], v[u + 1]);
+#pragma unroll
+            for (int u = 0; u < 8; u += 2)
+                if (q0 + u < rs4)
+                    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + q0 + u),
+                                 "f"(v[u].x), "f"(v[u].y), "f"(v[u].z), "f"(v[u].w), "f"(v[u + 1].x),
+                                 "f"(v[u + 1].y), "f"(v[u + 1].z), "f"(v[u + 1].w)
+                                 : "memory");
+        }
+        return;
+    }
     for (int q0 = 0; q0 < rs4; q0 += 8) {
         float4 v[8];
 #pragma unroll
