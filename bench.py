@@ -36,6 +36,10 @@ WORKLOADS = {
     "mw7-1m": ("MW7", 1_000_000, 0),
     "mw7-10m": ("MW7", 10_000_000, 0),
     "wta-p10-100k": ("WTA-P10", 100_000, 0),
+    # BASELINE configs[2]'s DAS-CMOP half (restated problems, SBX as the
+    # reference's operator_for gives every non-LIRCMOP suite)
+    "dascmop7-1m": ("DASCMOP7", 1_000_000, 0),
+    "dascmop9-1m": ("DASCMOP9", 1_000_000, 0),
 }
 METRIC = "individual-generations/sec at N=1M"
 

@@ -42,7 +42,8 @@ int gmpea_abi_version(void);
 /* ---- problems: replaces make_problem / ProblemDef (problems.hpp:19-45,
  * problems.cpp:531-550) and make_wta_problem / load_wta (wta.hpp:30-48).
  * Names: LIRCMOP1..14, C1-DTLZ1, C1-DTLZ3, C2-DTLZ2, C3-DTLZ4,
- * DC{1,2,3}-DTLZ{1,3}, WTA-P1..P10, MW1..MW14 (MW: not in the reference). */
+ * DC{1,2,3}-DTLZ{1,3}, WTA-P1..P10, MW1..MW14, DASCMOP1..9 (alias DAS-CMOP1..9;
+ * MW and DAS-CMOP are not in the reference: restated, parity unpinned). */
 int gmpea_problem_create(const char* name, gmpea_problem** out);
 /* custom WTA scenario (load_wta, wta.cpp:148-192): p holds sum(strikes)
  * interception probabilities, target-major */

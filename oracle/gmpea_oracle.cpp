@@ -16,6 +16,9 @@
 //   * MW1-MW14 (absent from the reference) — restated from the
 //     MW test-suite definitions (Ma & Wang, IEEE TEVC 2019, as distributed
 //     with PlatEMO);
+//   * DAS-CMOP1-9 (absent from the reference as well) — restated from the
+//     DAS-CMOP toolkit (Fan et al., Evolutionary Computation 28(3), 2020) with
+//     the difficulty triplet (eta, zeta, gamma) = (0.5, 0.5, 0.5);
 //   * reproduce() drawing from the Philox key schema (oracle/philox.h) instead
 //     of the reference's sequential mt19937_64 — it follows
 //     proj/src/gmpea.cpp:113-206 draw for draw (b==a redraw, jrand
@@ -47,7 +50,7 @@ thread_local std::string g_err;
 // ---------------------------------------------------------------------------
 // problems (reference: proj/src/problems.cpp, proj/src/wta.cpp)
 
-enum Family { FAM_LIR = 1, FAM_DTLZ = 2, FAM_WTA = 3, FAM_MW = 4 };
+enum Family { FAM_LIR = 1, FAM_DTLZ = 2, FAM_WTA = 3, FAM_MW = 4, FAM_DAS = 5 };
 enum DtlzKind {
     C1_DTLZ1 = 1, C1_DTLZ3, C2_DTLZ2, C3_DTLZ4, DC1_DTLZ1, DC1_DTLZ3,
     DC2_DTLZ1, DC2_DTLZ3, DC3_DTLZ1, DC3_DTLZ3
@@ -556,6 +559,66 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
     }
 }
 
+// --- DAS-CMOP1-9 (NOT in the reference; parity unpinned).  Restated from the
+// DAS-CMOP toolkit definitions (Fan et al., Evol. Comput. 28(3), 2020): D = 30,
+// x in [0,1]^D, difficulty triplet (eta, zeta, gamma) = (0.5, 0.5, 0.5), so
+// a = 20, b = 2 eta - 1 = 0, d = 0.5, e = d - ln(gamma), r = 0.5 zeta.
+// Constraints in the reference's "<= 0 feasible" form.
+void eval_das(int id, const double* x, int n, double* f, double* g) {
+    const double a = 20.0, b = 2.0 * 0.5 - 1.0, d = 0.5, e = d - std::log(0.5), r = 0.5 * 0.5;
+    const bool rast = id == 4 || id == 5 || id == 6 || id == 9;  // multimodal distance
+    const int m = id >= 7 ? 3 : 2;
+    const double shift = m == 2 ? std::sin(0.5 * kPi * x[0]) : 0.5;
+    double s = 0.0;
+    for (int j = m - 1; j < n; ++j) {
+        double y = x[j] - shift;
+        s += rast ? y * y - std::cos(20.0 * kPi * y) : y * y;
+    }
+    const double gg = rast ? static_cast<double>(n - m + 1) + s : s;
+    const double x1 = x[0];
+    g[0] = b - std::sin(a * kPi * x1);  // type I (diversity)
+    if (m == 2) {
+        f[0] = x1 + gg;
+        if (id == 1 || id == 4)
+            f[1] = 1.0 - x1 * x1 + gg;
+        else if (id == 2 || id == 5)
+            f[1] = 1.0 - std::sqrt(x1) + gg;
+        else
+            f[1] = 1.0 - std::sqrt(x1) + 0.5 * std::fabs(std::sin(5.0 * kPi * x1)) + gg;
+        g[1] = -((e - gg) * (gg - d));  // type II (convergence)
+        // type III (feasibility): nine rotated ellipses
+        const double p[9] = {0.0, 1.0, 0.0, 1.0, 2.0, 0.0, 1.0, 2.0, 3.0};
+        const double q[9] = {1.5, 0.5, 2.5, 1.5, 0.5, 3.5, 2.5, 1.5, 0.5};
+        const double ea = 0.3, eb = 1.2, th = -0.25 * kPi;
+        for (int k = 0; k < 9; ++k) {
+            double u = (f[0] - p[k]) * std::cos(th) - (f[1] - q[k]) * std::sin(th);
+            double v = (f[0] - p[k]) * std::sin(th) + (f[1] - q[k]) * std::cos(th);
+            g[2 + k] = r - (u * u / (ea * ea) + v * v / (eb * eb));
+        }
+        return;
+    }
+    const double x2 = x[1];
+    if (id == 7) {
+        f[0] = x1 * x2 + gg;
+        f[1] = x2 * (1.0 - x1) + gg;
+        f[2] = 1.0 - x2 + gg;
+    } else {
+        f[0] = std::cos(0.5 * kPi * x1) * std::cos(0.5 * kPi * x2) + gg;
+        f[1] = std::cos(0.5 * kPi * x1) * std::sin(0.5 * kPi * x2) + gg;
+        f[2] = std::sin(0.5 * kPi * x1) + gg;
+    }
+    g[1] = b - std::cos(a * kPi * x2);
+    g[2] = -((e - gg) * (gg - d));
+    // four spheres: the three axis points and the centroid direction
+    const double t = 1.0 / std::sqrt(3.0);
+    const double P[4][3] = {{1.0, 0.0, 0.0}, {0.0, 1.0, 0.0}, {0.0, 0.0, 1.0}, {t, t, t}};
+    for (int k = 0; k < 4; ++k) {
+        double s2 = 0.0;
+        for (int i = 0; i < 3; ++i) s2 += (f[i] - P[k][i]) * (f[i] - P[k][i]);
+        g[3 + k] = r * r - s2;
+    }
+}
+
 int mw_ncon(int id) {
     switch (id) {
         case 3: case 7: case 12: case 13: return 2;
@@ -590,6 +653,18 @@ Problem make_problem(const std::string& name) {
         p.nin = mw_ncon(id);
         p.lo.assign(p.d, 0.0);
         p.hi.assign(p.d, id == 14 ? 1.5 : 1.0);
+        return p;
+    }
+    if (name.rfind("DASCMOP", 0) == 0 || name.rfind("DAS-CMOP", 0) == 0) {
+        int id = std::stoi(name.substr(name[3] == '-' ? 8 : 7));
+        if (id < 1 || id > 9) throw std::invalid_argument("unknown problem: " + name);
+        p.fam = FAM_DAS;
+        p.id = id;
+        p.d = 30;
+        p.m = id >= 7 ? 3 : 2;
+        p.nin = id >= 7 ? 7 : 11;
+        p.lo.assign(p.d, 0.0);
+        p.hi.assign(p.d, 1.0);
         return p;
     }
     if (name.rfind("WTA-P", 0) == 0) {
@@ -633,6 +708,7 @@ void eval_row(const Problem& p, const double* x, double* f, double* g) {
         case FAM_DTLZ: eval_dtlz(p.id, x, p.d, p.m, f, g); break;
         case FAM_WTA: eval_wta(p.w, x, p.d, f, g); break;
         case FAM_MW: eval_mw(p.id, x, p.d, p.m, f, g); break;
+        case FAM_DAS: eval_das(p.id, x, p.d, f, g); break;
     }
 }
 

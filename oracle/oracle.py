@@ -432,7 +432,7 @@ class Reference(_Lib):
         return dict(X=X, F=F, C=Cm, cv=cv), hist[:rows.value].copy()
 
     def _info_any(self, name):
-        if name.startswith("MW"):
+        if name.startswith("MW") or name.startswith("DAS"):
             return Oracle().problem_info(name)
         return self.problem_info(name)
 

@@ -99,10 +99,10 @@ NeighborhoodTopology topo_of(const uint32_t* B1, std::size_t t1, const uint32_t*
     return t;
 }
 
-// reference problems, or (for MW*) the oracle's restated evaluator wrapped as
-// a reference ProblemDef so the reference loop can run it
+// reference problems, or (for MW* / DAS-CMOP*) the oracle's restated evaluator
+// wrapped as a reference ProblemDef so the reference loop can run it
 ProblemDef problem_for(const std::string& name) {
-    if (name.rfind("MW", 0) != 0) return make_problem(name);
+    if (name.rfind("MW", 0) != 0 && name.rfind("DAS", 0) != 0) return make_problem(name);
     int32_t d, m, nin, neq;
     std::vector<double> lo(64), hi(64);
     if (orc_problem_info(name.c_str(), &d, &m, &nin, &neq, lo.data(), hi.data()) != 0)

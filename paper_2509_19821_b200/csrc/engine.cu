@@ -276,6 +276,19 @@ std::unique_ptr<gmpea_problem> make_problem(const std::string& name) {
             return p;
         }
     }
+    if (name.rfind("DASCMOP", 0) == 0 || name.rfind("DAS-CMOP", 0) == 0) {
+        int id = num(name[3] == '-' ? 8 : 7);
+        if (id >= 1 && id <= 9) {
+            p->fam = FAM_DAS;
+            p->id = id;
+            p->d = 30;
+            p->m = id >= 7 ? 3 : 2;
+            p->nin = id >= 7 ? 7 : 11;
+            p->lo.assign(p->d, 0.0);
+            p->hi.assign(p->d, 1.0);
+            return p;
+        }
+    }
     if (name.rfind("WTA-", 0) == 0) {
         std::string sc = name.substr(4);
         int v = sc.size() >= 2 && sc[0] == 'P' ? num(5) : -1;
@@ -468,6 +481,7 @@ VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0) {
         case FAM_WTA:
             return d > 0 && mode == MODE_VARY ? pick_vary<EvalWta, 0, true, true>(mode, op)
                                               : pick_vary<EvalWta>(mode, op);
+        case FAM_DAS: return d == 30 ? pick_vary<EvalDas, 30>(mode, op) : pick_vary<EvalDas>(mode, op);
         default: return d == 15 ? pick_vary<EvalMw, 15>(mode, op) : pick_vary<EvalMw>(mode, op);
     }
 }
@@ -1233,6 +1247,7 @@ const char* gmpea_problem_names(void) {
             s += std::string(n) + "\n";
         for (int i = 1; i <= 10; ++i) s += "WTA-P" + std::to_string(i) + "\n";
         for (int i = 1; i <= 14; ++i) s += "MW" + std::to_string(i) + "\n";
+        for (int i = 1; i <= 9; ++i) s += "DASCMOP" + std::to_string(i) + "\n";
         return s;
     }();
     return names.c_str();

@@ -12,6 +12,9 @@
 //   MW1-MW14       not in the reference; restated from the MW
 //                  suite (Ma & Wang 2019, PlatEMO conventions), parity
 //                  unpinned, mirrored by oracle/gmpea_oracle.cpp eval_mw.
+//   DASCMOP1-9     not in the reference either; restated from Fan et al. 2020
+//                  (difficulty triplet (0.5, 0.5, 0.5)), parity unpinned,
+//                  mirrored by oracle/gmpea_oracle.cpp eval_das.
 // Precision policy: inputs are fp32; sums, products and the
 // per-individual transcendental terms are evaluated in fp64 (B200 runs fp64
 // at half the fp32 rate), the per-gene trigonometric terms of LIRCMOP5-12 in
@@ -23,7 +26,7 @@
 
 namespace gmpea_b200 {
 
-enum : int { FAM_LIR = 1, FAM_DTLZ = 2, FAM_WTA = 3, FAM_MW = 4 };
+enum : int { FAM_LIR = 1, FAM_DTLZ = 2, FAM_WTA = 3, FAM_MW = 4, FAM_DAS = 5 };
 enum : int {
     C1_DTLZ1 = 1, C1_DTLZ3, C2_DTLZ2, C3_DTLZ4, DC1_DTLZ1, DC1_DTLZ3,
     DC2_DTLZ1, DC2_DTLZ3, DC3_DTLZ1, DC3_DTLZ3
@@ -548,6 +551,103 @@ struct EvalMw {
                 emit(0, f[2] - 1.0 / 2.0 * sa);
                 return;
             }
+        }
+    }
+};
+
+// ---------------------------------------------------------------- DAS-CMOP (unpinned)
+// DAS-CMOP1-9 (Fan et al., Evol. Comput. 28(3), 2020; D = 30, x in [0,1]^D),
+// difficulty triplet (eta, zeta, gamma) = (0.5, 0.5, 0.5).  Not in the
+// reference; restated from the published definitions and
+// mirrored by oracle/gmpea_oracle.cpp eval_das.  Constraints are written in the
+// reference's "<= 0 feasible" form:
+//   type I   (diversity):    b - sin(a pi x1)  [DAS7-9 also b - cos(a pi x2)], a = 20, b = 2 eta - 1
+//   type II  (convergence):  -(e - g)(g - d),  d = 0.5, e = d - ln gamma
+//   type III (feasibility):  r - ellipse_k(f)  (DAS1-6, 9 ellipses, r = 0.5 zeta)
+//                            r^2 - |f - P_k|^2 (DAS7-9, 4 spheres)
+// The per-gene distance terms are fp64 (the DAS4-6/9 Rastrigin cosine has a
+// 20 pi argument: fp32 would lose 1e-5 relative in g).
+struct DasConst {
+    static constexpr double a = 20.0, b = 0.0;      // b = 2*0.5 - 1
+    static constexpr double d = 0.5;
+    static constexpr double e = 1.1931471805599454;  // 0.5 - ln(0.5)
+    static constexpr double r = 0.25;               // 0.5 * 0.5
+    static constexpr double ea = 0.3, eb = 1.2;     // ellipse semi-axes (DAS1-6)
+};
+
+struct EvalDas {
+    static constexpr bool kStream = false;
+    __device__ __forceinline__ void bind(unsigned long long*, int) {}
+    double xs[2];
+    double sh;  // sin(0.5 pi x1): the position shift of DAS1-6's distance genes
+    double gs;
+    bool rast;
+    __device__ __forceinline__ void begin(const ProbDev& P) {
+        gs = 0.0;
+        sh = 0.5;
+        rast = P.id == 4 || P.id == 5 || P.id == 6 || P.id == 9;
+    }
+    template <class T>
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, T xf) {
+        const double x = xf;
+        if (j < P.m - 1) {
+            if (j == 0) {
+                xs[0] = x;
+                if (P.m == 2) sh = sinpi(0.5 * x);
+            } else {
+                xs[1] = x;
+            }
+            return;
+        }
+        const double y = x - sh;
+        gs += rast ? y * y - cospi(20.0 * y) : y * y;
+    }
+    template <class G>
+    __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
+        using K = DasConst;
+        const int id = P.id;
+        const double g = rast ? (double)(P.d - P.m + 1) + gs : gs;
+        const double x1 = xs[0];
+        emit(0, K::b - sinpi(K::a * x1));
+        if (id <= 6) {
+            f[0] = x1 + g;
+            const int shape = (id - 1) % 3;  // 0: 1 - x^2, 1: 1 - sqrt x, 2: + 0.5|sin 5 pi x|
+            f[1] = (shape == 0 ? 1.0 - x1 * x1 : 1.0 - sqrt(x1)) + (shape == 2 ? 0.5 * fabs(sinpi(5.0 * x1)) : 0.0) + g;
+            emit(1, -((K::e - g) * (g - K::d)));
+            const double c = 0.7071067811865476, s = -0.7071067811865476;  // cos, sin(-pi/4)
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                const double p = k == 0 || k == 2 || k == 5 ? 0.0 : (k == 1 || k == 3 || k == 6 ? 1.0 : (k == 8 ? 3.0 : 2.0));
+                const double q = k == 0 || k == 3 || k == 7 ? 1.5 : (k == 1 || k == 4 || k == 8 ? 0.5 : (k == 2 || k == 6 ? 2.5 : 3.5));
+                const double u = (f[0] - p) * c - (f[1] - q) * s;
+                const double v = (f[0] - p) * s + (f[1] - q) * c;
+                emit(2 + k, K::r - (u * u / (K::ea * K::ea) + v * v / (K::eb * K::eb)));
+            }
+            return;
+        }
+        const double x2 = xs[1];
+        if (id == 7) {
+            f[0] = x1 * x2 + g;
+            f[1] = x2 * (1.0 - x1) + g;
+            f[2] = 1.0 - x2 + g;
+        } else {
+            double s0, c0, s1, c1;
+            sincospi(0.5 * x1, &s0, &c0);
+            sincospi(0.5 * x2, &s1, &c1);
+            f[0] = c0 * c1 + g;
+            f[1] = c0 * s1 + g;
+            f[2] = s0 + g;
+        }
+        emit(1, K::b - cospi(K::a * x2));
+        emit(2, -((K::e - g) * (g - K::d)));
+        const double t = 0.5773502691896258;  // 1/sqrt(3)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double px = k == 0 ? 1.0 : (k == 3 ? t : 0.0);
+            const double py = k == 1 ? 1.0 : (k == 3 ? t : 0.0);
+            const double pz = k == 2 ? 1.0 : (k == 3 ? t : 0.0);
+            const double a = f[0] - px, b = f[1] - py, cc = f[2] - pz;
+            emit(3 + k, K::r * K::r - (a * a + b * b + cc * cc));
         }
     }
 };

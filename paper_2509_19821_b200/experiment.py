@@ -112,6 +112,8 @@ def suite_of(problem: str) -> str:
         return "wta"
     if problem.startswith("MW"):
         return "mw"
+    if problem.startswith("DASCMOP") or problem.startswith("DAS-CMOP"):
+        return "dascmop"
     return "dtlz"
 
 

@@ -58,3 +58,4 @@ REF_PROBLEMS = ([f"LIRCMOP{i}" for i in range(1, 15)] +
                  "DC2-DTLZ1", "DC2-DTLZ3", "DC3-DTLZ1", "DC3-DTLZ3"] +
                 [f"WTA-P{i}" for i in range(1, 11)])
 MW_PROBLEMS = [f"MW{i}" for i in range(1, 15)]
+DAS_PROBLEMS = [f"DASCMOP{i}" for i in range(1, 10)]

@@ -9,7 +9,7 @@ decode, draws) bit-exact.
 import numpy as np
 import pytest
 
-from conftest import MW_PROBLEMS, REF_PROBLEMS, f32, golden, rel_close
+from conftest import DAS_PROBLEMS, MW_PROBLEMS, REF_PROBLEMS, f32, golden, rel_close
 
 pytestmark = pytest.mark.gpu
 
@@ -39,6 +39,30 @@ def test_evaluate_matches_oracle_500_points(g, orc, name):
     r = g.evaluate_population(g.make_problem(name), X)
     F, G, cv = orc.evaluate(name, X)
     assert rel_close(r.F, F).all() and rel_close(r.C, G).all() and rel_close(r.cv, cv).all()
+
+
+@pytest.mark.parametrize("name", DAS_PROBLEMS)
+def test_evaluate_dascmop_matches_oracle(g, orc, name):
+    """DAS-CMOP (unpinned restatement): GPU vs oracle on random rows and on
+    rows around the Pareto set, where g crosses the type-II band [d, e]."""
+    k = int(name[7:])
+    m = 3 if k >= 7 else 2
+    rng = np.random.default_rng(100 + k)
+    X = rng.random((600, 30))
+    opt = np.sin(0.5 * np.pi * X[:400, :1]) if m == 2 else np.full((400, 1), 0.5)
+    sd = np.where(np.arange(400) < 200, 0.02, 0.15)[:, None]
+    X[:400, m - 1:] = np.clip(opt + sd * rng.normal(0, 1, (400, 30 - m + 1)), 0, 1)
+    X = f32(X)
+    r = g.evaluate_population(g.make_problem(name), X)
+    F, G, cv = orc.evaluate(name, X)
+    assert rel_close(r.F, F).all(), np.abs(r.F - F).max()
+    assert rel_close(r.C, G).all(), np.abs(r.C - G).max()
+    assert rel_close(r.cv, cv).all()
+    # feasibility decided identically except where a constraint sits within
+    # the tolerance of its boundary
+    near = (np.abs(G) <= 1e-5 * np.maximum(1.0, np.abs(G))).any(1)
+    assert np.array_equal((r.cv == 0.0)[~near], (cv == 0.0)[~near])
+    assert g.make_problem(name.replace("DASCMOP", "DAS-CMOP")).m == m
 
 
 def test_evaluate_rejects_out_of_bounds_rows(g):
@@ -159,7 +183,7 @@ def test_selection_rejects_non_finite(g):
 
 # ------------------------------------------------------------------ variation
 @pytest.mark.parametrize("name,op", [("LIRCMOP13", 1), ("LIRCMOP1", 0), ("MW1", 0), ("C1-DTLZ1", 0),
-                                     ("WTA-P3", 0), ("MW14", 1)])
+                                     ("WTA-P3", 0), ("MW14", 1), ("DASCMOP7", 1), ("DASCMOP4", 0)])
 def test_reproduce_matches_oracle_draw_for_draw(g, orc, name, op):
     info = orc.problem_info(name)
     n = 400
@@ -262,21 +286,22 @@ def test_time_budget_discards_crossing_generation(g):
     assert all(b.wall_ms >= a.wall_ms for a, b in zip(h[1:], h[2:]))
 
 
-def test_engine_generation_matches_operator_chain(g, orc):
+@pytest.mark.parametrize("name,op", [("LIRCMOP13", 1), ("DASCMOP7", 1), ("DASCMOP2", 0)])
+def test_engine_generation_matches_operator_chain(g, orc, name, op):
     """One engine generation == oracle reproduce -> evaluate -> update_ideal ->
     environmental_selection on the same (fp32) state, with the engine's keys."""
-    name, n, seed = "LIRCMOP13", 300, 5
+    n, seed = 300, 5
     p = g.make_problem(name)
-    eng = g.Engine(p, g.RunConfig(n=n, k_max=1, seed=seed, op=g.VariationOp.de))
+    eng = g.Engine(p, g.RunConfig(n=n, k_max=1, seed=seed, op=g.VariationOp(op)))
     P1, P2 = eng.population(1), eng.population(2)
     topo = eng.neighborhoods()
     z0 = eng.ideal()
     eng.run()
     N1, N2 = eng.population(1), eng.population(2)
-    W = orc.reference_vectors(3, n)
+    W = orc.reference_vectors(p.m, n)
     offs = []
     for pop, nb, pid in ((P1, topo.b1, 1), (P2, topo.b2, 2)):
-        ox, _ = orc.reproduce(name, pop.X, nb, 1, seed, 1, pid)
+        ox, _ = orc.reproduce(name, pop.X, nb, op, seed, 1, pid)
         F, G, cv = orc.evaluate(name, f32(ox))
         offs.append(dict(X=f32(ox), F=f32(F), cv=f32(cv)))
     z = np.minimum(z0, np.minimum(offs[0]["F"].min(0), offs[1]["F"].min(0)))

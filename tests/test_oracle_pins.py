@@ -145,3 +145,86 @@ def test_oracle_reproduce_identities(orc):
     # DE with F = 0, CR = 1, no mutation: the trial equals the base vector
     off, _ = orc.reproduce("LIRCMOP1", X[:10], nb10, 1, 1, 1, 1, params=(1.0, 20, 20, 1.0, 0.0), pm_prob=0.0)
     assert np.array_equal(off, X[:10])
+
+
+# ------------------------------------------------------------------ DAS-CMOP
+# DAS-CMOP1-9 have no reference counterpart: "parity unpinned".
+# The oracle's restatement is cross-checked against a second, independent
+# vectorised restatement of the published definitions (Fan et al., Evol.
+# Comput. 28(3), 2020; difficulty triplet (0.5, 0.5, 0.5)) and against closed
+# forms on the Pareto set.
+def das_numpy(k, X):
+    a, b, d, r = 20.0, 0.0, 0.5, 0.25
+    e = d - np.log(0.5)
+    x1 = X[:, 0]
+    m = 3 if k >= 7 else 2
+    y = X[:, m - 1:] - (np.sin(0.5 * np.pi * x1)[:, None] if m == 2 else 0.5)
+    if k in (4, 5, 6, 9):
+        g = (X.shape[1] - m + 1) + np.sum(y * y - np.cos(20.0 * np.pi * y), axis=1)
+    else:
+        g = np.sum(y * y, axis=1)
+    cons = [b - np.sin(a * np.pi * x1)]
+    if m == 2:
+        h = {0: 1 - x1 ** 2, 1: 1 - np.sqrt(x1), 2: 1 - np.sqrt(x1) + 0.5 * np.abs(np.sin(5 * np.pi * x1))}[(k - 1) % 3]
+        F = np.stack([x1 + g, h + g], 1)
+        cons.append(-(e - g) * (g - d))
+        th = -0.25 * np.pi
+        for p, q in zip([0, 1, 0, 1, 2, 0, 1, 2, 3], [1.5, 0.5, 2.5, 1.5, 0.5, 3.5, 2.5, 1.5, 0.5]):
+            u = (F[:, 0] - p) * np.cos(th) - (F[:, 1] - q) * np.sin(th)
+            v = (F[:, 0] - p) * np.sin(th) + (F[:, 1] - q) * np.cos(th)
+            cons.append(r - (u ** 2 / 0.09 + v ** 2 / 1.44))
+    else:
+        x2 = X[:, 1]
+        if k == 7:
+            F = np.stack([x1 * x2, x2 * (1 - x1), 1 - x2], 1) + g[:, None]
+        else:
+            c0, s0 = np.cos(0.5 * np.pi * x1), np.sin(0.5 * np.pi * x1)
+            F = np.stack([c0 * np.cos(0.5 * np.pi * x2), c0 * np.sin(0.5 * np.pi * x2), s0], 1) + g[:, None]
+        cons.append(b - np.cos(a * np.pi * x2))
+        cons.append(-(e - g) * (g - d))
+        t = 1 / np.sqrt(3)
+        for P in ([1, 0, 0], [0, 1, 0], [0, 0, 1], [t, t, t]):
+            cons.append(r * r - np.sum((F - np.array(P)) ** 2, 1))
+    G = np.stack(cons, 1)
+    return F, G, np.maximum(G, 0).sum(1)
+
+
+@pytest.mark.parametrize("k", range(1, 10))
+def test_dascmop_oracle_vs_independent_restatement(orc, k):
+    rng = np.random.default_rng(k)
+    X = rng.random((300, 30))
+    # half the rows on / near the Pareto set (distance genes at their optimum)
+    m = 3 if k >= 7 else 2
+    opt = np.sin(0.5 * np.pi * X[:150, :1]) if m == 2 else np.full((150, 1), 0.5)
+    # noise 0.02: g near 0 (type II violated); 0.15: g near the feasible band [d, e]
+    sd = np.where(np.arange(150) < 75, 0.02, 0.15)[:, None]
+    X[:150, m - 1:] = np.clip(opt + sd * rng.normal(0, 1, (150, 30 - m + 1)), 0, 1)
+    F, G, cv = orc.evaluate(f"DASCMOP{k}", X)
+    Fn, Gn, cvn = das_numpy(k, X)
+    assert np.allclose(F, Fn, rtol=1e-12, atol=1e-12)
+    assert np.allclose(G, Gn, rtol=1e-12, atol=1e-12)
+    assert np.allclose(cv, cvn, rtol=1e-12, atol=1e-12)
+    assert G.shape[1] == (7 if k >= 7 else 11)
+    # both feasible and infeasible rows are exercised
+    assert (cv == 0).any() or k in (4, 5, 6, 9)
+
+
+def test_dascmop_known_answers(orc):
+    # DAS-CMOP1 on its unconstrained Pareto set (g = 0): f = (x1, 1 - x1^2)
+    x = np.zeros((1, 30))
+    x[0, 0] = 0.25
+    x[0, 1:] = np.sin(0.5 * np.pi * 0.25)
+    F, G, cv = orc.evaluate("DASCMOP1", x)
+    assert np.allclose(F[0], [0.25, 1 - 0.0625], atol=1e-15)
+    # type II with g = 0: -(e - 0)(0 - d) = e d > 0 (the unconstrained set is infeasible)
+    assert np.isclose(G[0, 1], 0.5 * (0.5 - np.log(0.5)))
+    # type I: b - sin(20 pi x1) = -sin(5 pi) = 0 at x1 = 0.25
+    assert abs(G[0, 0]) < 1e-14
+    # DAS-CMOP7 at x3.. = 0.5 (g = 0): f = (x1 x2, x2 (1 - x1), 1 - x2), sum 1
+    x = np.full((1, 30), 0.5)
+    x[0, :2] = [0.2, 0.6]
+    F, G, cv = orc.evaluate("DASCMOP7", x)
+    assert np.allclose(F[0], [0.12, 0.48, 0.4], atol=1e-15)
+    # DAS-CMOP9's Rastrigin distance vanishes at the same point: unit-sphere objectives
+    F, _, _ = orc.evaluate("DASCMOP9", x)
+    assert np.isclose(np.sum(F[0] ** 2), 1.0)
