@@ -135,6 +135,24 @@ int mw_ncon(int id) {
     }
 }
 
+// packs R into int16 offsets for select (pack_reverse_kernel); false when an
+// offset does not fit or GMPEA_NO_RPACK is set (select then reads R)
+bool device_pack_reverse(cudaStream_t s, int n, int maxdeg, const DevBuf<int>& R, long long ld,
+                         const DevBuf<int>& deg, DevBuf<uint2>& Rp) {
+    const char* off = getenv("GMPEA_NO_RPACK");
+    if (off && *off && *off != '0') return false;
+    const int nq = (std::max(maxdeg, 1) + 3) / 4;
+    Rp.alloc((size_t)nq * ld);
+    DevBuf<int> overflow(1);
+    overflow.zero(s);
+    pack_reverse_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, deg.p, R.p, ld, nq, Rp.p, overflow.p);
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, overflow.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return h == 0;
+}
+
 }  // namespace
 
 struct gmpea_problem {
@@ -618,6 +636,8 @@ struct gmpea_engine {
     long long rec_cap = 0;
     DevBuf<float4> U;
     DevBuf<int> B[2], R[2], Rdeg[2];
+    DevBuf<uint2> Rp[2];
+    bool rpack = false;  // select reads the int16-packed reverse neighbourhood
     int maxdeg[2] = {0, 0};
     PopBuf pop[2], off[2], undo[2];
     DevBuf<float4> eff[2];
@@ -742,6 +762,8 @@ struct gmpea_engine {
         }
         maxdeg[0] = device_reverse(s, n, t1, B[0].p, ld, Rdeg[0], R[0], (int)(v0 - e0), (int)(v1 - e0));
         maxdeg[1] = device_reverse(s, n, t2, B[1].p, ld, Rdeg[1], R[1], (int)(v0 - e0), (int)(v1 - e0));
+        rpack = device_pack_reverse(s, n, maxdeg[0], R[0], ld, Rdeg[0], Rp[0]) &&
+                device_pack_reverse(s, n, maxdeg[1], R[1], ld, Rdeg[1], Rp[1]);
 
         for (int q = 0; q < 2; ++q) {
             pop[q].alloc(n, geo.rs4, ld);
@@ -828,6 +850,7 @@ struct gmpea_engine {
             sp.oFcv[q] = off[q].Fcv.p;
             sp.eff[q] = eff[q].p;
             sp.R[q] = R[q].p;
+            sp.Rp[q] = rpack ? Rp[q].p : nullptr;
             sp.Rdeg[q] = Rdeg[q].p;
             sp.winner[q] = nullptr;
             if (time_mode) {
@@ -929,12 +952,20 @@ struct gmpea_engine {
         enqueue_phase2();  // select's last block also publishes the stop flag
     }
 
+    void launch_select() {
+        const dim3 grid(blocks_for(own1 - own0, 256), 2);
+        if (rpack)
+            select_kernel<true><<<grid, 256, 0, s>>>(sp);
+        else
+            select_kernel<false><<<grid, 256, 0, s>>>(sp);
+    }
+
     // phase 1: variation + evaluation (+ local ideal-point partial)
     void enqueue_phase1() { launch_vary(vary, vp, 2, s); }
     // phase 2: OP1, selection, bookkeeping (a sharded run all-reduces z in between)
     void enqueue_phase2() {
         op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
-        select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);  // + end_gen
+        launch_select();  // + end_gen
         if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
 
@@ -1140,7 +1171,7 @@ struct gmpea_engine {
             CK(cudaEventRecord(e[1], s));
             op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
             CK(cudaEventRecord(e[2], s));
-            select_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(sp);  // + end_gen
+            launch_select();  // + end_gen
             CK(cudaEventRecord(e[3], s));
             if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
             CK(cudaEventRecord(e[4], s));
@@ -1463,6 +1494,8 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
         CK(cudaMemcpy(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost));
         if (herr) throw std::invalid_argument("pbi: zero-norm reference vector");
         DevBuf<int> Bd[2], R[2], Rdeg[2];
+        DevBuf<uint2> Rp[2];
+        int md[2] = {0, 0};
         const uint32_t* Bh[2] = {B1, B2};
         const int ts[2] = {t1, t2};
         for (int q = 0; q < 2; ++q) {
@@ -1473,8 +1506,10 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
             u32_to_i32_kernel<<<blocks_for(n * ts[q], 256), 256>>>(bu.p, n * ts[q], Bd[q].p, (int)n, err.p);
             CK(cudaMemcpy(&herr, err.p, sizeof(int), cudaMemcpyDeviceToHost));
             if (herr) throw std::invalid_argument("environmental_selection: neighbour index out of range");
-            device_reverse(s, (int)n, ts[q], Bd[q].p, ld, Rdeg[q], R[q]);
+            md[q] = device_reverse(s, (int)n, ts[q], Bd[q].p, ld, Rdeg[q], R[q]);
         }
+        const bool pack = device_pack_reverse(s, (int)n, md[0], R[0], ld, Rdeg[0], Rp[0]) &&
+                          device_pack_reverse(s, (int)n, md[1], R[1], ld, Rdeg[1], Rp[1]);
         DevBuf<DevState> st(1);
         st.zero(s);
         set_z_kernel<<<1, 1>>>(st.p, m, (float)z[0], (float)z[1], m > 2 ? (float)z[2] : 0.0f);
@@ -1500,13 +1535,17 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
             sp.oFcv[q] = fcv[2 + q].p;
             sp.eff[q] = eff[q].p;
             sp.R[q] = R[q].p;
+            sp.Rp[q] = pack ? Rp[q].p : nullptr;
             sp.Rdeg[q] = Rdeg[q].p;
             sp.winner[q] = win[q].p;
         }
         sp.srcbits = sb.p;
         sp.apply = 0;
         sp.st = st.p;
-        select_kernel<<<dim3(blocks_for(n, 256), 2), 256>>>(sp);
+        if (pack)
+            select_kernel<true><<<dim3(blocks_for(n, 256), 2), 256>>>(sp);
+        else
+            select_kernel<false><<<dim3(blocks_for(n, 256), 2), 256>>>(sp);
         CK(cudaGetLastError());
         std::vector<int> w1(n), w2(n);
         CK(cudaMemcpy(w1.data(), win[0].p, n * sizeof(int), cudaMemcpyDeviceToHost));

@@ -799,6 +799,7 @@ struct SelParams {
     const float4* eff[2];
     const unsigned char* srcbits;
     const int* R[2];     // reverse neighbourhood, R[k*ldr + j] ascending in k
+    const uint2* Rp[2];  // the same packed: claimants 4q..4q+3 of j as int16 offsets c - j in Rp[q*ldr + j]
     const int* Rdeg[2];
     long long ldr;
     int* winner[2];      // optional: -1 parent, c: off1 row c, n + c: off2 row c
@@ -843,13 +844,23 @@ __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4*
     }
 }
 
-template <int POP>
+// PACK: claimants come from Rp (one 8 B coalesced load per four claimants,
+// half the bytes of R); the engine packs only when every |c - j| < 2^15.
+__device__ __forceinline__ void unpack_claims(const uint2 w, const int j, const int left, int cc[4]) {
+    cc[0] = left > 0 ? j + (int)(short)(w.x & 0xffffu) : -1;
+    cc[1] = left > 1 ? j + ((int)w.x >> 16) : -1;
+    cc[2] = left > 2 ? j + (int)(short)(w.y & 0xffffu) : -1;
+    cc[3] = left > 3 ? j + ((int)w.y >> 16) : -1;
+}
+
+template <int POP, bool PACK = false>
 __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
     const float4 par = p.Fcv[POP][j];
     const float4 u4 = p.U[j];
     const float gp = pbi(par, u4, z, p.theta);
     const int deg = p.Rdeg[POP][j];
     const int* __restrict__ R = p.R[POP];
+    const uint2* __restrict__ Rp = p.Rp[POP] + j;
     const float4* __restrict__ eff = p.eff[POP];
     bool have = false;
     float4 best = par;
@@ -861,16 +872,26 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     // batches of four claimants; the next batch's indices are loaded while
     // this batch's keys are gathered (one memory round trip per batch)
     int cc[4];
+    uint2 wn = make_uint2(0u, 0u);
+    if (PACK) {
+        if (deg > 0) wn = Rp[0];
+        unpack_claims(wn, j, deg, cc);
+    } else {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) cc[u] = u < deg ? R[(long long)u * p.ldr + j] : -1;
+        for (int u = 0; u < 4; ++u) cc[u] = u < deg ? R[(long long)u * p.ldr + j] : -1;
+    }
     for (int k0 = 0; k0 < deg; k0 += 4) {
         float4 ee[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (cc[u] >= 0) ee[u] = eff[cc[u]];
         int cn[4];
+        if (PACK) {
+            if (k0 + 4 < deg) wn = Rp[(long long)(k0 / 4 + 1) * p.ldr];
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cn[u] = k0 + 4 + u < deg ? R[(long long)(k0 + 4 + u) * p.ldr + j] : -1;
+            for (int u = 0; u < 4; ++u) cn[u] = k0 + 4 + u < deg ? R[(long long)(k0 + 4 + u) * p.ldr + j] : -1;
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int c = cc[u];
@@ -906,8 +927,12 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
                 bc = c;
             }
         }
+        if (PACK) {
+            unpack_claims(wn, j, deg - k0 - 4, cc);
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) cc[u] = cn[u];
+            for (int u = 0; u < 4; ++u) cc[u] = cn[u];
+        }
     }
     if (negcv) {
         atomicCAS(&p.st->err, 0, ERR_NEG_CV);
@@ -945,6 +970,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
 #ifndef GMPEA_SELECT_MINBLOCKS
 #define GMPEA_SELECT_MINBLOCKS 4
 #endif
+template <bool PACK = false>
 __device__ __forceinline__ void select_body(const SelParams& p, const int bx, const int by) {
     if (p.st->stop) return;
     const int j = p.row0 + bx * blockDim.x + threadIdx.x;
@@ -952,9 +978,9 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
     bool feas = false, off_taken = false;
     if (j < p.row_end) {
         if (by == 0)
-            off_taken = select_slot<0>(p, j, z, feas);
+            off_taken = select_slot<0, PACK>(p, j, z, feas);
         else
-            off_taken = select_slot<1>(p, j, z, feas);
+            off_taken = select_slot<1, PACK>(p, j, z, feas);
     }
     if (p.rec == nullptr) return;
     // feasible_ratio of pop1 (gmpea.cpp:411-417) and the replacement count
@@ -994,8 +1020,9 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     st->t_gen_start = globaltimer();
 }
 
+template <bool PACK = false>
 __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
-    select_body(p, blockIdx.x, blockIdx.y);
+    select_body<PACK>(p, blockIdx.x, blockIdx.y);
     if (p.done == nullptr) return;
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -232,4 +232,25 @@ __global__ void reverse_sort_kernel(int n, const int* deg, int* R, long long ld)
     }
 }
 
+// the reverse neighbourhood packed for select: claimants 4q..4q+3 of slot j
+// as int16 offsets c - j in Rp[q*ld + j] (zero past the in-degree); sets
+// *overflow when an offset does not fit (the engine then keeps R)
+__global__ void pack_reverse_kernel(int n, const int* deg, const int* R, long long ld, int nq, uint2* Rp,
+                                    int* overflow) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int d = deg[j];
+    for (int q = 0; q < nq; ++q) {
+        unsigned w[2] = {0u, 0u};
+        for (int u = 0; u < 4; ++u) {
+            const int k = 4 * q + u;
+            if (k >= d) break;
+            const int off = R[(long long)k * ld + j] - j;
+            if (off < -32768 || off > 32767) *overflow = 1;
+            w[u >> 1] |= ((unsigned)off & 0xffffu) << (16 * (u & 1));
+        }
+        Rp[(long long)q * ld + j] = make_uint2(w[0], w[1]);
+    }
+}
+
 }  // namespace gmpea_b200
