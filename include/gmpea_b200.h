@@ -120,8 +120,10 @@ int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, 
  * front candidates built and evaluated in fp64 on the device, feasible rows
  * only, nondominated-filtered, subsampled to n_points (subsample_front).
  * Writes *rows (<= n_points unless the front is smaller) rows of m values;
- * fails (status 2, the reference's runtime_error text) for problems without
- * an analytic front (MW, WTA).  cap: capacity of out in rows. */
+ * MW / DAS-CMOP (restated suites) use restated candidates: per position the
+ * smallest feasible distance value (level scan + bisection), realised in
+ * decision space.  Fails (status 2, the reference's runtime_error text) for
+ * WTA (no analytic front).  cap: capacity of out in rows. */
 int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, int64_t cap, int64_t* rows);
 
 /* ---- comparison-algorithm operators: replace baselines.hpp (baselines.cpp:22-190).

@@ -384,10 +384,14 @@ double mw_g_lin(const double* x, int n, int m) {  // MW3/7/11/14 distance
     return s;
 }
 
-void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
+// MW objectives and constraints from the position genes x[0 .. m-2] and the
+// distance sum gs (the per-kind g above): every MW problem depends on the
+// distance genes only through gs, which is what the restated front
+// candidates (mw_front_row) scan over.
+void eval_mw_level(int id, const double* x, int n, int m, double gs, double* f, double* g) {
     switch (id) {
         case 1: {
-            double gg = 1.0 + mw_g_exp(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = x[0];
             f[1] = gg * (1.0 - 0.85 * f[0] / gg);
             double l = std::sqrt(2.0) * f[1] - std::sqrt(2.0) * f[0];
@@ -395,7 +399,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 2: {
-            double gg = 1.0 + mw_g_cos(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = x[0];
             f[1] = gg * (1.0 - f[0] / gg);
             double l = std::sqrt(2.0) * f[1] - std::sqrt(2.0) * f[0];
@@ -403,7 +407,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 3: {
-            double gg = 1.0 + mw_g_lin(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = x[0];
             f[1] = gg * (1.0 - f[0] / gg);
             double l = std::sqrt(2.0) * f[1] - std::sqrt(2.0) * f[0];
@@ -414,7 +418,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
         }
         case 4:
         case 8: {
-            double gg = id == 4 ? mw_g_exp(x, n, m) : mw_g_cos(x, n, m);
+            double gg = gs;
             // f_k = (1+g) * prod_{i < m-1-k} c(x_i) * (k > 0 ? s(x_{m-1-k}) : 1)
             for (int k = 0; k < m; ++k) {
                 double v = 1.0 + gg;
@@ -439,7 +443,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 5: {
-            double gg = 1.0 + mw_g_exp(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0];
             double r = f[0] / gg;
             f[1] = gg * std::sqrt(1.0 - r * r);
@@ -455,7 +459,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 6: {
-            double gg = 1.0 + mw_g_cos(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0] * 1.0999;
             double r = f[0] / gg;
             f[1] = gg * std::sqrt(1.1 * 1.1 - r * r);
@@ -465,7 +469,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 7: {
-            double gg = 1.0 + mw_g_lin(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0];
             double r = f[0] / gg;
             f[1] = gg * std::sqrt(1.0 - r * r);
@@ -478,7 +482,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 9: {
-            double gg = 1.0 + mw_g_exp(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0];
             f[1] = gg * (1.0 - std::pow(f[0] / gg, 0.6));
             double f1s = f[0] * f[0];
@@ -490,7 +494,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 10: {
-            double gg = 1.0 + mw_g_cos(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * std::pow(x[0], static_cast<double>(n));
             double r = f[0] / gg;
             f[1] = gg * (1.0 - r * r);
@@ -501,7 +505,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 11: {
-            double gg = 1.0 + mw_g_lin(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0] * std::sqrt(1.9999);
             double r = f[0] / gg;
             f[1] = gg * std::sqrt(2.0 - r * r);
@@ -513,7 +517,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 12: {
-            double gg = 1.0 + mw_g_exp(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0];
             double r = f[0] / gg;
             f[1] = gg * (0.85 - 0.8 * r - 0.08 * std::fabs(std::sin(3.2 * kPi * r)));
@@ -529,7 +533,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 13: {
-            double gg = 1.0 + mw_g_cos(x, n, m);
+            double gg = 1.0 + gs;
             f[0] = gg * x[0] * 1.5;
             double r = f[0] / gg;
             f[1] = gg * (5.0 - std::exp(r) - std::fabs(0.5 * std::sin(3.0 * kPi * r)));
@@ -543,7 +547,7 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
             return;
         }
         case 14: {
-            double gg = mw_g_lin(x, n, m);
+            double gg = gs;
             double s = 0.0, sa = 0.0;
             for (int k = 0; k + 1 < m; ++k) {
                 f[k] = x[k];
@@ -559,13 +563,29 @@ void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
     }
 }
 
+int mw_kind(int id) {  // 0: exp distance, 1: cos distance, 2: linear distance
+    switch (id) {
+        case 1: case 4: case 5: case 9: case 12: return 0;
+        case 2: case 6: case 8: case 10: case 13: return 1;
+        default: return 2;
+    }
+}
+
+double mw_gsum(int id, const double* x, int n, int m) {
+    const int k = mw_kind(id);
+    return k == 0 ? mw_g_exp(x, n, m) : (k == 1 ? mw_g_cos(x, n, m) : mw_g_lin(x, n, m));
+}
+
+void eval_mw(int id, const double* x, int n, int m, double* f, double* g) {
+    eval_mw_level(id, x, n, m, mw_gsum(id, x, n, m), f, g);
+}
+
 // --- DAS-CMOP1-9 (NOT in the reference; parity unpinned).  Restated from the
 // DAS-CMOP toolkit definitions (Fan et al., Evol. Comput. 28(3), 2020): D = 30,
 // x in [0,1]^D, difficulty triplet (eta, zeta, gamma) = (0.5, 0.5, 0.5), so
 // a = 20, b = 2 eta - 1 = 0, d = 0.5, e = d - ln(gamma), r = 0.5 zeta.
 // Constraints in the reference's "<= 0 feasible" form.
-void eval_das(int id, const double* x, int n, double* f, double* g) {
-    const double a = 20.0, b = 2.0 * 0.5 - 1.0, d = 0.5, e = d - std::log(0.5), r = 0.5 * 0.5;
+double das_g(int id, const double* x, int n) {
     const bool rast = id == 4 || id == 5 || id == 6 || id == 9;  // multimodal distance
     const int m = id >= 7 ? 3 : 2;
     const double shift = m == 2 ? std::sin(0.5 * kPi * x[0]) : 0.5;
@@ -574,7 +594,13 @@ void eval_das(int id, const double* x, int n, double* f, double* g) {
         double y = x[j] - shift;
         s += rast ? y * y - std::cos(20.0 * kPi * y) : y * y;
     }
-    const double gg = rast ? static_cast<double>(n - m + 1) + s : s;
+    return rast ? static_cast<double>(n - m + 1) + s : s;
+}
+
+// objectives and constraints from the position genes and the distance g
+void eval_das_level(int id, const double* x, double gg, double* f, double* g) {
+    const double a = 20.0, b = 2.0 * 0.5 - 1.0, d = 0.5, e = d - std::log(0.5), r = 0.5 * 0.5;
+    const int m = id >= 7 ? 3 : 2;
     const double x1 = x[0];
     g[0] = b - std::sin(a * kPi * x1);  // type I (diversity)
     if (m == 2) {
@@ -617,6 +643,10 @@ void eval_das(int id, const double* x, int n, double* f, double* g) {
         for (int i = 0; i < 3; ++i) s2 += (f[i] - P[k][i]) * (f[i] - P[k][i]);
         g[3 + k] = r * r - s2;
     }
+}
+
+void eval_das(int id, const double* x, int n, double* f, double* g) {
+    eval_das_level(id, x, das_g(id, x, n), f, g);
 }
 
 int mw_ncon(int id) {
@@ -709,6 +739,147 @@ void eval_row(const Problem& p, const double* x, double* f, double* g) {
         case FAM_WTA: eval_wta(p.w, x, p.d, f, g); break;
         case FAM_MW: eval_mw(p.id, x, p.d, p.m, f, g); break;
         case FAM_DAS: eval_das(p.id, x, p.d, f, g); break;
+    }
+}
+
+// --- restated reference-front candidates for MW / DAS-CMOP (no reference
+// counterpart: the reference's front_candidates exist only for its own
+// suites, problems.cpp:203-393).  Every MW / DAS-CMOP objective vector is a
+// function of the position genes x_0 .. x_{m-2} and one distance value (MW:
+// the distance sum gs, DAS-CMOP: g), nondecreasing in that distance for a fixed
+// position, so a position's best feasible point is at its smallest feasible
+// distance.  That distance is located on kLevels steps of [0, kLevelMax],
+// refined by bisection, nudged 1e-9 into the feasible side and realised in
+// decision space (equal per-gene shares); pf_reference (fronts.cpp:54-79)
+// then evaluates, filters and subsamples the rows as for any problem.
+constexpr int kLevels = 600;
+constexpr double kLevelMax = 3.0;
+
+bool restated_front(const Problem& p) { return p.fam == FAM_MW || p.fam == FAM_DAS; }
+
+void eval_level(const Problem& p, const double* pos, double lvl, double* f, double* g) {
+    if (p.fam == FAM_MW)
+        eval_mw_level(p.id, pos, p.d, p.m, lvl, f, g);
+    else
+        eval_das_level(p.id, pos, lvl, f, g);
+}
+
+bool level_feasible(const Problem& p, const double* pos, double lvl) {
+    double f[3], g[16];
+    eval_level(p, pos, lvl, f, g);
+    for (int k = 0; k < p.nin + p.neq; ++k)
+        if (!(g[k] <= 0.0)) return false;
+    return true;
+}
+
+// smallest feasible distance at this position; -1 when none on the grid
+double min_feasible_level(const Problem& p, const double* pos) {
+    for (int k = 0; k <= kLevels; ++k) {
+        const double lvl = kLevelMax * k / kLevels;
+        if (!level_feasible(p, pos, lvl)) continue;
+        if (k == 0) return 0.0;
+        double lo = kLevelMax * (k - 1) / kLevels, hi = lvl;
+        for (int it = 0; it < 60; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (level_feasible(p, pos, mid))
+                hi = mid;
+            else
+                lo = mid;
+        }
+        return hi * (1.0 + 1e-9);
+    }
+    return -1.0;
+}
+
+// bisection for the increasing per-gene term t(v) = tau on [a, b]
+template <class T>
+double solve_term(T t, double tau, double a, double b) {
+    if (tau <= 0.0) return a;
+    if (t(b) <= tau) return b;
+    for (int it = 0; it < 80; ++it) {
+        const double mid = 0.5 * (a + b);
+        if (t(mid) < tau)
+            a = mid;
+        else
+            b = mid;
+    }
+    return 0.5 * (a + b);
+}
+
+// decision row at position pos whose distance value is lvl
+void realize_level(const Problem& p, const double* pos, double lvl, double* x) {
+    const int n = p.d, m = p.m, nd = n - m + 1;
+    for (int k = 0; k + 1 < m; ++k) x[k] = pos[k];
+    const double tau = std::max(lvl, 0.0) / nd;
+    if (p.fam == FAM_DAS) {
+        const bool rast = p.id == 4 || p.id == 5 || p.id == 6 || p.id == 9;
+        const double shift = m == 2 ? std::sin(0.5 * kPi * pos[0]) : 0.5;
+        const double y = rast ? solve_term([](double v) { return v * v + 1.0 - std::cos(20.0 * kPi * v); }, tau,
+                                           0.0, 0.05)
+                              : std::sqrt(tau);
+        for (int j = m - 1; j < n; ++j) x[j] = shift + y <= 1.0 ? shift + y : shift - y;
+        return;
+    }
+    const double lo = p.lo[0], hi = p.hi[0];
+    switch (mw_kind(p.id)) {
+        case 0: {  // 1 - exp(-10 t^2), t = x^(n-m) - c_j
+            const double e = static_cast<double>(n - m);
+            const double t = std::sqrt(-std::log(1.0 - std::min(tau, 0.999)) / 10.0);
+            for (int j = m - 1; j < n; ++j) {
+                const double c = 0.5 + static_cast<double>(j) / (2.0 * n);
+                const double v = c - t >= 0.0 ? c - t : c + t;
+                x[j] = std::min(std::pow(v, 1.0 / e), hi);
+            }
+            return;
+        }
+        case 1: {  // 1.5 + (0.1/n) z^2 - 1.5 cos(2 pi z), z = 1 - exp(-10 t^2), t = x - j/n
+            const double z = solve_term(
+                [n](double v) { return 1.5 + (0.1 / n) * v * v - 1.5 * std::cos(2.0 * kPi * v); }, tau, 0.0, 0.5);
+            const double t = std::sqrt(-std::log(1.0 - z) / 10.0);
+            for (int j = m - 1; j < n; ++j) {
+                const double b = static_cast<double>(j) / n;
+                x[j] = b + t <= hi ? b + t : b - t;
+            }
+            return;
+        }
+        default: {  // 2 t^2, t = x_j + (x_{j-1} - 0.5)^2 - 1
+            const double u = std::sqrt(tau / 2.0);
+            for (int j = m - 1; j < n; ++j) {
+                const double q = x[j - 1] - 0.5;
+                const double v = 1.0 - q * q - u;
+                x[j] = v >= lo ? v : std::min(1.0 - q * q + u, hi);
+            }
+            return;
+        }
+    }
+}
+
+// front_candidates(n_samples): m = 2 positions x_0 on n_samples even steps of
+// the first gene's range; m = 3 a side x side grid (side^2 >= n_samples)
+int64_t restated_front_rows(const Problem& p, int64_t n_samples) {
+    if (p.m == 2) return n_samples;
+    int64_t side = 1;
+    while (side * side < n_samples) ++side;
+    return side * side;
+}
+
+void restated_front_candidates(const Problem& p, int64_t n_samples, double* out) {
+    const int64_t rows = restated_front_rows(p, n_samples);
+    int64_t side = 1;
+    while (side * side < n_samples) ++side;
+    for (int64_t r = 0; r < rows; ++r) {
+        double pos[2] = {0.0, 0.0};
+        if (p.m == 2) {
+            const double t = n_samples == 1 ? 0.0 : static_cast<double>(r) / static_cast<double>(n_samples - 1);
+            pos[0] = p.lo[0] + (p.hi[0] - p.lo[0]) * t;
+        } else {
+            const double s1 = side == 1 ? 0.0 : static_cast<double>(r / side) / static_cast<double>(side - 1);
+            const double s2 = side == 1 ? 0.0 : static_cast<double>(r % side) / static_cast<double>(side - 1);
+            pos[0] = p.lo[0] + (p.hi[0] - p.lo[0]) * s1;
+            pos[1] = p.lo[1] + (p.hi[1] - p.lo[1]) * s2;
+        }
+        const double lvl = min_feasible_level(p, pos);
+        realize_level(p, pos, lvl < 0.0 ? 0.0 : lvl, out + r * p.d);
     }
 }
 
@@ -1283,6 +1454,30 @@ void* orc_problem_new(const char* name) {
     }
 }
 void orc_problem_free(void* h) { delete static_cast<Problem*>(h); }
+// restated front candidates by name (MW / DAS-CMOP): rows, or -1
+int64_t orc_front_candidates(const char* name, int64_t n_samples, double* out, int64_t cap) {
+    try {
+        Problem p = make_problem(name);
+        if (!restated_front(p)) throw std::invalid_argument("no restated front for " + p.name);
+        const int64_t rows = restated_front_rows(p, n_samples);
+        if (out) {
+            if (rows * p.d > cap) throw std::invalid_argument("front_candidates: cap too small");
+            restated_front_candidates(p, n_samples, out);
+        }
+        return rows;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+int64_t orc_problem_front_rows(const void* h, int64_t n_samples) {
+    const Problem& p = *static_cast<const Problem*>(h);
+    return restated_front(p) ? restated_front_rows(p, n_samples) : -1;
+}
+void orc_problem_front_candidates(const void* h, int64_t n_samples, double* out) {
+    restated_front_candidates(*static_cast<const Problem*>(h), n_samples, out);
+}
 void orc_problem_eval_row(const void* h, const double* x, double* f, double* g) {
     eval_row(*static_cast<const Problem*>(h), x, f, g);
 }

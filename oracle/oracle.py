@@ -88,6 +88,18 @@ class Oracle(_Lib):
         return dict(d=d.value, m=m.value, n_ineq=nin.value, n_eq=neq.value,
                     lo=lo[:d.value].copy(), hi=hi[:d.value].copy())
 
+    def front_candidates(self, name, n_samples):
+        """Restated MW / DAS-CMOP front candidates (decision rows)."""
+        f = self.lib.orc_front_candidates
+        f.restype = C.c_int64
+        rows = f(name.encode(), C.c_int64(n_samples), None, C.c_int64(0))
+        if rows < 0:
+            raise OracleError(self.lib.orc_last_error().decode())
+        d = self.problem_info(name)["d"]
+        out = np.zeros((rows, d))
+        f(name.encode(), C.c_int64(n_samples), _ptr(out, _dp), C.c_int64(out.size))
+        return out
+
     def evaluate(self, name, X):
         info = self.problem_info(name)
         X = _f64(X)
@@ -358,7 +370,7 @@ class Reference(_Lib):
         cap = max(npoints, 1) * 4 + 100000
         out = np.zeros((cap, 3))
         rows = C.c_int64()
-        m = self.problem_info(name)["m"]
+        m = self._info_any(name)["m"]
         out = np.zeros((cap, m))
         self._check(self.lib.ref_pf_reference(name.encode(), C.c_int64(npoints), _ptr(out, _dp),
                                               C.c_int64(cap), C.byref(rows)))

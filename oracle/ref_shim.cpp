@@ -37,6 +37,8 @@ extern "C" {
 void* orc_problem_new(const char* name);
 void orc_problem_free(void* h);
 void orc_problem_eval_row(const void* h, const double* x, double* f, double* g);
+int64_t orc_problem_front_rows(const void* h, int64_t n_samples);
+void orc_problem_front_candidates(const void* h, int64_t n_samples, double* out);
 int orc_problem_info(const char* name, int32_t* d, int32_t* m, int32_t* nin, int32_t* neq,
                      double* lo, double* hi);
 }
@@ -117,6 +119,13 @@ ProblemDef problem_for(const std::string& name) {
     std::shared_ptr<void> h(orc_problem_new(name.c_str()), orc_problem_free);
     p.eval_row = [h](std::span<const double> x, std::span<double> f, std::span<double> g) {
         orc_problem_eval_row(h.get(), x.data(), f.data(), g.data());
+    };
+    // the oracle's restated front candidates (no reference counterpart)
+    p.front_candidates = [h, d](std::size_t n_samples) {
+        const int64_t rows = orc_problem_front_rows(h.get(), static_cast<int64_t>(n_samples));
+        Matrix M(static_cast<std::size_t>(rows), static_cast<std::size_t>(d));
+        orc_problem_front_candidates(h.get(), static_cast<int64_t>(n_samples), M.data.data());
+        return M;
     };
     return p;
 }
@@ -267,7 +276,7 @@ int ref_metric_front(const double* F, const double* cv, int64_t n, int32_t m, do
 
 int ref_pf_reference(const char* name, int64_t npoints, double* out, int64_t cap, int64_t* rows) {
     return guarded([&] {
-        ProblemDef p = make_problem(name);
+        ProblemDef p = problem_for(name);
         Matrix fr = pf_reference(p, npoints);
         if (static_cast<int64_t>(fr.rows) > cap) throw std::invalid_argument("pf_reference: cap too small");
         put(fr, out);

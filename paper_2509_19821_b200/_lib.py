@@ -347,8 +347,10 @@ def hypervolume(points, ref_point) -> float:
 
 def pf_reference(problem: "Problem", n_points: int = 1000) -> np.ndarray:
     """pf_reference (fronts.cpp:54-84): the analytic Pareto front sampled to
-    n_points rows, built and evaluated in fp64 on the device.  RuntimeError
-    for problems without an analytic front (MW, WTA), as the reference."""
+    n_points rows, built and evaluated in fp64 on the device.  MW and
+    DAS-CMOP (restated suites) get restated front candidates: each position's
+    smallest feasible distance, found by a level scan and bisection.
+    RuntimeError for WTA (no analytic front), as the reference."""
     cap = max(int(n_points), 1)
     out = np.zeros((cap, problem.m))
     rows = C.c_int64()

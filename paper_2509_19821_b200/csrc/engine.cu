@@ -1642,6 +1642,8 @@ int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, in
                 pp.rnum = 1.0;
                 pp.rden = 0.0;
             }
+        } else if (p->fam == FAM_MW || p->fam == FAM_DAS) {
+            pp.kind = PF_LEVEL;  // restated fronts (no reference counterpart)
         } else {
             throw std::runtime_error("pf_reference: no analytic front for " + p->name +
                                      "; use the hypervolume metric instead");
@@ -1660,8 +1662,13 @@ int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, in
         };
         for (int attempt = 0; attempt < 4; ++attempt) {
             pp.n_samples = over;
-            if (pp.kind == PF_LIR && p->id <= 12) {
+            if ((pp.kind == PF_LIR && p->id <= 12) || (pp.kind == PF_LEVEL && m == 2)) {
                 pp.rows = over;
+            } else if (pp.kind == PF_LEVEL) {
+                long long side = 1;
+                while (side * side < over) ++side;
+                pp.h = side;
+                pp.rows = side * side;
             } else {
                 long long h = 1;
                 while ((h + 1) * (h + 2) / 2 < over) ++h;  // simplex_weights (problems.cpp:205-218)

@@ -18,13 +18,13 @@ namespace gmpea_b200 {
 constexpr int kPfMaxD = 64;
 constexpr double kPfPi = 3.141592653589793;
 
-enum : int { PF_LIR = 1, PF_DTLZ1 = 2, PF_SPHERE = 3 };
+enum : int { PF_LIR = 1, PF_DTLZ1 = 2, PF_SPHERE = 3, PF_LEVEL = 4 };
 
 struct PfParams {
     ProbDev P;
     int kind;             // PF_*
     long long n_samples;  // requested candidates (front_candidates(n))
-    long long h;          // simplex_weights grid: (h + 1)(h + 2) / 2 rows
+    long long h;          // simplex_weights grid: (h + 1)(h + 2) / 2 rows; PF_LEVEL m = 3: grid side
     long long rows;       // candidate rows generated
     double alpha, rnum, rden;  // sphere_front_rows parameters
     double* F;            // rows x m
@@ -149,6 +149,116 @@ __device__ void lir_front_row(const ProbDev& P, int id, int d, long long r, long
     // (the simplex row is supplied by the caller through x[0..2])
 }
 
+// ---- restated fronts of MW / DAS-CMOP (no reference counterpart; mirrors
+// oracle/gmpea_oracle.cpp restated_front_candidates).  The objectives depend on
+// the position genes and one distance value and are nondecreasing in it, so a
+// position's front point is at its smallest feasible distance: located on
+// kPfLevels steps of [0, kPfLevelMax], bisected, nudged 1e-9 into the
+// feasible side and realised in decision space with equal per-gene shares.
+constexpr int kPfLevels = 600;
+constexpr double kPfLevelMax = 3.0;
+
+template <class Ev>
+__device__ bool pf_level_feasible(const ProbDev& P, const double* pos, double lvl) {
+    Ev ev;
+    ev.set_level(P, pos, lvl);
+    double f[kMaxM];
+    bool ok = true;
+    ev.finish(P, f, [&](int, double g) { ok = ok && g <= 0.0; });
+    return ok;
+}
+
+template <class Ev>
+__device__ double pf_min_level(const ProbDev& P, const double* pos) {
+    for (int k = 0; k <= kPfLevels; ++k) {
+        const double lvl = kPfLevelMax * k / kPfLevels;
+        if (!pf_level_feasible<Ev>(P, pos, lvl)) continue;
+        if (k == 0) return 0.0;
+        double lo = kPfLevelMax * (k - 1) / kPfLevels, hi = lvl;
+        for (int it = 0; it < 60; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (pf_level_feasible<Ev>(P, pos, mid))
+                hi = mid;
+            else
+                lo = mid;
+        }
+        return hi * (1.0 + 1e-9);
+    }
+    return -1.0;
+}
+
+template <class T>
+__device__ double pf_solve_term(T t, double tau, double a, double b) {
+    if (tau <= 0.0) return a;
+    if (t(b) <= tau) return b;
+    for (int it = 0; it < 80; ++it) {
+        const double mid = 0.5 * (a + b);
+        if (t(mid) < tau)
+            a = mid;
+        else
+            b = mid;
+    }
+    return 0.5 * (a + b);
+}
+
+__device__ void pf_realize_level(const ProbDev& P, const double* pos, double lvl, double* x) {
+    const int n = P.d, m = P.m, nd = n - m + 1;
+    for (int k = 0; k + 1 < m; ++k) x[k] = pos[k];
+    const double tau = fmax(lvl, 0.0) / nd;
+    if (P.fam == FAM_DAS) {
+        const bool rast = P.id == 4 || P.id == 5 || P.id == 6 || P.id == 9;
+        const double shift = m == 2 ? sin(0.5 * kPfPi * pos[0]) : 0.5;
+        const double y = rast ? pf_solve_term([](double v) { return v * v + 1.0 - cos(20.0 * kPfPi * v); }, tau,
+                                              0.0, 0.05)
+                              : sqrt(tau);
+        for (int j = m - 1; j < n; ++j) x[j] = shift + y <= 1.0 ? shift + y : shift - y;
+        return;
+    }
+    const double lo = P.lob(0), hi = P.hib(0);
+    const int kd = EvalMw::kind(P.id);
+    if (kd == 0) {
+        const double e = (double)(n - m);
+        const double t = sqrt(-log(1.0 - fmin(tau, 0.999)) / 10.0);
+        for (int j = m - 1; j < n; ++j) {
+            const double c = 0.5 + (double)j / (2.0 * n);
+            const double v = c - t >= 0.0 ? c - t : c + t;
+            x[j] = fmin(pow(v, 1.0 / e), hi);
+        }
+    } else if (kd == 1) {
+        const double z = pf_solve_term(
+            [n](double v) { return 1.5 + (0.1 / n) * v * v - 1.5 * cos(2.0 * kPfPi * v); }, tau, 0.0, 0.5);
+        const double t = sqrt(-log(1.0 - z) / 10.0);
+        for (int j = m - 1; j < n; ++j) {
+            const double b = (double)j / n;
+            x[j] = b + t <= hi ? b + t : b - t;
+        }
+    } else {
+        const double u = sqrt(tau / 2.0);
+        for (int j = m - 1; j < n; ++j) {
+            const double q = x[j - 1] - 0.5;
+            const double v = 1.0 - q * q - u;
+            x[j] = v >= lo ? v : fmin(1.0 - q * q + u, hi);
+        }
+    }
+}
+
+__device__ void pf_level_row(const PfParams& p, long long r, double* x) {
+    const ProbDev& P = p.P;
+    double pos[2] = {0.0, 0.0};
+    if (P.m == 2) {
+        const double t = p.n_samples == 1 ? 0.0 : (double)r / (double)(p.n_samples - 1);
+        pos[0] = (double)P.lob(0) + ((double)P.hib(0) - (double)P.lob(0)) * t;
+    } else {
+        const long long side = p.h;
+        const double s1 = side == 1 ? 0.0 : (double)(r / side) / (double)(side - 1);
+        const double s2 = side == 1 ? 0.0 : (double)(r % side) / (double)(side - 1);
+        pos[0] = (double)P.lob(0) + ((double)P.hib(0) - (double)P.lob(0)) * s1;
+        pos[1] = (double)P.lob(1) + ((double)P.hib(1) - (double)P.lob(1)) * s2;
+    }
+    const double lvl = P.fam == FAM_MW ? pf_min_level<EvalMw>(P, pos) : pf_min_level<EvalDas>(P, pos);
+    pf_realize_level(P, pos, lvl < 0.0 ? 0.0 : lvl, x);
+}
+
 __global__ void pf_candidates_kernel(PfParams p) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= p.rows) return;
@@ -158,6 +268,8 @@ __global__ void pf_candidates_kernel(PfParams p) {
     for (int j = 0; j < d; ++j) x[j] = 0.5;
     if (p.kind == PF_LIR && P.id <= 12) {
         lir_front_row(P, P.id, d, r, p.n_samples, x);
+    } else if (p.kind == PF_LEVEL) {
+        pf_level_row(p, r, x);
     } else {
         double w[3];
         simplex_row(r, p.h, w);
@@ -210,6 +322,16 @@ __global__ void pf_candidates_kernel(PfParams p) {
     em.cv.init(P.nin);
     if (P.fam == FAM_LIR) {
         EvalLir ev;
+        ev.begin(P);
+        for (int j = 0; j < d; ++j) ev.gene(P, j, x[j]);
+        ev.finish(P, f, em);
+    } else if (P.fam == FAM_MW) {
+        EvalMw ev;
+        ev.begin(P);
+        for (int j = 0; j < d; ++j) ev.gene(P, j, x[j]);
+        ev.finish(P, f, em);
+    } else if (P.fam == FAM_DAS) {
+        EvalDas ev;
         ev.begin(P);
         for (int j = 0; j < d; ++j) ev.gene(P, j, x[j]);
         ev.finish(P, f, em);

@@ -853,55 +853,65 @@ __device__ __forceinline__ void unpack_claims(const uint2 w, const int j, const 
     cc[3] = left > 3 ? j + ((int)w.y >> 16) : -1;
 }
 
-template <int POP, bool PACK = false>
+template <int POP, bool PACK = false, int NBP = 4>
 __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
-    const float4 par = p.Fcv[POP][j];
+    // claimants per batch: 4 (R), NBP (4 or 8) from the packed Rp
+    constexpr int NB = PACK ? NBP : 4;
+    constexpr int NW = NB / 4;
+    // only the parent's cv and PBI stay live (the full keys are re-read at the
+    // end), which keeps select at 48 registers (5 blocks of 256 per SM)
+    const float4 par4 = p.Fcv[POP][j];
     const float4 u4 = p.U[j];
-    const float gp = pbi(par, u4, z, p.theta);
+    const float gp = pbi(par4, u4, z, p.theta);
+    const float pw = par4.w;
     const int deg = p.Rdeg[POP][j];
     const int* __restrict__ R = p.R[POP];
     const uint2* __restrict__ Rp = p.Rp[POP] + j;
     const float4* __restrict__ eff = p.eff[POP];
     bool have = false;
-    float4 best = par;
+    float bw = pw;
     float bg = 0.0f;
     int bc = -1;
     int mex = 0;
     bool mex_open = true;
     bool negcv = false;
-    // batches of four claimants; the next batch's indices are loaded while
+    // batches of NB claimants; the next batch's indices are loaded while
     // this batch's keys are gathered (one memory round trip per batch)
-    int cc[4];
-    uint2 wn = make_uint2(0u, 0u);
+    int cc[NB];
+    uint2 wn[NW];
     if (PACK) {
-        if (deg > 0) wn = Rp[0];
-        unpack_claims(wn, j, deg, cc);
+#pragma unroll
+        for (int h = 0; h < NW; ++h) wn[h] = 4 * h < deg ? Rp[(long long)h * p.ldr] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int h = 0; h < NW; ++h) unpack_claims(wn[h], j, deg - 4 * h, cc + 4 * h);
     } else {
 #pragma unroll
         for (int u = 0; u < 4; ++u) cc[u] = u < deg ? R[(long long)u * p.ldr + j] : -1;
     }
-    for (int k0 = 0; k0 < deg; k0 += 4) {
-        float4 ee[4];
+    for (int k0 = 0; k0 < deg; k0 += NB) {
+        float4 ee[NB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < NB; ++u)
             if (cc[u] >= 0) ee[u] = eff[cc[u]];
         int cn[4];
         if (PACK) {
-            if (k0 + 4 < deg) wn = Rp[(long long)(k0 / 4 + 1) * p.ldr];
+#pragma unroll
+            for (int h = 0; h < NW; ++h)
+                if (k0 + NB + 4 * h < deg) wn[h] = Rp[(long long)((k0 + NB) / 4 + h) * p.ldr];
         } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u) cn[u] = k0 + 4 + u < deg ? R[(long long)(k0 + 4 + u) * p.ldr + j] : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < NB; ++u) {
             const int c = cc[u];
             if (c < 0) continue;
             const float4 e = ee[u];
             const float g = pbi(e, u4, z, p.theta);
             bool mark;
             if (POP == 0) {  // fpr_better (scalarize.cpp:91-96)
-                negcv |= (e.w < 0.0f) || (par.w < 0.0f);
-                mark = (e.w == par.w) ? (g < gp) : (e.w < par.w);
+                negcv |= (e.w < 0.0f) || (pw < 0.0f);
+                mark = (e.w == pw) ? (g < gp) : (e.w < pw);
             } else {
                 mark = g < gp;
             }
@@ -917,18 +927,19 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
             if (!have)
                 better = true;
             else if (POP == 0)
-                better = e.w < best.w || (e.w == best.w && (g < bg || (g == bg && c < bc)));
+                better = e.w < bw || (e.w == bw && (g < bg || (g == bg && c < bc)));
             else
                 better = g < bg || (g == bg && c < bc);
             if (better) {
                 have = true;
-                best = e;
+                bw = e.w;
                 bg = g;
                 bc = c;
             }
         }
         if (PACK) {
-            unpack_claims(wn, j, deg - k0 - 4, cc);
+#pragma unroll
+            for (int h = 0; h < NW; ++h) unpack_claims(wn[h], j, deg - k0 - NB - 4 * h, cc + 4 * h);
         } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u) cc[u] = cn[u];
@@ -942,7 +953,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     bool off_wins = false;
     if (have) {
         if (POP == 0)
-            off_wins = best.w < par.w || (best.w == par.w && (bg < gp || (bg == gp && bc < mex)));
+            off_wins = bw < pw || (bw == pw && (bg < gp || (bg == gp && bc < mex)));
         else
             off_wins = bg < gp || (bg == gp && bc < mex);
     }
@@ -953,24 +964,24 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
         code = from2 ? p.n + bc : bc;
     }
     if (p.winner[POP]) p.winner[POP][j] = code;
-    feas = (off_wins ? best.w : par.w) == 0.0f;
+    feas = (off_wins ? bw : pw) == 0.0f;
     if (!off_wins || !p.apply) return off_wins;
     const int src = code >= p.n ? 1 : 0;
     float4* dst = p.X[POP] + (long long)j * p.rs4;
     if (p.ustamp[POP]) {
         copy_row(p.uX[POP] + (long long)j * p.rs4, dst, p.rs4);
-        p.uFcv[POP][j] = par;
+        p.uFcv[POP][j] = p.Fcv[POP][j];
         p.ustamp[POP][j] = p.st->gen;
     }
     copy_row(dst, p.oX[src] + (long long)bc * p.rs4, p.rs4);  // copy_row, gmpea.cpp:372-377
-    p.Fcv[POP][j] = best;
+    p.Fcv[POP][j] = eff[bc];
     return true;
 }
 
 #ifndef GMPEA_SELECT_MINBLOCKS
-#define GMPEA_SELECT_MINBLOCKS 4
+#define GMPEA_SELECT_MINBLOCKS 5
 #endif
-template <bool PACK = false>
+template <bool PACK = false, int NBP = 4>
 __device__ __forceinline__ void select_body(const SelParams& p, const int bx, const int by) {
     if (p.st->stop) return;
     const int j = p.row0 + bx * blockDim.x + threadIdx.x;
@@ -978,9 +989,9 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
     bool feas = false, off_taken = false;
     if (j < p.row_end) {
         if (by == 0)
-            off_taken = select_slot<0, PACK>(p, j, z, feas);
+            off_taken = select_slot<0, PACK, NBP>(p, j, z, feas);
         else
-            off_taken = select_slot<1, PACK>(p, j, z, feas);
+            off_taken = select_slot<1, PACK, NBP>(p, j, z, feas);
     }
     if (p.rec == nullptr) return;
     // feasible_ratio of pop1 (gmpea.cpp:411-417) and the replacement count
@@ -1020,9 +1031,9 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     st->t_gen_start = globaltimer();
 }
 
-template <bool PACK = false>
+template <bool PACK = false, int NBP = 4>
 __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
-    select_body<PACK>(p, blockIdx.x, blockIdx.y);
+    select_body<PACK, NBP>(p, blockIdx.x, blockIdx.y);
     if (p.done == nullptr) return;
     __syncthreads();
     if (threadIdx.x == 0) {

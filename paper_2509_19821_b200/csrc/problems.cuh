@@ -338,9 +338,11 @@ struct EvalMw {
     double prev;
     double gs;
     int kd;
+    bool ref;  // fp64 front candidates: reference-rounded trigonometry (trig_sin)
     __device__ __forceinline__ void begin(const ProbDev& P) {
         gs = 0.0;
         kd = kind(P.id);
+        ref = false;
     }
     __device__ __forceinline__ static int kind(int id) {
         // 0: exp distance (MW1/4/5/9/12), 1: cos distance (2/6/8/10/13), 2: linear (3/7/11/14)
@@ -350,9 +352,21 @@ struct EvalMw {
             default: return 2;
         }
     }
-    __device__ __forceinline__ void gene(const ProbDev& P, int j, float xf) {
+    // front candidates (pf_reference): the distance value itself
+    __device__ __forceinline__ void set_level(const ProbDev& P, const double* pos, double lvl) {
+        xs[0] = pos[0];
+        xs[1] = pos[1];
+        gs = lvl;
+        kd = kind(P.id);
+        ref = true;
+    }
+    // T = float: generation rows (fp32 per-gene terms); T = double: front
+    // candidates, evaluated fully in fp64
+    template <class T>
+    __device__ __forceinline__ void gene(const ProbDev& P, int j, T xf) {
         const double x = xf;
         const int n = P.d, m = P.m;
+        ref = std::is_same<T, double>::value;
         if (j < m - 1) {  // static indices keep xs[] in registers
             if (j == 0)
                 xs[0] = x;
@@ -364,6 +378,22 @@ struct EvalMw {
         // per-gene terms: argument in fp64, the exponential / cosine in fp32
         // (each term < 1e-7 off; the sum accumulates in fp64)
         // (MUFU exp2 for the exponential: argument in [-25, 0], ~2 ulp)
+        if (std::is_same<T, double>::value) {  // oracle form (mw_g_exp / _cos / _lin)
+            if (kd == 0) {
+                double t = pow(x, (double)(n - m)) - 0.5 - (double)j / (2.0 * n);
+                gs += 1.0 - exp(-10.0 * t * t);
+            } else if (kd == 1) {
+                double t = x - (double)j / n;
+                double z = 1.0 - exp(-10.0 * t * t);
+                gs += 1.5 + (0.1 / n) * z * z - 1.5 * trig_cos(true, 2.0, z);
+            } else {
+                double q = prev - 0.5;
+                double t = x + q * q - 1.0;
+                gs += 2.0 * t * t;
+            }
+            prev = x;
+            return;
+        }
         if (kd == 0) {
             const int e = n - m;  // 13 or 12 for the registered D = 15
             const double x2 = x * x, x4 = x2 * x2, x8 = x4 * x4;
@@ -391,7 +421,7 @@ struct EvalMw {
                 f[0] = xs[0];
                 f[1] = id == 1 ? g * (1.0 - 0.85 * f[0] / g) : g * (1.0 - f[0] / g);
                 double l = r2 * f[1] - r2 * f[0];
-                emit(0, f[0] + f[1] - 1.0 - 0.5 * ipow(sinpi((id == 1 ? 2.0 : 3.0) * l), 8));
+                emit(0, f[0] + f[1] - 1.0 - 0.5 * ipow(trig_sin(ref, id == 1 ? 2.0 : 3.0, l), 8));
                 return;
             }
             case 3: {
@@ -400,7 +430,7 @@ struct EvalMw {
                 f[1] = g * (1.0 - f[0] / g);
                 double l = r2 * f[1] - r2 * f[0];
                 double s = f[0] + f[1];
-                double sn = sinpi(0.75 * l);
+                double sn = trig_sin(ref, 0.75, l);
                 emit(0, s - 1.05 - 0.45 * ipow(sn, 6));
                 emit(1, 0.85 - s + 0.3 * sn * sn);
                 return;
@@ -415,7 +445,12 @@ struct EvalMw {
                         c[i] = xs[i];
                         s[i] = 1.0 - xs[i];
                     } else {
-                        sincospi(0.5 * xs[i], &s[i], &c[i]);
+                        if (ref) {
+                            s[i] = trig_sin(true, 0.5, xs[i]);
+                            c[i] = trig_cos(true, 0.5, xs[i]);
+                        } else {
+                            sincospi(0.5 * xs[i], &s[i], &c[i]);
+                        }
                     }
                 }
                 f[0] = (1.0 + g) * c[0] * c[1];
@@ -424,7 +459,7 @@ struct EvalMw {
                 if (id == 4) {
                     double l = f[2] - f[0] - f[1];
                     double sum = f[0] + f[1] + f[2];
-                    emit(0, sum - (1.0 + 0.4 * ipow(sinpi(2.5 * l), 8)));
+                    emit(0, sum - (1.0 + 0.4 * ipow(trig_sin(ref, 2.5, l), 8)));
                 } else {
                     double q = f[0] * f[0] + f[1] * f[1] + f[2] * f[2];
                     double l = asin(f[2] / sqrt(q));
@@ -481,8 +516,10 @@ struct EvalMw {
                 double s = f[0] * f[0];
                 double t1 = (1.0 - 0.64 * s - f[1]) * (1.0 - 0.36 * s - f[1]);
                 double a = f[0] + 0.35, b = f[0] + 0.15;
-                double t2 = 1.35 * 1.35 - a * a - f[1];
-                double t3 = 1.15 * 1.15 - b * b - f[1];
+                // uncontracted (the reference is built -ffp-contract=off): t2 is
+                // exactly 0 on the front's end point x1 = 1, g = 1
+                double t2 = __dsub_rn(__dsub_rn(__dmul_rn(1.35, 1.35), __dmul_rn(a, a)), f[1]);
+                double t3 = __dsub_rn(__dsub_rn(__dmul_rn(1.15, 1.15), __dmul_rn(b, b)), f[1]);
                 emit(0, fmin(t1, t2 * t3));
                 return;
             }
@@ -513,11 +550,11 @@ struct EvalMw {
                 double g = 1.0 + gs;
                 f[0] = g * xs[0];
                 double r = f[0] / g;
-                f[1] = g * (0.85 - 0.8 * r - 0.08 * fabs(sinpi(3.2 * r)));
-                double a = 1.0 - 0.8 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] - f[0] / 1.5));
-                double b = 1.8 - 1.125 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] / 1.8 - f[0] / 1.6));
-                double c = 1.0 - 0.625 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] - f[0] / 1.6));
-                double e = 1.4 - 0.875 * f[0] - f[1] + 0.08 * sinpi(2.0 * (f[1] / 1.4 - f[0] / 1.6));
+                f[1] = g * (0.85 - 0.8 * r - 0.08 * fabs(trig_sin(ref, 3.2, r)));
+                double a = 1.0 - 0.8 * f[0] - f[1] + 0.08 * trig_sin(ref, 2.0, (f[1] - f[0] / 1.5));
+                double b = 1.8 - 1.125 * f[0] - f[1] + 0.08 * trig_sin(ref, 2.0, (f[1] / 1.8 - f[0] / 1.6));
+                double c = 1.0 - 0.625 * f[0] - f[1] + 0.08 * trig_sin(ref, 2.0, (f[1] - f[0] / 1.6));
+                double e = 1.4 - 0.875 * f[0] - f[1] + 0.08 * trig_sin(ref, 2.0, (f[1] / 1.4 - f[0] / 1.6));
                 emit(0, a * b);
                 emit(1, -(c * e));
                 return;
@@ -526,8 +563,8 @@ struct EvalMw {
                 double g = 1.0 + gs;
                 f[0] = g * xs[0] * 1.5;
                 double r = f[0] / g;
-                f[1] = g * (5.0 - exp(r) - fabs(0.5 * sinpi(3.0 * r)));
-                double s3 = 0.5 * sinpi(3.0 * f[0]);
+                f[1] = g * (5.0 - exp(r) - fabs(0.5 * trig_sin(ref, 3.0, r)));
+                double s3 = 0.5 * trig_sin(ref, 3.0, f[0]);
                 double a = 5.0 - exp(f[0]) - s3 - f[1];
                 double b = 5.0 - (1.0 + 0.4 * f[0]) - s3 - f[1];
                 double c = 5.0 - (1.0 + f[0] + 0.5 * f[0] * f[0]) - s3 - f[1];
@@ -543,7 +580,7 @@ struct EvalMw {
                 for (int k = 0; k < 2; ++k) {
                     f[k] = xs[k];
                     double q = f[k] * f[k];
-                    double sn = sinpi(1.1 * q);
+                    double sn = trig_sin(ref, 1.1, q);
                     s += 6.0 - exp(f[k]) - 1.5 * sn;
                     sa += 6.1 - (1.0 + f[k] + 0.5 * q + 1.5 * sn);
                 }
@@ -582,25 +619,36 @@ struct EvalDas {
     double sh;  // sin(0.5 pi x1): the position shift of DAS1-6's distance genes
     double gs;
     bool rast;
+    bool ref;  // fp64 front candidates: reference-rounded trigonometry (trig_sin)
     __device__ __forceinline__ void begin(const ProbDev& P) {
         gs = 0.0;
         sh = 0.5;
         rast = P.id == 4 || P.id == 5 || P.id == 6 || P.id == 9;
+        ref = false;
+    }
+    // front candidates (pf_reference): g itself
+    __device__ __forceinline__ void set_level(const ProbDev& P, const double* pos, double lvl) {
+        begin(P);
+        xs[0] = pos[0];
+        xs[1] = pos[1];
+        gs = rast ? lvl - (double)(P.d - P.m + 1) : lvl;
+        ref = true;
     }
     template <class T>
     __device__ __forceinline__ void gene(const ProbDev& P, int j, T xf) {
         const double x = xf;
+        ref = std::is_same<T, double>::value;
         if (j < P.m - 1) {
             if (j == 0) {
                 xs[0] = x;
-                if (P.m == 2) sh = sinpi(0.5 * x);
+                if (P.m == 2) sh = trig_sin(ref, 0.5, x);
             } else {
                 xs[1] = x;
             }
             return;
         }
         const double y = x - sh;
-        gs += rast ? y * y - cospi(20.0 * y) : y * y;
+        gs += rast ? y * y - trig_cos(ref, 20.0, y) : y * y;
     }
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
@@ -608,11 +656,11 @@ struct EvalDas {
         const int id = P.id;
         const double g = rast ? (double)(P.d - P.m + 1) + gs : gs;
         const double x1 = xs[0];
-        emit(0, K::b - sinpi(K::a * x1));
+        emit(0, K::b - trig_sin(ref, K::a, x1));
         if (id <= 6) {
             f[0] = x1 + g;
             const int shape = (id - 1) % 3;  // 0: 1 - x^2, 1: 1 - sqrt x, 2: + 0.5|sin 5 pi x|
-            f[1] = (shape == 0 ? 1.0 - x1 * x1 : 1.0 - sqrt(x1)) + (shape == 2 ? 0.5 * fabs(sinpi(5.0 * x1)) : 0.0) + g;
+            f[1] = (shape == 0 ? 1.0 - x1 * x1 : 1.0 - sqrt(x1)) + (shape == 2 ? 0.5 * fabs(trig_sin(ref, 5.0, x1)) : 0.0) + g;
             emit(1, -((K::e - g) * (g - K::d)));
             const double c = 0.7071067811865476, s = -0.7071067811865476;  // cos, sin(-pi/4)
 #pragma unroll
@@ -632,13 +680,20 @@ struct EvalDas {
             f[2] = 1.0 - x2 + g;
         } else {
             double s0, c0, s1, c1;
-            sincospi(0.5 * x1, &s0, &c0);
-            sincospi(0.5 * x2, &s1, &c1);
+            if (ref) {
+                s0 = trig_sin(true, 0.5, x1);
+                c0 = trig_cos(true, 0.5, x1);
+                s1 = trig_sin(true, 0.5, x2);
+                c1 = trig_cos(true, 0.5, x2);
+            } else {
+                sincospi(0.5 * x1, &s0, &c0);
+                sincospi(0.5 * x2, &s1, &c1);
+            }
             f[0] = c0 * c1 + g;
             f[1] = c0 * s1 + g;
             f[2] = s0 + g;
         }
-        emit(1, K::b - cospi(K::a * x2));
+        emit(1, K::b - trig_cos(ref, K::a, x2));
         emit(2, -((K::e - g) * (g - K::d)));
         const double t = 0.5773502691896258;  // 1/sqrt(3)
 #pragma unroll

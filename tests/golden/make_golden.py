@@ -22,7 +22,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from oracle import Oracle, Reference, build_ref  # noqa: E402
 
-from conftest import MW_PROBLEMS, REF_PROBLEMS, f32  # noqa: E402
+from conftest import DAS_PROBLEMS, MW_PROBLEMS, REF_PROBLEMS, f32  # noqa: E402
 
 
 def eval_fixture(ref, orc, rng):
@@ -154,6 +154,60 @@ def pf_fixture(ref):
     np.savez_compressed(os.path.join(HERE, "pf_ref.npz"), **out)
 
 
+def nondominated_rows(F):
+    """fronts.cpp:15-42 (m = 2: lexicographic sweep, duplicates dropped; m = 3:
+    pairwise Pareto dominance, duplicates kept)."""
+    n = len(F)
+    if F.shape[1] == 2:
+        order = sorted(range(n), key=lambda i: (F[i, 0], F[i, 1]))  # stable
+        keep, best = [], np.inf
+        for i in order:
+            if F[i, 1] < best:
+                keep.append(i)
+                best = F[i, 1]
+        return np.array(sorted(keep), dtype=np.int64)
+    keep = []
+    for i in range(n):
+        le = np.all(F <= F[i], axis=1) & np.any(F < F[i], axis=1)
+        if not le.any():
+            keep.append(i)
+    return np.array(keep, dtype=np.int64)
+
+
+def restated_nd_set(orc, name, n_points):
+    """The nondominated candidate set pf_reference (fronts.cpp:54-79) subsamples
+    for n_points, from the oracle's restated candidates."""
+    m = orc.problem_info(name)["m"]
+    over = max(8 * n_points, 2000)
+    if m >= 3:
+        over = min(over, 12000)
+    for attempt in range(4):
+        X = orc.front_candidates(name, over)
+        F, G, cv = orc.evaluate(name, X)
+        Ff = F[cv == 0.0]
+        if len(Ff) >= max(n_points, 1):
+            nd = Ff[nondominated_rows(Ff)]
+            if len(nd) >= n_points or attempt == 3:
+                return nd
+        over *= 4
+        if m >= 3:
+            over = min(over, 50000)
+    raise RuntimeError("no feasible front")
+
+
+def restated_fronts_fixture(ref, orc):
+    """MW / DAS-CMOP fronts: the reference's own pf_reference pipeline
+    (fronts.cpp:54-103: evaluate, feasible filter, nondominated filter,
+    subsample) over the oracle's restated front candidates (these suites have
+    no reference counterpart; the candidates are wired in by oracle/ref_shim.cpp)."""
+    out = {}
+    for name in MW_PROBLEMS + DAS_PROBLEMS:
+        for npts in (64, 1000):
+            out[f"{name}/{npts}"] = ref.pf_reference(name, npts)
+        out[f"{name}/nd64"] = restated_nd_set(orc, name, 64)
+    np.savez_compressed(os.path.join(HERE, "pf_restated.npz"), **out)
+
+
 def runs_fixture(ref):
     """Final IGD of the reference's own run_gmpea over 30 seeds (statistical parity)."""
     fronts = np.load(os.path.join(HERE, "fronts.npz"))
@@ -190,6 +244,9 @@ def main():
     if not build_ref():
         raise SystemExit("reference sources not available")
     ref, orc = Reference(), Oracle()
+    if "--restated-fronts" in sys.argv:  # only the MW / DAS-CMOP front fixture
+        restated_fronts_fixture(ref, orc)
+        return
     rng = np.random.default_rng(20250919)
     eval_fixture(ref, orc, rng)
     selection_fixture(ref, orc, rng)
@@ -197,6 +254,7 @@ def main():
     metrics_fixture(ref, rng)
     fronts_fixture(ref)
     pf_fixture(ref)
+    restated_fronts_fixture(ref, orc)
     runs_fixture(ref)
     baseline_runs_fixture(ref)
     print("golden fixtures written to", HERE)
