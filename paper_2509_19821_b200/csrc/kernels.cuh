@@ -724,8 +724,16 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 #undef GMPEA_LO
 #undef GMPEA_HI
 
+// blocks per SM: 8 (63 registers); the MW kernel (d = 15, smaller rows and
+// evaluator state) runs faster at 10 (48 registers) despite a small spill,
+// LIRCMOP13 slower (A/B)
+template <class Ev, int DC>
+constexpr int vary_minblocks() {
+    return DC == 15 && std::is_same<Ev, EvalMw>::value ? 10 : GMPEA_VARY_MINBLOCKS;
+}
+
 template <class Ev, int MODE, int OP, int DC = 0, bool UB = false>
-__global__ void __launch_bounds__(128, GMPEA_VARY_MINBLOCKS) vary_eval_kernel(VaryParams p) {
+__global__ void __launch_bounds__(128, (vary_minblocks<Ev, DC>())) vary_eval_kernel(VaryParams p) {
     vary_body<Ev, MODE, OP, DC, UB>(p, blockIdx.x, blockIdx.y);
 }
 
