@@ -200,11 +200,17 @@ def main():
 
     import torch
 
+    # GMPEA_DIST_BACKEND=gloo: a functional check of the sharded path with
+    # several ranks on fewer GPUs (host-staged exchange, no rank's kernel waits
+    # on another's); never a bench number.  The product path is NCCL.
+    backend = os.environ.get("GMPEA_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     import paper_2509_19821_b200 as g
 
     stream = torch.cuda.Stream()  # the engine's launching stream (events are recorded on it)
@@ -345,6 +351,8 @@ def main():
                    "sample": f"unavailable: {e}"}
     eng.close()
 
+    if backend != "nccl":
+        config["functional_check"] = f"{world} ranks over {backend} on {torch.cuda.device_count()} GPU(s): not a bench number"
     line = {"metric": METRIC, "value": value, "unit": "ind-gen/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong",  # N = 1M slots in total, split into weight-region shards

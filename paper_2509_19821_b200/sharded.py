@@ -67,15 +67,38 @@ class TorchComm:
         self.dist = dist
         self.group = group
 
+        # gloo (CPU tests, functional checks of several ranks on one GPU) moves
+        # host tensors only: device tensors are staged through host memory
+        self.staged = dist.get_backend(group) == "gloo"
+
+    def _host(self, t):
+        return t.cpu() if (self.staged and t is not None and t.is_cuda) else t
+
     def allreduce_min_(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        h = self._host(t)
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.MIN, group=self.group)
+        if h is not t:
+            t.copy_(h)
 
     def allreduce_sum_(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        h = self._host(t)
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+        if h is not t:
+            t.copy_(h)
 
     def exchange(self, ops):
         """ops: list of (peer, send_tensor, recv_tensor); all posted at once."""
         d = self.dist
+        if self.staged:
+            hops = [(peer, self._host(snd), self._host(rcv)) for peer, snd, rcv in ops]
+            self._exchange(d, hops)
+            for (_, _, rcv), (_, _, hr) in zip(ops, hops):
+                if rcv is not None and hr is not rcv:
+                    rcv.copy_(hr)
+            return
+        self._exchange(d, ops)
+
+    def _exchange(self, d, ops):
         p2p = []
         for peer, snd, rcv in ops:
             if snd is not None:
