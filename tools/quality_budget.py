@@ -42,10 +42,18 @@ def main():
     fronts.update({k.split("/")[0]: rest[k] for k in rest.files if k.endswith("/1000")})
     ref = Reference() if Reference.available() else None
     rows = []
+    def score(fr, front):
+        # IGD against the front; problems without one (WTA) keep the front
+        # for the normalised HV computed over all runs below
+        if front is None:
+            return {"front": fr}
+        return {"igd": float(g.igd(fr, front)) if len(fr) else float("inf")}
+
     for name in args.problems.split(","):
         op = 1 if name.startswith("LIRCMOP") else 0  # suite default (experiment.cpp:117-123)
-        front = fronts[name]
+        front = fronts.get(name)
         p = g.make_problem(name)
+        prob_rows = []
         for seed in range(1, args.seeds + 1):
             rec = {"problem": name, "seed": seed, "budget_s": args.budget}
             if ref is not None:
@@ -54,12 +62,11 @@ def main():
                                               time_budget_s=args.budget, record_walltime=True)
                 except Exception as e:  # the same PM hazard in the reference itself
                     pop = None
-                    rec["reference"] = {"n": args.ref_n, "error": str(e), "igd": float("inf"), "generations": -1}
+                    rec["reference"] = {"n": args.ref_n, "error": str(e), "generations": -1,
+                                        **({"igd": float("inf")} if front is not None else {"hv": 0.0})}
             if ref is not None and pop is not None:
                 fr = ref.metric_front(pop["F"], pop["cv"])
-                rec["reference"] = {"n": args.ref_n, "generations": int(hist[-1][0]),  # (the hazard
-                                    # raises here too when it occurs)
-                                    "igd": float(ref.igd(fr, front)) if len(fr) else float("inf")}
+                rec["reference"] = {"n": args.ref_n, "generations": int(hist[-1][0]), **score(fr, front)}
             for n in (int(x) for x in args.gpu_n.split(",")):
                 try:
                     r = g.run_gmpea(p, g.RunConfig(n=n, time_budget_s=args.budget, seed=seed, op=op))
@@ -68,12 +75,26 @@ def main():
                     # SBX child mutated into NaN fails evaluation), reproduced
                     # faithfully; tens of thousands of generations per second
                     # meet it where the reference's few hundred rarely do
-                    rec[f"b200_n{n}"] = {"n": n, "error": str(e), "igd": float("inf"), "generations": -1}
+                    rec[f"b200_n{n}"] = {"n": n, "error": str(e), "generations": -1,
+                                         **({"igd": float("inf")} if front is not None else {"hv": 0.0})}
                     continue
                 fr = g.metric_front(r.pop1)
                 rec[f"b200_n{n}"] = {"n": n, "generations": r.history[-1].gen,
-                                     "loop_ms": r.history[-1].wall_ms,
-                                     "igd": float(g.igd(fr, front)) if len(fr) else float("inf")}
+                                     "loop_ms": r.history[-1].wall_ms, **score(fr, front)}
+            prob_rows.append(rec)
+        if front is None:
+            # experiment.cpp:241-276: HV after normalising every run's front by
+            # the ideal / nadir over all runs of the problem, reference point 1.1
+            fs = [v["front"] for r in prob_rows for v in r.values() if isinstance(v, dict) and "front" in v]
+            allf = np.concatenate([f for f in fs if len(f)]) if any(len(f) for f in fs) else np.zeros((0, p.m))
+            ideal, nadir = allf.min(0), allf.max(0)
+            nadir = np.where(nadir > ideal, nadir, ideal + 1.0)
+            for r in prob_rows:
+                for v in r.values():
+                    if isinstance(v, dict) and "front" in v:
+                        f = v.pop("front")
+                        v["hv"] = float(g.hypervolume((f - ideal) / (nadir - ideal), np.full(p.m, 1.1))) if len(f) else 0.0
+        for rec in prob_rows:
             rows.append(rec)
             print(json.dumps(rec), flush=True)
     summary = {}
@@ -82,7 +103,8 @@ def main():
         s = {}
         for key in rs[0]:
             if isinstance(rs[0][key], dict):
-                s[key] = {"median_igd": float(np.median([r[key]["igd"] for r in rs])),
+                mkey = "igd" if "igd" in rs[0][key] else "hv"
+                s[key] = {f"median_{mkey}": float(np.median([r[key].get(mkey, np.nan) for r in rs])),
                           "median_generations": float(np.median([r[key]["generations"] for r in rs])),
                           "failed_runs": sum(1 for r in rs if "error" in r[key])}
         summary[name] = s
