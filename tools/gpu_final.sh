@@ -1,0 +1,12 @@
+# headline bench line, reference arm, workload lines, launch list and one
+# ncu --set full capture of the steady-state kernels (each after its plain run)
+mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench.log | cut -c1-400
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref=$?
+for w in mw1-1m mw7-1m lircmop14-1m dascmop7-1m wta-p10-100k; do
+  timeout 300 python bench.py --workload $w --no-cpu-baseline > gpurun_out/bench_$w.log 2>&1; echo $w=$?
+done
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo launches=$?
+ncu --set full --import-source on --clock-control none -k regex:"vary_eval|select_kernel|op1_kernel" --launch-skip 120 --launch-count 3 \
+    -o gpurun_out/prof_final -f python bench.py --steps 40 --warmup 40 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo full=$?
