@@ -475,7 +475,11 @@ using VaryKernel = void (*)(VaryParams);
 // the dimension-specialised generation kernels also assume uniform bounds
 // (true of every registered suite; checked by the caller)
 template <class Ev, int DC = 0, bool VARY_ONLY = false, bool UBF = false>
-VaryKernel pick_vary(int mode, int op) {
+VaryKernel pick_vary(int mode, int op, bool tour = false) {
+    if (tour) {  // the comparison algorithms: SBX children of tournament parents
+        constexpr bool UBT = DC > 0 || UBF;
+        return vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UBT, true>;
+    }
     if (!VARY_ONLY) {
         if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
         if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
@@ -485,22 +489,24 @@ VaryKernel pick_vary(int mode, int op) {
 }
 
 // the generation kernel is compiled for the registered suites' dimension
-VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0) {
+VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0, bool tour = false) {
+    tour = tour && mode == MODE_VARY;
     switch (fam) {
         case FAM_LIR:
-            if (d != 30 || mode != MODE_VARY) return pick_vary<EvalLir>(mode, op);
-            return id <= 4 ? pick_vary<EvalLirT<1>, 30, true>(mode, op)
-                           : (id <= 8 ? pick_vary<EvalLirT<5>, 30, true>(mode, op)
-                                      : (id <= 12 ? pick_vary<EvalLirT<9>, 30, true>(mode, op)
-                                                  : pick_vary<EvalLirT<13>, 30, true>(mode, op)));
+            if (d != 30 || mode != MODE_VARY) return pick_vary<EvalLir>(mode, op, tour);
+            return id <= 4 ? pick_vary<EvalLirT<1>, 30, true>(mode, op, tour)
+                           : (id <= 8 ? pick_vary<EvalLirT<5>, 30, true>(mode, op, tour)
+                                      : (id <= 12 ? pick_vary<EvalLirT<9>, 30, true>(mode, op, tour)
+                                                  : pick_vary<EvalLirT<13>, 30, true>(mode, op, tour)));
         case FAM_DTLZ:
-            return d == 7 ? pick_vary<EvalDtlz, 7>(mode, op)
-                          : (d == 12 ? pick_vary<EvalDtlz, 12>(mode, op) : pick_vary<EvalDtlz>(mode, op));
+            return d == 7 ? pick_vary<EvalDtlz, 7>(mode, op, tour)
+                          : (d == 12 ? pick_vary<EvalDtlz, 12>(mode, op, tour) : pick_vary<EvalDtlz>(mode, op, tour));
         case FAM_WTA:
-            return d > 0 && mode == MODE_VARY ? pick_vary<EvalWta, 0, true, true>(mode, op)
-                                              : pick_vary<EvalWta>(mode, op);
-        case FAM_DAS: return d == 30 ? pick_vary<EvalDas, 30>(mode, op) : pick_vary<EvalDas>(mode, op);
-        default: return d == 15 ? pick_vary<EvalMw, 15>(mode, op) : pick_vary<EvalMw>(mode, op);
+            return d > 0 && mode == MODE_VARY ? pick_vary<EvalWta, 0, true, true>(mode, op, tour)
+                                              : pick_vary<EvalWta>(mode, op, tour);
+        case FAM_DAS:
+            return d == 30 ? pick_vary<EvalDas, 30>(mode, op, tour) : pick_vary<EvalDas>(mode, op, tour);
+        default: return d == 15 ? pick_vary<EvalMw, 15>(mode, op, tour) : pick_vary<EvalMw>(mode, op, tour);
     }
 }
 
@@ -2421,7 +2427,7 @@ struct BaselineRun {
         vp.un = make_uidx((unsigned long long)n);
         for (int q = 0; q < npop; ++q) vp.bad_rows[q] = bad[q].p;
         init_k = vary_kernel_for(p->fam, MODE_INIT, 0);
-        vary_k = vary_kernel_for(p->fam, MODE_VARY, OP_SBX, p->dev.uniform ? d : 0, p->dev.id);
+        vary_k = vary_kernel_for(p->fam, MODE_VARY, OP_SBX, p->dev.uniform ? d : 0, p->dev.id, true);
     }
 
     void check() {

@@ -152,10 +152,20 @@ __device__ __forceinline__ unsigned half16(const u32x4& w, int k8) {
     return (k8 & 1) ? (word >> 16) : (word & 0xffffu);
 }
 
+// Rare draws (coin tails, p = 2^-16 per gene).  The SBX kernels, which draw
+// two coin streams per gene group, take them out of line (fewer inlined Philox
+// copies: -2.7 % DAS-CMOP7, -0.9 % MW7 generation time); inlined they suit the
+// DE kernel's register allocation better (+2 % LIRCMOP13 out of line).
+__device__ __noinline__ unsigned philox_x_rare(unsigned c0, unsigned c1, unsigned c2, unsigned c3, unsigned k0,
+                                               unsigned k1) {
+    return philox4x32_10(c0, c1, c2, c3, k0, k1).x;
+}
+
 // Eight exact 32-bit coins "w <= T" (T in [-1, 2^32 - 1]) from the 16-bit
 // heads of one counter: bit k is set when gene j0 + k wins.  A head equal to
 // T's head is refined with the tail drawn from its own counter (probability
 // 2^-16 per gene), so the result equals the full 32-bit comparison.
+template <bool OUTLINE = false>
 __device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngenes, unsigned slot, unsigned gen,
                                            unsigned tag_ref, unsigned j0, const PhiloxKey& K) {
     if (T < 0) return 0u;
@@ -175,7 +185,9 @@ __device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngen
     while (tie) {  // rare
         const int k = __ffs(tie) - 1;
         tie &= tie - 1u;
-        const unsigned l = philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, K).x & 0xffffu;
+        const unsigned l = (OUTLINE ? philox_x_rare(slot, gen, tag_ref, j0 + (unsigned)k, K.k[0], K.k[1])
+                                    : philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, K).x) &
+                           0xffffu;
         win |= (unsigned)(l <= tlo) << k;
     }
     return win;
@@ -389,7 +401,14 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #endif
 // DC > 0 compiles the kernel for a fixed decision dimension (the registered
 // suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
-template <class Ev, int MODE, int OP, int DC = 0, bool UB = false>
+// TOUR: tournament parent picks (the comparison algorithms' instantiation;
+// the GMPEA kernels carry no tournament code)
+// (the DE kernels keep the run-time branch: its absence costs LIRCMOP13 13 %
+// through a worse register allocation, A/B in DESIGN.md)
+#ifndef GMPEA_TOUR_COND
+#define GMPEA_TOUR_COND (TOUR || (OP == OP_DE && p.tour))
+#endif
+template <class Ev, int MODE, int OP, int DC = 0, bool UB = false, bool TOUR = false>
 __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, const int by) {
     extern __shared__ float4 sm4[];
     DevState* st = p.st;
@@ -442,7 +461,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             bool cross = true;
             if (MODE == MODE_VARY && active) {
                 PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key, 0u, {}};
-                if (p.tour) {
+                if (GMPEA_TOUR_COND) {
                     auto tournament = [&]() {
                         const unsigned a = ps.index(p.un), b = ps.index(p.un);
                         if (p.tour == 1) {
@@ -545,13 +564,13 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         }
                         // per-gene SBX coin u <= 0.5 <=> w <= 2^31 (gmpea.cpp:119), DE CR coin, PM coin
                         const unsigned xbits =
-                            OP == OP_SBX ? (cross ? coins8(xc, 0x80000000ll, ng, slot, gen, philox_tag(pid, STREAM_XREF),
+                            OP == OP_SBX ? (cross ? coins8<OP == OP_SBX>(xc, 0x80000000ll, ng, slot, gen, philox_tag(pid, STREAM_XREF),
                                                            (unsigned)jb, K)
                                                   : 0u)
                                          : (de_all ? (1u << ng) - 1u
-                                                   : coins8(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
+                                                   : coins8<OP == OP_SBX>(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
                                                             (unsigned)jb, K));
-                        const unsigned mbits = coins8(mc, p.pm_T, ng, slot, gen, philox_tag(pid, STREAM_MREF),
+                        const unsigned mbits = coins8<OP == OP_SBX>(mc, p.pm_T, ng, slot, gen, philox_tag(pid, STREAM_MREF),
                                                       (unsigned)jb, K);
                         float v[8];
                         auto comp = [](const float4& f, int kk) {
@@ -732,9 +751,9 @@ constexpr int vary_minblocks() {
     return DC == 15 && std::is_same<Ev, EvalMw>::value ? 10 : GMPEA_VARY_MINBLOCKS;
 }
 
-template <class Ev, int MODE, int OP, int DC = 0, bool UB = false>
+template <class Ev, int MODE, int OP, int DC = 0, bool UB = false, bool TOUR = false>
 __global__ void __launch_bounds__(128, (vary_minblocks<Ev, DC>())) vary_eval_kernel(VaryParams p) {
-    vary_body<Ev, MODE, OP, DC, UB>(p, blockIdx.x, blockIdx.y);
+    vary_body<Ev, MODE, OP, DC, UB, TOUR>(p, blockIdx.x, blockIdx.y);
 }
 
 // ---- PBI in fp32 on unit reference vectors (scalarize.cpp:72-89):

@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+for W in lircmop13-1m dascmop7-1m mw7-1m; do W=$W REPS="1 2" bash ab/run.sh before.so outl.so tour_only.so; done
