@@ -654,6 +654,7 @@ struct gmpea_engine {
     DevBuf<unsigned> done_ctr;
     DevBuf<double> staging;  // f64 row-major staging for population transfers
     DevBuf<int> rowsbuf;
+    DevBuf<int> nbad_buf;
     int* host_flag_dev = nullptr;
 
     VaryParams vp{};
@@ -662,6 +663,7 @@ struct gmpea_engine {
     RestoreParams rp{};
     VaryKernel vary = nullptr;
     cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph_first = nullptr;
 
     long long gens_enqueued = 0;  // generations launched (host view)
     long long gen_limit = 0;      // max generations allowed by k_max / eval budget (-1 = inf)
@@ -669,6 +671,7 @@ struct gmpea_engine {
 
     ~gmpea_engine() {
         if (graph) cudaGraphExecDestroy(graph);
+        if (graph_first) cudaGraphExecDestroy(graph_first);
         if (host_flag) cudaFreeHost(host_flag);
         if (own_stream && s) cudaStreamDestroy(s);
     }
@@ -882,6 +885,14 @@ struct gmpea_engine {
         rp.row_end = (int)(own1 - e0);
         rp.rs4 = geo.rs4;
         rp.st = st.p;
+        // transfer buffers and the generation graph are made here, so that
+        // set_population / step / get_population allocate nothing and the
+        // first step does not instantiate the graph (the graph's parameters
+        // never change after construction)
+        staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
+        rowsbuf.alloc(std::max(n, 1));
+        nbad_buf.alloc(1);
+        if (!sharded) build_graph();
         CK(cudaStreamSynchronize(s));
         check_errors(0);
     }
@@ -910,10 +921,6 @@ struct gmpea_engine {
                            sizeof(DevState) - offsetof(DevState, t_gen_start), cudaMemcpyHostToDevice, s));
         gens_enqueued = 0;
         finished = false;
-        if (graph) {
-            cudaGraphExecDestroy(graph);
-            graph = nullptr;
-        }
     }
 
     void set_population(int which, const double* X) {
@@ -924,7 +931,7 @@ struct gmpea_engine {
         DevBuf<double>& h = staging;
         // X holds all N rows; this engine keeps its window [e0, e1)
         CK(cudaMemcpyAsync(h.p, X + e0 * d, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
-        DevBuf<int> nbad(1);
+        DevBuf<int>& nbad = nbad_buf;
         nbad.zero(s);
         if (rowsbuf.n < (size_t)std::max(n, 1)) rowsbuf.alloc(std::max(n, 1));
         DevBuf<int>& rows = rowsbuf;
@@ -975,20 +982,30 @@ struct gmpea_engine {
         if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
 
-    void build_graph() {
-        if (graph) return;
+    // two graphs of one generation: graph_first also restarts the loop clock
+    // (the first generation of a step() call), so step(1) is one launch
+    cudaGraphExec_t capture_generation(bool clock) {
         cudaStream_t cs;
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         cudaGraph_t g;
+        cudaGraphExec_t x;
         CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
         cudaStream_t saved = s;
         s = cs;
+        if (clock) start_loop_clock();
         enqueue_generation();
         s = saved;
         CK(cudaStreamEndCapture(cs, &g));
-        CK(cudaGraphInstantiate(&graph, g, 0));
+        CK(cudaGraphInstantiate(&x, g, 0));
         CK(cudaGraphDestroy(g));
         CK(cudaStreamDestroy(cs));
+        return x;
+    }
+
+    void build_graph() {
+        if (graph) return;
+        graph = capture_generation(false);
+        graph_first = capture_generation(true);
     }
 
     // the loop clock restarts at every step() so host work between calls
@@ -999,9 +1016,9 @@ struct gmpea_engine {
     long long step(long long k) {
         if (gen_limit >= 0) k = std::min(k, gen_limit - gens_enqueued);
         if (k <= 0) return 0;
-        start_loop_clock();
         build_graph();
-        for (long long i = 0; i < k; ++i) CK(cudaGraphLaunch(graph, s));
+        CK(cudaGraphLaunch(graph_first, s));
+        for (long long i = 1; i < k; ++i) CK(cudaGraphLaunch(graph, s));
         gens_enqueued += k;
         return k;
     }
