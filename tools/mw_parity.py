@@ -1,5 +1,6 @@
-"""BASELINE.json configs[1]: MW1-MW14, N = 10,000, 30 seeds — final-population
-quality of the engine vs the reference's own run_gmpea on the same problems.
+"""BASELINE.json configs[1]: MW1-MW14 (and DAS-CMOP1-9), N = 10,000, 30 seeds —
+final-population quality of the engine vs the reference's own run_gmpea on the
+same problems.
 
 The reference has no MW problems, so its loop runs the oracle's
 restated MW evaluators wrapped as reference ProblemDefs (oracle/ref_shim.cpp,
@@ -7,7 +8,9 @@ problem_for) — "reference loop + restated evaluator".  Neither side has an
 analytic MW front, so the metric is the reference harness's normalised
 hypervolume (experiment.cpp:240-281: ideal/nadir over the runs' fronts,
 reference point 1.1): here the bounds come from the reference runs and are
-applied to both arms.
+applied to both arms.  Since the restated fronts exist
+(tests/golden/pf_restated.npz, the reference's pf_reference over the restated
+candidates), the final IGD against them is compared as well.
 
     python tools/mw_parity.py ref   [--seeds 30 --n 10000 --gens 200 --procs 8]
         runs the reference here (CPU) -> tests/golden/mw_ref_hv.json
@@ -46,6 +49,15 @@ def hv_of(front, lo, hi, hv_fn):
     return float(hv_fn((front - lo) / span, np.full(front.shape[1], 1.1)))
 
 
+def restated_front(name):
+    fx = np.load(os.path.join(ROOT, "tests", "golden", "pf_restated.npz"))
+    return fx[f"{name}/1000"]
+
+
+def igd_of(front, ref_front, igd_fn):
+    return float(igd_fn(front, ref_front)) if len(front) else float("inf")
+
+
 def cmd_ref(args):
     from oracle import Reference
 
@@ -61,12 +73,15 @@ def cmd_ref(args):
     for name in probs:
         allf = [f for f in fronts[name].values() if len(f)]
         if not allf:
-            out["problems"][name] = {"ideal": None, "nadir": None, "hv": [0.0] * args.seeds}
+            out["problems"][name] = {"ideal": None, "nadir": None, "hv": [0.0] * args.seeds,
+                                     "igd": [float("inf")] * args.seeds}
             continue
         cat = np.concatenate(allf)
         lo, hi = cat.min(0), cat.max(0)
         hvs = [hv_of(fronts[name][s], lo, hi, ref.hypervolume) for s in range(1, args.seeds + 1)]
-        out["problems"][name] = {"ideal": lo.tolist(), "nadir": hi.tolist(), "hv": hvs}
+        pf = restated_front(name)
+        igds = [igd_of(fronts[name][s], pf, ref.igd) for s in range(1, args.seeds + 1)]
+        out["problems"][name] = {"ideal": lo.tolist(), "nadir": hi.tolist(), "hv": hvs, "igd": igds}
     with open(args.ref_json, "w") as f:
         json.dump(out, f, indent=1)
 
@@ -81,7 +96,8 @@ def cmd_gpu(args):
     for name in ref["problems"]:
         rp = ref["problems"][name]
         p = g.make_problem(name)
-        hvs = []
+        hvs, igds = [], []
+        pf = restated_front(name)
         for seed in range(1, ref["seeds"] + 1):
             r = g.run_gmpea(p, g.RunConfig(n=ref["n"], k_max=ref["gens"], seed=seed, op=g.VariationOp.sbx_pm))
             fr = g.metric_front(r.pop1)
@@ -89,15 +105,30 @@ def cmd_gpu(args):
                 hvs.append(0.0)
             else:
                 hvs.append(hv_of(fr, np.array(rp["ideal"]), np.array(rp["nadir"]), g.hypervolume))
-        a, b = np.array(hvs), np.array(rp["hv"])
-        if np.all(a == a[0]) and np.all(b == a[0]):
-            pval = 1.0
-        else:
-            pval = float(mannwhitneyu(a, b, alternative="two-sided").pvalue)
-        res[name] = {"b200_median_hv": float(np.median(a)), "ref_median_hv": float(np.median(b)), "p_value": pval,
-                     "verdict": "=" if pval >= 0.05 else ("+" if np.mean(a) > np.mean(b) else "-"),
-                     "b200_feasible_runs": int((a > 0).sum()), "ref_feasible_runs": int((b > 0).sum()),
-                     "b200_hv": [float(x) for x in a]}
+            igds.append(igd_of(fr, pf, g.igd))
+
+        def compare(a, b, higher_better):
+            a, b = np.asarray(a, float), np.asarray(b, float)
+            if np.array_equal(np.unique(a), np.unique(b)) and len(np.unique(a)) == 1:
+                return 1.0, "="
+            # infinite IGD (no feasible point) ranks last: map it to a large finite value
+            fin = np.concatenate([a, b])[np.isfinite(np.concatenate([a, b]))]
+            big = (fin.max() * 10 + 1) if len(fin) else 1.0
+            a2, b2 = np.where(np.isfinite(a), a, big), np.where(np.isfinite(b), b, big)
+            pv = float(mannwhitneyu(a2, b2, alternative="two-sided").pvalue)
+            better = np.median(a2) > np.median(b2) if higher_better else np.median(a2) < np.median(b2)
+            return pv, "=" if pv >= 0.05 else ("+" if better else "-")
+
+        pval, verdict = compare(hvs, rp["hv"], True)
+        res[name] = {"b200_median_hv": float(np.median(hvs)), "ref_median_hv": float(np.median(rp["hv"])),
+                     "p_value": pval, "verdict": verdict,
+                     "b200_feasible_runs": int((np.array(hvs) > 0).sum()),
+                     "ref_feasible_runs": int((np.array(rp["hv"]) > 0).sum()),
+                     "b200_hv": [float(x) for x in hvs]}
+        if "igd" in rp:
+            pi, vi = compare(igds, rp["igd"], False)
+            res[name].update({"b200_median_igd": float(np.median(igds)), "ref_median_igd": float(np.median(rp["igd"])),
+                              "igd_p_value": pi, "igd_verdict": vi, "b200_igd": igds})
         print(name, res[name], flush=True)
     with open(args.out, "w") as f:
         json.dump({"config": {k: ref[k] for k in ("n", "gens", "seeds")}, "results": res}, f, indent=1)
