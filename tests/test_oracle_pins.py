@@ -228,3 +228,18 @@ def test_dascmop_known_answers(orc):
     # DAS-CMOP9's Rastrigin distance vanishes at the same point: unit-sphere objectives
     F, _, _ = orc.evaluate("DASCMOP9", x)
     assert np.isclose(np.sum(F[0] ** 2), 1.0)
+
+
+@pytest.mark.parametrize("name", MW_PROBLEMS + [f"DASCMOP{k}" for k in range(1, 10)])
+def test_restated_front_candidates_are_feasible_and_in_bounds(orc, name):
+    """Restated MW / DAS-CMOP front candidates (no reference counterpart):
+    every row lies in the box, and the rows realise a feasible distance —
+    positions that have one (the level scan found it; MW10 has few) give rows that
+    evaluate feasible through the ordinary evaluator."""
+    info = orc.problem_info(name)
+    X = orc.front_candidates(name, 400)
+    assert X.shape[1] == info["d"]
+    assert np.all(X >= info["lo"]) and np.all(X <= info["hi"])
+    F, G, cv = orc.evaluate(name, X)
+    assert np.isfinite(F).all()
+    assert (cv == 0.0).mean() >= 0.05, (cv == 0.0).mean()  # MW10: 8.5 % of positions
