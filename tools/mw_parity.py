@@ -38,7 +38,7 @@ def _ref_run(job):
     from oracle import Reference
 
     r = Reference()
-    pop, _ = r.run_gmpea(name, n, k_max=gens, seed=seed, op=0, record_walltime=False)
+    pop, _ = r.run_gmpea(name, n, k_max=gens, seed=seed, op=suite_op(name), record_walltime=False)
     return name, seed, r.metric_front(pop["F"], pop["cv"])
 
 
@@ -50,8 +50,17 @@ def hv_of(front, lo, hi, hv_fn):
 
 
 def restated_front(name):
+    """IGD reference front: the reference's own pf_reference (fronts.npz) for
+    its suites, the restated fronts (pf_restated.npz) for MW / DAS-CMOP."""
+    ref = np.load(os.path.join(ROOT, "tests", "golden", "fronts.npz"))
+    if name in ref.files:
+        return ref[name]
     fx = np.load(os.path.join(ROOT, "tests", "golden", "pf_restated.npz"))
     return fx[f"{name}/1000"]
+
+
+def suite_op(name):
+    return 1 if name.startswith("LIRCMOP") else 0  # experiment.cpp:117-123
 
 
 def igd_of(front, ref_front, igd_fn):
@@ -99,7 +108,8 @@ def cmd_gpu(args):
         hvs, igds = [], []
         pf = restated_front(name)
         for seed in range(1, ref["seeds"] + 1):
-            r = g.run_gmpea(p, g.RunConfig(n=ref["n"], k_max=ref["gens"], seed=seed, op=g.VariationOp.sbx_pm))
+            r = g.run_gmpea(p, g.RunConfig(n=ref["n"], k_max=ref["gens"], seed=seed,
+                                           op=g.VariationOp(suite_op(name))))
             fr = g.metric_front(r.pop1)
             if rp["ideal"] is None:
                 hvs.append(0.0)
