@@ -899,8 +899,6 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     float bw = pw;
     float bg = 0.0f;
     int bc = -1;
-    int mex = 0;
-    bool mex_open = true;
     bool negcv = false;
     // batches of NB claimants; the next batch's indices are loaded while
     // this batch's keys are gathered (one memory round trip per batch)
@@ -943,13 +941,6 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
                 mark = g < gp;
             }
             if (!mark) continue;
-            // claims arrive in ascending c: the parent sits at their mex (gmpea.cpp:343-348)
-            if (mex_open) {
-                if (c == mex)
-                    ++mex;
-                else if (c > mex)
-                    mex_open = false;
-            }
             bool better;
             if (!have)
                 better = true;
@@ -976,14 +967,13 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
         atomicCAS(&p.st->err, 0, ERR_NEG_CV);
         p.st->stop = 1;
     }
-    // the parent competes with index mex (gmpea.cpp:349-371)
-    bool off_wins = false;
-    if (have) {
-        if (POP == 0)
-            off_wins = bw < pw || (bw == pw && (bg < gp || (bg == gp && bc < mex)));
-        else
-            off_wins = bg < gp || (bg == gp && bc < mex);
-    }
+    // The reference puts the parent into the argmin at index mex(claims)
+    // (gmpea.cpp:343-371), where that index decides only an exact key tie
+    // between the parent and the best claimant.  Every claimant marked j, i.e.
+    // is strictly better than the parent under the same key function (OP2's
+    // fpr_better / PBI, recomputed identically in OP3), so the best claimant is
+    // too: the tie never occurs and an offspring wins iff some claimant marked j.
+    const bool off_wins = have;
     int code = -1;
     if (off_wins) {
         const unsigned char sb = p.srcbits[bc];
