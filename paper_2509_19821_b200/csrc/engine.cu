@@ -228,7 +228,10 @@ struct gmpea_problem {
                 base += wta.cap[v];
             }
             dev.wta_ncap = base;
-            dev.wta_n8 = base + 2 * wta.vehicles + (d + 63) / 64;  // EvalWta scratch words
+            // EvalWta scratch (32-bit words; its keys hold the slot in 8 bits:
+            // kWtaMaxSlots <= 256)
+            dev.wta_n32 = base + 2 * wta.vehicles + (d + 31) / 32;
+            dev.wta_n8 = (dev.wta_n32 + 1) / 2;
         }
     }
 };

@@ -437,7 +437,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
     float4* const grow = p.out[pi] + (long long)i * rs4;  // this child's global row
     float4* const wr4 = ST ? my4 : grow;
     Ev ev;
-    ev.bind(reinterpret_cast<unsigned long long*>(sm4) + tid, (int)blockDim.x);
+    ev.bind(sm4, tid, (int)blockDim.x);
     const bool stream_eval = !ST && MODE == MODE_VARY && p.eval && active;
     if (stream_eval) ev.begin(p.P);
 

@@ -34,7 +34,7 @@ enum : int {
 
 constexpr int kWtaMaxVehicles = 16;
 constexpr int kWtaMaxCap = 8;
-constexpr int kWtaMaxSlots = 128;
+constexpr int kWtaMaxSlots = 128;  // <= 256: EvalWta keys hold the slot in 8 bits
 constexpr int kMaxCon = kWtaMaxVehicles + kWtaMaxSlots;
 
 struct ProbDev {
@@ -58,7 +58,7 @@ struct ProbDev {
     // of its candidate list in the per-thread scratch; total scratch words
     int wta_capv[kWtaMaxVehicles];
     int wta_base[kWtaMaxVehicles];
-    int wta_ncap, wta_n8;
+    int wta_ncap, wta_n32, wta_n8;  // scratch: 32-bit words, and 8-byte units for sizing
 };
 
 // c·pi·x trigonometry.  The generation path uses the exact-pi forms
@@ -75,7 +75,7 @@ __device__ __forceinline__ double trig_cos(bool ref, double c, double x) { retur
 template <int SUB = 0>
 struct EvalLirT {
     static constexpr bool kStream = false;
-    __device__ __forceinline__ void bind(unsigned long long*, int) {}
+    __device__ __forceinline__ void bind(void*, int, int) {}
     double g1, g2, x0, x1, s0, c0;
     float x0f;
     bool ref;  // fp64 candidate rows: reference-rounded trigonometry
@@ -205,7 +205,7 @@ using EvalLir = EvalLirT<0>;
 // ---------------------------------------------------------------- C/DC-DTLZ
 struct EvalDtlz {
     static constexpr bool kStream = false;
-    __device__ __forceinline__ void bind(unsigned long long*, int) {}
+    __device__ __forceinline__ void bind(void*, int, int) {}
     double pos[2];
     double rast, sph;
     bool ref;  // fp64 candidate rows: reference-rounded trigonometry
@@ -333,7 +333,7 @@ __device__ __forceinline__ double ipow(double x, int e) {
 
 struct EvalMw {
     static constexpr bool kStream = false;
-    __device__ __forceinline__ void bind(unsigned long long*, int) {}
+    __device__ __forceinline__ void bind(void*, int, int) {}
     double xs[2];
     double prev;
     double gs;
@@ -614,7 +614,7 @@ struct DasConst {
 
 struct EvalDas {
     static constexpr bool kStream = false;
-    __device__ __forceinline__ void bind(unsigned long long*, int) {}
+    __device__ __forceinline__ void bind(void*, int, int) {}
     double xs[2];
     double sh;  // sin(0.5 pi x1): the position shift of DAS1-6's distance genes
     double gs;
@@ -728,40 +728,45 @@ struct EvalDas {
 // per thread): [lists | counts (V) | minima (V) | mask (ceil(D / 64))].
 struct EvalWta {
     static constexpr bool kStream = true;
-    unsigned long long* L;
+    // 32-bit scratch words in shared memory, one column per thread (stride S):
+    // [lists (ncap) | counts (V) | minima (V) | selection mask ((d + 31) / 32)]
+    unsigned* L;
     int S;
-    int v;
-    __device__ __forceinline__ void bind(unsigned long long* base, int stride) {
-        L = base;
-        S = stride;
+    int v, slot;  // vehicle and strike slot of the next gene (j = slot V + v)
+    __device__ __forceinline__ void bind(void* smem, int tid, int nthreads) {
+        L = reinterpret_cast<unsigned*>(smem) + tid;
+        S = nthreads;
     }
-    __device__ __forceinline__ unsigned long long& at(int k) const { return L[(long long)k * S]; }
+    __device__ __forceinline__ unsigned& at(int k) const { return L[k * S]; }
     __device__ __forceinline__ void begin(const ProbDev& P) {
         v = 0;
-        const int V = P.wta_vehicles;
-        for (int k = P.wta_ncap; k < P.wta_n8; ++k) at(k) = 0ull;
-        (void)V;
+        slot = 0;
+        for (int k = P.wta_ncap; k < P.wta_n32; ++k) at(k) = 0u;
     }
-    __device__ __forceinline__ void gene(const ProbDev& P, int j, float x) {
+    // A vehicle's candidates are ranked by (value desc, slot asc), i.e. the
+    // reference's stable order restricted to one vehicle (its genes are
+    // j = slot V + v).  Candidates lie in [0.5, 1]: the fp32 bit pattern minus
+    // that of 0.5 orders them in 24 bits, the slot (< 256) takes the low byte.
+    __device__ __forceinline__ void gene(const ProbDev& P, int, float x) {
         const int V = P.wta_vehicles;
         if (x >= 0.5f) {
-            const unsigned long long key = ((unsigned long long)__float_as_uint(x) << 32) | (0xffffffffu - (unsigned)j);
+            const unsigned key = ((__float_as_uint(x) - 0x3F000000u) << 8) | (255u - (unsigned)slot);
             const int cap = P.wta_capv[v], base = P.wta_base[v];
             const int kc = P.wta_ncap + v, km = P.wta_ncap + V + v;
             const int c = (int)at(kc);
             if (c < cap) {
                 at(base + c) = key;
-                at(kc) = (unsigned long long)(c + 1);
+                at(kc) = (unsigned)(c + 1);
                 if (c + 1 == cap) {
-                    unsigned long long mn = key;
+                    unsigned mn = key;
                     for (int e = 0; e < c; ++e) mn = min(mn, at(base + e));
                     at(km) = mn;
                 }
             } else if (cap > 0 && key > at(km)) {
-                const unsigned long long old = at(km);
-                unsigned long long mn = key;
+                const unsigned old = at(km);
+                unsigned mn = key;
                 for (int e = 0; e < cap; ++e) {
-                    unsigned long long k2 = at(base + e);
+                    unsigned k2 = at(base + e);
                     if (k2 == old) {
                         at(base + e) = key;
                         k2 = key;
@@ -771,7 +776,10 @@ struct EvalWta {
                 at(km) = mn;
             }
         }
-        v = v + 1 == V ? 0 : v + 1;
+        if (++v == V) {
+            v = 0;
+            ++slot;
+        }
     }
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
@@ -780,21 +788,21 @@ struct EvalWta {
         for (int u = 0; u < V; ++u) {
             const int c = (int)at(P.wta_ncap + u);
             for (int e = 0; e < c; ++e) {
-                const unsigned j = 0xffffffffu - (unsigned)(at(P.wta_base[u] + e) & 0xffffffffull);
-                at(k0 + (int)(j >> 6)) |= 1ull << (j & 63);
+                const unsigned j = (255u - (at(P.wta_base[u] + e) & 0xffu)) * (unsigned)V + (unsigned)u;
+                at(k0 + (int)(j >> 5)) |= 1u << (j & 31);
             }
             emit(u, (double)c - (double)P.wta_capv[u]);  // per-vehicle capacity (wta.cpp:99-100)
         }
-        const unsigned long long vm = V >= 64 ? ~0ull : (1ull << V) - 1ull;
+        const unsigned vm = V >= 32 ? ~0u : (1u << V) - 1u;
         double f1 = 0.0, f2 = 0.0;
         int s = 0;
         for (int i = 0; i < T; ++i) {
             double surv = 1.0, strikes = 0.0;
             for (int k = 0; k < P.wta_strikes[i]; ++k, ++s) {
-                const int b = s * V, w = b >> 6, o = b & 63;
-                unsigned long long bits = at(k0 + w) >> o;
-                if (o + V > 64) bits |= at(k0 + w + 1) << (64 - o);
-                const double hd = (double)__popcll(bits & vm);
+                const int b = s * V, w = b >> 5, o = b & 31;
+                unsigned bits = at(k0 + w) >> o;
+                if (o + V > 32) bits |= at(k0 + w + 1) << (32 - o);
+                const double hd = (double)__popc(bits & vm);
                 surv *= 1.0 - P.wta_p[s] * hd;
                 f2 += hd;
                 strikes += hd;
