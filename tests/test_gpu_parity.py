@@ -438,3 +438,15 @@ def test_pf_reference_restated_fronts(g, name):
     near = np.sqrt(((got[:, None, :] - dense[None, :, :]) ** 2).sum(-1)).min(1)
     assert near.mean() <= spacing and near.max() <= 3 * spacing, (near.mean(), near.max(), spacing)
     assert _igd(got, dense) <= spacing, (_igd(got, dense), spacing)
+
+
+def test_select_packed_and_int32_reverse_tables_agree(g, monkeypatch):
+    """select reads the int16-packed reverse neighbourhood unless an offset
+    does not fit (then the int32 table): both give the same run, bit for bit."""
+    p = g.make_problem("LIRCMOP13")
+    cfg = g.RunConfig(n=3000, k_max=6, seed=4, op=g.VariationOp.de, record_walltime=False)
+    a = g.run_gmpea(p, cfg)
+    monkeypatch.setenv("GMPEA_NO_RPACK", "1")
+    b = g.run_gmpea(p, cfg)
+    assert np.array_equal(a.pop1.X, b.pop1.X) and np.array_equal(a.pop1.F, b.pop1.F)
+    assert [r.feasible_ratio for r in a.history] == [r.feasible_ratio for r in b.history]
