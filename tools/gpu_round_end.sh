@@ -1,4 +1,3 @@
-# end-of-round validation (one gpurun call): see profiles/INDEX.md for where the outputs go
 # end-of-round validation: GPU tests, smoke, headline bench + reference arm,
 # steady-state ncu capture of the final build and its source attribution
 mkdir -p gpurun_out
