@@ -1039,7 +1039,9 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
     const float3 z = load_z(p.st, p.m);
     bool feas = false, off_taken = false;
     if (j < p.row_end) {
-        if (by == 0)
+        // blockIdx.y = 0 is pop2 (~4x the claimants per slot): the long
+        // blocks are dispatched first and pop1's short ones fill the tail
+        if (by == 1)
             off_taken = select_slot<0, PACK, NBP>(p, j, z, feas);
         else
             off_taken = select_slot<1, PACK, NBP>(p, j, z, feas);
@@ -1048,7 +1050,7 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
     // feasible_ratio of pop1 (gmpea.cpp:411-417) and the replacement count
     // (diagnostic): block counts, one atomic each
     __shared__ unsigned cnt[8], rep[8];
-    const unsigned b = __popc(__ballot_sync(0xffffffffu, by == 0 && feas && j < p.row_end));
+    const unsigned b = __popc(__ballot_sync(0xffffffffu, by == 1 && feas && j < p.row_end));
     const unsigned r = __popc(__ballot_sync(0xffffffffu, off_taken));
     if ((threadIdx.x & 31) == 0) {
         cnt[threadIdx.x >> 5] = b;
