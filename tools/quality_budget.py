@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--gpu-n", default="1000,100000")
     ap.add_argument("--ref-n", type=int, default=1000)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_quality_1s.json"))
+    ap.add_argument("--no-ref", action="store_true", help="engine arm only")
     args = ap.parse_args()
     import paper_2509_19821_b200 as g
     from oracle import Reference  # the reference arm (checker / baseline only)
@@ -40,7 +41,7 @@ def main():
     fronts = dict(np.load(os.path.join(ROOT, "tests", "golden", "fronts.npz")))
     rest = np.load(os.path.join(ROOT, "tests", "golden", "pf_restated.npz"))
     fronts.update({k.split("/")[0]: rest[k] for k in rest.files if k.endswith("/1000")})
-    ref = Reference() if Reference.available() else None
+    ref = Reference() if Reference.available() and not args.no_ref else None
     rows = []
     def score(fr, front):
         # IGD against the front; problems without one (WTA) keep the front
@@ -67,7 +68,7 @@ def main():
             if ref is not None and pop is not None:
                 fr = ref.metric_front(pop["F"], pop["cv"])
                 rec["reference"] = {"n": args.ref_n, "generations": int(hist[-1][0]), **score(fr, front)}
-            for n in (int(x) for x in args.gpu_n.split(",")):
+            for n in (int(x) for x in args.gpu_n.split(",") if x):
                 try:
                     r = g.run_gmpea(p, g.RunConfig(n=n, time_budget_s=args.budget, seed=seed, op=op))
                 except RuntimeError as e:
