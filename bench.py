@@ -127,12 +127,15 @@ def dist_env():
     return world, rank, local
 
 
-def ncu_traffic(kernel):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+def ncu_traffic(kernel, workload):
+    """dram bytes per launch of `kernel` from the committed ncu --set full
+    summary: the entry "kernel@workload", or the plain "kernel" entry, which
+    is the headline workload's capture (None for other workloads without one)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s.get(kernel, {}).get("dram_bytes_per_launch")
+        e = s.get(f"{kernel}@{workload}") or (s.get(kernel) if workload == "lircmop13-1m" else None)
+        return (e or {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
@@ -328,7 +331,7 @@ def main():
     units = 2 * n if dom != "op1" else n
     per_unit = ab[dom] * (2 if dom == "op1" else 1)
     achieved = per_unit * units / (kms[di] * 1e-3) / 1e9
-    traffic = ncu_traffic(dom)
+    traffic = ncu_traffic(dom, args.workload)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
                 "alg_bytes_per_unit": per_unit, "units_per_launch": units,

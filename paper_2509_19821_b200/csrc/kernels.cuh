@@ -651,24 +651,38 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         if (ST) {
                             mmask |= (Mask)mbits << (jb - w0);
                         } else {
-                            // inline polynomial mutation + clip, then the evaluator
+                            // inline polynomial mutation + clip, then the evaluator, as
+                            // rolled loops over the group: one code copy of the PM draw
+                            // and of the evaluator's gene step instead of eight (the
+                            // unrolled copies overflowed the instruction cache: the WTA
+                            // kernel's top stall was "no instruction").  Genes are read
+                            // from and written to v[] by compile-time-indexed selects.
+                            auto sel = [&](const int k) {
+                                float x = v[0];
 #pragma unroll
-                            for (int k = 0; k < 8; ++k) {
-                                if (k < ng && ((mbits >> k) & 1u)) {
-                                    const int j = jb + k;
-                                    const float lo = GMPEA_LO(j), hi = GMPEA_HI(j);
-                                    const u32x4 mu =
-                                        philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, K);
-                                    v[k] = clamp_ref(pm_apply(v[k], lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
-                                }
+                                for (int kk = 1; kk < 8; ++kk) x = k == kk ? v[kk] : x;
+                                return x;
+                            };
+                            unsigned mb = mbits & ((2u << (ng - 1)) - 1u);
+#pragma unroll 1
+                            while (mb) {
+                                const int k = __ffs(mb) - 1;
+                                mb &= mb - 1u;
+                                const int j = jb + k;
+                                const float lo = GMPEA_LO(j), hi = GMPEA_HI(j);
+                                const u32x4 mu = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MU), (unsigned)j, K);
+                                const float y = clamp_ref(pm_apply(sel(k), lo, hi, mu.x, p.pm_e1, p.pm_einv), lo, hi);
+#pragma unroll
+                                for (int kk = 0; kk < 8; ++kk)
+                                    if (kk == k) v[kk] = y;
                             }
                             if (stream_eval) {
-#pragma unroll
-                                for (int k = 0; k < 8; ++k) {
-                                    if (k >= ng) continue;
+#pragma unroll 1
+                                for (int k = 0; k < ng; ++k) {
                                     const int j = jb + k;
-                                    if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
-                                    ev.gene(p.P, j, v[k]);
+                                    const float x = sel(k);
+                                    if (!(x >= GMPEA_LO(j) && x <= GMPEA_HI(j))) bad = true;
+                                    ev.gene(p.P, j, x);
                                 }
                             }
                         }

@@ -286,7 +286,10 @@ def test_time_budget_discards_crossing_generation(g):
     assert all(b.wall_ms >= a.wall_ms for a, b in zip(h[1:], h[2:]))
 
 
-@pytest.mark.parametrize("name,op", [("LIRCMOP13", 1), ("DASCMOP7", 1), ("DASCMOP2", 0)])
+# WTA: the split generation kernel (two threads per child, evaluator states
+# merged in shared memory) against the same chain
+@pytest.mark.parametrize("name,op", [("LIRCMOP13", 1), ("DASCMOP7", 1), ("DASCMOP2", 0), ("WTA-P10", 0),
+                                     ("WTA-P3", 0), ("WTA-P1", 1)])
 def test_engine_generation_matches_operator_chain(g, orc, name, op):
     """One engine generation == oracle reproduce -> evaluate -> update_ideal ->
     environmental_selection on the same (fp32) state, with the engine's keys."""
