@@ -648,7 +648,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         for (int k = 0; k < 8; ++k)
                             if (k < ng && !((mbits >> k) & 1u))
                                 v[k] = fminf(fmaxf(v[k], GMPEA_LO(jb + k)), GMPEA_HI(jb + k));
-                        if (ST) {
+                        if constexpr (ST) {
                             mmask |= (Mask)mbits << (jb - w0);
                         } else {
                             // inline polynomial mutation + clip, then the evaluator, as
@@ -677,13 +677,16 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                                     if (kk == k) v[kk] = y;
                             }
                             if (stream_eval) {
-#pragma unroll 1
-                                for (int k = 0; k < ng; ++k) {
-                                    const int j = jb + k;
-                                    const float x = sel(k);
-                                    if (!(x >= GMPEA_LO(j) && x <= GMPEA_HI(j))) bad = true;
-                                    ev.gene(p.P, j, x);
+                                // bounds test and candidate mask on the group's registers;
+                                // the evaluator visits the candidates only
+                                unsigned cand = 0u;
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    if (k >= ng) continue;
+                                    if (!(v[k] >= GMPEA_LO(jb + k) && v[k] <= GMPEA_HI(jb + k))) bad = true;
+                                    if (Ev::candidate(v[k])) cand |= 1u << k;
                                 }
+                                ev.group(p.P, ng, cand, sel);
                             }
                         }
                         wr4[q] = make_float4(v[0], v[1], v[2], v[3]);

@@ -747,35 +747,64 @@ struct EvalWta {
     // reference's stable order restricted to one vehicle (its genes are
     // j = slot V + v).  Candidates lie in [0.5, 1]: the fp32 bit pattern minus
     // that of 0.5 orders them in 24 bits, the slot (< 256) takes the low byte.
-    __device__ __forceinline__ void gene(const ProbDev& P, int, float x) {
+    // keeps key among vehicle u's cap_u best (the keys of one vehicle are
+    // distinct, so the kept set does not depend on the arrival order)
+    __device__ __forceinline__ void insert(const ProbDev& P, int u, unsigned key) {
         const int V = P.wta_vehicles;
-        if (x >= 0.5f) {
-            const unsigned key = ((__float_as_uint(x) - 0x3F000000u) << 8) | (255u - (unsigned)slot);
-            const int cap = P.wta_capv[v], base = P.wta_base[v];
-            const int kc = P.wta_ncap + v, km = P.wta_ncap + V + v;
-            const int c = (int)at(kc);
-            if (c < cap) {
-                at(base + c) = key;
-                at(kc) = (unsigned)(c + 1);
-                if (c + 1 == cap) {
-                    unsigned mn = key;
-                    for (int e = 0; e < c; ++e) mn = min(mn, at(base + e));
-                    at(km) = mn;
-                }
-            } else if (cap > 0 && key > at(km)) {
-                const unsigned old = at(km);
+        const int cap = P.wta_capv[u], base = P.wta_base[u];
+        const int kc = P.wta_ncap + u, km = P.wta_ncap + V + u;
+        const int c = (int)at(kc);
+        if (c < cap) {
+            at(base + c) = key;
+            at(kc) = (unsigned)(c + 1);
+            if (c + 1 == cap) {
                 unsigned mn = key;
-                for (int e = 0; e < cap; ++e) {
-                    unsigned k2 = at(base + e);
-                    if (k2 == old) {
-                        at(base + e) = key;
-                        k2 = key;
-                    }
-                    mn = min(mn, k2);
-                }
+                for (int e = 0; e < c; ++e) mn = min(mn, at(base + e));
                 at(km) = mn;
             }
+        } else if (cap > 0 && key > at(km)) {
+            const unsigned old = at(km);
+            unsigned mn = key;
+            for (int e = 0; e < cap; ++e) {
+                unsigned k2 = at(base + e);
+                if (k2 == old) {
+                    at(base + e) = key;
+                    k2 = key;
+                }
+                mn = min(mn, k2);
+            }
+            at(km) = mn;
         }
+    }
+    __device__ __forceinline__ static bool candidate(float x) { return x >= 0.5f; }
+    __device__ __forceinline__ unsigned key(float x, int s) const {
+        return ((__float_as_uint(x) - 0x3F000000u) << 8) | (255u - (unsigned)s);
+    }
+    // the next ng genes at once (the generation kernel's gene groups): only the
+    // candidates (bit k of cand: gene k of the group is >= 0.5, value sel(k))
+    // are visited, then the (vehicle, slot) cursor moves on by ng
+    template <class Sel>
+    __device__ __forceinline__ void group(const ProbDev& P, int ng, unsigned cand, Sel&& sel) {
+        const int V = P.wta_vehicles;
+        while (cand) {
+            const int k = __ffs(cand) - 1;
+            cand &= cand - 1u;
+            int u = v + k, s = slot;
+            while (u >= V) {
+                u -= V;
+                ++s;
+            }
+            insert(P, u, key(sel(k), s));
+        }
+        v += ng;
+        while (v >= V) {
+            v -= V;
+            ++slot;
+        }
+    }
+    __device__ __forceinline__ void gene(const ProbDev& P, int, float x) {
+        const int V = P.wta_vehicles;
+        if (candidate(x)) insert(P, v, key(x, slot));
         if (++v == V) {
             v = 0;
             ++slot;
