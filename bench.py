@@ -41,6 +41,17 @@ WORKLOADS = {
     "dascmop7-1m": ("DASCMOP7", 1_000_000, 0),
     "dascmop9-1m": ("DASCMOP9", 1_000_000, 0),
 }
+# which BASELINE.json config each workload measures
+CONFIG_OF = {
+    "lircmop13-1m": "BASELINE configs[2]",
+    "lircmop14-1m": "BASELINE configs[2]",
+    "dascmop7-1m": "BASELINE configs[2]",
+    "dascmop9-1m": "BASELINE configs[2]",
+    "mw1-1m": "north-star MW target at N=1M",
+    "mw7-1m": "BASELINE configs[4] sweep point",
+    "mw7-10m": "BASELINE configs[4] sweep point",
+    "wta-p10-100k": "BASELINE configs[3]",
+}
 METRIC = "individual-generations/sec at N=1M"
 
 
@@ -174,7 +185,7 @@ def main():
     args = ap.parse_args()
     world, rank, local = dist_env()
     problem, n, op = WORKLOADS[args.workload]
-    config = {"workload": f"{args.workload}: {problem} (BASELINE configs[2]), N={n}, t1=5, t2=20, "
+    config = {"workload": f"{args.workload}: {problem} ({CONFIG_OF[args.workload]}), N={n}, t1=5, t2=20, "
                           f"theta=5, op={'de' if op else 'sbx_pm'}, seed=1",
               "problem": problem, "N": n, "l2": "working set > 126 MB L2 (no flush needed)"}
 
