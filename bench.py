@@ -40,6 +40,8 @@ WORKLOADS = {
     # reference's operator_for gives every non-LIRCMOP suite)
     "dascmop7-1m": ("DASCMOP7", 1_000_000, 0),
     "dascmop9-1m": ("DASCMOP9", 1_000_000, 0),
+    # a reference-suite C-DTLZ problem at the same population size
+    "c1dtlz1-1m": ("C1-DTLZ1", 1_000_000, 0),
 }
 # which BASELINE.json config each workload measures
 CONFIG_OF = {
@@ -51,6 +53,7 @@ CONFIG_OF = {
     "mw7-1m": "BASELINE configs[4] sweep point",
     "mw7-10m": "BASELINE configs[4] sweep point",
     "wta-p10-100k": "BASELINE configs[3]",
+    "c1dtlz1-1m": "reference suite at N=1M",
 }
 METRIC = "individual-generations/sec at N=1M"
 

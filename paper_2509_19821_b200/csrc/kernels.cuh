@@ -723,10 +723,11 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             // (already done in the gene loop for streaming evaluators)
             // MW / DAS-CMOP: the staged row through one rolled gene loop (one
             // copy of the evaluator's gene step instead of d: instruction fetch;
-            // A/B vary: MW1 -4.6 %, MW7 -2.6 %, DAS-CMOP7 -1.4 %, DAS-CMOP9 -4.3 %;
+            // A/B vary: MW1 -4.6 %, MW7 -2.6 %, DAS-CMOP7 -1.4 %, DAS-CMOP9 -4.3 %,
+            // C1-DTLZ1 -1.1 %;
             // the LIRCMOP kernels lose 8-11 % rolled and keep the unrolled loop)
-            constexpr bool ROLL_EVAL =
-                ST && (std::is_same<Ev, EvalMw>::value || std::is_same<Ev, EvalDas>::value);
+            constexpr bool ROLL_EVAL = ST && (std::is_same<Ev, EvalMw>::value || std::is_same<Ev, EvalDas>::value ||
+                                              std::is_same<Ev, EvalDtlz>::value);
             if constexpr (ROLL_EVAL) {
                 ev.begin(p.P);
                 const float* rd = reinterpret_cast<const float*>(my4);
