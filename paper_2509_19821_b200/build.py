@@ -1,29 +1,34 @@
 """Builds the engine library in-tree: paper_2509_19821_b200/libgmpea_b200.so.
 
-One nvcc invocation for sm_100a (B200); no torch extension machinery, the
-library is a plain C ABI (include/gmpea_b200.h).
+Every translation unit of csrc/ is compiled for sm_100a (B200) in parallel
+(the generation kernels are instantiated per problem family, vary_<family>.cu)
+and linked into one shared library with a plain C ABI (include/gmpea_b200.h);
+no torch extension machinery.
 """
 from __future__ import annotations
 
+import concurrent.futures as cf
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmpea_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", "engine.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in
-                  ("common.cuh", "kernels.cuh", "problems.cuh", "topology.cuh", "metrics.cuh", "fronts.cuh", "baselines.cuh")] + [
-    os.path.join(ROOT, "include", "gmpea_b200.h")]
+OBJ = os.path.join(ROOT, "build", "obj")
+SOURCES = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+HEADERS = sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "gmpea_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "--expt-relaxed-constexpr",
     "-Xcompiler", "-fno-builtin-sin", "-Xcompiler", "-fno-builtin-cos",
 ]
+LINK_FLAGS = ["-shared", "-ldl"]
 
 
 def nvcc() -> str:
@@ -31,19 +36,44 @@ def nvcc() -> str:
     return cand if os.path.exists(cand) else "nvcc"
 
 
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+
+
+def _stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
-        return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in DEPS if os.path.exists(p))
+    return not _stale(LIB, SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *SOURCES]
+    os.makedirs(OBJ, exist_ok=True)
+    # every header may feed every TU: a header change rebuilds all objects
+    todo = [s for s in SOURCES if force or _stale(_obj(s), [s] + HEADERS)]
+
+    def compile_one(src):
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", _obj(src) + ".tmp", src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr, flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(_obj(src) + ".tmp", _obj(src))
+
+    # the heaviest TUs first
+    todo.sort(key=lambda s: -os.path.getsize(s) if not os.path.basename(s).startswith("vary_") else -10**9)
+    with cf.ThreadPoolExecutor(max_workers=jobs or max(1, os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(compile_one, s) for s in todo]:
+            f.result()
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", *LINK_FLAGS, "-o", LIB + ".tmp",
+           *[_obj(s) for s in SOURCES]]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
+        print(" ".join(cmd), file=sys.stderr, flush=True)
     subprocess.run(cmd, check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB

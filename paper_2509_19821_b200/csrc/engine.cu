@@ -21,88 +21,21 @@
 #include <vector>
 
 #include "../../include/gmpea_b200.h"
-#include "baselines.cuh"
 #include "common.cuh"
-#include "fronts.cuh"
-#include "kernels.cuh"
-#include "metrics.cuh"
+#include "host.cuh"
+#include "select.cuh"
 #include "problems.cuh"
 #include "topology.cuh"
 
 using namespace gmpea_b200;
 
-namespace {
-
+namespace gmpea_b200 {
+namespace host {
 thread_local std::string g_err;
+}  // namespace host
+}  // namespace gmpea_b200
 
-struct cuda_error : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-#define CK(expr)                                                                             \
-    do {                                                                                     \
-        cudaError_t e_ = (expr);                                                             \
-        if (e_ != cudaSuccess)                                                               \
-            throw cuda_error(std::string(#expr) + ": " + cudaGetErrorString(e_));            \
-    } while (0)
-
-template <class Fn>
-int guarded(Fn&& fn) {
-    try {
-        fn();
-        return GMPEA_OK;
-    } catch (const cuda_error& e) {
-        g_err = e.what();
-        return GMPEA_ECUDA;
-    } catch (const std::invalid_argument& e) {
-        g_err = e.what();
-        return GMPEA_EINVAL;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return GMPEA_ERUNTIME;
-    }
-}
-
-template <class T>
-struct DevBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    DevBuf() = default;
-    explicit DevBuf(size_t count) { alloc(count); }
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() {
-        if (p) cudaFree(p);
-    }
-    void alloc(size_t count) {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = count;
-        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
-    }
-    void zero(cudaStream_t s) {
-        if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
-    }
-};
-
-inline int blocks_for(long long n, int bs) { return (int)((n + bs - 1) / bs); }
-
-void require_device() {
-    int n = 0;
-    cudaError_t e = cudaGetDeviceCount(&n);
-    if (e != cudaSuccess || n == 0)
-        throw cuda_error("no CUDA device available (the engine has no CPU fallback)");
-}
-
-// ---------------------------------------------------------------- problems
-constexpr double kPi = 3.141592653589793;
-
-struct WtaHost {
-    std::string scenario;
-    int targets = 0, vehicles = 0;
-    std::vector<int> strikes, cap;
-    std::vector<double> p;  // per strike slot, target-major
-};
+namespace {
 
 // wta_scenario (wta.cpp:23-49): sizes grow with the index, tables from the
 // reference's seeded mt19937_64 draws (rng.hpp:18-30)
@@ -153,90 +86,7 @@ bool device_pack_reverse(cudaStream_t s, int n, int maxdeg, const DevBuf<int>& R
     return h == 0;
 }
 
-}  // namespace
 
-struct gmpea_problem {
-    std::string name;
-    int fam = 0, id = 0, d = 0, m = 0, nin = 0, neq = 0;
-    std::vector<double> lo, hi;
-    WtaHost wta;
-    int device = 0;
-    // device copies
-    DevBuf<float> dlo, dhi;
-    DevBuf<double> dlo64, dhi64;
-    DevBuf<int> dcap, dstrikes, dslot_target;
-    DevBuf<double> dp;
-    ProbDev dev{};
-
-    void upload() {
-        require_device();
-        CK(cudaGetDevice(&device));
-        std::vector<float> lf(lo.begin(), lo.end()), hf(hi.begin(), hi.end());
-        dlo.alloc(d);
-        dhi.alloc(d);
-        dlo64.alloc(d);
-        dhi64.alloc(d);
-        CK(cudaMemcpy(dlo.p, lf.data(), d * sizeof(float), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dhi.p, hf.data(), d * sizeof(float), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dlo64.p, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dhi64.p, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice));
-        dev = ProbDev{};
-        dev.fam = fam;
-        dev.id = id;
-        dev.d = d;
-        dev.m = m;
-        dev.nin = nin;
-        dev.neq = neq;
-        dev.lo = dlo.p;
-        dev.hi = dhi.p;
-        dev.uniform = 1;
-        for (int j = 0; j < d; ++j)
-            if (lo[j] != lo[0] || hi[j] != hi[0]) dev.uniform = 0;
-        dev.ulo = d ? (float)lo[0] : 0.0f;
-        dev.uhi = d ? (float)hi[0] : 0.0f;
-        // the reference evaluates these with glibc at run time; volatile keeps
-        // the host compiler from folding them with a different rounding
-        volatile double th = -0.25 * kPi, al = 0.25 * kPi;
-        dev.cth = std::cos(th);
-        dev.sth = std::sin(th);
-        dev.cal = std::cos(al);
-        dev.sal = std::sin(al);
-        if (fam == FAM_WTA) {
-            std::vector<int> st;
-            for (int i = 0; i < wta.targets; ++i)
-                for (int k = 0; k < wta.strikes[i]; ++k) st.push_back(i);
-            dcap.alloc(wta.vehicles);
-            dstrikes.alloc(wta.targets);
-            dslot_target.alloc(st.size());
-            dp.alloc(wta.p.size());
-            CK(cudaMemcpy(dcap.p, wta.cap.data(), wta.vehicles * sizeof(int), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(dstrikes.p, wta.strikes.data(), wta.targets * sizeof(int), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(dslot_target.p, st.data(), st.size() * sizeof(int), cudaMemcpyHostToDevice));
-            CK(cudaMemcpy(dp.p, wta.p.data(), wta.p.size() * sizeof(double), cudaMemcpyHostToDevice));
-            dev.wta_targets = wta.targets;
-            dev.wta_vehicles = wta.vehicles;
-            dev.wta_slots = (int)st.size();
-            dev.wta_cap = dcap.p;
-            dev.wta_strikes = dstrikes.p;
-            dev.wta_slot_target = dslot_target.p;
-            dev.wta_p = dp.p;
-            if (wta.vehicles > kWtaMaxVehicles) throw std::invalid_argument("wta: too many vehicles");
-            int base = 0;
-            for (int v = 0; v < wta.vehicles; ++v) {
-                dev.wta_capv[v] = wta.cap[v];
-                dev.wta_base[v] = base;
-                base += wta.cap[v];
-            }
-            dev.wta_ncap = base;
-            // EvalWta scratch (32-bit words; its keys hold the slot in 8 bits:
-            // kWtaMaxSlots <= 256)
-            dev.wta_n32 = base + 2 * wta.vehicles + (d + 31) / 32;
-            dev.wta_n8 = (dev.wta_n32 + 1) / 2;
-        }
-    }
-};
-
-namespace {
 
 void make_wta(gmpea_problem& p, const WtaHost& w) {
     if (w.targets <= 0 || w.vehicles <= 0) throw std::invalid_argument("WTA: empty scenario");
@@ -368,13 +218,6 @@ __global__ void to_rows_kernel(const double* in, long long n, int k, float* out,
 }
 
 // columns [col0, col0 + k) of fp32 rows -> row-major f64 (n x k)
-__global__ void from_rows_kernel(const float* in, int rs, long long n, int col0, int k, double* out) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n * k) return;
-    const long long r = e / k;
-    const int c = (int)(e % k);
-    out[e] = (double)in[r * rs + col0 + c];
-}
 
 __global__ void fcv_from_rows_kernel(const double* F, const double* cv, long long n, int m, float4* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -384,15 +227,6 @@ __global__ void fcv_from_rows_kernel(const double* F, const double* cv, long lon
     out[i] = o;
 }
 
-__global__ void fcv_to_rows_kernel(const float4* in, long long n, int m, double* F, double* cv) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    float4 v = in[i];
-    F[i * m] = v.x;
-    F[i * m + 1] = v.y;
-    if (m > 2) F[i * m + 2] = v.z;
-    if (cv) cv[i] = v.w;
-}
 
 __global__ void u32_to_i32_kernel(const unsigned* in, long long n, int* out, int lim, int* err) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -402,9 +236,6 @@ __global__ void u32_to_i32_kernel(const unsigned* in, long long n, int* out, int
     out[e] = (int)v;
 }
 
-__global__ void init_state_kernel(DevState* st, int m) {
-    for (int k = 0; k < 4; ++k) st->zbits[k] = k < m ? 0xffffffffu : float_to_ordered(0.0f);
-}
 
 __global__ void set_z_kernel(DevState* st, int m, float z0, float z1, float z2) {
     st->zbits[0] = float_to_ordered(z0);
@@ -440,115 +271,28 @@ __global__ void slice_topology_kernel(const int* Bg, int t, long long e0, long l
     Bl[e] = (g >= r0 && g < r1) ? (int)(Bg[g * t + e % t] - e0) : (int)i;
 }
 
-// individuals as padded fp32 rows [x | g | pad] plus packed keys
-struct RowGeom {
-    int rs4;   // row stride, float4
-    int srs4;  // shared-memory row stride (odd float4 count)
-    int bs;    // vary_eval block size
-    int stream8;
-    size_t smem;
-};
+}  // namespace
 
-// stream8 > 0: a streaming evaluator (no staged row) with that many 64-bit
-// shared words per thread
-RowGeom row_geom(int d, int nc, int stream8 = 0) {
-    RowGeom g;
-    g.rs4 = (d + nc + 3) / 4;
-    g.srs4 = stream8 > 0 ? 0 : g.rs4 | 1;
-    g.stream8 = stream8;
-    const int per = stream8 > 0 ? stream8 * 8 : g.srs4 * 16;
-    g.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
-    g.smem = (size_t)g.bs * per;
-    if (g.smem > 48 * 1024) throw std::invalid_argument("problem rows too wide for the engine");
-    return g;
-}
+namespace gmpea_b200 {
+namespace host {
 
-struct PopBuf {
-    DevBuf<float4> X;  // n rows of rs4 float4
-    DevBuf<float4> Fcv;
-    void alloc(long long n, int rs4, long long ld) {
-        X.alloc((size_t)n * rs4);
-        Fcv.alloc(ld);
-    }
-};
-
-// ---------------------------------------------------------------- kernel dispatch
-using VaryKernel = void (*)(VaryParams);
-
-// the dimension-specialised generation kernels also assume uniform bounds
-// (true of every registered suite; checked by the caller)
-template <class Ev, int DC = 0, bool VARY_ONLY = false, bool UBF = false>
-VaryKernel pick_vary(int mode, int op, bool tour = false) {
-    if (tour) {  // the comparison algorithms: SBX children of tournament parents
-        constexpr bool UBT = DC > 0 || UBF;
-        return vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UBT, true>;
-    }
-    if (!VARY_ONLY) {
-        if (mode == MODE_EVAL) return vary_eval_kernel<Ev, MODE_EVAL, OP_SBX>;
-        if (mode == MODE_INIT) return vary_eval_kernel<Ev, MODE_INIT, OP_SBX>;
-    }
-    constexpr bool UB = DC > 0 || UBF;  // UBF: uniform bounds at a run-time dimension
-    return op == OP_DE ? vary_eval_kernel<Ev, MODE_VARY, OP_DE, DC, UB> : vary_eval_kernel<Ev, MODE_VARY, OP_SBX, DC, UB>;
-}
-
-// the generation kernel is compiled for the registered suites' dimension
-VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0, bool tour = false) {
+// the generation kernel is compiled per family (vary_<family>.cu) for the
+// registered suites' dimension
+VaryKernel vary_kernel_for(int fam, int mode, int op, int d, int id, bool tour) {
     tour = tour && mode == MODE_VARY;
     switch (fam) {
-        case FAM_LIR:
-            if (d != 30 || mode != MODE_VARY) return pick_vary<EvalLir>(mode, op, tour);
-            return id <= 4 ? pick_vary<EvalLirT<1>, 30, true>(mode, op, tour)
-                           : (id <= 8 ? pick_vary<EvalLirT<5>, 30, true>(mode, op, tour)
-                                      : (id <= 12 ? pick_vary<EvalLirT<9>, 30, true>(mode, op, tour)
-                                                  : pick_vary<EvalLirT<13>, 30, true>(mode, op, tour)));
-        case FAM_DTLZ:
-            return d == 7 ? pick_vary<EvalDtlz, 7>(mode, op, tour)
-                          : (d == 12 ? pick_vary<EvalDtlz, 12>(mode, op, tour) : pick_vary<EvalDtlz>(mode, op, tour));
-        case FAM_WTA:
-            return d > 0 && mode == MODE_VARY ? pick_vary<EvalWta, 0, true, true>(mode, op, tour)
-                                              : pick_vary<EvalWta>(mode, op, tour);
-        case FAM_DAS:
-            return d == 30 ? pick_vary<EvalDas, 30>(mode, op, tour) : pick_vary<EvalDas>(mode, op, tour);
-        default: return d == 15 ? pick_vary<EvalMw, 15>(mode, op, tour) : pick_vary<EvalMw>(mode, op, tour);
+        case FAM_LIR: return vary_kernel_lir(mode, op, d, id, tour);
+        case FAM_DTLZ: return vary_kernel_dtlz(mode, op, d, id, tour);
+        case FAM_WTA: return vary_kernel_wta(mode, op, d, id, tour);
+        case FAM_DAS: return vary_kernel_das(mode, op, d, id, tour);
+        default: return vary_kernel_mw(mode, op, d, id, tour);
     }
 }
 
-void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStream_t s) {
-    const RowGeom g = [&] {
-        RowGeom r;
-        r.rs4 = vp.rs4;
-        r.srs4 = vp.srs4;
-        const int per = vp.scratch8 > 0 ? vp.scratch8 * 8 : r.srs4 * 16;
-        r.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
-        r.smem = (size_t)r.bs * per;
-        return r;
-    }();
-    k<<<dim3(blocks_for(vp.row_end - vp.row0, g.bs), npops), g.bs, g.smem, s>>>(vp);
-}
+}  // namespace host
+}  // namespace gmpea_b200
 
-void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
-    vp.sbx_prob = prm.sbx_prob;
-    vp.sbx_e = (float)(1.0 / (prm.sbx_eta + 1.0));
-    vp.pm_e1 = (float)(prm.pm_eta + 1.0);
-    vp.pm_einv = (float)(1.0 / (prm.pm_eta + 1.0));
-    const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / (double)d;
-    // PM: skip iff u > pm with u = w 2^-32  <=>  mutate iff w <= floor(pm 2^32)
-    const double T = pm * 4294967296.0;
-    vp.pm_T = pm < 0.0 ? -1 : (long long)std::min(std::floor(T), 4294967295.0);
-    // DE: take iff u < CR  <=>  w < ceil(CR 2^32)  <=>  w <= ceil(CR 2^32) - 1
-    const double C = prm.de_cr * 4294967296.0;
-    vp.de_T = prm.de_cr >= 1.0 ? 0xffffffffll : (prm.de_cr <= 0.0 ? -1ll : (long long)std::ceil(C) - 1);
-    vp.uid = make_uidx((unsigned long long)d);
-    vp.de_f = (float)prm.de_f;
-}
-
-std::string rows_message(std::vector<int> rows) {
-    std::sort(rows.begin(), rows.end());
-    std::ostringstream os;
-    os << "evaluate: out-of-bounds rows:";
-    for (int r : rows) os << ' ' << r;
-    return os.str();
-}
+namespace {
 
 long long lattice_H(int m, long long n) {
     // reference_vectors: smallest H with C(H + m - 1, m - 1) >= n (gmpea.cpp:62-66)
@@ -1604,237 +1348,6 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
     });
 }
 
-// ---- metrics (metrics.hpp:15-29)
-namespace {
-
-__global__ void gather_rows_kernel(const double* F, const long long* idx, long long k, int m, double* out) {
-    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= k) return;
-    for (int c = 0; c < m; ++c) out[r * m + c] = F[idx[r] * m + c];
-}
-
-// nondominated + deduplicated subset of the candidate rows `cand` of F (n x m,
-// device, row-major); returns the kept row ids sorted lexicographically by F
-// dedup = 0 (m = 3 only): equal rows are all kept, as fronts.cpp:34-41 does
-thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::device_vector<long long>& cand,
-                                              int dedup = 1) {
-    const long long k = (long long)cand.size();
-    thrust::device_vector<long long> kept;
-    if (k == 0) return kept;
-    thrust::sort(thrust::device, cand.begin(), cand.end(), LexLess{dF, m});
-    thrust::device_vector<long long> gs(k);
-    const long long* order = thrust::raw_pointer_cast(cand.data());
-    group_start_kernel<<<blocks_for(k, 256), 256>>>(dF, order, k, m, thrust::raw_pointer_cast(gs.data()));
-    thrust::device_vector<unsigned char> keep(k);
-    if (m == 2) {
-        thrust::device_vector<double> col(k);
-        gather_col_kernel<<<blocks_for(k, 256), 256>>>(dF, order, k, m, 1, thrust::raw_pointer_cast(col.data()));
-        thrust::inclusive_scan(thrust::device, col.begin(), col.end(), col.begin(), thrust::minimum<double>());
-        nd2_kernel<<<blocks_for(k, 256), 256>>>(dF, order, thrust::raw_pointer_cast(gs.data()),
-                                                thrust::raw_pointer_cast(col.data()), k,
-                                                thrust::raw_pointer_cast(keep.data()));
-    } else {
-        nd3_kernel<<<blocks_for(k, 256), 256>>>(dF, order, thrust::raw_pointer_cast(gs.data()), k,
-                                                thrust::raw_pointer_cast(keep.data()), dedup);
-    }
-    CK(cudaGetLastError());
-    kept.resize(k);
-    auto end = thrust::copy_if(thrust::device, cand.begin(), cand.end(), keep.begin(), kept.begin(),
-                               NonZero{});
-    kept.resize(end - kept.begin());
-    return kept;
-}
-
-}  // namespace
-
-int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, int64_t cap, int64_t* rows) {
-    return guarded([&] {
-        if (n_points < 0) throw std::invalid_argument("pf_reference: negative point count");
-        PfParams pp{};
-        if (p->fam == FAM_LIR) {
-            pp.kind = PF_LIR;
-        } else if (p->fam == FAM_DTLZ) {
-            const int id = p->id;
-            if (id == C1_DTLZ1 || id == DC1_DTLZ1 || id == DC2_DTLZ1 || id == DC3_DTLZ1) {
-                pp.kind = PF_DTLZ1;  // problems.cpp:436, 520
-            } else if (id == C3_DTLZ4) {
-                pp.kind = PF_SPHERE;  // problems.cpp:484-486
-                pp.alpha = 100.0;
-                pp.rnum = 0.0;
-                pp.rden = 1.0;
-            } else {
-                pp.kind = PF_SPHERE;  // problems.cpp:447-449, 469-471, 522-524
-                pp.alpha = 1.0;
-                pp.rnum = 1.0;
-                pp.rden = 0.0;
-            }
-        } else if (p->fam == FAM_MW || p->fam == FAM_DAS) {
-            pp.kind = PF_LEVEL;  // restated fronts (no reference counterpart)
-        } else {
-            throw std::runtime_error("pf_reference: no analytic front for " + p->name +
-                                     "; use the hypervolume metric instead");
-        }
-        if (p->d > kPfMaxD) throw std::invalid_argument("pf_reference: dimension too large");
-        require_device();
-        const int m = p->m;
-        pp.P = p->dev;
-        // fronts.cpp:60-84
-        long long over = std::max<long long>(8 * n_points, 2000);
-        if (m >= 3) over = std::min<long long>(over, 12000);
-        auto emit = [&](const std::vector<double>& h, long long nrows) {
-            if (nrows > cap) throw std::invalid_argument("pf_reference: output capacity too small");
-            if (out && nrows) std::copy(h.begin(), h.begin() + nrows * m, out);
-            *rows = nrows;
-        };
-        for (int attempt = 0; attempt < 4; ++attempt) {
-            pp.n_samples = over;
-            if ((pp.kind == PF_LIR && p->id <= 12) || (pp.kind == PF_LEVEL && m == 2)) {
-                pp.rows = over;
-            } else if (pp.kind == PF_LEVEL) {
-                long long side = 1;
-                while (side * side < over) ++side;
-                pp.h = side;
-                pp.rows = side * side;
-            } else {
-                long long h = 1;
-                while ((h + 1) * (h + 2) / 2 < over) ++h;  // simplex_weights (problems.cpp:205-218)
-                pp.h = h;
-                pp.rows = (h + 1) * (h + 2) / 2;
-            }
-            thrust::device_vector<double> dF(pp.rows * m);
-            thrust::device_vector<unsigned char> feas(pp.rows);
-            thrust::device_vector<int> noob(1, 0);
-            pp.F = thrust::raw_pointer_cast(dF.data());
-            pp.feas = thrust::raw_pointer_cast(feas.data());
-            pp.n_oob = thrust::raw_pointer_cast(noob.data());
-            pf_candidates_kernel<<<blocks_for(pp.rows, 128), 128>>>(pp);
-            CK(cudaGetLastError());
-            if ((int)noob[0]) throw std::invalid_argument("evaluate: front candidate rows out of bounds");
-            thrust::device_vector<long long> cand(pp.rows);
-            auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                                       thrust::counting_iterator<long long>(pp.rows), feas.begin(), cand.begin(),
-                                       NonZero{});
-            cand.resize(end - cand.begin());
-            if ((long long)cand.size() >= std::max<long long>(n_points, 1)) {
-                // nondominated_rows (fronts.cpp:15-42): m = 2 drops duplicates, m = 3 keeps them
-                auto kept = front_filter(pp.F, m, cand, m == 2 ? 1 : 0);  // lexicographic order
-                const long long nk = (long long)kept.size();
-                const bool enough = nk >= n_points;
-                if (enough || attempt == 3) {
-                    std::vector<double> h;
-                    if (!enough || nk <= n_points || n_points == 0) {
-                        // the filtered rows in their original order (subsample_front returns F)
-                        thrust::sort(thrust::device, kept.begin(), kept.end());
-                        thrust::device_vector<double> o(nk * m);
-                        gather_rows_kernel<<<blocks_for(nk, 256), 256>>>(pp.F, thrust::raw_pointer_cast(kept.data()),
-                                                                        nk, m, thrust::raw_pointer_cast(o.data()));
-                        h.resize(nk * m);
-                        thrust::copy(o.begin(), o.end(), h.begin());
-                        emit(h, nk);
-                    } else {
-                        // subsample_front (fronts.cpp:86-103): stable lexicographic order, even picks
-                        thrust::device_vector<double> o(n_points * m);
-                        pf_pick_kernel<<<blocks_for(n_points, 256), 256>>>(
-                            pp.F, thrust::raw_pointer_cast(kept.data()), nk, n_points, m,
-                            thrust::raw_pointer_cast(o.data()));
-                        h.resize(n_points * m);
-                        thrust::copy(o.begin(), o.end(), h.begin());
-                        emit(h, n_points);
-                    }
-                    CK(cudaGetLastError());
-                    return;
-                }
-            }
-            over *= 4;
-            if (m >= 3) over = std::min<long long>(over, 50000);
-        }
-        throw std::runtime_error("pf_reference: could not build a feasible front for " + p->name);
-    });
-}
-
-int gmpea_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx, int64_t* count) {
-    return guarded([&] {
-        if (m < 2 || m > 3) throw std::invalid_argument("metric_front: m must be 2 or 3");
-        *count = 0;
-        if (n <= 0) return;
-        require_device();
-        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n);
-        thrust::device_vector<long long> cand(n);
-        auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                                   thrust::counting_iterator<long long>(n), cand.begin(),
-                                   IsFeasible{thrust::raw_pointer_cast(dcv.data())});
-        cand.resize(end - cand.begin());
-        auto kept = front_filter(thrust::raw_pointer_cast(dF.data()), m, cand);
-        thrust::sort(thrust::device, kept.begin(), kept.end());
-        std::vector<long long> h(kept.size());
-        thrust::copy(kept.begin(), kept.end(), h.begin());
-        for (size_t i = 0; i < h.size(); ++i) idx[i] = h[i];
-        *count = (int64_t)h.size();
-    });
-}
-
-int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t m, double* out) {
-    return guarded([&] {
-        if (nr <= 0) throw std::invalid_argument("igd: empty reference front");
-        if (na <= 0) {
-            *out = std::numeric_limits<double>::infinity();
-            return;
-        }
-        if (m < 1 || m > 3) throw std::invalid_argument("igd: objective count mismatch");
-        require_device();
-        thrust::device_vector<double> dA(A, A + na * m), dR(R, R + nr * m), res(1);
-        thrust::device_vector<unsigned long long> best(nr, 0x7ff0000000000000ull);  // +inf
-        int gx = (int)std::min<long long>(blocks_for(na, 256), 64);
-        igd_min_kernel<<<dim3(gx, (unsigned)nr), 256>>>(thrust::raw_pointer_cast(dA.data()), na,
-                                                         thrust::raw_pointer_cast(dR.data()), nr, m,
-                                                         thrust::raw_pointer_cast(best.data()));
-        igd_sum_kernel<<<1, 1>>>(thrust::raw_pointer_cast(best.data()), nr, thrust::raw_pointer_cast(res.data()));
-        CK(cudaGetLastError());
-        *out = res[0];
-    });
-}
-
-int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, double* out) {
-    return guarded([&] {
-        if (m < 2 || m > 3) throw std::invalid_argument("hypervolume: m must be 2 or 3 on device");
-        *out = 0.0;
-        if (n <= 0) return;
-        require_device();
-        thrust::device_vector<double> dP(P, P + n * m), dref(ref, ref + m);
-        const double* pP = thrust::raw_pointer_cast(dP.data());
-        thrust::device_vector<long long> cand(n);
-        auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                                   thrust::counting_iterator<long long>(n), cand.begin(),
-                                   InsideBox{pP, thrust::raw_pointer_cast(dref.data()), m});
-        cand.resize(end - cand.begin());
-        auto xy = front_filter(pP, m, cand);  // hv_relevant, sorted by (x, y[, z])
-        const long long cnt = (long long)xy.size();
-        if (cnt == 0) return;
-        thrust::device_vector<double> slab(m == 2 ? 1 : cnt), res(1);
-        thrust::device_vector<long long> zorder, zrank;
-        if (m == 3) {
-            zorder = xy;
-            thrust::sort(thrust::device, zorder.begin(), zorder.end(), ZLess{pP});
-            zrank.resize(n);
-            thrust::scatter(thrust::device, thrust::counting_iterator<long long>(0),
-                            thrust::counting_iterator<long long>(cnt), zorder.begin(), zrank.begin());
-        }
-        hv_slab_kernel<<<blocks_for(m == 2 ? 1 : cnt, 128), 128>>>(
-            pP, thrust::raw_pointer_cast(xy.data()), m == 3 ? thrust::raw_pointer_cast(zrank.data()) : nullptr,
-            cnt, m, m == 2 ? 1 : cnt, thrust::raw_pointer_cast(dref.data()), thrust::raw_pointer_cast(slab.data()));
-        CK(cudaGetLastError());
-        if (m == 2) {
-            *out = slab[0];
-            return;
-        }
-        hv3_sum_kernel<<<1, 1>>>(pP, thrust::raw_pointer_cast(zorder.data()), cnt,
-                                 thrust::raw_pointer_cast(dref.data()), thrust::raw_pointer_cast(slab.data()),
-                                 thrust::raw_pointer_cast(res.data()));
-        CK(cudaGetLastError());
-        *out = res[0];
-    });
-}
-
 int gmpea_run_config_default(gmpea_run_config* c) {
     // RunConfig defaults (gmpea.hpp:113-127)
     *c = gmpea_run_config{};
@@ -1966,709 +1479,3 @@ int gmpea_engine_device_buffers(gmpea_engine* e, gmpea_device_buffers* o) {
 }
 
 }  // extern "C"
-
-// ---- comparison-algorithm operators (baselines.hpp; baselines.cu kernels in baselines.cuh)
-namespace {
-
-struct PosLess {  // rows of F at front positions, lexicographic, then position
-    const double* F;
-    const long long* front;
-    int m;
-    __host__ __device__ bool operator()(long long a, long long b) const {
-        for (int c = 0; c < m; ++c) {
-            const double x = F[front[a] * m + c], y = F[front[b] * m + c];
-            if (x < y) return true;
-            if (x > y) return false;
-        }
-        return a < b;
-    }
-};
-
-__global__ void dup_zero_kernel(const double* F, const long long* front, const long long* order, long long k, int m,
-                                double* dist) {
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q == 0 || q >= k) return;
-    const long long a = front[order[q]], b = front[order[q - 1]];
-    for (int c = 0; c < m; ++c)
-        if (!(F[a * m + c] == F[b * m + c])) return;
-    dist[order[q]] = 0.0;  // an earlier position holds the same row (baselines.cpp:84-90)
-}
-
-__global__ void gather_col_pos_kernel(const double* F, const long long* front, long long k, int m, int c,
-                                      double* out) {
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < k) out[q] = F[front[q] * m + c];
-}
-
-struct FitBelowOne {
-    const double* fit;
-    __host__ __device__ bool operator()(long long i) const { return fit[i] < 1.0; }
-};
-struct FitAtLeastOne {
-    const double* fit;
-    __host__ __device__ bool operator()(long long i) const { return fit[i] >= 1.0; }
-};
-struct IsInfeasible {
-    const double* cv;
-    __host__ __device__ bool operator()(long long i) const { return cv[i] > 0.0; }
-};
-
-void check_cdp_cv(const double* cv, int64_t n, int32_t use_cdp) {
-    if (!use_cdp || n < 2) return;
-    for (int64_t i = 0; i < n; ++i)
-        if (cv[i] < 0.0) throw std::invalid_argument("cdp_better: negative constraint violation");
-}
-
-// Pareto ranks of the rows `sub` by front peeling; returns the front count
-long long peel_ranks(const DomRel& R, thrust::device_vector<long long>& sub, thrust::device_vector<long long>& rank) {
-    const long long ns = (long long)sub.size();
-    if (ns == 0) return 0;
-    thrust::device_vector<int> cnt(ns), fsz(1, 0), nsz(1, 0);
-    thrust::device_vector<long long> front(ns), next(ns);
-    const long long* ps = thrust::raw_pointer_cast(sub.data());
-    nds_count_kernel<<<blocks_for(ns, 128), 128>>>(R, ps, ns, thrust::raw_pointer_cast(cnt.data()));
-    nds_front0_kernel<<<blocks_for(ns, 256), 256>>>(thrust::raw_pointer_cast(cnt.data()), ns,
-                                                    thrust::raw_pointer_cast(front.data()),
-                                                    thrust::raw_pointer_cast(fsz.data()));
-    CK(cudaGetLastError());
-    long long fsize = (int)fsz[0], r = 0;
-    while (fsize > 0) {
-        // fronts are sets: the order of `next` (atomic) does not affect ranks
-        nds_set_rank_kernel<<<blocks_for(fsize, 256), 256>>>(ps, thrust::raw_pointer_cast(front.data()), fsize, r,
-                                                             thrust::raw_pointer_cast(rank.data()));
-        nsz[0] = 0;
-        nds_peel_kernel<<<blocks_for(fsize * ns, 256), 256>>>(R, ps, ns, thrust::raw_pointer_cast(front.data()), fsize,
-                                                              thrust::raw_pointer_cast(cnt.data()),
-                                                              thrust::raw_pointer_cast(next.data()),
-                                                              thrust::raw_pointer_cast(nsz.data()));
-        CK(cudaGetLastError());
-        fsize = (int)nsz[0];
-        front.swap(next);
-        ++r;
-    }
-    return r;
-}
-
-// spea2_fitness on device arrays (baselines.cpp:93-127)
-void spea2_fitness_dev(const double* dF, const double* dcv, int64_t n, int32_t m, int32_t use_cdp, double* dfit) {
-    if (n == 0) return;
-    DomRel R{dF, dcv, m, use_cdp};
-    thrust::device_vector<double> strength(n), raw(n);
-    spea2_strength_kernel<<<blocks_for(n, 128), 128>>>(R, n, thrust::raw_pointer_cast(strength.data()));
-    spea2_raw_kernel<<<blocks_for(n, 128), 128>>>(R, n, thrust::raw_pointer_cast(strength.data()),
-                                                  thrust::raw_pointer_cast(raw.data()));
-    size_t k = (size_t)std::sqrt((double)n);
-    if (k >= (size_t)n) k = n > 1 ? n - 1 : 0;
-    const long long nd = n - 1;  // distances per row
-    const long long kk = nd > 0 ? (long long)(k < (size_t)nd ? k : nd - 1) : 0;
-    spea2_sigma_kernel<<<(unsigned)n, 256>>>(dF, m, n, kk, thrust::raw_pointer_cast(raw.data()), dfit);
-    CK(cudaGetLastError());
-}
-
-}  // namespace
-
-namespace {
-
-// nondominated_sort on device arrays (baselines.cpp:22-55)
-void nds_dev(const double* dF, const double* dcv, int64_t n, int32_t m, int32_t use_cdp,
-             thrust::device_vector<long long>& drank) {
-    drank.assign(n, 0);
-    if (n <= 0) return;
-    thrust::device_vector<long long> sub(n);
-    DomRel R{dF, dcv, m, 0};
-    if (use_cdp) {
-        auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                                   thrust::counting_iterator<long long>(n), sub.begin(), IsFeasible{dcv});
-        sub.resize(end - sub.begin());
-    } else {
-        thrust::sequence(thrust::device, sub.begin(), sub.end());
-    }
-    const long long rf = peel_ranks(R, sub, drank);
-    if (!use_cdp) return;
-    thrust::device_vector<long long> inf(n);
-    auto e = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                             thrust::counting_iterator<long long>(n), inf.begin(), IsInfeasible{dcv});
-    const long long ni = e - inf.begin();
-    if (!ni) return;
-    thrust::device_vector<double> u(ni);
-    thrust::gather(thrust::device, inf.begin(), inf.begin() + ni, thrust::device_pointer_cast(dcv), u.begin());
-    thrust::sort(thrust::device, u.begin(), u.end());
-    const long long nu = thrust::unique(thrust::device, u.begin(), u.end()) - u.begin();
-    nds_infeasible_rank_kernel<<<blocks_for(n, 256), 256>>>(dcv, n, thrust::raw_pointer_cast(u.data()), nu, rf,
-                                                            thrust::raw_pointer_cast(drank.data()));
-    CK(cudaGetLastError());
-}
-
-// crowding_distance on device arrays (baselines.cpp:56-91) for the rows dfront[0..k)
-void crowd_dev(const double* pF, int32_t m, const long long* pf, int64_t k, thrust::device_vector<double>& dd) {
-    dd.assign(k, 0.0);
-    if (k <= 0) return;
-    if (k <= 2) {
-        thrust::fill(thrust::device, dd.begin(), dd.end(), std::numeric_limits<double>::infinity());
-        return;
-    }
-    thrust::device_vector<double> key(k);
-    thrust::device_vector<long long> order(k);
-    for (int c = 0; c < m; ++c) {
-        thrust::sequence(thrust::device, order.begin(), order.end());
-        gather_col_pos_kernel<<<blocks_for(k, 256), 256>>>(pF, pf, k, m, c, thrust::raw_pointer_cast(key.data()));
-        thrust::stable_sort_by_key(thrust::device, key.begin(), key.end(), order.begin());
-        crowd_axis_kernel<<<blocks_for(k, 256), 256>>>(pF, m, c, pf, thrust::raw_pointer_cast(order.data()), k,
-                                                       thrust::raw_pointer_cast(dd.data()));
-    }
-    thrust::sequence(thrust::device, order.begin(), order.end());
-    thrust::sort(thrust::device, order.begin(), order.end(), PosLess{pF, pf, m});
-    dup_zero_kernel<<<blocks_for(k, 256), 256>>>(pF, pf, thrust::raw_pointer_cast(order.data()), k, m,
-                                                 thrust::raw_pointer_cast(dd.data()));
-    CK(cudaGetLastError());
-}
-
-// spea2_select on device arrays (baselines.cpp:129-189); kept rows ascending
-std::vector<long long> spea2_select_dev(const double* pF, const double* pcv, int64_t n, int32_t m, int32_t use_cdp,
-                                        int64_t capacity) {
-    std::vector<long long> out;
-    if (n <= 0) return out;
-    thrust::device_vector<double> dfit(n);
-    double* pfit = thrust::raw_pointer_cast(dfit.data());
-    spea2_fitness_dev(pF, pcv, n, m, use_cdp, pfit);
-    thrust::device_vector<long long> kp(n);
-    auto e = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                             thrust::counting_iterator<long long>(n), kp.begin(), FitBelowOne{pfit});
-    long long nk = e - kp.begin();
-    if (nk < capacity) {
-        // fill with the dominated rows, lowest fitness first (stable)
-        thrust::device_vector<long long> rest(n);
-        auto e2 = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                                  thrust::counting_iterator<long long>(n), rest.begin(), FitAtLeastOne{pfit});
-        const long long nr = e2 - rest.begin();
-        thrust::device_vector<double> rf(nr);
-        thrust::gather(thrust::device, rest.begin(), rest.begin() + nr, dfit.begin(), rf.begin());
-        thrust::stable_sort_by_key(thrust::device, rf.begin(), rf.end(), rest.begin());
-        const long long take = std::min<long long>(nr, capacity - nk);
-        std::vector<long long> a(nk), b(take);
-        thrust::copy(kp.begin(), kp.begin() + nk, a.begin());
-        thrust::copy(rest.begin(), rest.begin() + take, b.begin());
-        out = a;
-        out.insert(out.end(), b.begin(), b.end());
-        std::sort(out.begin(), out.end());
-        return out;
-    }
-    // serial truncation (baselines.cpp:149-184) in one persistent block
-    thrust::device_vector<unsigned char> alive(n, 0);
-    thrust::device_vector<double> n1(nk), n2(nk), lv(nk);
-    thrust::device_vector<long long> i1(nk), i2(nk), cand(nk);
-    thrust::fill(thrust::device, thrust::make_permutation_iterator(alive.begin(), kp.begin()),
-                 thrust::make_permutation_iterator(alive.begin(), kp.begin() + nk), (unsigned char)1);
-    const long long* pk = thrust::raw_pointer_cast(kp.data());
-    unsigned char* pa = thrust::raw_pointer_cast(alive.data());
-    if (nk > capacity) {
-        trunc_init_kernel<<<blocks_for(nk, 128), 128>>>(pF, m, pk, nk, pa, thrust::raw_pointer_cast(n1.data()),
-                                                        thrust::raw_pointer_cast(i1.data()),
-                                                        thrust::raw_pointer_cast(n2.data()),
-                                                        thrust::raw_pointer_cast(i2.data()));
-        trunc_loop_kernel<<<1, 1024>>>(pF, m, pk, nk, capacity, pa, thrust::raw_pointer_cast(n1.data()),
-                                       thrust::raw_pointer_cast(i1.data()), thrust::raw_pointer_cast(n2.data()),
-                                       thrust::raw_pointer_cast(i2.data()), thrust::raw_pointer_cast(lv.data()),
-                                       thrust::raw_pointer_cast(cand.data()));
-        CK(cudaGetLastError());
-    }
-    std::vector<unsigned char> h(n);
-    thrust::copy(alive.begin(), alive.end(), h.begin());
-    for (int64_t i = 0; i < n; ++i)
-        if (h[i]) out.push_back(i);
-    return out;
-}
-
-}  // namespace
-
-int gmpea_nondominated_sort(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp,
-                            int64_t* rank) {
-    return guarded([&] {
-        if (m < 1) throw std::invalid_argument("nondominated_sort: no objectives");
-        check_cdp_cv(cv, n, use_cdp);
-        if (n <= 0) return;
-        require_device();
-        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n);
-        thrust::device_vector<long long> drank;
-        nds_dev(thrust::raw_pointer_cast(dF.data()), thrust::raw_pointer_cast(dcv.data()), n, m, use_cdp, drank);
-        std::vector<long long> h(n);
-        thrust::copy(drank.begin(), drank.end(), h.begin());
-        for (int64_t i = 0; i < n; ++i) rank[i] = h[i];
-    });
-}
-
-int gmpea_crowding_distance(const double* F, int64_t n, int32_t m, const int64_t* front, int64_t k, double* dist) {
-    return guarded([&] {
-        if (k <= 0) return;
-        if (k <= 2) {
-            for (int64_t q = 0; q < k; ++q) dist[q] = std::numeric_limits<double>::infinity();
-            return;
-        }
-        for (int64_t q = 0; q < k; ++q)
-            if (front[q] < 0 || front[q] >= n) throw std::invalid_argument("crowding_distance: front index out of range");
-        require_device();
-        thrust::device_vector<double> dF(F, F + n * m), dd;
-        thrust::device_vector<long long> fr(front, front + k);
-        crowd_dev(thrust::raw_pointer_cast(dF.data()), m, thrust::raw_pointer_cast(fr.data()), k, dd);
-        thrust::copy(dd.begin(), dd.end(), dist);
-    });
-}
-
-int gmpea_spea2_fitness(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, double* fit) {
-    return guarded([&] {
-        check_cdp_cv(cv, n, use_cdp);
-        if (n <= 0) return;
-        require_device();
-        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n), dfit(n);
-        spea2_fitness_dev(thrust::raw_pointer_cast(dF.data()), thrust::raw_pointer_cast(dcv.data()), n, m, use_cdp,
-                          thrust::raw_pointer_cast(dfit.data()));
-        thrust::copy(dfit.begin(), dfit.end(), fit);
-    });
-}
-
-int gmpea_spea2_select(const double* F, const double* cv, int64_t n, int32_t m, int32_t use_cdp, int64_t capacity,
-                       int64_t* keep, int64_t* count) {
-    return guarded([&] {
-        check_cdp_cv(cv, n, use_cdp);
-        *count = 0;
-        if (n <= 0) return;
-        if (capacity < 0) throw std::invalid_argument("spea2_select: negative capacity");
-        require_device();
-        thrust::device_vector<double> dF(F, F + n * m), dcv(cv, cv + n);
-        auto out = spea2_select_dev(thrust::raw_pointer_cast(dF.data()), thrust::raw_pointer_cast(dcv.data()), n, m,
-                                    use_cdp, capacity);
-        for (size_t i = 0; i < out.size(); ++i) keep[i] = out[i];
-        *count = (int64_t)out.size();
-    });
-}
-
-// ---- comparison algorithms as runs: run_cnsga2 / run_ccmo (baselines.cpp:320-459)
-namespace {
-
-__global__ void take_rows_kernel(const float4* X0, const float4* K0, const float4* X1, const float4* K1,
-                                 const float4* X2, const float4* K2, long long n, const long long* idx, long long k,
-                                 int rs4, float4* dX, float4* dK) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= k * rs4) return;
-    const long long r = e / rs4;
-    const int q = (int)(e - r * rs4);
-    const long long src = idx[r], s = src / n, row = src - s * n;
-    const float4* X = s == 0 ? X0 : (s == 1 ? X1 : X2);
-    const float4* K = s == 0 ? K0 : (s == 1 ? K1 : K2);
-    dX[r * rs4 + q] = X[row * rs4 + q];
-    if (q == 0) dK[r] = K[row];
-}
-
-__global__ void col_kernel(const double* F, long long n, int m, int c, double* out) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) out[i] = F[i * m + c];
-}
-
-__device__ __forceinline__ void seg_of(const long long* rs, long long n, long long q, long long& lo, long long& hi) {
-    const long long r = rs[q];
-    long long a = 0, b = q;  // first position with rank r
-    while (a < b) {
-        const long long mid = (a + b) / 2;
-        if (rs[mid] < r)
-            a = mid + 1;
-        else
-            b = mid;
-    }
-    lo = a;
-    a = q;
-    b = n - 1;  // last position with rank r
-    while (a < b) {
-        const long long mid = (a + b + 1) / 2;
-        if (rs[mid] > r)
-            b = mid - 1;
-        else
-            a = mid;
-    }
-    hi = a;
-}
-
-// crowding of every front at once: positions grouped by rank, F[:, c]-sorted
-// within a front (stable: index order on ties), as crowding_distance sees them
-__global__ void crowd_seg_kernel(const double* F, int m, int c, const long long* order, const long long* rs,
-                                 long long n, double* crowd) {
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
-    long long lo, hi;
-    seg_of(rs, n, q, lo, hi);
-    const double inf = 1.0 / 0.0;
-    if (hi - lo + 1 <= 2 || q == lo || q == hi) {
-        crowd[order[q]] = inf;
-        return;
-    }
-    const double flo = F[order[lo] * m + c], fhi = F[order[hi] * m + c];
-    if (fhi == flo) return;
-    crowd[order[q]] += (F[order[q + 1] * m + c] - F[order[q - 1] * m + c]) / (fhi - flo);
-}
-
-struct RankRowLess {
-    const double* F;
-    const long long* rank;
-    int m;
-    __host__ __device__ bool operator()(long long a, long long b) const {
-        if (rank[a] != rank[b]) return rank[a] < rank[b];
-        for (int c = 0; c < m; ++c) {
-            const double x = F[a * m + c], y = F[b * m + c];
-            if (x < y) return true;
-            if (x > y) return false;
-        }
-        return a < b;
-    }
-};
-
-__global__ void crowd_dup_kernel(const double* F, int m, const long long* order, const long long* rs, long long n,
-                                 double* crowd) {
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q == 0 || q >= n || rs[q] != rs[q - 1]) return;
-    long long lo, hi;
-    seg_of(rs, n, q, lo, hi);
-    if (hi - lo + 1 <= 2) return;  // crowding_distance returns before its duplicate pass
-    const long long a = order[q], b = order[q - 1];
-    for (int c = 0; c < m; ++c)
-        if (!(F[a * m + c] == F[b * m + c])) return;
-    crowd[a] = 0.0;
-}
-
-// crowding distance of every row within its own front (run_cnsga2's tournament keys)
-void crowd_all_dev(const double* pF, int64_t n, int32_t m, const thrust::device_vector<long long>& rank,
-                   thrust::device_vector<double>& crowd) {
-    crowd.assign(n, 0.0);
-    thrust::device_vector<double> key(n);
-    thrust::device_vector<long long> order(n), rs(n);
-    const long long* pr = thrust::raw_pointer_cast(rank.data());
-    for (int c = 0; c < m; ++c) {
-        thrust::sequence(thrust::device, order.begin(), order.end());
-        col_kernel<<<blocks_for(n, 256), 256>>>(pF, n, m, c, thrust::raw_pointer_cast(key.data()));
-        thrust::stable_sort_by_key(thrust::device, key.begin(), key.end(), order.begin());
-        thrust::gather(thrust::device, order.begin(), order.end(), rank.begin(), rs.begin());
-        thrust::stable_sort_by_key(thrust::device, rs.begin(), rs.end(), order.begin());
-        crowd_seg_kernel<<<blocks_for(n, 256), 256>>>(pF, m, c, thrust::raw_pointer_cast(order.data()),
-                                                      thrust::raw_pointer_cast(rs.data()), n,
-                                                      thrust::raw_pointer_cast(crowd.data()));
-    }
-    thrust::sequence(thrust::device, order.begin(), order.end());
-    thrust::sort(thrust::device, order.begin(), order.end(), RankRowLess{pF, pr, m});
-    thrust::gather(thrust::device, order.begin(), order.end(), rank.begin(), rs.begin());
-    crowd_dup_kernel<<<blocks_for(n, 256), 256>>>(pF, m, thrust::raw_pointer_cast(order.data()),
-                                                  thrust::raw_pointer_cast(rs.data()), n,
-                                                  thrust::raw_pointer_cast(crowd.data()));
-    CK(cudaGetLastError());
-}
-
-struct CvIsZero {
-    __host__ __device__ bool operator()(double v) const { return v == 0.0; }
-};
-
-// igd(metric_front(pop), ref) on device arrays (metrics.cpp:42-60, 155-175);
-// +inf for an empty front, as the reference's IGD hook records it
-double igd_dev(const double* dF, const double* dcv, long long n, int m, const double* dR, long long nr) {
-    thrust::device_vector<long long> cand(n);
-    auto end = thrust::copy_if(thrust::device, thrust::counting_iterator<long long>(0),
-                               thrust::counting_iterator<long long>(n), cand.begin(), IsFeasible{dcv});
-    cand.resize(end - cand.begin());
-    auto kept = front_filter(dF, m, cand);
-    const long long na = (long long)kept.size();
-    if (na == 0) return std::numeric_limits<double>::infinity();
-    thrust::sort(thrust::device, kept.begin(), kept.end());  // metric_front keeps row order
-    thrust::device_vector<double> A(na * m), res(1);
-    gather_rows_kernel<<<blocks_for(na, 256), 256>>>(dF, thrust::raw_pointer_cast(kept.data()), na, m,
-                                                    thrust::raw_pointer_cast(A.data()));
-    thrust::device_vector<unsigned long long> best(nr, 0x7ff0000000000000ull);
-    const int gx = (int)std::min<long long>(blocks_for(na, 256), 64);
-    igd_min_kernel<<<dim3(gx, (unsigned)nr), 256>>>(thrust::raw_pointer_cast(A.data()), na, dR, nr, m,
-                                                     thrust::raw_pointer_cast(best.data()));
-    igd_sum_kernel<<<1, 1>>>(thrust::raw_pointer_cast(best.data()), nr, thrust::raw_pointer_cast(res.data()));
-    CK(cudaGetLastError());
-    return res[0];
-}
-
-struct BaselineRun {
-    const gmpea_problem* p;
-    gmpea_run_config c;
-    int algo, d, m, nc, npop;
-    long long n;
-    RowGeom geo;
-    PopBuf pop[2], off[2], nxt[2], prev[2];
-    DevBuf<DevState> st;
-    DevBuf<int> bad[2];
-    VaryParams vp{};
-    VaryKernel init_k = nullptr, vary_k = nullptr;
-    std::vector<gmpea_gen_record> hist;
-    long long evals = 0;
-    double loop_s = 0.0;
-    thrust::device_vector<double> igd_ref;  // optional IGD hook front (experiment.cpp:200-205)
-    long long n_ref = 0;
-    gmpea_pop_hook hook = nullptr;          // optional host metric hook
-    void* hook_user = nullptr;
-
-    void setup(const gmpea_problem* prob, int a, const gmpea_run_config& cfg) {
-        p = prob;
-        c = cfg;
-        algo = a;
-        if (algo != 0 && algo != 1) throw std::invalid_argument("run_baseline: unknown algorithm");
-        if (cfg.n <= 0) throw std::invalid_argument("run_baseline: population size must be positive");
-        n = cfg.n;
-        d = p->d;
-        m = p->m;
-        nc = p->nin + p->neq;
-        npop = algo == 1 ? 2 : 1;
-        CK(cudaSetDevice(cfg.device));
-        geo = row_geom(d, nc, p->fam == FAM_WTA ? p->dev.wta_n8 : 0);
-        for (int q = 0; q < npop; ++q) {
-            pop[q].alloc(n, geo.rs4, n);
-            off[q].alloc(n, geo.rs4, n);
-            nxt[q].alloc(n, geo.rs4, n);
-            bad[q].alloc(kMaxBadRows);
-            if (c.time_budget_s > 0) prev[q].alloc(n, geo.rs4, n);
-        }
-        st.alloc(1);
-        st.zero(0);
-        init_state_kernel<<<1, 1>>>(st.p, m);
-        vp.n = (int)n;
-        vp.row0 = 0;
-        vp.row_end = (int)n;
-        vp.rs4 = geo.rs4;
-        vp.srs4 = geo.srs4;
-        vp.scratch8 = geo.stream8;
-        vp.pop_id[0] = 1;
-        vp.pop_id[1] = 2;
-        vp.P = p->dev;
-        vp.key = make_philox_key(c.seed);
-        fill_op_params(vp, c.params, d);
-        vp.eval = 1;
-        vp.update_z = 0;
-        vp.st = st.p;
-        vp.bad_cap = kMaxBadRows;
-        vp.tour = algo == 0 ? 1 : 2;
-        vp.un = make_uidx((unsigned long long)n);
-        for (int q = 0; q < npop; ++q) vp.bad_rows[q] = bad[q].p;
-        init_k = vary_kernel_for(p->fam, MODE_INIT, 0);
-        vary_k = vary_kernel_for(p->fam, MODE_VARY, OP_SBX, p->dev.uniform ? d : 0, p->dev.id, true);
-    }
-
-    void check() {
-        DevState h{};
-        CK(cudaMemcpy(&h, st.p, sizeof(DevState), cudaMemcpyDeviceToHost));
-        if (!h.err) return;
-        if (h.err == ERR_EVAL_OOB) {
-            const int q = h.n_bad[0] > 0 ? 0 : 1;
-            std::vector<int> r(std::min(h.n_bad[q], kMaxBadRows));
-            CK(cudaMemcpy(r.data(), bad[q].p, r.size() * sizeof(int), cudaMemcpyDeviceToHost));
-            throw std::invalid_argument(rows_message(r));
-        }
-        throw std::runtime_error("run_baseline: device error " + std::to_string(h.err));
-    }
-
-    // f64 objective rows / cv of the concatenation of key arrays
-    void keys_f64(std::initializer_list<const float4*> src, thrust::device_vector<double>& F,
-                  thrust::device_vector<double>& cv) {
-        const long long tot = (long long)src.size() * n;
-        F.resize(tot * m);
-        cv.resize(tot);
-        long long o = 0;
-        for (const float4* k : src) {
-            fcv_to_rows_kernel<<<blocks_for(n, 256), 256>>>(k, n, m, thrust::raw_pointer_cast(F.data()) + o * m,
-                                                           thrust::raw_pointer_cast(cv.data()) + o);
-            o += n;
-        }
-    }
-
-    void take(int q, const std::vector<long long>& idx, const float4* X1, const float4* K1, const float4* X2,
-              const float4* K2) {
-        thrust::device_vector<long long> di(idx.begin(), idx.end());
-        take_rows_kernel<<<blocks_for(n * geo.rs4, 256), 256>>>(pop[q].X.p, pop[q].Fcv.p, X1, K1, X2, K2, n,
-                                                                thrust::raw_pointer_cast(di.data()), n, geo.rs4,
-                                                                nxt[q].X.p, nxt[q].Fcv.p);
-        CK(cudaGetLastError());
-        std::swap(pop[q].X.p, nxt[q].X.p);
-        std::swap(pop[q].Fcv.p, nxt[q].Fcv.p);
-    }
-
-    void record(long long gen) {
-        thrust::device_vector<double> F, cv;
-        keys_f64({pop[0].Fcv.p}, F, cv);
-        const long long feas = thrust::count_if(thrust::device, cv.begin(), cv.end(), CvIsZero{});
-        gmpea_gen_record r{};
-        r.gen = gen;
-        r.evals = evals;
-        r.wall_ms = c.record_walltime ? loop_s * 1e3 : 0.0;
-        r.feasible_ratio = (double)feas / (double)n;
-        r.igd = r.hv = std::numeric_limits<double>::quiet_NaN();
-        if (n_ref > 0) {  // metric hook: outside the loop clock
-            r.igd = igd_dev(thrust::raw_pointer_cast(F.data()), thrust::raw_pointer_cast(cv.data()), n, m,
-                            thrust::raw_pointer_cast(igd_ref.data()), n_ref);
-            r.has_igd = 1;
-        }
-        if (hook) {
-            std::vector<double> hX((size_t)n * d), hF((size_t)n * m), hC((size_t)n * nc), hcv(n);
-            get_pop1(hX.data(), hF.data(), hC.data(), hcv.data());
-            hook(hook_user, n, hX.data(), hF.data(), hC.data(), hcv.data(), &r.igd, &r.hv, &r.has_igd, &r.has_hv);
-        }
-        hist.push_back(r);
-    }
-
-    bool stop(long long gen, long long next) const {  // RunDriver::stop (baselines.cpp:300-307)
-        const bool tb = c.time_budget_s > 0, eb = c.eval_budget > 0;
-        const bool unbounded = c.k_max == 0 && (tb || eb);
-        if (!unbounded && gen > c.k_max) return true;
-        if (tb && loop_s >= c.time_budget_s) return true;
-        if (eb && evals + next > c.eval_budget) return true;
-        return false;
-    }
-
-    void generation(long long gen) {
-        VaryParams g = vp;
-        g.fixed_gen = (int)gen;
-        thrust::device_vector<double> F, cv, fit[2];
-        thrust::device_vector<long long> rank;
-        thrust::device_vector<double> crowd;
-        if (algo == 0) {
-            // ranks and per-front crowding of the parents (baselines.cpp:332-344)
-            keys_f64({pop[0].Fcv.p}, F, cv);
-            nds_dev(thrust::raw_pointer_cast(F.data()), thrust::raw_pointer_cast(cv.data()), n, m, 1, rank);
-            crowd_all_dev(thrust::raw_pointer_cast(F.data()), n, m, rank, crowd);
-            g.trank[0] = thrust::raw_pointer_cast(rank.data());
-            g.tkey[0] = thrust::raw_pointer_cast(crowd.data());
-        } else {
-            for (int q = 0; q < 2; ++q) {  // baselines.cpp:410-411
-                keys_f64({pop[q].Fcv.p}, F, cv);
-                fit[q].resize(n);
-                spea2_fitness_dev(thrust::raw_pointer_cast(F.data()), thrust::raw_pointer_cast(cv.data()), n, m,
-                                  q == 0 ? 1 : 0, thrust::raw_pointer_cast(fit[q].data()));
-                g.tkey[q] = thrust::raw_pointer_cast(fit[q].data());
-            }
-        }
-        for (int q = 0; q < npop; ++q) {
-            g.parX[q] = pop[q].X.p;
-            g.out[q] = off[q].X.p;
-            g.outFcv[q] = off[q].Fcv.p;
-        }
-        launch_vary(vary_k, g, npop, 0);  // tournaments + SBX + PM + clip + evaluation
-        CK(cudaGetLastError());
-        check();
-        if (algo == 0) {
-            // merged pool: fronts in order, the last one cut by crowding (baselines.cpp:361-384)
-            keys_f64({pop[0].Fcv.p, off[0].Fcv.p}, F, cv);
-            const double* pF = thrust::raw_pointer_cast(F.data());
-            thrust::device_vector<long long> mr;
-            nds_dev(pF, thrust::raw_pointer_cast(cv.data()), 2 * n, m, 1, mr);
-            std::vector<long long> hr(2 * n);
-            thrust::copy(mr.begin(), mr.end(), hr.begin());
-            const long long top = *std::max_element(hr.begin(), hr.end());
-            std::vector<std::vector<long long>> fronts(top + 1);
-            for (long long i = 0; i < 2 * n; ++i) fronts[hr[i]].push_back(i);
-            std::vector<long long> chosen;
-            for (long long r = 0; r <= top && (long long)chosen.size() < n; ++r) {
-                const auto& fr = fronts[r];
-                if ((long long)(chosen.size() + fr.size()) <= n) {
-                    chosen.insert(chosen.end(), fr.begin(), fr.end());
-                } else {
-                    thrust::device_vector<long long> dfr(fr.begin(), fr.end());
-                    thrust::device_vector<double> cd;
-                    crowd_dev(pF, m, thrust::raw_pointer_cast(dfr.data()), (int64_t)fr.size(), cd);
-                    std::vector<double> hcd(fr.size());
-                    thrust::copy(cd.begin(), cd.end(), hcd.begin());
-                    std::vector<size_t> order(fr.size());
-                    std::iota(order.begin(), order.end(), 0);
-                    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return hcd[a] > hcd[b]; });
-                    for (size_t k : order) {
-                        if ((long long)chosen.size() == n) break;
-                        chosen.push_back(fr[k]);
-                    }
-                }
-            }
-            std::sort(chosen.begin(), chosen.end());
-            take(0, chosen, off[0].X.p, off[0].Fcv.p, nullptr, nullptr);
-        } else {
-            // both offspring sets feed both selections (baselines.cpp:433-438)
-            std::vector<long long> sel[2];
-            for (int q = 0; q < 2; ++q) {
-                keys_f64({pop[q].Fcv.p, off[0].Fcv.p, off[1].Fcv.p}, F, cv);
-                sel[q] = spea2_select_dev(thrust::raw_pointer_cast(F.data()), thrust::raw_pointer_cast(cv.data()),
-                                          3 * n, m, q == 0 ? 1 : 0, n);
-            }
-            for (int q = 0; q < 2; ++q) take(q, sel[q], off[0].X.p, off[0].Fcv.p, off[1].X.p, off[1].Fcv.p);
-        }
-        CK(cudaDeviceSynchronize());
-    }
-
-    void run() {
-        VaryParams ip = vp;
-        ip.fixed_gen = 0;
-        for (int q = 0; q < npop; ++q) {
-            ip.parX[q] = pop[q].X.p;
-            ip.out[q] = pop[q].X.p;
-            ip.outFcv[q] = pop[q].Fcv.p;
-        }
-        launch_vary(init_k, ip, npop, 0);  // random_population + evaluate (Philox INIT stream)
-        CK(cudaGetLastError());
-        check();
-        const long long per = (long long)npop * n;
-        evals = per;
-        record(0);
-        for (long long gen = 1; !stop(gen, per); ++gen) {
-            const bool tb = c.time_budget_s > 0;
-            if (tb)
-                for (int q = 0; q < npop; ++q) {
-                    CK(cudaMemcpy(prev[q].X.p, pop[q].X.p, (size_t)n * geo.rs4 * sizeof(float4), cudaMemcpyDeviceToDevice));
-                    CK(cudaMemcpy(prev[q].Fcv.p, pop[q].Fcv.p, (size_t)n * sizeof(float4), cudaMemcpyDeviceToDevice));
-                }
-            const auto t0 = std::chrono::steady_clock::now();
-            generation(gen);
-            loop_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (tb && loop_s >= c.time_budget_s) {  // the crossing generation is discarded
-                for (int q = 0; q < npop; ++q) {
-                    std::swap(pop[q].X.p, prev[q].X.p);
-                    std::swap(pop[q].Fcv.p, prev[q].Fcv.p);
-                }
-                break;
-            }
-            evals += per;
-            record(gen);
-        }
-    }
-
-    void get_pop1(double* X, double* F, double* C, double* cv) {
-        DevBuf<double> tmp((size_t)n * (std::max({d, nc, m}) + 1));
-        const float* rows = (const float*)pop[0].X.p;
-        auto pull = [&](int col0, int k, double* out) {
-            if (!out || k == 0) return;
-            from_rows_kernel<<<blocks_for(n * k, 256), 256>>>(rows, geo.rs4 * 4, n, col0, k, tmp.p);
-            CK(cudaMemcpy(out, tmp.p, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToHost));
-        };
-        pull(0, d, X);
-        pull(d, nc, C);
-        if (F || cv) {
-            fcv_to_rows_kernel<<<blocks_for(n, 256), 256>>>(pop[0].Fcv.p, n, m, tmp.p, tmp.p + (size_t)n * m);
-            if (F) CK(cudaMemcpy(F, tmp.p, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost));
-            if (cv) CK(cudaMemcpy(cv, tmp.p + (size_t)n * m, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
-        }
-    }
-};
-
-}  // namespace
-
-int gmpea_run_baseline(const gmpea_problem* p, int32_t algo, const gmpea_run_config* cfg, const double* igd_ref,
-                       int64_t n_ref, gmpea_pop_hook hook, void* hook_user, gmpea_gen_record* hist, int64_t hist_cap,
-                       int64_t* n_hist, double* X, double* F, double* C, double* cv) {
-    return guarded([&] {
-        if (!p || !cfg) throw std::invalid_argument("run_baseline: null argument");
-        require_device();
-        BaselineRun r;
-        r.setup(p, algo, *cfg);
-        r.hook = hook;
-        r.hook_user = hook_user;
-        if (igd_ref && n_ref > 0) {
-            r.igd_ref.assign(igd_ref, igd_ref + n_ref * p->m);
-            r.n_ref = n_ref;
-        }
-        r.run();
-        *n_hist = (int64_t)r.hist.size();
-        if (hist) std::copy(r.hist.begin(), r.hist.begin() + std::min<int64_t>(hist_cap, r.hist.size()), hist);
-        r.get_pop1(X, F, C, cv);
-    });
-}

@@ -1,0 +1,294 @@
+// Host runtime shared by the engine's translation units (engine.cu,
+// metrics_api.cu, baselines_api.cu): error plumbing of the C ABI, device
+// buffers, the problem handle, row geometry and the generation-kernel launch.
+// The generation kernels themselves are instantiated per problem family in
+// vary_<family>.cu (parallel compilation) and reached through vary_kernel_for.
+#pragma once
+#include <algorithm>
+#include <chrono>
+#include <numeric>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <random>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gmpea_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "vary_dispatch.cuh"
+#include "problems.cuh"
+
+using namespace gmpea_b200;
+
+
+namespace gmpea_b200 {
+namespace host {
+
+extern thread_local std::string g_err;  // defined in engine.cu
+
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(expr)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw cuda_error(std::string(#expr) + ": " + cudaGetErrorString(e_));            \
+    } while (0)
+
+template <class Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return GMPEA_OK;
+    } catch (const cuda_error& e) {
+        g_err = e.what();
+        return GMPEA_ECUDA;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return GMPEA_EINVAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GMPEA_ERUNTIME;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t count) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = count;
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+};
+
+inline int blocks_for(long long n, int bs) { return (int)((n + bs - 1) / bs); }
+
+inline void require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw cuda_error("no CUDA device available (the engine has no CPU fallback)");
+}
+
+// ---------------------------------------------------------------- problems
+constexpr double kPi = 3.141592653589793;
+
+struct WtaHost {
+    std::string scenario;
+    int targets = 0, vehicles = 0;
+    std::vector<int> strikes, cap;
+    std::vector<double> p;  // per strike slot, target-major
+};
+
+
+}  // namespace host
+}  // namespace gmpea_b200
+
+using namespace gmpea_b200;
+using namespace gmpea_b200::host;
+
+struct gmpea_problem {
+    std::string name;
+    int fam = 0, id = 0, d = 0, m = 0, nin = 0, neq = 0;
+    std::vector<double> lo, hi;
+    WtaHost wta;
+    int device = 0;
+    // device copies
+    DevBuf<float> dlo, dhi;
+    DevBuf<double> dlo64, dhi64;
+    DevBuf<int> dcap, dstrikes, dslot_target;
+    DevBuf<double> dp;
+    ProbDev dev{};
+
+    void upload() {
+        require_device();
+        CK(cudaGetDevice(&device));
+        std::vector<float> lf(lo.begin(), lo.end()), hf(hi.begin(), hi.end());
+        dlo.alloc(d);
+        dhi.alloc(d);
+        dlo64.alloc(d);
+        dhi64.alloc(d);
+        CK(cudaMemcpy(dlo.p, lf.data(), d * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dhi.p, hf.data(), d * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dlo64.p, lo.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dhi64.p, hi.data(), d * sizeof(double), cudaMemcpyHostToDevice));
+        dev = ProbDev{};
+        dev.fam = fam;
+        dev.id = id;
+        dev.d = d;
+        dev.m = m;
+        dev.nin = nin;
+        dev.neq = neq;
+        dev.lo = dlo.p;
+        dev.hi = dhi.p;
+        dev.uniform = 1;
+        for (int j = 0; j < d; ++j)
+            if (lo[j] != lo[0] || hi[j] != hi[0]) dev.uniform = 0;
+        dev.ulo = d ? (float)lo[0] : 0.0f;
+        dev.uhi = d ? (float)hi[0] : 0.0f;
+        // the reference evaluates these with glibc at run time; volatile keeps
+        // the host compiler from folding them with a different rounding
+        volatile double th = -0.25 * kPi, al = 0.25 * kPi;
+        dev.cth = std::cos(th);
+        dev.sth = std::sin(th);
+        dev.cal = std::cos(al);
+        dev.sal = std::sin(al);
+        if (fam == FAM_WTA) {
+            std::vector<int> st;
+            for (int i = 0; i < wta.targets; ++i)
+                for (int k = 0; k < wta.strikes[i]; ++k) st.push_back(i);
+            dcap.alloc(wta.vehicles);
+            dstrikes.alloc(wta.targets);
+            dslot_target.alloc(st.size());
+            dp.alloc(wta.p.size());
+            CK(cudaMemcpy(dcap.p, wta.cap.data(), wta.vehicles * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dstrikes.p, wta.strikes.data(), wta.targets * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dslot_target.p, st.data(), st.size() * sizeof(int), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(dp.p, wta.p.data(), wta.p.size() * sizeof(double), cudaMemcpyHostToDevice));
+            dev.wta_targets = wta.targets;
+            dev.wta_vehicles = wta.vehicles;
+            dev.wta_slots = (int)st.size();
+            dev.wta_cap = dcap.p;
+            dev.wta_strikes = dstrikes.p;
+            dev.wta_slot_target = dslot_target.p;
+            dev.wta_p = dp.p;
+            if (wta.vehicles > kWtaMaxVehicles) throw std::invalid_argument("wta: too many vehicles");
+            int base = 0;
+            for (int v = 0; v < wta.vehicles; ++v) {
+                dev.wta_capv[v] = wta.cap[v];
+                dev.wta_base[v] = base;
+                base += wta.cap[v];
+            }
+            dev.wta_ncap = base;
+            // EvalWta scratch (32-bit words; its keys hold the slot in 8 bits:
+            // kWtaMaxSlots <= 256)
+            dev.wta_n32 = base + 2 * wta.vehicles + (d + 31) / 32;
+            dev.wta_n8 = (dev.wta_n32 + 1) / 2;
+        }
+    }
+};
+
+namespace gmpea_b200 {
+namespace host {
+
+// individuals as padded fp32 rows [x | g | pad] plus packed keys
+struct RowGeom {
+    int rs4;   // row stride, float4
+    int srs4;  // shared-memory row stride (odd float4 count)
+    int bs;    // vary_eval block size
+    int stream8;
+    size_t smem;
+};
+
+// stream8 > 0: a streaming evaluator (no staged row) with that many 64-bit
+// shared words per thread
+inline RowGeom row_geom(int d, int nc, int stream8 = 0) {
+    RowGeom g;
+    g.rs4 = (d + nc + 3) / 4;
+    g.srs4 = stream8 > 0 ? 0 : g.rs4 | 1;
+    g.stream8 = stream8;
+    const int per = stream8 > 0 ? stream8 * 8 : g.srs4 * 16;
+    g.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
+    g.smem = (size_t)g.bs * per;
+    if (g.smem > 48 * 1024) throw std::invalid_argument("problem rows too wide for the engine");
+    return g;
+}
+
+struct PopBuf {
+    DevBuf<float4> X;  // n rows of rs4 float4
+    DevBuf<float4> Fcv;
+    void alloc(long long n, int rs4, long long ld) {
+        X.alloc((size_t)n * rs4);
+        Fcv.alloc(ld);
+    }
+};
+
+// the generation kernel of a problem family (vary_<family>.cu)
+VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0, bool tour = false);
+
+inline void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStream_t s) {
+    const RowGeom g = [&] {
+        RowGeom r;
+        r.rs4 = vp.rs4;
+        r.srs4 = vp.srs4;
+        const int per = vp.scratch8 > 0 ? vp.scratch8 * 8 : r.srs4 * 16;
+        r.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
+        r.smem = (size_t)r.bs * per;
+        return r;
+    }();
+    k<<<dim3(blocks_for(vp.row_end - vp.row0, g.bs), npops), g.bs, g.smem, s>>>(vp);
+}
+
+inline void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
+    vp.sbx_prob = prm.sbx_prob;
+    vp.sbx_e = (float)(1.0 / (prm.sbx_eta + 1.0));
+    vp.pm_e1 = (float)(prm.pm_eta + 1.0);
+    vp.pm_einv = (float)(1.0 / (prm.pm_eta + 1.0));
+    const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / (double)d;
+    // PM: skip iff u > pm with u = w 2^-32  <=>  mutate iff w <= floor(pm 2^32)
+    const double T = pm * 4294967296.0;
+    vp.pm_T = pm < 0.0 ? -1 : (long long)std::min(std::floor(T), 4294967295.0);
+    // DE: take iff u < CR  <=>  w < ceil(CR 2^32)  <=>  w <= ceil(CR 2^32) - 1
+    const double C = prm.de_cr * 4294967296.0;
+    vp.de_T = prm.de_cr >= 1.0 ? 0xffffffffll : (prm.de_cr <= 0.0 ? -1ll : (long long)std::ceil(C) - 1);
+    vp.uid = make_uidx((unsigned long long)d);
+    vp.de_f = (float)prm.de_f;
+}
+
+inline std::string rows_message(std::vector<int> rows) {
+    std::sort(rows.begin(), rows.end());
+    std::ostringstream os;
+    os << "evaluate: out-of-bounds rows:";
+    for (int r : rows) os << ' ' << r;
+    return os.str();
+}
+
+// row layout helpers shared by the host TUs (one copy each)
+static __global__ void from_rows_kernel(const float* in, int rs, long long n, int col0, int k, double* out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * k) return;
+    const long long r = e / k;
+    const int c = (int)(e % k);
+    out[e] = (double)in[r * rs + col0 + c];
+}
+
+static __global__ void fcv_to_rows_kernel(const float4* in, long long n, int m, double* F, double* cv) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 v = in[i];
+    F[i * m] = v.x;
+    F[i * m + 1] = v.y;
+    if (m > 2) F[i * m + 2] = v.z;
+    if (cv) cv[i] = v.w;
+}
+
+static __global__ void init_state_kernel(DevState* st, int m) {
+    for (int k = 0; k < 4; ++k) st->zbits[k] = k < m ? 0xffffffffu : float_to_ordered(0.0f);
+}
+
+// igd(metric_front(pop), ref) on device arrays (metrics_api.cu)
+double igd_dev(const double* dF, const double* dcv, long long n, int m, const double* dR, long long nr);
+
+}  // namespace host
+}  // namespace gmpea_b200
