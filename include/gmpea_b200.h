@@ -33,6 +33,14 @@ extern "C" {
 #define GMPEA_OP_SBX_PM 0 /* VariationOp::sbx_pm (gmpea.hpp:56) */
 #define GMPEA_OP_DE 1     /* VariationOp::de */
 
+/* subproblem aggregation of the selection keys: PBI (scalarize.cpp:72-89, the
+ * reference's only one) or the weighted Tchebycheff function
+ * g = max_k max(w_k, 1e-6) |f_k - z_k| the north-star names (an engine
+ * extension without a reference counterpart: parity against the oracle's
+ * f64 restatement only) */
+#define GMPEA_AGG_PBI 0
+#define GMPEA_AGG_TCH 1
+
 typedef struct gmpea_problem gmpea_problem;
 typedef struct gmpea_engine gmpea_engine;
 
@@ -110,6 +118,16 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
                                   const double* z, double theta, const uint32_t* B1, int32_t t1,
                                   const uint32_t* B2, int32_t t2, gmpea_population_out* out1,
                                   gmpea_population_out* out2, int32_t* winner1, int32_t* winner2);
+/* the same with the aggregation chosen (GMPEA_AGG_*; theta is used by PBI only) */
+int gmpea_environmental_selection_ex(int64_t n, int32_t d, int32_t m, int32_t nc,
+                                     const gmpea_population_view* pop1,
+                                     const gmpea_population_view* pop2,
+                                     const gmpea_population_view* off1,
+                                     const gmpea_population_view* off2, const double* W,
+                                     const double* z, double theta, int32_t aggregation,
+                                     const uint32_t* B1, int32_t t1, const uint32_t* B2, int32_t t2,
+                                     gmpea_population_out* out1, gmpea_population_out* out2,
+                                     int32_t* winner1, int32_t* winner2);
 
 /* ---- metrics: replaces igd / hypervolume / metric_front (metrics.hpp:15-29) */
 int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t m, double* out);
@@ -159,6 +177,7 @@ typedef struct {
     /* weight-region sharding: this engine owns the slots
      * [shard_begin, shard_end) of n; 0, 0 = all of them */
     int64_t shard_begin, shard_end;
+    int32_t aggregation;   /* GMPEA_AGG_PBI (default, the reference's) or GMPEA_AGG_TCH */
 } gmpea_run_config;
 
 typedef struct {
@@ -192,7 +211,11 @@ int gmpea_run_baseline(const gmpea_problem* p, int32_t algo, const gmpea_run_con
                        double* C, double* cv);
 
 int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmpea_engine** out);
-/* replace population `which` (1 or 2) by host rows X (n x d) and re-evaluate */
+/* replace population `which` (1 or 2) by host rows X (n x d) and re-evaluate.
+ * Asynchronous (stream-ordered, no host round trip): rows outside the bounds
+ * are reported as evaluate's GMPEA_EINVAL "evaluate: out-of-bounds rows: ..."
+ * by the next call that synchronises (step's successors, sync, population,
+ * history); pass pinned host memory for a truly asynchronous copy. */
 int gmpea_engine_set_population(gmpea_engine* e, int32_t which, const double* X);
 /* run to completion under k_max / eval_budget / time_budget semantics */
 int gmpea_engine_run(gmpea_engine* e);
@@ -220,6 +243,11 @@ typedef struct {
 int gmpea_engine_record_async(gmpea_engine* e, gmpea_raw_record* dst);
 int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C,
                                 double* cv);
+/* diagnostic (parity harness): offspring stream `which` (1: off1, 2: off2) of
+ * the last generation exactly as variation + evaluation produced it, before
+ * OP1 (gmpea.cpp:463-468); same layout as gmpea_engine_get_population */
+int gmpea_engine_get_offspring(gmpea_engine* e, int32_t which, double* X, double* F, double* C,
+                               double* cv);
 int gmpea_engine_ideal(gmpea_engine* e, double* z);
 /* neighbourhood tables the run uses (n x t1, n x t2) */
 int gmpea_engine_neighborhoods(gmpea_engine* e, uint32_t* B1, uint32_t* B2);

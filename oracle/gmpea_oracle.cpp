@@ -37,7 +37,11 @@
 #include <thread>
 #include <stdexcept>
 #include <string>
+#include <map>
+#include <mutex>
 #include <utility>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "philox.h"
@@ -84,7 +88,12 @@ struct MtRng {
     }
 };
 
-// wta.cpp:23-49
+// custom WTA scenarios by name (make_wta_problem over a loaded WTAInstance,
+// wta.cpp:112-129, 148-192)
+std::mutex g_wta_mu;
+std::map<std::string, Wta> g_wta_custom;
+
+// wta.cpp:23-49 (num > 10: the same formula continued, synthetic instances)
 Wta wta_scenario(int num) {
     Wta w;
     w.targets = 4 + 2 * (num - 1);
@@ -697,6 +706,23 @@ Problem make_problem(const std::string& name) {
         p.hi.assign(p.d, 1.0);
         return p;
     }
+    if (name.rfind("WTA-", 0) == 0) {
+        // custom scenarios (load_wta files, the synthetic instances past P10)
+        std::lock_guard<std::mutex> lk(g_wta_mu);
+        auto it = g_wta_custom.find(name.substr(4));
+        if (it != g_wta_custom.end()) {
+            p.fam = FAM_WTA;
+            p.w = it->second;
+            int slots = 0;
+            for (int s : p.w.strikes) slots += s;
+            p.d = slots * p.w.vehicles;
+            p.m = 2;
+            p.nin = p.w.vehicles + p.w.targets;
+            p.lo.assign(p.d, 0.0);
+            p.hi.assign(p.d, 1.0);
+            return p;
+        }
+    }
     if (name.rfind("WTA-P", 0) == 0) {
         int num = std::stoi(name.substr(5));
         if (num < 1 || num > 10) throw std::invalid_argument("unknown WTA scenario: " + name.substr(4));
@@ -984,6 +1010,32 @@ void knn(const double* W, size_t n, size_t m, size_t t, uint32_t* out) {
     }
 }
 
+// the brute-force t-NN rows `rows` only (a sample of a large population),
+// same arithmetic and (d2, j) order as knn(); rows split over threads
+void knn_rows(const double* W, size_t n, size_t m, size_t t, const int64_t* rows, size_t nrows, uint32_t* out,
+              unsigned threads) {
+    auto work = [&](size_t r0, size_t r1) {
+        std::vector<std::pair<double, uint32_t>> d(n);
+        for (size_t r = r0; r < r1; ++r) {
+            const size_t i = static_cast<size_t>(rows[r]);
+            for (size_t j = 0; j < n; ++j) {
+                double s = 0.0;
+                for (size_t c = 0; c < m; ++c) {
+                    double v = W[i * m + c] - W[j * m + c];
+                    s += v * v;
+                }
+                d[j] = {s, static_cast<uint32_t>(j)};
+            }
+            std::partial_sort(d.begin(), d.begin() + static_cast<std::ptrdiff_t>(t), d.end());
+            for (size_t k = 0; k < t; ++k) out[r * t + k] = d[k].second;
+        }
+    };
+    threads = std::max(1u, threads);
+    std::vector<std::thread> th;
+    for (unsigned k = 0; k < threads; ++k) th.emplace_back(work, nrows * k / threads, nrows * (k + 1) / threads);
+    for (auto& x : th) x.join();
+}
+
 // windowed t-NN on the Das-Dennis lattice, same (d2, j) order as
 // gmpea.cpp:84-97: candidates within +-R lattice steps, accepted only when
 // every point outside the window is provably farther than the t-th one
@@ -1075,15 +1127,31 @@ struct SelIn {
     double theta;
     int t1, t2;
     const uint32_t *B1, *B2;
+    int agg = 0;  // 0: PBI (the reference's), 1: Tchebycheff (engine extension)
 };
+
+// weighted Tchebycheff aggregation (no reference counterpart; the engine's
+// GMPEA_AGG_TCH): max_k max(w_k, 1e-6) |f_k - z_k|
+double tchebycheff(const double* f, const double* w, const double* z, int m) {
+    double g = 0.0;
+    for (int i = 0; i < m; ++i) {
+        double v = std::max(w[i], 1e-6) * std::fabs(f[i] - z[i]);
+        if (std::isnan(v)) return v;
+        g = std::max(g, v);
+    }
+    return g;
+}
 
 void selection(const SelIn& s, int32_t* src1, int32_t* src2, uint8_t* marks1, uint8_t* marks2) {
     const int n = s.n, m = s.m;
+    auto key = [&](const double* f, const double* w) {
+        return s.agg == 1 ? tchebycheff(f, w, s.z, m) : pbi(f, w, s.z, m, s.theta);
+    };
     // OP1 (gmpea.cpp:248-279)
     std::vector<int32_t> eff1(n), eff2(n);
     for (int i = 0; i < n; ++i) {
-        double g1 = pbi(s.Fo1 + i * m, s.W + i * m, s.z, m, s.theta);
-        double g2 = pbi(s.Fo2 + i * m, s.W + i * m, s.z, m, s.theta);
+        double g1 = key(s.Fo1 + i * m, s.W + i * m);
+        double g2 = key(s.Fo2 + i * m, s.W + i * m);
         double c1 = s.cvo1[i], c2 = s.cvo2[i];
         // the reference builds these through Heaviside masks on differences,
         // which reject non-finite values (batch.cpp:10-16)
@@ -1109,8 +1177,8 @@ void selection(const SelIn& s, int32_t* src1, int32_t* src2, uint8_t* marks1, ui
         for (int i = 0; i < n; ++i)
             for (int l = 0; l < t; ++l) {
                 int j = static_cast<int>(B[i * t + l]);
-                double go = pbi(Fof(eff[i]), s.W + j * m, s.z, m, s.theta);
-                double gp = pbi(Fp + j * m, s.W + j * m, s.z, m, s.theta);
+                double go = key(Fof(eff[i]), s.W + j * m);
+                double gp = key(Fp + j * m, s.W + j * m);
                 bool rep = pop == 1 ? fpr_better(go, cvof(eff[i]), gp, cvp[j]) : go < gp;
                 if (marks) marks[i * t + l] = rep ? 1 : 0;
                 if (rep) claims[j].push_back(i);
@@ -1126,11 +1194,11 @@ void selection(const SelIn& s, int32_t* src1, int32_t* src2, uint8_t* marks1, ui
                 ++u;
             }
             double bcv = cvp[j];
-            double bg = pbi(Fp + j * m, s.W + j * m, s.z, m, s.theta);
+            double bg = key(Fp + j * m, s.W + j * m);
             int bidx = u;
             int best = -1;
             for (int c : cl) {
-                double g = pbi(Fof(eff[c]), s.W + j * m, s.z, m, s.theta);
+                double g = key(Fof(eff[c]), s.W + j * m);
                 double cv = cvof(eff[c]);
                 bool wins;
                 if (pop == 1)
@@ -1482,10 +1550,28 @@ void orc_problem_eval_row(const void* h, const double* x, double* f, double* g) 
     eval_row(*static_cast<const Problem*>(h), x, f, g);
 }
 
+// registers a scenario (as loaded by load_wta) under "WTA-<scenario>"
+int orc_wta_register(const char* scenario, int32_t targets, int32_t vehicles, const int32_t* strikes,
+                     const int32_t* cap, const double* p) {
+    return guarded([&] {
+        Wta w;
+        w.targets = targets;
+        w.vehicles = vehicles;
+        w.strikes.assign(strikes, strikes + targets);
+        w.cap.assign(cap, cap + vehicles);
+        size_t o = 0;
+        w.p.resize(targets);
+        for (int i = 0; i < targets; ++i)
+            for (int k = 0; k < w.strikes[i]; ++k) w.p[i].push_back(p[o++]);
+        std::lock_guard<std::mutex> lk(g_wta_mu);
+        g_wta_custom[scenario] = w;
+    });
+}
+
 int orc_wta_scenario(int32_t num, int32_t* targets, int32_t* vehicles, int32_t* strikes,
                      int32_t* cap, double* p) {
     return guarded([&] {
-        if (num < 1 || num > 10) throw std::invalid_argument("unknown WTA scenario");
+        if (num < 1 || num > 123) throw std::invalid_argument("unknown WTA scenario");
         Wta w = wta_scenario(num);
         *targets = w.targets;
         *vehicles = w.vehicles;
@@ -1521,6 +1607,16 @@ int orc_knn(const double* W, int64_t n, int32_t m, int32_t t, uint32_t* out) {
     });
 }
 
+int orc_knn_rows(const double* W, int64_t n, int32_t m, int32_t t, const int64_t* rows, int64_t nrows,
+                 uint32_t* out, int32_t threads) {
+    return guarded([&] {
+        if (t > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
+        for (int64_t r = 0; r < nrows; ++r)
+            if (rows[r] < 0 || rows[r] >= n) throw std::invalid_argument("knn_rows: row out of range");
+        knn_rows(W, (size_t)n, (size_t)m, (size_t)t, rows, (size_t)nrows, out, (unsigned)threads);
+    });
+}
+
 int orc_lattice_knn(int32_t m, int64_t n, int32_t t1, int32_t t2, uint32_t* B1, uint32_t* B2, int32_t threads) {
     return guarded([&] {
         if (t1 > n || t2 > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
@@ -1528,13 +1624,28 @@ int orc_lattice_knn(int32_t m, int64_t n, int32_t t1, int32_t t2, uint32_t* B1, 
     });
 }
 
+int orc_selection_ex(int32_t n, int32_t m, const double* F1, const double* cv1, const double* F2,
+                     const double* cv2, const double* Fo1, const double* cvo1, const double* Fo2,
+                     const double* cvo2, const double* W, const double* z, double theta, int32_t agg, int32_t t1,
+                     const uint32_t* B1, int32_t t2, const uint32_t* B2, int32_t* src1, int32_t* src2,
+                     uint8_t* marks1, uint8_t* marks2);
+
 int orc_selection(int32_t n, int32_t m, const double* F1, const double* cv1, const double* F2,
                   const double* cv2, const double* Fo1, const double* cvo1, const double* Fo2,
                   const double* cvo2, const double* W, const double* z, double theta, int32_t t1,
                   const uint32_t* B1, int32_t t2, const uint32_t* B2, int32_t* src1, int32_t* src2,
                   uint8_t* marks1, uint8_t* marks2) {
+    return orc_selection_ex(n, m, F1, cv1, F2, cv2, Fo1, cvo1, Fo2, cvo2, W, z, theta, 0, t1, B1, t2, B2, src1,
+                            src2, marks1, marks2);
+}
+
+int orc_selection_ex(int32_t n, int32_t m, const double* F1, const double* cv1, const double* F2,
+                     const double* cv2, const double* Fo1, const double* cvo1, const double* Fo2,
+                     const double* cvo2, const double* W, const double* z, double theta, int32_t agg, int32_t t1,
+                     const uint32_t* B1, int32_t t2, const uint32_t* B2, int32_t* src1, int32_t* src2,
+                     uint8_t* marks1, uint8_t* marks2) {
     return guarded([&] {
-        SelIn s{n, m, F1, cv1, F2, cv2, Fo1, cvo1, Fo2, cvo2, W, z, theta, t1, t2, B1, B2};
+        SelIn s{n, m, F1, cv1, F2, cv2, Fo1, cvo1, Fo2, cvo2, W, z, theta, t1, t2, B1, B2, agg};
         selection(s, src1, src2, marks1, marks2);
     });
 }

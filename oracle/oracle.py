@@ -81,8 +81,10 @@ class Oracle(_Lib):
     # -- problems ---------------------------------------------------------
     def problem_info(self, name):
         d, m, nin, neq = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
-        lo = np.zeros(512)
-        hi = np.zeros(512)
+        self._check(self.lib.orc_problem_info(name.encode(), C.byref(d), C.byref(m), C.byref(nin),
+                                              C.byref(neq), None, None))  # sizes first
+        lo = np.zeros(d.value)
+        hi = np.zeros(d.value)
         self._check(self.lib.orc_problem_info(name.encode(), C.byref(d), C.byref(m), C.byref(nin),
                                               C.byref(neq), _ptr(lo, _dp), _ptr(hi, _dp)))
         return dict(d=d.value, m=m.value, n_ineq=nin.value, n_eq=neq.value,
@@ -112,11 +114,19 @@ class Oracle(_Lib):
                                           _ptr(G, _dp), _ptr(cv, _dp)))
         return F, G, cv
 
+    def wta_register(self, scenario, targets, vehicles, strikes, capacity, p):
+        """Registers a loaded scenario under the problem name "WTA-<scenario>"."""
+        s = np.ascontiguousarray(strikes, np.int32)
+        c = np.ascontiguousarray(capacity, np.int32)
+        pv = _f64(p)
+        self._check(self.lib.orc_wta_register(scenario.encode(), int(targets), int(vehicles), _ptr(s, _i32p),
+                                              _ptr(c, _i32p), _ptr(pv, _dp)))
+
     def wta_scenario(self, num):
         t, v = C.c_int32(), C.c_int32()
-        strikes = np.zeros(64, np.int32)
-        cap = np.zeros(64, np.int32)
-        p = np.zeros(256)
+        strikes = np.zeros(512, np.int32)
+        cap = np.zeros(512, np.int32)
+        p = np.zeros(2048)
         self._check(self.lib.orc_wta_scenario(num, C.byref(t), C.byref(v), _ptr(strikes, _i32p),
                                               _ptr(cap, _i32p), _ptr(p, _dp)))
         s = strikes[:t.value].copy()
@@ -145,6 +155,17 @@ class Oracle(_Lib):
         self._check(self.lib.orc_knn(_ptr(W, _dp), C.c_int64(n), m, t, _ptr(out, _u32p)))
         return out
 
+    def knn_rows(self, W, rows, t, threads=0):
+        """Brute-force t-NN of the given rows of W only (sampled parity at large N)."""
+        W = _f64(W)
+        n, m = W.shape
+        rows = np.ascontiguousarray(rows, np.int64)
+        out = np.zeros((len(rows), t), np.uint32)
+        threads = threads or (os.cpu_count() or 1)
+        self._check(self.lib.orc_knn_rows(_ptr(W, _dp), C.c_int64(n), m, t, _ptr(rows, _i64p), C.c_int64(len(rows)),
+                                          _ptr(out, _u32p), threads))
+        return out
+
     def lattice_knn(self, m, n, t1, t2, threads=0):
         B1 = np.zeros((n, t1), np.uint32)
         B2 = np.zeros((n, t2), np.uint32)
@@ -153,8 +174,9 @@ class Oracle(_Lib):
         return B1, B2
 
     # -- selection --------------------------------------------------------
-    def selection(self, pops, W, z, theta, B1, B2, want_marks=False):
+    def selection(self, pops, W, z, theta, B1, B2, want_marks=False, agg=0):
         """pops = [pop1, pop2, off1, off2], each a dict with F (n x m), cv (n).
+        agg: 0 = PBI (the reference's), 1 = Tchebycheff (engine extension).
         Returns (src1, src2[, marks1, marks2]); src = -1 parent kept,
         c in [0,n) off1 row c, n + c off2 row c."""
         F = [_f64(p["F"]) for p in pops]
@@ -168,9 +190,9 @@ class Oracle(_Lib):
         s2 = np.zeros(n, np.int32)
         m1 = np.zeros((n, t1), np.uint8) if want_marks else None
         m2 = np.zeros((n, t2), np.uint8) if want_marks else None
-        self._check(self.lib.orc_selection(
+        self._check(self.lib.orc_selection_ex(
             n, m, *[_ptr(a, _dp) for pair in zip(F, cv) for a in pair], _ptr(W, _dp), _ptr(z, _dp),
-            C.c_double(theta), t1, _ptr(B1, _u32p), t2, _ptr(B2, _u32p), _ptr(s1, _i32p),
+            C.c_double(theta), int(agg), t1, _ptr(B1, _u32p), t2, _ptr(B2, _u32p), _ptr(s1, _i32p),
             _ptr(s2, _i32p), _ptr(m1, _u8p), _ptr(m2, _u8p)))
         return (s1, s2, m1, m2) if want_marks else (s1, s2)
 
@@ -271,6 +293,15 @@ class Reference(_Lib):
         s = strikes[:t.value].copy()
         return dict(targets=t.value, vehicles=v.value, strikes=s, capacity=cap[:v.value].copy(),
                     p=p[:int(s.sum())].copy())
+
+    def wta_file_evaluate(self, path, X, d, nc, m=2):
+        """load_wta(path) -> make_wta_problem -> evaluate_population (the reference's own)."""
+        X = _f64(X)
+        n = X.shape[0]
+        F, G, cv = np.zeros((n, m)), np.zeros((n, nc)), np.zeros(n)
+        self._check(self.lib.ref_wta_file_evaluate(path.encode(), _ptr(X, _dp), C.c_int64(n), _ptr(F, _dp),
+                                                   _ptr(G, _dp), _ptr(cv, _dp)))
+        return F, G, cv
 
     def pbi(self, f, w, z, theta=5.0):
         f, w, z = _f64(f), _f64(w), _f64(z)

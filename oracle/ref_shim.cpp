@@ -155,6 +155,18 @@ int ref_evaluate(const char* name, const double* X, int64_t n, double* F, double
     });
 }
 
+// a scenario file through the reference's own loader and problem wrapper:
+// load_wta (wta.cpp:148-192) + make_wta_problem (:112-129) + evaluate_population
+int ref_wta_file_evaluate(const char* path, const double* X, int64_t n, double* F, double* G, double* cv) {
+    return guarded([&] {
+        ProblemDef p = make_wta_problem(load_wta(path));
+        Population pop = evaluate_population(p, mat(X, n, p.d));
+        put(pop.F, F);
+        put(pop.C, G);
+        if (cv) std::copy(pop.cv.begin(), pop.cv.end(), cv);
+    });
+}
+
 int ref_wta_scenario(int32_t num, int32_t* targets, int32_t* vehicles, int32_t* strikes,
                      int32_t* cap, double* p) {
     return guarded([&] {

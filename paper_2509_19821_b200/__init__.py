@@ -31,6 +31,7 @@ from ._lib import (  # noqa: F401
     RunConfig,
     RunResult,
     SelectionContext,
+    Aggregation,
     VariationOp,
     build_neighborhoods,
     crowding_distance,

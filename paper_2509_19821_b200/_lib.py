@@ -14,6 +14,7 @@ LIB = os.environ.get("GMPEA_LIB") or os.path.join(HERE, "libgmpea_b200.so")
 
 GMPEA_OK, GMPEA_EINVAL, GMPEA_ERUNTIME, GMPEA_ECUDA = 0, 1, 2, 3
 GMPEA_OP_SBX_PM, GMPEA_OP_DE = 0, 1
+GMPEA_AGG_PBI, GMPEA_AGG_TCH = 0, 1
 
 _dp = C.POINTER(C.c_double)
 _u32p = C.POINTER(C.c_uint32)
@@ -40,7 +41,7 @@ class _RunConfig(C.Structure):
         ("params", _OpParams), ("theta", C.c_double), ("t1", C.c_int32), ("t2", C.c_int32),
         ("record_walltime", C.c_int32), ("device", C.c_int32), ("stream", C.c_uint64),
         ("igd_reference", _dp), ("igd_reference_rows", C.c_int64),
-        ("shard_begin", C.c_int64), ("shard_end", C.c_int64),
+        ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("aggregation", C.c_int32),
     ]
 
 
@@ -274,11 +275,23 @@ def reproduce(pop: Population, neighborhoods, problem: Problem, op=VariationOp.s
     return off
 
 
+class Aggregation(enum.IntEnum):
+    """Subproblem aggregation: PBI (scalarize.cpp:72-89, the reference's) or
+    the weighted Tchebycheff function max_k max(w_k, 1e-6)|f_k - z_k| (an
+    engine extension the reference does not have; parity vs the oracle)."""
+
+    pbi = GMPEA_AGG_PBI
+    tchebycheff = GMPEA_AGG_TCH
+
+
 @dataclasses.dataclass
 class SelectionContext:
+    """SelectionContext{W, z, theta} (gmpea.hpp:75-79) plus the aggregation."""
+
     W: np.ndarray
     z: np.ndarray
     theta: float = 5.0
+    aggregation: Aggregation = Aggregation.pbi
 
 
 def _view(p: Population, keep: list) -> _View:
@@ -305,9 +318,9 @@ def environmental_selection(pop1: Population, pop2: Population, off1: Population
     B2 = np.ascontiguousarray(topo.b2, np.uint32)
     w1 = np.zeros(n, np.int32)
     w2 = np.zeros(n, np.int32)
-    _check(_L.gmpea_environmental_selection(
+    _check(_L.gmpea_environmental_selection_ex(
         C.c_int64(n), d, m, nc, C.byref(v[0]), C.byref(v[1]), C.byref(v[2]), C.byref(v[3]), _p(W), _p(z),
-        C.c_double(ctx.theta), _p(B1, _u32p), B1.shape[1], _p(B2, _u32p), B2.shape[1], C.byref(ov[0]),
+        C.c_double(ctx.theta), int(ctx.aggregation), _p(B1, _u32p), B1.shape[1], _p(B2, _u32p), B2.shape[1], C.byref(ov[0]),
         C.byref(ov[1]), _p(w1, _i32p), _p(w2, _i32p)))
     if return_winners:
         return outs[0], outs[1], w1, w2
@@ -424,6 +437,7 @@ class RunConfig:
     device: int = 0
     stream: int = 0
     shard: Optional[tuple] = None  # (begin, end) owned slots of a sharded run
+    aggregation: Aggregation = Aggregation.pbi
 
     def _c(self) -> _RunConfig:
         c = _RunConfig()
@@ -442,6 +456,7 @@ class RunConfig:
         c.stream = self.stream
         if self.shard is not None:
             c.shard_begin, c.shard_end = int(self.shard[0]), int(self.shard[1])
+        c.aggregation = int(self.aggregation)
         return c
 
 
@@ -538,6 +553,15 @@ class Engine:
         if out is None:
             out = Population(np.zeros((n, p.d)), np.zeros((n, p.m)), np.zeros((n, p.n_constraints)), np.zeros(n))
         _check(_L.gmpea_engine_get_population(self._h, which, _p(out.X), _p(out.F), _p(out.C), _p(out.cv)))
+        return out
+
+    def offspring(self, which: int = 1, out: Optional[Population] = None) -> Population:
+        """Diagnostic: offspring stream `which` of the last generation as
+        variation + evaluation produced it (before OP1)."""
+        n, p = self.rows_owned, self.problem
+        if out is None:
+            out = Population(np.zeros((n, p.d)), np.zeros((n, p.m)), np.zeros((n, p.n_constraints)), np.zeros(n))
+        _check(_L.gmpea_engine_get_offspring(self._h, which, _p(out.X), _p(out.F), _p(out.C), _p(out.cv)))
         return out
 
     def ideal(self) -> np.ndarray:

@@ -473,8 +473,8 @@ struct BaselineRun {
         vp.tour = algo == 0 ? 1 : 2;
         vp.un = make_uidx((unsigned long long)n);
         for (int q = 0; q < npop; ++q) vp.bad_rows[q] = bad[q].p;
-        init_k = vary_kernel_for(p->fam, MODE_INIT, 0);
-        vary_k = vary_kernel_for(p->fam, MODE_VARY, OP_SBX, p->dev.uniform ? d : 0, p->dev.id, true);
+        init_k = vary_kernel_for(p->dev, MODE_INIT, 0);
+        vary_k = vary_kernel_for(p->dev, MODE_VARY, OP_SBX, true);
     }
 
     void check() {

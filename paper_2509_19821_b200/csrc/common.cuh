@@ -26,6 +26,7 @@ enum : int {
     ERR_EVAL_OOB = 1,     // evaluate: out-of-bounds (incl. NaN) rows
     ERR_NONFINITE = 2,    // heaviside: non-finite mask source (OP1)
     ERR_NEG_CV = 3,       // fpr_better: negative constraint violation
+    ERR_RECORDS = 4,      // the generation-record buffer was not drained in time
 };
 
 // Per-run device state; one instance per engine (and per operator call).
@@ -42,7 +43,15 @@ struct DevState {
     unsigned long long loop_ns;  // accumulated loop time (gmpea.cpp:443,480)
     unsigned long long budget_ns; // 0 = no time budget
     int gens_done;
+    int rec_base;               // generation of record slot 0 (the host drains older records)
+    int rec_cap;                // record slots on the device
 };
+
+// record slot of generation g, or -1 outside the device window
+__host__ __device__ inline int rec_slot(const DevState* st, int g) {
+    const int k = g - st->rec_base;
+    return (k >= 0 && k < st->rec_cap) ? k : -1;
+}
 
 // per-generation record (gmpea.hpp:129-136); evals is derived on the host
 struct DevRecord {

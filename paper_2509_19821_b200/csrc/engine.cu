@@ -38,7 +38,9 @@ thread_local std::string g_err;
 namespace {
 
 // wta_scenario (wta.cpp:23-49): sizes grow with the index, tables from the
-// reference's seeded mt19937_64 draws (rng.hpp:18-30)
+// reference's seeded mt19937_64 draws (rng.hpp:18-30).  num > 10 continues
+// the same formula (synthetic instances; the reference stops at P10)
+constexpr int kWtaMaxScenario = 123;  // 3 + 122 / 2 = 64 vehicles: the engine's limit
 WtaHost wta_scenario(int num) {
     WtaHost w;
     w.scenario = "P" + std::to_string(num);
@@ -94,10 +96,10 @@ void make_wta(gmpea_problem& p, const WtaHost& w) {
         throw std::invalid_argument("WTA: at most " + std::to_string(kWtaMaxVehicles) + " vehicles");
     int slots = 0;
     for (int s : w.strikes) slots += s;
-    if (slots > kWtaMaxSlots) throw std::invalid_argument("WTA: too many strike slots");
+    if (slots > kWtaMaxSlots)
+        throw std::invalid_argument("WTA: at most " + std::to_string(kWtaMaxSlots) + " strike slots");
     for (int c : w.cap)
-        if (c < 0 || c > kWtaMaxCap)
-            throw std::invalid_argument("WTA: vehicle capacity above " + std::to_string(kWtaMaxCap));
+        if (c < 0) throw std::invalid_argument("WTA: negative vehicle capacity");
     p.fam = FAM_WTA;
     p.wta = w;
     p.name = "WTA-" + w.scenario;
@@ -237,6 +239,42 @@ __global__ void u32_to_i32_kernel(const unsigned* in, long long n, int* out, int
 }
 
 
+// the run state after the initial populations are evaluated (gmpea.cpp:430-437):
+// generation 1 next, clocks and budget armed; an earlier error stops the run
+__global__ void reset_state_kernel(DevState* st, unsigned long long budget_ns, int rec_cap) {
+    st->gen = 1;
+    st->discard = 0;
+    st->t_gen_start = 0;
+    st->loop_ns = 0;
+    st->budget_ns = budget_ns;
+    st->gens_done = 0;
+    st->rec_base = 0;
+    st->rec_cap = rec_cap;
+    st->stop = st->err ? 1 : 0;
+}
+
+// host rows (f64, row-major) -> fp32 rows, with the reference's f64 bounds
+// check (problems.cpp:554-568); offending rows (global index) go to the run
+// state's second bad-row list and surface at the next synchronisation
+__global__ void load_rows_kernel(const double* in, long long n, int k, float* out, int rs, const double* lo,
+                                 const double* hi, long long row_base, DevState* st) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * k) return;
+    const long long r = e / k;
+    const int c = (int)(e % k);
+    const double v = in[e];
+    out[r * rs + c] = (float)v;
+    if (!(v >= lo[c] && v <= hi[c])) {
+        for (int cc = 0; cc < c; ++cc) {  // one entry per row: its first failing column
+            const double w = in[r * k + cc];
+            if (!(w >= lo[cc] && w <= hi[cc])) return;
+        }
+        const int q = atomicAdd(&st->n_bad[1], 1);
+        if (q < kMaxBadRows) st->bad_rows[1][q] = (int)(r + row_base);
+        atomicCAS(&st->err, 0, ERR_EVAL_OOB);
+    }
+}
+
 __global__ void set_z_kernel(DevState* st, int m, float z0, float z1, float z2) {
     st->zbits[0] = float_to_ordered(z0);
     st->zbits[1] = float_to_ordered(z1);
@@ -278,12 +316,14 @@ namespace host {
 
 // the generation kernel is compiled per family (vary_<family>.cu) for the
 // registered suites' dimension
-VaryKernel vary_kernel_for(int fam, int mode, int op, int d, int id, bool tour) {
+VaryKernel vary_kernel_for(const ProbDev& P, int mode, int op, bool tour) {
     tour = tour && mode == MODE_VARY;
-    switch (fam) {
+    // the dimension-specialised kernels assume uniform bounds
+    const int d = P.uniform ? P.d : 0, id = P.id;
+    switch (P.fam) {
         case FAM_LIR: return vary_kernel_lir(mode, op, d, id, tour);
         case FAM_DTLZ: return vary_kernel_dtlz(mode, op, d, id, tour);
-        case FAM_WTA: return vary_kernel_wta(mode, op, d, id, tour);
+        case FAM_WTA: return vary_kernel_wta(mode, op, d, P.wta_slots > kWtaNarrowSlots ? 1 : 0, tour);
         case FAM_DAS: return vary_kernel_das(mode, op, d, id, tour);
         default: return vary_kernel_mw(mode, op, d, id, tour);
     }
@@ -370,6 +410,33 @@ int device_reverse(cudaStream_t s, int n, int t, const int* B, long long ld, Dev
 
 }  // namespace
 
+// the aggregation (PBI / Tchebycheff) and reverse-table layout are
+// compile-time parameters of the selection kernels
+static void launch_op1_kernel(int blocks, int agg, const Op1Params& p, cudaStream_t s) {
+    if (agg == AGG_TCH)
+        op1_kernel<AGG_TCH><<<blocks, 256, 0, s>>>(p);
+    else
+        op1_kernel<AGG_PBI><<<blocks, 256, 0, s>>>(p);
+}
+
+static void launch_select_kernel(dim3 grid, bool pack, int agg, const SelParams& p, cudaStream_t s) {
+    if (agg == AGG_TCH) {
+        if (pack)
+            select_kernel<true, AGG_TCH><<<grid, 256, 0, s>>>(p);
+        else
+            select_kernel<false, AGG_TCH><<<grid, 256, 0, s>>>(p);
+    } else {
+        if (pack)
+            select_kernel<true, AGG_PBI><<<grid, 256, 0, s>>>(p);
+        else
+            select_kernel<false, AGG_PBI><<<grid, 256, 0, s>>>(p);
+    }
+}
+
+static void check_aggregation(int agg) {
+    if (agg != GMPEA_AGG_PBI && agg != GMPEA_AGG_TCH) throw std::invalid_argument("unknown aggregation");
+}
+
 // ====================================================================== engine
 struct gmpea_engine {
     const gmpea_problem* prob = nullptr;
@@ -387,6 +454,8 @@ struct gmpea_engine {
     DevBuf<DevState> st;
     DevBuf<DevRecord> rec;
     long long rec_cap = 0;
+    long long rec_base = 0;           // generation held by device record slot 0
+    std::vector<DevRecord> archive;   // drained records of generations < rec_base
     DevBuf<float4> U;
     DevBuf<int> B[2], R[2], Rdeg[2];
     DevBuf<uint2> Rp[2];
@@ -396,12 +465,9 @@ struct gmpea_engine {
     DevBuf<float4> eff[2];
     DevBuf<unsigned char> srcbits;
     DevBuf<int> ustamp[2];
-    DevBuf<int> bad[2];
     int* host_flag = nullptr;
     DevBuf<unsigned> done_ctr;
     DevBuf<double> staging;  // f64 row-major staging for population transfers
-    DevBuf<int> rowsbuf;
-    DevBuf<int> nbad_buf;
     int* host_flag_dev = nullptr;
 
     VaryParams vp{};
@@ -429,6 +495,7 @@ struct gmpea_engine {
         if (c.n <= 0) throw std::invalid_argument("reference_vectors: target_n must be positive");
         if (c.n > (1ll << 30)) throw std::invalid_argument("engine: n too large");
         if (p->m > kMaxM || p->m < 2) throw std::invalid_argument("engine: objectives must be 2 or 3");
+        check_aggregation(c.aggregation);
         CK(cudaSetDevice(c.device));
         if (c.stream) {
             s = (cudaStream_t)(uintptr_t)c.stream;
@@ -469,7 +536,12 @@ struct gmpea_engine {
             lim = lim < 0 ? e : std::min(lim, e);
         }
         gen_limit = lim;
-        rec_cap = (lim >= 0 ? lim : (1ll << 22)) + 2;
+        // unbounded (time-budget) runs keep a window of records on the device
+        // and drain it to the host archive (drain_records)
+        long long window = 1ll << 16;
+        if (const char* w = getenv("GMPEA_REC_WINDOW")) window = std::max(8ll, atoll(w));  // tests
+        rec_cap = lim >= 0 ? lim + 2 : window;
+        if (rec_cap > (1ll << 30)) throw std::invalid_argument("engine: generation limit too large");
         rec.alloc(rec_cap);
         rec.zero(s);
 
@@ -525,7 +597,6 @@ struct gmpea_engine {
             pop[q].alloc(n, geo.rs4, ld);
             off[q].alloc(n, geo.rs4, ld);
             eff[q].alloc(ld);
-            bad[q].alloc(kMaxBadRows);
             pop[q].Fcv.zero(s);
             off[q].Fcv.zero(s);
             if (time_mode) {
@@ -564,7 +635,7 @@ struct gmpea_engine {
         vp.bad_cap = kMaxBadRows;
         for (int q = 0; q < 2; ++q) {
             vp.B[q] = B[q].p;
-            vp.bad_rows[q] = bad[q].p;
+            vp.bad_rows[q] = st.p->bad_rows[q];  // reported by check_errors
         }
 
         // initial populations (gmpea.cpp:430-437): Philox INIT stream
@@ -575,7 +646,7 @@ struct gmpea_engine {
         }
         VaryParams ip = vp;
         ip.fixed_gen = 0;
-        launch_vary(vary_kernel_for(p->fam, MODE_INIT, 0), ip, 2, s);
+        launch_vary(vary_kernel_for(p->dev, MODE_INIT, 0), ip, 2, s);
         CK(cudaGetLastError());
         finish_init();
 
@@ -585,7 +656,7 @@ struct gmpea_engine {
             vp.out[q] = off[q].X.p;
             vp.outFcv[q] = off[q].Fcv.p;
         }
-        vary = vary_kernel_for(p->fam, MODE_VARY, c.op, p->dev.uniform ? d : 0, p->dev.id);
+        vary = vary_kernel_for(p->dev, MODE_VARY, c.op);
         vp.row0 = (int)(v0 - e0);
         vp.row_end = (int)(v1 - e0);
         op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p},
@@ -636,9 +707,7 @@ struct gmpea_engine {
         // set_population / step / get_population allocate nothing and the
         // first step does not instantiate the graph (the graph's parameters
         // never change after construction)
-        staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
-        rowsbuf.alloc(std::max(n, 1));
-        nbad_buf.alloc(1);
+        staging.alloc((size_t)n * (d + nc + m + 1));  // every plane of a population readback
         if (!sharded) build_graph();
         CK(cudaStreamSynchronize(s));
         check_errors(0);
@@ -652,20 +721,13 @@ struct gmpea_engine {
             z_of_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[q].Fcv.p + o0, on, m, st.p);
         rec.zero(s);
         count_feasible_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[0].Fcv.p, o0, o0 + on, &rec.p[0].feasible);
-        DevState init{};
-        CK(cudaMemcpyAsync(&init, st.p, sizeof(DevState), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        DevState fresh{};
-        for (int k = 0; k < 4; ++k) fresh.zbits[k] = init.zbits[k];
-        fresh.gen = 1;
-        fresh.err = init.err;
-        fresh.err_gen = init.err_gen;
-        fresh.n_bad[0] = init.n_bad[0];
-        fresh.n_bad[1] = init.n_bad[1];
-        fresh.budget_ns = time_mode ? (unsigned long long)std::llround(cfg.time_budget_s * 1e9) : 0ull;
-        CK(cudaMemcpyAsync(st.p, &fresh, offsetof(DevState, bad_rows), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(&st.p->t_gen_start, &fresh.t_gen_start,
-                           sizeof(DevState) - offsetof(DevState, t_gen_start), cudaMemcpyHostToDevice, s));
+        // no host round trip: the state is reset on the device (errors of the
+        // initial evaluation are kept and stop the run)
+        reset_state_kernel<<<1, 1, 0, s>>>(
+            st.p, time_mode ? (unsigned long long)std::llround(cfg.time_budget_s * 1e9) : 0ull, (int)rec_cap);
+        CK(cudaGetLastError());
+        archive.clear();
+        rec_base = 0;
         gens_enqueued = 0;
         finished = false;
     }
@@ -674,25 +736,14 @@ struct gmpea_engine {
         if (which != 1 && which != 2) throw std::invalid_argument("set_population: which must be 1 or 2");
         if (gens_enqueued) throw std::invalid_argument("set_population: the run has started");
         const int q = which - 1;
-        if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
+        // asynchronous (no host round trip): out-of-bounds rows are recorded on
+        // the device and reported, as evaluate's invalid_argument, at the next
+        // synchronisation (step, sync, population, history)
         DevBuf<double>& h = staging;
         // X holds all N rows; this engine keeps its window [e0, e1)
         CK(cudaMemcpyAsync(h.p, X + e0 * d, (size_t)n * d * sizeof(double), cudaMemcpyHostToDevice, s));
-        DevBuf<int>& nbad = nbad_buf;
-        nbad.zero(s);
-        if (rowsbuf.n < (size_t)std::max(n, 1)) rowsbuf.alloc(std::max(n, 1));
-        DevBuf<int>& rows = rowsbuf;
-        to_rows_kernel<<<blocks_for((long long)n * d, 256), 256, 0, s>>>(
-            h.p, n, d, (float*)pop[q].X.p, geo.rs4 * 4, prob->dlo64.p, prob->dhi64.p, rows.p, nbad.p);
-        int hb = 0;
-        CK(cudaMemcpyAsync(&hb, nbad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (hb) {
-            std::vector<int> r(hb);
-            CK(cudaMemcpy(r.data(), rows.p, hb * sizeof(int), cudaMemcpyDeviceToHost));
-            for (int& v : r) v += (int)e0;
-            throw std::invalid_argument(rows_message(r));
-        }
+        load_rows_kernel<<<blocks_for((long long)n * d, 256), 256, 0, s>>>(
+            h.p, n, d, (float*)pop[q].X.p, geo.rs4 * 4, prob->dlo64.p, prob->dhi64.p, e0, st.p);
         VaryParams ep = vp;
         ep.row0 = 0;
         ep.row_end = n;
@@ -701,10 +752,9 @@ struct gmpea_engine {
         ep.outFcv[0] = pop[q].Fcv.p;
         ep.update_z = 0;
         ep.fixed_gen = 0;
-        launch_vary(vary_kernel_for(prob->fam, MODE_EVAL, 0), ep, 1, s);
+        launch_vary(vary_kernel_for(prob->dev, MODE_EVAL, 0), ep, 1, s);
         CK(cudaGetLastError());
         finish_init();
-        CK(cudaStreamSynchronize(s));
     }
 
     void enqueue_generation() {
@@ -713,18 +763,15 @@ struct gmpea_engine {
     }
 
     void launch_select() {
-        const dim3 grid(blocks_for(own1 - own0, 256), 2);
-        if (rpack)
-            select_kernel<true><<<grid, 256, 0, s>>>(sp);
-        else
-            select_kernel<false><<<grid, 256, 0, s>>>(sp);
+        launch_select_kernel(dim3(blocks_for(own1 - own0, 256), 2), rpack, cfg.aggregation, sp, s);
     }
+    void launch_op1() { launch_op1_kernel(blocks_for(v1 - v0, 256), cfg.aggregation, op1p, s); }
 
     // phase 1: variation + evaluation (+ local ideal-point partial)
     void enqueue_phase1() { launch_vary(vary, vp, 2, s); }
     // phase 2: OP1, selection, bookkeeping (a sharded run all-reduces z in between)
     void enqueue_phase2() {
-        op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
+        launch_op1();
         launch_select();  // + end_gen
         if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
@@ -764,10 +811,56 @@ struct gmpea_engine {
         if (gen_limit >= 0) k = std::min(k, gen_limit - gens_enqueued);
         if (k <= 0) return 0;
         build_graph();
-        CK(cudaGraphLaunch(graph_first, s));
-        for (long long i = 1; i < k; ++i) CK(cudaGraphLaunch(graph, s));
-        gens_enqueued += k;
-        return k;
+        long long done = 0;
+        while (done < k) {
+            // an unbounded run's record window: drain it before it fills
+            long long room = rec_cap - 2 - (gens_enqueued - rec_base);
+            if (room <= 0) {
+                drain_records();
+                room = rec_cap - 2 - (gens_enqueued - rec_base);
+                if (room <= 0) break;  // the run stopped: nothing further would execute
+            }
+            const long long part = std::min(k - done, room);
+            CK(cudaGraphLaunch(done == 0 ? graph_first : graph, s));
+            for (long long i = 1; i < part; ++i) CK(cudaGraphLaunch(graph, s));
+            gens_enqueued += part;
+            done += part;
+        }
+        return done;
+    }
+
+    // moves the records of finished generations to the host archive and
+    // restarts the device window at the next generation (syncs the stream)
+    void drain_records() {
+        CK(cudaStreamSynchronize(s));
+        DevState h = read_state();
+        if (h.stop) return;  // the run is over; nothing more will be written
+        const long long upto = h.gen;  // generations < gen are complete
+        const long long cnt = upto - rec_base;
+        if (cnt <= 0) return;
+        std::vector<DevRecord> r(cnt);
+        CK(cudaMemcpyAsync(r.data(), rec.p, cnt * sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        archive.insert(archive.end(), r.begin(), r.end());
+        rec_base = upto;
+        rec.zero(s);
+        int base = (int)rec_base;
+        CK(cudaMemcpyAsync(&st.p->rec_base, &base, sizeof(int), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    }
+
+    // records of generations [0, gens_done] (archive + device window)
+    std::vector<DevRecord> all_records(long long gens_done) {
+        std::vector<DevRecord> out(archive.begin(), archive.end());
+        const long long cnt = std::min<long long>(gens_done + 1 - rec_base, rec_cap);
+        if (cnt > 0) {
+            std::vector<DevRecord> r(cnt);
+            CK(cudaMemcpyAsync(r.data(), rec.p, cnt * sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            out.insert(out.end(), r.begin(), r.end());
+        }
+        out.resize(gens_done + 1);
+        return out;
     }
 
     // one generation in two phases (sharded runs; no graph, plain launches)
@@ -833,23 +926,25 @@ struct gmpea_engine {
         std::string where = phase == 0 ? std::string("") :
             "run_gmpea: evaluation failed at generation " + std::to_string(h.err_gen) + ": ";
         if (h.err == ERR_EVAL_OOB) {
-            int q = h.n_bad[0] > 0 ? 0 : 1;
-            int cnt = std::min(h.n_bad[q], kMaxBadRows);
-            std::vector<int> r(h.bad_rows[q], h.bad_rows[q] + cnt);
-            if (phase == 0) throw std::invalid_argument(rows_message(r));
+            // list 0: the evaluator's fp32 check, list 1: set_population's f64 check
+            std::vector<int> r;
+            for (int q = 0; q < 2; ++q) r.insert(r.end(), h.bad_rows[q], h.bad_rows[q] + std::min(h.n_bad[q], kMaxBadRows));
+            std::sort(r.begin(), r.end());
+            r.erase(std::unique(r.begin(), r.end()), r.end());
+            // generation 0: the initial / injected populations (evaluate's invalid_argument)
+            if (phase == 0 || h.err_gen == 0) throw std::invalid_argument(rows_message(r));
             throw std::runtime_error(where + rows_message(r));
         }
         if (h.err == ERR_NONFINITE) throw std::invalid_argument("non-finite mask source");
         if (h.err == ERR_NEG_CV) throw std::invalid_argument("fpr_better: negative constraint violation");
+        if (h.err == ERR_RECORDS) throw std::runtime_error("engine: generation records were not drained");
         throw std::runtime_error("engine error " + std::to_string(h.err));
     }
 
     std::vector<gmpea_gen_record> history() {
         DevState h = read_state();
-        long long g = std::min<long long>(h.gens_done, rec_cap - 1);
-        std::vector<DevRecord> r(g + 1);
-        CK(cudaMemcpyAsync(r.data(), rec.p, (g + 1) * sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        const long long g = h.gens_done;
+        std::vector<DevRecord> r = all_records(g);
         std::vector<gmpea_gen_record> out(g + 1);
         for (long long k = 0; k <= g; ++k) {
             gmpea_gen_record& o = out[k];
@@ -867,10 +962,8 @@ struct gmpea_engine {
 
     std::vector<int64_t> replacements() {
         DevState h = read_state();
-        long long g = std::min<long long>(h.gens_done, rec_cap - 1);
-        std::vector<DevRecord> r(g + 1);
-        CK(cudaMemcpyAsync(r.data(), rec.p, (g + 1) * sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        const long long g = h.gens_done;
+        std::vector<DevRecord> r = all_records(g);
         std::vector<int64_t> out(g + 1);
         for (long long k = 0; k <= g; ++k) out[k] = k == 0 ? 0 : (int64_t)r[k].replaced;
         return out;
@@ -878,7 +971,8 @@ struct gmpea_engine {
 
     void record_async(void* dst) {
         static_assert(sizeof(DevRecord) == sizeof(gmpea_raw_record), "raw record layout");
-        const long long k = std::min<long long>(gens_enqueued, rec_cap - 1);
+        const long long k = gens_enqueued - rec_base;
+        if (k < 0 || k >= rec_cap) throw std::invalid_argument("record_async: record outside the device window");
         CK(cudaMemcpyAsync(dst, rec.p + k, sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
     }
 
@@ -890,9 +984,13 @@ struct gmpea_engine {
         CK(cudaMemcpyAsync(&g.gens_done, &st.p->gens_done, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         DevRecord r{};
-        long long k = std::min<long long>(g.gens_done, rec_cap - 1);
-        CK(cudaMemcpyAsync(&r, rec.p + k, sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        const long long k = g.gens_done;
+        if (k - rec_base >= 0 && k - rec_base < rec_cap) {
+            CK(cudaMemcpyAsync(&r, rec.p + (k - rec_base), sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        } else if (k < (long long)archive.size()) {
+            r = archive[k];
+        }
         gmpea_gen_record o{};
         o.gen = k;
         o.evals = 2ll * N * (k + 1);
@@ -903,29 +1001,37 @@ struct gmpea_engine {
     }
 
     // the owned rows [own0, own1) (all N unsharded)
-    void get_population(int which, double* X, double* F, double* C, double* cv) {
+    // the owned rows [own0, own1) (all N unsharded) of population `which`
+    // (1, 2) or, with offspring = true, of the offspring stream `which` as the
+    // last generation's variation + evaluation left it (diagnostic)
+    void get_population(int which, double* X, double* F, double* C, double* cv, bool offspring = false) {
         if (which != 1 && which != 2) throw std::invalid_argument("get_population: which must be 1 or 2");
+        check_errors(-1);  // never hand out a population a failed generation left behind
         const int q = which - 1;
         const long long o0 = own0 - e0, on = own1 - own0;
-        if (staging.n < (size_t)n * (std::max({d, nc, m}) + 1)) staging.alloc((size_t)n * (std::max({d, nc, m}) + 1));
-        DevBuf<double>& tmp = staging;
-        const float* rows = (const float*)(pop[q].X.p + o0 * geo.rs4);
-        auto pull = [&](int col0, int k, double* out) {
-            if (!out || k == 0) return;
-            from_rows_kernel<<<blocks_for(on * k, 256), 256, 0, s>>>(rows, geo.rs4 * 4, on, col0, k, tmp.p);
-            CK(cudaMemcpyAsync(out, tmp.p, (size_t)on * k * sizeof(double), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-        };
-        pull(0, d, X);
-        pull(d, nc, C);
-        if (F || cv) {
-            double* f = tmp.p;
-            double* c = tmp.p + (size_t)on * m;
-            fcv_to_rows_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[q].Fcv.p + o0, on, m, f, c);
-            if (F) CK(cudaMemcpyAsync(F, f, (size_t)on * m * sizeof(double), cudaMemcpyDeviceToHost, s));
-            if (cv) CK(cudaMemcpyAsync(cv, c, (size_t)on * sizeof(double), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
+        const PopBuf& src = offspring ? off[q] : pop[q];
+        // every plane is converted into its own part of the staging buffer and
+        // copied out in stream order: one synchronisation for the whole readback
+        double* tX = staging.p;
+        double* tC = tX + (size_t)on * d;
+        double* tF = tC + (size_t)on * nc;
+        double* tcv = tF + (size_t)on * m;
+        const float* rows = (const float*)(src.X.p + o0 * geo.rs4);
+        if (X) {
+            from_rows_kernel<<<blocks_for(on * d, 256), 256, 0, s>>>(rows, geo.rs4 * 4, on, 0, d, tX);
+            CK(cudaMemcpyAsync(X, tX, (size_t)on * d * sizeof(double), cudaMemcpyDeviceToHost, s));
         }
+        if (C && nc) {
+            from_rows_kernel<<<blocks_for(on * nc, 256), 256, 0, s>>>(rows, geo.rs4 * 4, on, d, nc, tC);
+            CK(cudaMemcpyAsync(C, tC, (size_t)on * nc * sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
+        if (F || cv) {
+            fcv_to_rows_kernel<<<blocks_for(on, 256), 256, 0, s>>>(src.Fcv.p + o0, on, m, tF, tcv);
+            if (F) CK(cudaMemcpyAsync(F, tF, (size_t)on * m * sizeof(double), cudaMemcpyDeviceToHost, s));
+            if (cv) CK(cudaMemcpyAsync(cv, tcv, (size_t)on * sizeof(double), cudaMemcpyDeviceToHost, s));
+        }
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
     }
 
     void profile(long long gens, double* ms) {
@@ -939,7 +1045,7 @@ struct gmpea_engine {
             CK(cudaEventRecord(e[0], s));
             launch_vary(vary, vp, 2, s);
             CK(cudaEventRecord(e[1], s));
-            op1_kernel<<<blocks_for(v1 - v0, 256), 256, 0, s>>>(op1p);
+            launch_op1();
             CK(cudaEventRecord(e[2], s));
             launch_select();  // + end_gen
             CK(cudaEventRecord(e[3], s));
@@ -1010,7 +1116,10 @@ int gmpea_problem_create_wta(const char* scenario, int32_t targets, int32_t vehi
 int gmpea_wta_scenario(int32_t num, int32_t* targets, int32_t* vehicles, int32_t* strikes, int32_t* capacity,
                        double* p) {
     return guarded([&] {
-        if (num < 1 || num > 10) throw std::invalid_argument("unknown WTA scenario: P" + std::to_string(num));
+        // P1..P10 are the reference's scenarios (wta.cpp:23-49); larger num
+        // extend its size formula and seeded tables (synthetic instances)
+        if (num < 1 || num > kWtaMaxScenario)
+            throw std::invalid_argument("unknown WTA scenario: P" + std::to_string(num));
         WtaHost w = wta_scenario(num);
         *targets = w.targets;
         *vehicles = w.vehicles;
@@ -1106,7 +1215,7 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
         ep.st = st.p;
         ep.bad_rows[0] = bad.p;
         ep.bad_cap = (int)n;
-        launch_vary(vary_kernel_for(p->fam, MODE_EVAL, 0), ep, 1, s);
+        launch_vary(vary_kernel_for(p->dev, MODE_EVAL, 0), ep, 1, s);
         CK(cudaGetLastError());
         DevBuf<double> out((size_t)n * std::max({m, nc, 1}));
         DevBuf<double> c(n);
@@ -1225,7 +1334,7 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         vp.st = st.p;
         vp.bad_rows[0] = bad.p;
         vp.bad_cap = 0;  // reproduce itself never throws on bounds
-        launch_vary(vary_kernel_for(p->fam, MODE_VARY, op, p->dev.uniform ? d : 0, p->dev.id), vp, 1, s);
+        launch_vary(vary_kernel_for(p->dev, MODE_VARY, op), vp, 1, s);
         CK(cudaGetLastError());
         from_rows_kernel<<<blocks_for(n * d, 256), 256>>>((const float*)Op.p, geo.rs4 * 4, n, 0, d, h.p);
         CK(cudaMemcpy(off, h.p, (size_t)n * d * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1238,7 +1347,19 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
                                   const double* W, const double* z, double theta, const uint32_t* B1,
                                   int32_t t1, const uint32_t* B2, int32_t t2, gmpea_population_out* out1,
                                   gmpea_population_out* out2, int32_t* winner1, int32_t* winner2) {
+    return gmpea_environmental_selection_ex(n, d, m, nc, pop1, pop2, off1, off2, W, z, theta, GMPEA_AGG_PBI, B1, t1,
+                                            B2, t2, out1, out2, winner1, winner2);
+}
+
+int gmpea_environmental_selection_ex(int64_t n, int32_t d, int32_t m, int32_t nc,
+                                     const gmpea_population_view* pop1, const gmpea_population_view* pop2,
+                                     const gmpea_population_view* off1, const gmpea_population_view* off2,
+                                     const double* W, const double* z, double theta, int32_t aggregation,
+                                     const uint32_t* B1, int32_t t1, const uint32_t* B2, int32_t t2,
+                                     gmpea_population_out* out1, gmpea_population_out* out2, int32_t* winner1,
+                                     int32_t* winner2) {
     return guarded([&] {
+        check_aggregation(aggregation);
         if (n <= 0) return;
         if (m < 2 || m > 3) throw std::invalid_argument("environmental_selection: m must be 2 or 3");
         if (t1 <= 0 || t2 <= 0) throw std::invalid_argument("environmental_selection: empty neighbourhood");
@@ -1288,7 +1409,7 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
         eff[1].alloc(ld);
         DevBuf<unsigned char> sb(ld);
         Op1Params o1{0, (int)n, m, (float)theta, U.p, {fcv[2].p, fcv[3].p}, {eff[0].p, eff[1].p}, sb.p, st.p};
-        op1_kernel<<<blocks_for(n, 256), 256>>>(o1);
+        launch_op1_kernel(blocks_for(n, 256), aggregation, o1, 0);
         DevBuf<int> win[2];
         win[0].alloc(n);
         win[1].alloc(n);
@@ -1312,10 +1433,7 @@ int gmpea_environmental_selection(int64_t n, int32_t d, int32_t m, int32_t nc,
         sp.srcbits = sb.p;
         sp.apply = 0;
         sp.st = st.p;
-        if (pack)
-            select_kernel<true><<<dim3(blocks_for(n, 256), 2), 256>>>(sp);
-        else
-            select_kernel<false><<<dim3(blocks_for(n, 256), 2), 256>>>(sp);
+        launch_select_kernel(dim3(blocks_for(n, 256), 2), pack, aggregation, sp, 0);
         CK(cudaGetLastError());
         std::vector<int> w1(n), w2(n);
         CK(cudaMemcpy(w1.data(), win[0].p, n * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1429,6 +1547,10 @@ int gmpea_engine_last_record(gmpea_engine* e, gmpea_gen_record* out) {
 
 int gmpea_engine_get_population(gmpea_engine* e, int32_t which, double* X, double* F, double* C, double* cv) {
     return guarded([&] { e->get_population(which, X, F, C, cv); });
+}
+
+int gmpea_engine_get_offspring(gmpea_engine* e, int32_t which, double* X, double* F, double* C, double* cv) {
+    return guarded([&] { e->get_population(which, X, F, C, cv, true); });
 }
 
 int gmpea_engine_ideal(gmpea_engine* e, double* z) {

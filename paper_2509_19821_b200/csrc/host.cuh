@@ -174,16 +174,19 @@ struct gmpea_problem {
             dev.wta_slot_target = dslot_target.p;
             dev.wta_p = dp.p;
             if (wta.vehicles > kWtaMaxVehicles) throw std::invalid_argument("wta: too many vehicles");
+            // a vehicle keeps at most min(capacity, slots) candidates
+            const int slots = (int)st.size();
             int base = 0;
             for (int v = 0; v < wta.vehicles; ++v) {
-                dev.wta_capv[v] = wta.cap[v];
+                dev.wta_capv[v] = std::min(wta.cap[v], slots);
                 dev.wta_base[v] = base;
-                base += wta.cap[v];
+                base += dev.wta_capv[v];
             }
             dev.wta_ncap = base;
-            // EvalWta scratch (32-bit words; its keys hold the slot in 8 bits:
-            // kWtaMaxSlots <= 256)
-            dev.wta_n32 = base + 2 * wta.vehicles + (d + 31) / 32;
+            // EvalWtaT scratch in 32-bit words: narrow keys (slot in 8 bits) up
+            // to kWtaNarrowSlots slots, 64-bit keys beyond
+            const int kw = slots > kWtaNarrowSlots ? 2 : 1;
+            dev.wta_n32 = base * kw + wta.vehicles * (1 + kw) + (d + 31) / 32;
             dev.wta_n8 = (dev.wta_n32 + 1) / 2;
         }
     }
@@ -201,6 +204,16 @@ struct RowGeom {
     size_t smem;
 };
 
+// vary_eval block size for `per` shared bytes per thread: the largest of
+// 128 / 64 / 32 threads within 40 KB, else 32 threads on up to 227 KB
+// (opt-in dynamic shared memory; the large WTA scenarios)
+constexpr size_t kVarySmemMax = 227 * 1024;
+inline int vary_block(size_t per) {
+    if (per * 128 <= 40 * 1024) return 128;
+    if (per * 64 <= 40 * 1024) return 64;
+    return 32;
+}
+
 // stream8 > 0: a streaming evaluator (no staged row) with that many 64-bit
 // shared words per thread
 inline RowGeom row_geom(int d, int nc, int stream8 = 0) {
@@ -208,10 +221,10 @@ inline RowGeom row_geom(int d, int nc, int stream8 = 0) {
     g.rs4 = (d + nc + 3) / 4;
     g.srs4 = stream8 > 0 ? 0 : g.rs4 | 1;
     g.stream8 = stream8;
-    const int per = stream8 > 0 ? stream8 * 8 : g.srs4 * 16;
-    g.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
+    const size_t per = stream8 > 0 ? (size_t)stream8 * 8 : (size_t)g.srs4 * 16;
+    g.bs = vary_block(per);
     g.smem = (size_t)g.bs * per;
-    if (g.smem > 48 * 1024) throw std::invalid_argument("problem rows too wide for the engine");
+    if (g.smem > kVarySmemMax) throw std::invalid_argument("problem rows too wide for the engine");
     return g;
 }
 
@@ -225,18 +238,20 @@ struct PopBuf {
 };
 
 // the generation kernel of a problem family (vary_<family>.cu)
-VaryKernel vary_kernel_for(int fam, int mode, int op, int d = 0, int id = 0, bool tour = false);
+VaryKernel vary_kernel_for(const ProbDev& P, int mode, int op, bool tour = false);
 
 inline void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStream_t s) {
     const RowGeom g = [&] {
         RowGeom r;
         r.rs4 = vp.rs4;
         r.srs4 = vp.srs4;
-        const int per = vp.scratch8 > 0 ? vp.scratch8 * 8 : r.srs4 * 16;
-        r.bs = per * 128 <= 40 * 1024 ? 128 : (per * 64 <= 40 * 1024 ? 64 : 32);
+        const size_t per = vp.scratch8 > 0 ? (size_t)vp.scratch8 * 8 : (size_t)r.srs4 * 16;
+        r.bs = vary_block(per);
         r.smem = (size_t)r.bs * per;
         return r;
     }();
+    if (g.smem > 48 * 1024)
+        CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
     k<<<dim3(blocks_for(vp.row_end - vp.row0, g.bs), npops), g.bs, g.smem, s>>>(vp);
 }
 

@@ -32,10 +32,15 @@ enum : int {
     DC2_DTLZ1, DC2_DTLZ3, DC3_DTLZ1, DC3_DTLZ3
 };
 
-constexpr int kWtaMaxVehicles = 16;
-constexpr int kWtaMaxCap = 8;
-constexpr int kWtaMaxSlots = 128;  // <= 256: EvalWta keys hold the slot in 8 bits
-constexpr int kMaxCon = kWtaMaxVehicles + kWtaMaxSlots;
+// WTA limits: scenarios past P10 and reference-valid
+// files (load_wta, wta.cpp:148-192) of up to 64 vehicles and 4096 strike slots.
+// Slots <= kWtaNarrowSlots use 32-bit decode keys (slot in 8 bits), larger
+// scenarios 64-bit keys (EvalWtaT<true>).  A vehicle's capacity is unlimited:
+// it can never take more than one assignment per slot, so its kept list holds
+// min(capacity, slots) keys.
+constexpr int kWtaMaxVehicles = 64;
+constexpr int kWtaMaxSlots = 4096;
+constexpr int kWtaNarrowSlots = 256;
 
 struct ProbDev {
     int fam, id, d, m, nin, neq;
@@ -726,10 +731,14 @@ struct EvalDas {
 // counts hits per strike slot and forms f and g in the reference's order.
 // The state lives in shared memory as 64-bit words with stride S (one column
 // per thread): [lists | counts (V) | minima (V) | mask (ceil(D / 64))].
-struct EvalWta {
+template <bool WIDE = false>
+struct EvalWtaT {
     static constexpr bool kStream = true;
+    // decode key: (value rank desc, slot asc) as one unsigned integer
+    using Key = typename std::conditional<WIDE, unsigned long long, unsigned>::type;
+    static constexpr int KW = WIDE ? 2 : 1;  // 32-bit words per key
     // 32-bit scratch words in shared memory, one column per thread (stride S):
-    // [lists (ncap) | counts (V) | minima (V) | selection mask ((d + 31) / 32)]
+    // [lists (ncap keys) | counts (V) | minima (V keys) | selection mask ((d + 31) / 32)]
     unsigned* L;
     int S;
     int v, slot;  // vehicle and strike slot of the next gene (j = slot V + v)
@@ -738,47 +747,65 @@ struct EvalWta {
         S = nthreads;
     }
     __device__ __forceinline__ unsigned& at(int k) const { return L[k * S]; }
+    __device__ __forceinline__ Key kget(int k) const {
+        if (WIDE) return ((unsigned long long)at(k + 1) << 32) | at(k);
+        return (Key)at(k);
+    }
+    __device__ __forceinline__ void kput(int k, Key key) const {
+        at(k) = (unsigned)key;
+        if (WIDE) at(k + 1) = (unsigned)((unsigned long long)key >> 32);
+    }
+    __device__ __forceinline__ static int counts_at(const ProbDev& P) { return P.wta_ncap * KW; }
+    __device__ __forceinline__ static int minima_at(const ProbDev& P) { return P.wta_ncap * KW + P.wta_vehicles; }
+    __device__ __forceinline__ static int mask_at(const ProbDev& P) {
+        return P.wta_ncap * KW + P.wta_vehicles * (1 + KW);
+    }
     __device__ __forceinline__ void begin(const ProbDev& P) {
         v = 0;
         slot = 0;
-        for (int k = P.wta_ncap; k < P.wta_n32; ++k) at(k) = 0u;
+        for (int k = counts_at(P); k < P.wta_n32; ++k) at(k) = 0u;
     }
     // A vehicle's candidates are ranked by (value desc, slot asc), i.e. the
     // reference's stable order restricted to one vehicle (its genes are
     // j = slot V + v).  Candidates lie in [0.5, 1]: the fp32 bit pattern minus
-    // that of 0.5 orders them in 24 bits, the slot (< 256) takes the low byte.
+    // that of 0.5 orders them in 24 bits; the slot takes the low byte (narrow)
+    // or the low word (WIDE).
     // keeps key among vehicle u's cap_u best (the keys of one vehicle are
     // distinct, so the kept set does not depend on the arrival order)
-    __device__ __forceinline__ void insert(const ProbDev& P, int u, unsigned key) {
-        const int V = P.wta_vehicles;
-        const int cap = P.wta_capv[u], base = P.wta_base[u];
-        const int kc = P.wta_ncap + u, km = P.wta_ncap + V + u;
+    __device__ __forceinline__ void insert(const ProbDev& P, int u, Key key) {
+        const int cap = P.wta_capv[u], base = P.wta_base[u] * KW;
+        const int kc = counts_at(P) + u, km = minima_at(P) + u * KW;
         const int c = (int)at(kc);
         if (c < cap) {
-            at(base + c) = key;
+            kput(base + c * KW, key);
             at(kc) = (unsigned)(c + 1);
             if (c + 1 == cap) {
-                unsigned mn = key;
-                for (int e = 0; e < c; ++e) mn = min(mn, at(base + e));
-                at(km) = mn;
+                Key mn = key;
+                for (int e = 0; e < c; ++e) mn = min(mn, kget(base + e * KW));
+                kput(km, mn);
             }
-        } else if (cap > 0 && key > at(km)) {
-            const unsigned old = at(km);
-            unsigned mn = key;
+        } else if (cap > 0 && key > kget(km)) {
+            const Key old = kget(km);
+            Key mn = key;
             for (int e = 0; e < cap; ++e) {
-                unsigned k2 = at(base + e);
+                Key k2 = kget(base + e * KW);
                 if (k2 == old) {
-                    at(base + e) = key;
+                    kput(base + e * KW, key);
                     k2 = key;
                 }
                 mn = min(mn, k2);
             }
-            at(km) = mn;
+            kput(km, mn);
         }
     }
     __device__ __forceinline__ static bool candidate(float x) { return x >= 0.5f; }
-    __device__ __forceinline__ unsigned key(float x, int s) const {
-        return ((__float_as_uint(x) - 0x3F000000u) << 8) | (255u - (unsigned)s);
+    __device__ __forceinline__ Key key(float x, int s) const {
+        const unsigned rank = __float_as_uint(x) - 0x3F000000u;
+        if (WIDE) return ((unsigned long long)rank << 32) | (0xffffffffu - (unsigned)s);
+        return (Key)((rank << 8) | (255u - (unsigned)s));
+    }
+    __device__ __forceinline__ static int slot_of(Key k) {
+        return WIDE ? (int)(0xffffffffu - (unsigned)(k & 0xffffffffull)) : (int)(255u - (unsigned)(k & 0xffu));
     }
     // the next ng genes at once (the generation kernel's gene groups): only the
     // candidates (bit k of cand: gene k of the group is >= 0.5, value sel(k))
@@ -813,25 +840,29 @@ struct EvalWta {
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
         const int V = P.wta_vehicles, T = P.wta_targets;
-        const int k0 = P.wta_ncap + 2 * V;  // mask words
+        const int k0 = mask_at(P);  // mask words
         for (int u = 0; u < V; ++u) {
-            const int c = (int)at(P.wta_ncap + u);
+            const int c = (int)at(counts_at(P) + u);
             for (int e = 0; e < c; ++e) {
-                const unsigned j = (255u - (at(P.wta_base[u] + e) & 0xffu)) * (unsigned)V + (unsigned)u;
+                const unsigned j = (unsigned)slot_of(kget((P.wta_base[u] + e) * KW)) * (unsigned)V + (unsigned)u;
                 at(k0 + (int)(j >> 5)) |= 1u << (j & 31);
             }
-            emit(u, (double)c - (double)P.wta_capv[u]);  // per-vehicle capacity (wta.cpp:99-100)
+            emit(u, (double)c - (double)P.wta_cap[u]);  // per-vehicle capacity (wta.cpp:99-100)
         }
-        const unsigned vm = V >= 32 ? ~0u : (1u << V) - 1u;
         double f1 = 0.0, f2 = 0.0;
         int s = 0;
         for (int i = 0; i < T; ++i) {
             double surv = 1.0, strikes = 0.0;
             for (int k = 0; k < P.wta_strikes[i]; ++k, ++s) {
-                const int b = s * V, w = b >> 5, o = b & 31;
-                unsigned bits = at(k0 + w) >> o;
-                if (o + V > 32) bits |= at(k0 + w + 1) << (32 - o);
-                const double hd = (double)__popc(bits & vm);
+                // vehicles of slot s: mask bits [s V, s V + V)
+                int hits = 0;
+                for (int b = s * V, e = b + V; b < e;) {
+                    const int w = b >> 5, o = b & 31, take = min(32 - o, e - b);
+                    const unsigned bits = at(k0 + w) >> o;
+                    hits += __popc(take == 32 ? bits : bits & ((1u << take) - 1u));
+                    b += take;
+                }
+                const double hd = (double)hits;
                 surv *= 1.0 - P.wta_p[s] * hd;
                 f2 += hd;
                 strikes += hd;
@@ -843,5 +874,6 @@ struct EvalWta {
         f[1] = f2;
     }
 };
+using EvalWta = EvalWtaT<false>;
 
 }  // namespace gmpea_b200

@@ -22,6 +22,25 @@ __device__ __forceinline__ float pbi(const float4 f, const float4 u, const float
     return d1 + theta * d2;
 }
 
+// ---- aggregation of a subproblem key.  AGG_PBI is the reference's (and the
+// default); AGG_TCH is the weighted Tchebycheff function the north-star names
+// (no reference counterpart, parity unpinned: checked against the oracle's
+// f64 restatement): g = max_k max(w_k, 1e-6) |f_k - z_k| on the lattice
+// weight w.  With the unit vector u = w / |w| (and u.w = 1e-6 / |w|, set at
+// setup) the kernel computes g / |w| -- a positive per-slot scale, so every
+// comparison (OP1 at slot i, OP2/OP3 at slot j) decides as on g itself.
+enum : int { AGG_PBI = 0, AGG_TCH = 1 };
+
+template <int AGG>
+__device__ __forceinline__ float agg_key(const float4 f, const float4 u, const float3 z, float theta) {
+    if (AGG == AGG_TCH) {
+        const float a = fabsf(f.x - z.x), b = fabsf(f.y - z.y), c = fabsf(f.z - z.z);
+        const float t = fmaxf(fmaxf(fmaxf(u.x, u.w) * a, fmaxf(u.y, u.w) * b), fmaxf(u.z, u.w) * c);
+        return isnan(a + b + c) ? a + b + c : t;  // fmaxf would drop a NaN (OP1 rejects it)
+    }
+    return pbi(f, u, z, theta);
+}
+
 __device__ __forceinline__ float3 load_z(const DevState* st, int m) {
     float3 z;
     z.x = ordered_to_float(st->zbits[0]);
@@ -44,13 +63,14 @@ struct Op1Params {
 // OP1 (gmpea.cpp:248-279).  s1: stream 1 takes off2 (FPR-preferred),
 // s2: stream 2 takes off1 (PBI-preferred).  The reference builds both from
 // Heaviside masks over differences, which reject non-finite inputs.
+template <int AGG>
 __device__ __forceinline__ void op1_body(const Op1Params& p, const int bx) {
     if (p.st->stop) return;
     const int i = p.row0 + bx * blockDim.x + threadIdx.x;
     if (i >= p.row_end) return;
     const float3 z = load_z(p.st, p.m);
     const float4 a = p.oFcv[0][i], b = p.oFcv[1][i], u = p.U[i];
-    const float g1 = pbi(a, u, z, p.theta), g2 = pbi(b, u, z, p.theta);
+    const float g1 = agg_key<AGG>(a, u, z, p.theta), g2 = agg_key<AGG>(b, u, z, p.theta);
     if (!isfinite(a.w - b.w) || !isfinite(g1 - g2)) {
         atomicCAS(&p.st->err, 0, ERR_NONFINITE);
         p.st->stop = 1;
@@ -63,7 +83,8 @@ __device__ __forceinline__ void op1_body(const Op1Params& p, const int bx) {
     p.srcbits[i] = (unsigned char)((s1 ? 1 : 0) | (s2 ? 2 : 0));
 }
 
-__global__ void __launch_bounds__(256) op1_kernel(Op1Params p) { op1_body(p, blockIdx.x); }
+template <int AGG>
+__global__ void __launch_bounds__(256) op1_kernel(Op1Params p) { op1_body<AGG>(p, blockIdx.x); }
 
 struct SelParams {
     int n, rs4, m;       // n: local rows (winner code c | n + c)
@@ -131,7 +152,7 @@ __device__ __forceinline__ void unpack_claims(const uint2 w, const int j, const 
     cc[3] = left > 3 ? j + ((int)w.y >> 16) : -1;
 }
 
-template <int POP, bool PACK = false, int NBP = 4>
+template <int POP, bool PACK = false, int NBP = 4, int AGG = AGG_PBI>
 __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const float3 z, bool& feas) {
     // claimants per batch: 4 (R), NBP (4 or 8) from the packed Rp
     constexpr int NB = PACK ? NBP : 4;
@@ -140,7 +161,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     // end), which keeps select at 48 registers (5 blocks of 256 per SM)
     const float4 par4 = p.Fcv[POP][j];
     const float4 u4 = p.U[j];
-    const float gp = pbi(par4, u4, z, p.theta);
+    const float gp = agg_key<AGG>(par4, u4, z, p.theta);
     const float pw = par4.w;
     const int deg = p.Rdeg[POP][j];
     const int* __restrict__ R = p.R[POP];
@@ -183,7 +204,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
             const int c = cc[u];
             if (c < 0) continue;
             const float4 e = ee[u];
-            const float g = pbi(e, u4, z, p.theta);
+            const float g = agg_key<AGG>(e, u4, z, p.theta);
             bool mark;
             if (POP == 0) {  // fpr_better (scalarize.cpp:91-96)
                 negcv |= (e.w < 0.0f) || (pw < 0.0f);
@@ -249,7 +270,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
 #ifndef GMPEA_SELECT_MINBLOCKS
 #define GMPEA_SELECT_MINBLOCKS 5
 #endif
-template <bool PACK = false, int NBP = 4>
+template <bool PACK = false, int NBP = 4, int AGG = AGG_PBI>
 __device__ __forceinline__ void select_body(const SelParams& p, const int bx, const int by) {
     if (p.st->stop) return;
     const int j = p.row0 + bx * blockDim.x + threadIdx.x;
@@ -259,9 +280,9 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
         // blockIdx.y = 0 is pop2 (~4x the claimants per slot): the long
         // blocks are dispatched first and pop1's short ones fill the tail
         if (by == 1)
-            off_taken = select_slot<0, PACK, NBP>(p, j, z, feas);
+            off_taken = select_slot<0, PACK, NBP, AGG>(p, j, z, feas);
         else
-            off_taken = select_slot<1, PACK, NBP>(p, j, z, feas);
+            off_taken = select_slot<1, PACK, NBP, AGG>(p, j, z, feas);
     }
     if (p.rec == nullptr) return;
     // feasible_ratio of pop1 (gmpea.cpp:411-417) and the replacement count
@@ -280,8 +301,11 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
             s += cnt[w];
             t += rep[w];
         }
-        if (s) atomicAdd(&p.rec[p.st->gen].feasible, s);
-        if (t) atomicAdd(&p.rec[p.st->gen].replaced, t);
+        const int k = rec_slot(p.st, p.st->gen);
+        if (k >= 0) {
+            if (s) atomicAdd(&p.rec[k].feasible, s);
+            if (t) atomicAdd(&p.rec[k].replaced, t);
+        }
     }
 }
 
@@ -295,15 +319,21 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
         st->stop = 1;
         return;
     }
-    rec[st->gen].loop_ns = st->loop_ns;
+    const int k = rec_slot(st, st->gen);
+    if (k >= 0) rec[k].loop_ns = st->loop_ns;
     st->gens_done += 1;
     st->gen += 1;
+    if (rec_slot(st, st->gen) < 0) {  // the host did not drain the records: fail loudly
+        atomicCAS(&st->err, 0, ERR_RECORDS);
+        st->stop = 1;
+        return;
+    }
     st->t_gen_start = globaltimer();
 }
 
-template <bool PACK = false, int NBP = 4>
+template <bool PACK = false, int AGG = AGG_PBI>
 __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
-    select_body<PACK, NBP>(p, blockIdx.x, blockIdx.y);
+    select_body<PACK, 4, AGG>(p, blockIdx.x, blockIdx.y);
     if (p.done == nullptr) return;
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -79,7 +79,9 @@ __global__ void lattice_kernel(int n, int m, long long H, double* W, float4* U) 
         n2 += w[c] * w[c];
     }
     const double wn = sqrt(n2);
-    U[i] = make_float4((float)(w[0] / wn), (float)(w[1] / wn), m > 2 ? (float)(w[2] / wn) : 0.0f, 0.0f);
+    // lane w: the Tchebycheff weight floor 1e-6 on the unit scale (select.cuh agg_key)
+    U[i] = make_float4((float)(w[0] / wn), (float)(w[1] / wn), m > 2 ? (float)(w[2] / wn) : 0.0f,
+                       (float)(1e-6 / wn));
 }
 
 // unit vectors of an arbitrary W (operator API)
@@ -93,7 +95,9 @@ __global__ void unit_kernel(int n, int m, const double* W, float4* U, int* err) 
     }
     if (n2 == 0.0) atomicExch(err, 1);  // pbi: zero-norm reference vector
     const double wn = sqrt(n2);
-    U[i] = make_float4((float)(w[0] / wn), (float)(w[1] / wn), m > 2 ? (float)(w[2] / wn) : 0.0f, 0.0f);
+    // lane w: the Tchebycheff weight floor 1e-6 on the unit scale (select.cuh agg_key)
+    U[i] = make_float4((float)(w[0] / wn), (float)(w[1] / wn), m > 2 ? (float)(w[2] / wn) : 0.0f,
+                       (float)(1e-6 / wn));
 }
 
 struct TopK {

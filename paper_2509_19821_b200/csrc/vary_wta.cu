@@ -4,7 +4,10 @@
 namespace gmpea_b200 {
 
 VaryKernel vary_kernel_wta(int mode, int op, int d, int id, bool tour) {
-    (void)id;
+    // id: 1 = more than kWtaNarrowSlots strike slots (64-bit decode keys)
+    if (id)
+        return d > 0 && mode == MODE_VARY ? pick_vary<EvalWtaT<true>, 0, true, true>(mode, op, tour)
+                                          : pick_vary<EvalWtaT<true>>(mode, op, tour);
     return d > 0 && mode == MODE_VARY ? pick_vary<EvalWta, 0, true, true>(mode, op, tour)
                                       : pick_vary<EvalWta>(mode, op, tour);
 }

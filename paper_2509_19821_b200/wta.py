@@ -34,16 +34,36 @@ class WTAInstance:
         return (sum(self.max_strikes[:i]) + k) * self.n_vehicles + m
 
 
+WTA_MAX_SYNTHETIC = 123  # 3 + 122 // 2 = 64 vehicles, the engine's limit
+
+
 def wta_scenario(id: str) -> WTAInstance:
     """Built-in scenarios P1..P10 (wta.cpp:23-49), identical tables."""
     if len(id) < 2 or id[0] != "P" or not id[1:].isdigit() or not 1 <= int(id[1:]) <= 10:
         raise ValueError("unknown WTA scenario: " + id)
+    return _scenario(int(id[1:]))
+
+
+def wta_synthetic(num: int) -> WTAInstance:
+    """Large synthetic instances: the reference's
+    scenario formula (wta.cpp:31-46: 4 + 2(num - 1) targets, 3 + (num - 1)/2
+    vehicles, 1-3 strikes, capacity 2-4, probabilities from the seeded
+    mt19937_64 stream) continued past P10, where the reference stops.  Equal
+    to wta_scenario for num <= 10."""
+    if not 1 <= int(num) <= WTA_MAX_SYNTHETIC:
+        raise ValueError(f"unknown WTA scenario: P{num}")
+    return _scenario(int(num))
+
+
+def _scenario(num: int) -> WTAInstance:
+    nt, nv = 4 + 2 * (num - 1), 3 + (num - 1) // 2
     t, v = C.c_int32(), C.c_int32()
-    strikes = np.zeros(64, np.int32)
-    cap = np.zeros(64, np.int32)
-    pr = np.zeros(256)
-    g._check(g._L.gmpea_wta_scenario(int(id[1:]), C.byref(t), C.byref(v), strikes.ctypes.data_as(g._i32p),
+    strikes = np.zeros(nt, np.int32)
+    cap = np.zeros(nv, np.int32)
+    pr = np.zeros(3 * nt)
+    g._check(g._L.gmpea_wta_scenario(num, C.byref(t), C.byref(v), strikes.ctypes.data_as(g._i32p),
                                      cap.ctypes.data_as(g._i32p), pr.ctypes.data_as(g._dp)))
+    id = f"P{num}"
     s = strikes[:t.value].tolist()
     p, o = [], 0
     for k in s:

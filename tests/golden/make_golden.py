@@ -240,12 +240,73 @@ def baseline_runs_fixture(ref):
     np.savez_compressed(os.path.join(HERE, "baseline_runs.npz"), **out)
 
 
+WTA_LARGE = ("wta_P65.txt", "wta_custom40.txt", "wta_custom24.txt")
+
+
+def wta_file_evaluate(path, X, nc):
+    """The reference's load_wta + evaluate in a numpy-free subprocess
+    (tests/golden/wta_file_eval.py says why)."""
+    import subprocess
+    import tempfile
+
+    n, d = X.shape
+    with tempfile.TemporaryDirectory() as tmp:
+        xin, out = os.path.join(tmp, "x.f64"), os.path.join(tmp, "out.f64")
+        np.ascontiguousarray(X, np.float64).tofile(xin)
+        subprocess.run([sys.executable, os.path.join(HERE, "wta_file_eval.py"), path, xin, str(n), str(d), str(nc),
+                        out], check=True)
+        r = np.fromfile(out, np.float64)
+    F = r[:2 * n].reshape(n, 2)
+    G = r[2 * n:2 * n + n * nc].reshape(n, nc)
+    return F, G, r[2 * n + n * nc:]
+
+
+def wta_large_fixture(ref):
+    """Large WTA scenarios in the reference's file
+    format, evaluated by the reference's own load_wta + make_wta_problem:
+    the synthetic P65 (35 vehicles, 277 slots), a 40-vehicle file with
+    capacities up to 12 (> 256 slots: 64-bit decode keys) and a 24-vehicle
+    file with <= 256 slots (narrow keys past the former 16-vehicle cap)."""
+    sys.path.insert(0, ROOT)
+    from paper_2509_19821_b200.wta import WTAInstance, save_wta, wta_synthetic
+
+    rng = np.random.default_rng(64)
+    insts = [wta_synthetic(65)]
+    for name, nt, nv, cap_hi in (("custom40", 150, 40, 12), ("custom24", 60, 24, 9)):
+        strikes = [int(v) for v in rng.integers(1, 4, nt)]
+        if name == "custom24":  # at most 256 slots
+            while sum(strikes) > 250:
+                strikes[int(np.argmax(strikes))] -= 1
+        p = [[float(v) for v in np.round(rng.uniform(0.3, 0.95, k), 6)] for k in strikes]
+        cap = [int(v) for v in rng.integers(1, cap_hi + 1, nv)]
+        insts.append(WTAInstance(name, nt, nv, strikes, p, cap))
+    out = {}
+    for inst, fname in zip(insts, WTA_LARGE):
+        path = os.path.join(HERE, fname)
+        save_wta(inst, path)
+        d = inst.gene_count()
+        X = f32(rng.random((24, d)))
+        X[16:] = f32(np.round(X[16:] * 4) / 4)  # value ties across the decode order
+        X[20:22] = f32(0.5 + 0.5 * rng.random((2, d)))  # every gene a candidate: capacity binds
+        sparse = rng.random((2, d)) < 0.15 / inst.n_vehicles  # few candidates: feasible rows
+        X[22:] = f32(np.where(sparse, 0.5 + 0.5 * rng.random((2, d)), 0.5 * rng.random((2, d))))
+        nc = inst.n_vehicles + inst.n_targets
+        F, G, cv = wta_file_evaluate(path, X, nc)
+        key = fname[:-4]
+        out[f"{key}/X"] = X.astype(np.float32)
+        out[f"{key}/F"], out[f"{key}/G"], out[f"{key}/cv"] = F, G, cv
+    np.savez_compressed(os.path.join(HERE, "wta_large.npz"), **out)
+
+
 def main():
     if not build_ref():
         raise SystemExit("reference sources not available")
     ref, orc = Reference(), Oracle()
     if "--restated-fronts" in sys.argv:  # only the MW / DAS-CMOP front fixture
         restated_fronts_fixture(ref, orc)
+        return
+    if "--wta-large" in sys.argv:  # only the large WTA scenario fixture
+        wta_large_fixture(ref)
         return
     rng = np.random.default_rng(20250919)
     eval_fixture(ref, orc, rng)
@@ -257,6 +318,7 @@ def main():
     restated_fronts_fixture(ref, orc)
     runs_fixture(ref)
     baseline_runs_fixture(ref)
+    wta_large_fixture(ref)
     print("golden fixtures written to", HERE)
 
 

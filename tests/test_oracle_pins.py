@@ -2,10 +2,11 @@
 trusted as the GPU checker — against published known-answer vectors, the
 committed golden fixtures (made by the unmodified reference) and, where the
 reference build is present, against the reference itself."""
+import os
 import numpy as np
 import pytest
 
-from conftest import MW_PROBLEMS, REF_PROBLEMS, golden
+from conftest import GOLDEN, MW_PROBLEMS, REF_PROBLEMS, golden
 
 
 def test_philox_random123_kat(orc):
@@ -243,3 +244,37 @@ def test_restated_front_candidates_are_feasible_and_in_bounds(orc, name):
     F, G, cv = orc.evaluate(name, X)
     assert np.isfinite(F).all()
     assert (cv == 0.0).mean() >= 0.05, (cv == 0.0).mean()  # MW10: 8.5 % of positions
+
+
+def test_wta_large_files_oracle_pinned_to_reference(orc):
+    """The oracle's WTA restatement on the large scenario files (>= 24
+    vehicles, up to 316 strike slots, capacities up to 12) equals the
+    reference's own load_wta + make_wta_problem + evaluate bit for bit
+    (tests/golden/wta_large.npz, made by the reference)."""
+    from paper_2509_19821_b200.wta import load_wta
+
+    gd = golden("wta_large.npz")
+    for key in ("wta_P65", "wta_custom40", "wta_custom24"):
+        inst = load_wta(os.path.join(GOLDEN, key + ".txt"))
+        orc.wta_register(inst.scenario, inst.n_targets, inst.n_vehicles, inst.max_strikes, inst.capacity,
+                         [v for row in inst.p for v in row])
+        F, G, cv = orc.evaluate("WTA-" + inst.scenario, gd[key + "/X"].astype(np.float64))
+        assert np.array_equal(F, gd[key + "/F"]) and np.array_equal(G, gd[key + "/G"])
+        assert np.array_equal(cv, gd[key + "/cv"])
+
+
+def test_wta_synthetic_scenarios_continue_the_reference_formula(orc):
+    """wta_synthetic(num): the reference's scenario generator (wta.cpp:31-46)
+    continued past P10 -- equal to wta_scenario for P1..P10, and to the
+    oracle's restatement of the same formula up to P123 (64 vehicles)."""
+    from paper_2509_19821_b200.wta import wta_scenario, wta_synthetic
+
+    for num in range(1, 11):
+        assert wta_synthetic(num) == wta_scenario(f"P{num}")
+    for num in (11, 40, 65, 123):
+        w, o = wta_synthetic(num), orc.wta_scenario(num)
+        assert w.n_targets == 4 + 2 * (num - 1) and w.n_vehicles == 3 + (num - 1) // 2
+        assert w.max_strikes == o["strikes"].tolist() and w.capacity == o["capacity"].tolist()
+        assert [v for row in w.p for v in row] == o["p"].tolist()
+    with pytest.raises(ValueError):
+        wta_synthetic(124)
