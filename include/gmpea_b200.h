@@ -29,6 +29,7 @@ extern "C" {
 #define GMPEA_EINVAL 1   /* std::invalid_argument in the reference */
 #define GMPEA_ERUNTIME 2 /* std::runtime_error in the reference */
 #define GMPEA_ECUDA 3    /* CUDA runtime failure / no device */
+#define GMPEA_ENCCL 4    /* NCCL failure (sharded multi-process runs) */
 
 #define GMPEA_OP_SBX_PM 0 /* VariationOp::sbx_pm (gmpea.hpp:56) */
 #define GMPEA_OP_DE 1     /* VariationOp::de */
@@ -178,6 +179,14 @@ typedef struct {
      * [shard_begin, shard_end) of n; 0, 0 = all of them */
     int64_t shard_begin, shard_end;
     int32_t aggregation;   /* GMPEA_AGG_PBI (default, the reference's) or GMPEA_AGG_TCH */
+    /* weight-region sharding over NCCL, one process per GPU:
+     * world > 1 ranks, this process is `rank` and owns the balanced slot range
+     * [rank n / world, (rank + 1) n / world); nccl_id points to the 128-byte
+     * id gmpea_nccl_unique_id made on rank 0 and the caller shared.  The
+     * ideal-point all-reduce and the boundary-row exchange run inside every
+     * generation's CUDA graph; rank 0 keeps the loop clock of a time budget. */
+    int32_t world, rank;
+    const void* nccl_id;
 } gmpea_run_config;
 
 typedef struct {
@@ -211,6 +220,16 @@ int gmpea_run_baseline(const gmpea_problem* p, int32_t algo, const gmpea_run_con
                        double* C, double* cv);
 
 int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmpea_engine** out);
+/* one handle driving a sharded run over several devices of this process
+ * (SURVEY.md §8(b) devices[] / ndev): shard k on devices[k] owns the balanced
+ * slot range k of ndev; each generation is one multi-device CUDA graph (ideal
+ * point MIN over peer memory, boundary rows by peer copies).  Every other
+ * gmpea_engine_* call works on the handle as on an unsharded engine (pop1 /
+ * history of all N slots).  A device may repeat (shards sharing a GPU). */
+int gmpea_engine_create_multi(const gmpea_problem* p, const gmpea_run_config* cfg, const int32_t* devices,
+                              int32_t ndev, gmpea_engine** out);
+/* a new NCCL unique id (128 bytes) for gmpea_run_config.nccl_id */
+int gmpea_nccl_unique_id(void* id128);
 /* replace population `which` (1 or 2) by host rows X (n x d) and re-evaluate.
  * Asynchronous (stream-ordered, no host round trip): rows outside the bounds
  * are reported as evaluate's GMPEA_EINVAL "evaluate: out-of-bounds rows: ..."

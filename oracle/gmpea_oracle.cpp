@@ -1661,6 +1661,104 @@ int orc_reproduce(const char* name, const double* X, int64_t n, const uint32_t* 
     });
 }
 
+// The whole loop of run_gmpea (gmpea.cpp:421-493, k_max semantics) in f64
+// with the engine's Philox draws: init (INIT stream) -> per generation
+// reproduce x2 (B1 / B2) -> evaluate x2 -> update_ideal -> OP1/OP2/OP3.
+// fp32 != 0 rounds the stored state (X, F, C, cv) to fp32 after every step,
+// as the engine stores it, so the three arms reference (mt19937, f64) /
+// oracle (Philox, f64) / oracle (Philox, fp32 storage) separate the draw
+// schema from the arithmetic (the LIRCMOP1 statistics).
+int orc_run_gmpea(const char* name, int64_t n64, int64_t k_max, uint64_t seed, int32_t op, int32_t fp32,
+                  double* Xout, double* Fout, double* cvout) {
+    return guarded([&] {
+        const Problem p = make_problem(name);
+        const size_t n = static_cast<size_t>(n64), d = p.d, m = p.m, nc = p.nin + p.neq;
+        const size_t t1 = std::min<size_t>(5, n), t2 = std::min<size_t>(20, n);
+        std::vector<double> W = reference_vectors(m, n);
+        std::vector<uint32_t> B1(n * t1), B2(n * t2);
+        lattice_knn(m, n, t1, t2, B1.data(), B2.data(), 1);
+        auto rnd = [&](std::vector<double>& v) {
+            if (fp32)
+                for (double& x : v) x = static_cast<double>(static_cast<float>(x));
+        };
+        struct Pop { std::vector<double> X, F, G, cv; };
+        auto eval = [&](Pop& P) {
+            P.F.assign(n * m, 0.0);
+            P.G.assign(n * nc, 0.0);
+            P.cv.assign(n, 0.0);
+            for (size_t r = 0; r < n; ++r) {
+                for (size_t c = 0; c < d; ++c)
+                    if (!(P.X[r * d + c] >= p.lo[c] && P.X[r * d + c] <= p.hi[c]))
+                        throw std::runtime_error("run_gmpea: evaluation failed: out-of-bounds row " +
+                                                 std::to_string(r));
+                eval_row(p, P.X.data() + r * d, P.F.data() + r * m, P.G.data() + r * nc);
+                P.cv[r] = cv_raw(P.G.data() + r * nc, p.nin, p.neq);
+            }
+            rnd(P.F);
+            rnd(P.G);
+            rnd(P.cv);
+        };
+        Pop pop[2];
+        const uint32_t key[2] = {static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32)};
+        for (int q = 0; q < 2; ++q) {
+            pop[q].X.resize(n * d);
+            for (size_t r = 0; r < n; ++r)
+                for (size_t c = 0; c < d; ++c) {
+                    uint32_t ctr[4] = {static_cast<uint32_t>(r), 0u, orc_tag(q + 1, ORC_STREAM_INIT),
+                                       static_cast<uint32_t>(c / 2)};
+                    uint32_t o[4];
+                    orc_philox4x32_10(ctr, key, o);
+                    uint64_t v = (c % 2 == 0) ? ((uint64_t)o[1] << 32 | o[0]) : ((uint64_t)o[3] << 32 | o[2]);
+                    pop[q].X[r * d + c] = p.lo[c] + (p.hi[c] - p.lo[c]) * (static_cast<double>(v >> 11) * 0x1.0p-53);
+                }
+            rnd(pop[q].X);
+            eval(pop[q]);
+        }
+        std::vector<double> z(m, std::numeric_limits<double>::infinity());
+        auto upd = [&](const Pop& P) {
+            for (size_t r = 0; r < n; ++r)
+                for (size_t c = 0; c < m; ++c) z[c] = std::min(z[c], P.F[r * m + c]);
+        };
+        upd(pop[0]);
+        upd(pop[1]);
+        const OpParams prm{1.0, 20.0, 20.0, 1.0, 0.5, -1.0};
+        for (int64_t gen = 1; gen <= k_max; ++gen) {
+            Pop off[2];
+            for (int q = 0; q < 2; ++q) {
+                off[q].X.assign(n * d, 0.0);
+                reproduce(p, pop[q].X.data(), n, q ? B2.data() : B1.data(), q ? t2 : t1, op, prm, seed,
+                          static_cast<uint32_t>(gen), q + 1, off[q].X.data(), nullptr);
+                rnd(off[q].X);
+                eval(off[q]);
+            }
+            upd(off[0]);
+            upd(off[1]);
+            SelIn s{static_cast<int>(n), static_cast<int>(m), pop[0].F.data(), pop[0].cv.data(), pop[1].F.data(),
+                    pop[1].cv.data(), off[0].F.data(), off[0].cv.data(), off[1].F.data(), off[1].cv.data(),
+                    W.data(), z.data(), 5.0, static_cast<int>(t1), static_cast<int>(t2), B1.data(), B2.data()};
+            std::vector<int32_t> src[2] = {std::vector<int32_t>(n), std::vector<int32_t>(n)};
+            selection(s, src[0].data(), src[1].data(), nullptr, nullptr);
+            for (int q = 0; q < 2; ++q) {
+                Pop next = pop[q];
+                for (size_t j = 0; j < n; ++j) {
+                    const int32_t c = src[q][j];
+                    if (c < 0) continue;
+                    const Pop& o = off[c < static_cast<int32_t>(n) ? 0 : 1];
+                    const size_t r = static_cast<size_t>(c) % n;
+                    std::copy(o.X.begin() + r * d, o.X.begin() + (r + 1) * d, next.X.begin() + j * d);
+                    std::copy(o.F.begin() + r * m, o.F.begin() + (r + 1) * m, next.F.begin() + j * m);
+                    std::copy(o.G.begin() + r * nc, o.G.begin() + (r + 1) * nc, next.G.begin() + j * nc);
+                    next.cv[j] = o.cv[r];
+                }
+                pop[q] = std::move(next);
+            }
+        }
+        std::copy(pop[0].X.begin(), pop[0].X.end(), Xout);
+        std::copy(pop[0].F.begin(), pop[0].F.end(), Fout);
+        std::copy(pop[0].cv.begin(), pop[0].cv.end(), cvout);
+    });
+}
+
 // initial population draws (INIT stream): X[r][c] = lo + (hi - lo) * u53
 int orc_init_population(const char* name, int64_t n, uint64_t seed, uint32_t pop, double* X) {
     return guarded([&] {

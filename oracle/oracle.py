@@ -211,6 +211,16 @@ class Oracle(_Lib):
                                            _ptr(off, _dp), _ptr(picks, _i32p), C.c_uint32(slot_base)))
         return off, picks
 
+    def run_gmpea(self, name, n, k_max, seed=1, op=0, fp32=False):
+        """run_gmpea's loop in f64 with the engine's Philox draws (fp32=True:
+        state rounded to fp32 after every step, as the engine stores it).
+        Returns pop1 (X, F, cv)."""
+        info = self.problem_info(name)
+        X, F, cv = np.zeros((n, info["d"])), np.zeros((n, info["m"])), np.zeros(n)
+        self._check(self.lib.orc_run_gmpea(name.encode(), C.c_int64(n), C.c_int64(k_max), C.c_uint64(seed), op,
+                                           1 if fp32 else 0, _ptr(X, _dp), _ptr(F, _dp), _ptr(cv, _dp)))
+        return X, F, cv
+
     def init_population(self, name, n, seed, pop):
         d = self.problem_info(name)["d"]
         X = np.zeros((n, d))

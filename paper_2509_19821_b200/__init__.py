@@ -45,6 +45,7 @@ from ._lib import (  # noqa: F401
     make_problem,
     make_wta_problem,
     metric_front,
+    nccl_unique_id,
     nondominated_sort,
     pf_reference,
     problem_names,

@@ -42,6 +42,7 @@ class _RunConfig(C.Structure):
         ("record_walltime", C.c_int32), ("device", C.c_int32), ("stream", C.c_uint64),
         ("igd_reference", _dp), ("igd_reference_rows", C.c_int64),
         ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("aggregation", C.c_int32),
+        ("world", C.c_int32), ("rank", C.c_int32), ("nccl_id", C.c_void_p),
     ]
 
 
@@ -436,8 +437,13 @@ class RunConfig:
     record_walltime: bool = True
     device: int = 0
     stream: int = 0
-    shard: Optional[tuple] = None  # (begin, end) owned slots of a sharded run
+    shard: Optional[tuple] = None  # (begin, end) owned slots of a caller-driven sharded run
     aggregation: Aggregation = Aggregation.pbi
+    # weight-region shards over NCCL, one process per GPU: this
+    # rank of `world`, with the 128-byte id of nccl_unique_id() from rank 0
+    world: int = 0
+    rank: int = 0
+    nccl_id: Optional[bytes] = None
 
     def _c(self) -> _RunConfig:
         c = _RunConfig()
@@ -457,6 +463,12 @@ class RunConfig:
         if self.shard is not None:
             c.shard_begin, c.shard_end = int(self.shard[0]), int(self.shard[1])
         c.aggregation = int(self.aggregation)
+        c.world, c.rank = int(self.world), int(self.rank)
+        if self.nccl_id is not None:
+            if len(self.nccl_id) != 128:
+                raise ValueError("nccl_id: 128 bytes expected")
+            self._nccl_buf = C.create_string_buffer(bytes(self.nccl_id), 128)  # kept alive with the config
+            c.nccl_id = C.cast(self._nccl_buf, C.c_void_p)
         return c
 
 
@@ -477,15 +489,29 @@ class RunResult:
     effective_n: int
 
 
-class Engine:
-    """One run on one device (the engine behind run_gmpea)."""
+def nccl_unique_id() -> bytes:
+    """A new NCCL unique id for RunConfig.nccl_id (rank 0 makes it, the caller
+    shares it with the other ranks)."""
+    buf = C.create_string_buffer(128)
+    _check(_L.gmpea_nccl_unique_id(buf))
+    return buf.raw
 
-    def __init__(self, problem: Problem, cfg: RunConfig):
+
+class Engine:
+    """One run (the engine behind run_gmpea): on one device, one NCCL rank of a
+    sharded run (cfg.world / rank / nccl_id), or -- with devices -- one handle
+    driving a sharded run over several devices of this process."""
+
+    def __init__(self, problem: Problem, cfg: RunConfig, devices: Optional[Sequence[int]] = None):
         self.problem = problem
         self.cfg = cfg
         self._c = cfg._c()
         h = C.c_void_p()
-        _check(_L.gmpea_engine_create(problem._h, C.byref(self._c), C.byref(h)))
+        if devices is not None:
+            dv = np.ascontiguousarray(devices, np.int32)
+            _check(_L.gmpea_engine_create_multi(problem._h, C.byref(self._c), _p(dv, _i32p), len(dv), C.byref(h)))
+        else:
+            _check(_L.gmpea_engine_create(problem._h, C.byref(self._c), C.byref(h)))
         self._h = h
         self.n = int(_L.gmpea_engine_effective_n(h))
         info = self.shard_info()

@@ -45,7 +45,16 @@ struct DevState {
     int gens_done;
     int rec_base;               // generation of record slot 0 (the host drains older records)
     int rec_cap;                // record slots on the device
+    int follower;               // a sharded time-budget run's shard > 0: rank 0 keeps the loop clock
 };
+
+// stops the run after an error.  zbits[3] (no objective uses it; 0x80000000
+// otherwise) doubles as the shards' go flag: the ideal-point MIN exchange of
+// a sharded run carries a 0 to every shard, whose OP1 then stops too.
+__device__ __forceinline__ void halt(DevState* st) {
+    st->stop = 1;
+    st->zbits[3] = 0u;
+}
 
 // record slot of generation g, or -1 outside the device window
 __host__ __device__ inline int rec_slot(const DevState* st, int g) {

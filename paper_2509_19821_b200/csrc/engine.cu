@@ -22,6 +22,10 @@
 
 #include "../../include/gmpea_b200.h"
 #include "common.cuh"
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include "exchange.cuh"
 #include "host.cuh"
 #include "select.cuh"
 #include "problems.cuh"
@@ -36,6 +40,54 @@ thread_local std::string g_err;
 }  // namespace gmpea_b200
 
 namespace {
+
+// NCCL, resolved at run time from the process's libnccl.so.2 (torch's own when
+// a torch process already loaded it, else the system one): only sharded
+// multi-process runs need it, and the library links no NCCL at build time.
+struct Nccl {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+    static Nccl& get() {
+        static Nccl n = [] {
+            Nccl x;
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) return x;
+            auto sym = [&](auto& f, const char* name) { f = reinterpret_cast<std::decay_t<decltype(f)>>(dlsym(h, name)); };
+            sym(x.GetUniqueId, "ncclGetUniqueId");
+            sym(x.CommInitRank, "ncclCommInitRank");
+            sym(x.CommDestroy, "ncclCommDestroy");
+            sym(x.AllReduce, "ncclAllReduce");
+            sym(x.Broadcast, "ncclBroadcast");
+            sym(x.Send, "ncclSend");
+            sym(x.Recv, "ncclRecv");
+            sym(x.GroupStart, "ncclGroupStart");
+            sym(x.GroupEnd, "ncclGroupEnd");
+            sym(x.GetErrorString, "ncclGetErrorString");
+            return x;
+        }();
+        if (!n.GroupEnd || !n.AllReduce || !n.Send || !n.CommInitRank || !n.GetErrorString)
+            throw std::runtime_error("NCCL (libnccl.so.2) is not available: a multi-process sharded run needs it");
+        return n;
+    }
+};
+
+#define NK(expr)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t r_ = (expr);                                                                  \
+        if (r_ != ncclSuccess)                                                                     \
+            throw nccl_error(std::string(#expr) + ": " + Nccl::get().GetErrorString(r_));         \
+    } while (0)
 
 // wta_scenario (wta.cpp:23-49): sizes grow with the index, tables from the
 // reference's seeded mt19937_64 draws (rng.hpp:18-30).  num > 10 continues
@@ -250,7 +302,8 @@ __global__ void reset_state_kernel(DevState* st, unsigned long long budget_ns, i
     st->gens_done = 0;
     st->rec_base = 0;
     st->rec_cap = rec_cap;
-    st->stop = st->err ? 1 : 0;
+    st->stop = 0;
+    if (st->err) halt(st);
 }
 
 // host rows (f64, row-major) -> fp32 rows, with the reference's f64 bounds
@@ -279,6 +332,7 @@ __global__ void set_z_kernel(DevState* st, int m, float z0, float z1, float z2) 
     st->zbits[0] = float_to_ordered(z0);
     st->zbits[1] = float_to_ordered(z1);
     st->zbits[2] = m > 2 ? float_to_ordered(z2) : float_to_ordered(0.0f);
+    st->zbits[3] = float_to_ordered(0.0f);  // the go flag (common.cuh halt)
 }
 
 __global__ void z_of_kernel(const float4* Fcv, long long n, int m, DevState* st) {
@@ -482,14 +536,43 @@ struct gmpea_engine {
     long long gen_limit = 0;      // max generations allowed by k_max / eval budget (-1 = inf)
     bool finished = false;
 
+    // ---- weight-region shards with the exchange inside the engine
+    int world = 1, rank = 0;   // shards of the run, this one's index
+    bool exchange = false;     // the engine exchanges z / boundary rows itself
+    bool member = false;       // a shard of a multi-device handle (the handle captures)
+    bool follower = false;     // time budget: rank 0 keeps the loop clock
+    ncclComm_t comm = nullptr; // one process per GPU
+    struct Halo {
+        int peer;
+        long long send0, send1, recv0, recv1;  // global slot ranges
+    };
+    std::vector<Halo> halos;
+    DevBuf<LeadState> lead;    // rank 0's loop state (time budget)
+    int* lead_flag = nullptr;  // host-mapped: the run's agreed stop flag
+    int* lead_flag_dev = nullptr;
+    // multi-device handle (gmpea_engine_create_multi): one shard per device
+    std::vector<std::unique_ptr<gmpea_problem>> member_prob;
+    std::vector<std::unique_ptr<gmpea_engine>> members;
+    std::vector<int> member_dev;
+
     ~gmpea_engine() {
+        if (!members.empty()) {
+            sync_all();
+            destroy_group_events();
+        }
+        members.clear();
         if (graph) cudaGraphExecDestroy(graph);
         if (graph_first) cudaGraphExecDestroy(graph_first);
         if (host_flag) cudaFreeHost(host_flag);
+        if (lead_flag) cudaFreeHost(lead_flag);
+        if (comm) Nccl::get().CommDestroy(comm);
         if (own_stream && s) cudaStreamDestroy(s);
     }
 
-    void setup(const gmpea_problem* p, const gmpea_run_config& c) {
+    bool is_group() const { return !members.empty(); }
+
+    // member_world > 0: shard member_rank of a multi-device handle
+    void setup(const gmpea_problem* p, const gmpea_run_config& c, int member_world = 0, int member_rank = 0) {
         prob = p;
         cfg = c;
         if (c.n <= 0) throw std::invalid_argument("reference_vectors: target_n must be positive");
@@ -514,19 +597,38 @@ struct gmpea_engine {
         H = lattice_H(m, N);
         own0 = 0;
         own1 = N;
-        if (c.shard_end > c.shard_begin) {
+        if (member_world > 0 || c.world > 1 || (c.world == 1 && c.nccl_id)) {
+            // balanced weight-region shards, exchange inside the engine
+            world = member_world > 0 ? member_world : c.world;
+            rank = member_world > 0 ? member_rank : c.rank;
+            if (world > kMaxShards) throw std::invalid_argument("engine: at most 16 shards");
+            if (rank < 0 || rank >= world) throw std::invalid_argument("engine: rank outside [0, world)");
+            if (c.shard_end > c.shard_begin) throw std::invalid_argument("engine: world and shard range are exclusive");
+            if (member_world == 0 && !c.nccl_id) throw std::invalid_argument("engine: world > 1 needs an nccl_id");
+            own0 = (long long)rank * N / world;
+            own1 = (long long)(rank + 1) * N / world;
+            sharded = world > 1;
+            exchange = true;
+            member = member_world > 0;
+            follower = time_mode && rank > 0;
+        } else if (c.shard_end > c.shard_begin) {
             if (c.shard_begin < 0 || c.shard_end > N)
                 throw std::invalid_argument("engine: shard range outside [0, n)");
             own0 = c.shard_begin;
             own1 = c.shard_end;
             sharded = own0 > 0 || own1 < N;
         }
-        if (sharded && time_mode)
+        // the caller-driven shards (gmpea_engine_phase) cannot agree on a deadline
+        if (sharded && time_mode && !exchange)
             throw std::invalid_argument("engine: a sharded run takes k_max / eval budgets (the deadline would differ per rank)");
 
         st.alloc(1);
         st.zero(s);
         init_state_kernel<<<1, 1, 0, s>>>(st.p, m);
+        if (follower) {
+            static const int one = 1;
+            CK(cudaMemcpyAsync(&st.p->follower, &one, sizeof(int), cudaMemcpyHostToDevice, s));
+        }
         // generation limit (gmpea.cpp:456-459)
         bool unbounded = c.k_max == 0 && (time_mode || c.eval_budget > 0);
         long long lim = c.k_max > 0 ? c.k_max : (unbounded ? -1 : 0);
@@ -566,9 +668,16 @@ struct gmpea_engine {
                 CK(cudaMemcpyAsync(&hr, r.p, sizeof(int), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 reach = hr;
-                if (own1 - own0 < 2 * reach)
+                const long long narrowest = exchange ? N / world : own1 - own0;
+                if (narrowest < 2 * reach)
                     throw std::invalid_argument("engine: shard narrower than twice the neighbourhood reach (" +
                                                 std::to_string(2 * reach) + " slots)");
+                // boundary rows: my first / last 2r owned rows to the neighbours,
+                // theirs into my window (the exchange after every generation)
+                if (exchange && reach > 0) {
+                    if (rank > 0) halos.push_back({rank - 1, own0, own0 + 2 * reach, own0 - 2 * reach, own0});
+                    if (rank < world - 1) halos.push_back({rank + 1, own1 - 2 * reach, own1, own1, own1 + 2 * reach});
+                }
             }
             e0 = std::max(0ll, own0 - 2 * reach);
             e1 = std::min(N, own1 + 2 * reach);
@@ -609,6 +718,13 @@ struct gmpea_engine {
         CK(cudaHostAlloc(&host_flag, sizeof(int), cudaHostAllocMapped));
         *host_flag = 0;
         CK(cudaHostGetDevicePointer((void**)&host_flag_dev, host_flag, 0));
+        if (exchange && time_mode) {
+            lead.alloc(1);
+            lead.zero(s);
+            CK(cudaHostAlloc(&lead_flag, sizeof(int), cudaHostAllocMapped));
+            *lead_flag = 0;
+            CK(cudaHostGetDevicePointer((void**)&lead_flag_dev, lead_flag, 0));
+        }
 
         // kernel parameter blocks
         vp = VaryParams{};
@@ -708,9 +824,47 @@ struct gmpea_engine {
         // first step does not instantiate the graph (the graph's parameters
         // never change after construction)
         staging.alloc((size_t)n * (d + nc + m + 1));  // every plane of a population readback
-        if (!sharded) build_graph();
+        if (exchange && !member) {
+            // one process per GPU: the communicator, then one eager exchange
+            // (the initial ideal point is global, gmpea.cpp:435-437; it also
+            // connects NCCL's channels before the generation graph captures them)
+            ncclUniqueId id;
+            std::memcpy(&id, c.nccl_id, sizeof(id));
+            NK(Nccl::get().CommInitRank(&comm, world, id, rank));
+            exchange_z();
+            exchange_halo();
+        }
+        if (!sharded || comm) build_graph();
         CK(cudaStreamSynchronize(s));
         check_errors(0);
+    }
+
+    // ---- the exchange steps of one generation (NCCL; a multi-device handle
+    // runs the peer-memory forms of the same steps, group_generation)
+    void exchange_z() {
+        // ideal point MIN and the go flag (zbits[3]) over the shards
+        if (comm) NK(Nccl::get().AllReduce(st.p->zbits, st.p->zbits, 4, ncclUint32, ncclMin, comm, s));
+    }
+    void exchange_lead(const LeadState* leader_lead) {
+        // time budget: every shard adopts rank 0's clock / deadline decision
+        if (!lead.p) return;
+        if (rank == 0) lead_pack_kernel<<<1, 1, 0, s>>>(st.p, lead.p);
+        if (comm) NK(Nccl::get().Broadcast(lead.p, lead.p, sizeof(LeadState), ncclUint8, 0, comm, s));
+        follow_kernel<<<1, 1, 0, s>>>(st.p, comm ? lead.p : leader_lead, lead_flag_dev);
+    }
+    void exchange_halo() {
+        if (!comm || halos.empty()) return;
+        const Nccl& nc_ = Nccl::get();
+        const size_t rb = (size_t)geo.rs4 * 16;
+        NK(nc_.GroupStart());
+        for (int q = 0; q < 2; ++q)
+            for (const Halo& h : halos) {
+                NK(nc_.Send(pop[q].X.p + (h.send0 - e0) * geo.rs4, (size_t)(h.send1 - h.send0) * rb, ncclUint8, h.peer,
+                            comm, s));
+                NK(nc_.Recv(pop[q].X.p + (h.recv0 - e0) * geo.rs4, (size_t)(h.recv1 - h.recv0) * rb, ncclUint8, h.peer,
+                            comm, s));
+            }
+        NK(nc_.GroupEnd());
     }
 
     // evaluation of the initial populations done: z, record 0, gen = 1
@@ -735,6 +889,7 @@ struct gmpea_engine {
     void set_population(int which, const double* X) {
         if (which != 1 && which != 2) throw std::invalid_argument("set_population: which must be 1 or 2");
         if (gens_enqueued) throw std::invalid_argument("set_population: the run has started");
+        if (is_group()) return group_set_population(which, X);
         const int q = which - 1;
         // asynchronous (no host round trip): out-of-bounds rows are recorded on
         // the device and reported, as evaluate's invalid_argument, at the next
@@ -755,10 +910,12 @@ struct gmpea_engine {
         launch_vary(vary_kernel_for(prob->dev, MODE_EVAL, 0), ep, 1, s);
         CK(cudaGetLastError());
         finish_init();
+        exchange_z();  // NCCL shards: the ideal point of the new populations is global (all ranks call this)
     }
 
     void enqueue_generation() {
         enqueue_phase1();
+        exchange_z();      // sharded (NCCL): ideal point over the shards, in the graph
         enqueue_phase2();  // select's last block also publishes the stop flag
     }
 
@@ -773,6 +930,11 @@ struct gmpea_engine {
     void enqueue_phase2() {
         launch_op1();
         launch_select();  // + end_gen
+        exchange_lead(nullptr);
+        launch_restore();
+        exchange_halo();
+    }
+    void launch_restore() {
         if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
 
@@ -783,7 +945,8 @@ struct gmpea_engine {
         CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
         cudaGraph_t g;
         cudaGraphExec_t x;
-        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        // NCCL may touch its own streams while its calls are captured
+        CK(cudaStreamBeginCapture(cs, comm ? cudaStreamCaptureModeRelaxed : cudaStreamCaptureModeThreadLocal));
         cudaStream_t saved = s;
         s = cs;
         if (clock) start_loop_clock();
@@ -810,6 +973,7 @@ struct gmpea_engine {
     long long step(long long k) {
         if (gen_limit >= 0) k = std::min(k, gen_limit - gens_enqueued);
         if (k <= 0) return 0;
+        if (is_group()) return group_step(k);
         build_graph();
         long long done = 0;
         while (done < k) {
@@ -849,7 +1013,9 @@ struct gmpea_engine {
         CK(cudaStreamSynchronize(s));
     }
 
-    // records of generations [0, gens_done] (archive + device window)
+    // records of generations [0, gens_done] (archive + device window); the
+    // feasible / replaced counts of every shard summed (a sharded run: all
+    // ranks call this together)
     std::vector<DevRecord> all_records(long long gens_done) {
         std::vector<DevRecord> out(archive.begin(), archive.end());
         const long long cnt = std::min<long long>(gens_done + 1 - rec_base, rec_cap);
@@ -860,11 +1026,49 @@ struct gmpea_engine {
             out.insert(out.end(), r.begin(), r.end());
         }
         out.resize(gens_done + 1);
+        if (comm && !out.empty()) {
+            std::vector<unsigned> c(2 * out.size());
+            for (size_t k = 0; k < out.size(); ++k) {
+                c[2 * k] = out[k].feasible;
+                c[2 * k + 1] = out[k].replaced;
+            }
+            DevBuf<unsigned> dc(c.size());
+            CK(cudaMemcpyAsync(dc.p, c.data(), c.size() * sizeof(unsigned), cudaMemcpyHostToDevice, s));
+            NK(Nccl::get().AllReduce(dc.p, dc.p, c.size(), ncclUint32, ncclSum, comm, s));
+            CK(cudaMemcpyAsync(c.data(), dc.p, c.size() * sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            for (size_t k = 0; k < out.size(); ++k) {
+                out[k].feasible = c[2 * k];
+                out[k].replaced = c[2 * k + 1];
+            }
+        }
         return out;
     }
 
+    // the run's records [0, gens_done]: a multi-device handle sums its shards
+    std::vector<DevRecord> run_records() {
+        if (!is_group()) return all_records(read_state().gens_done);
+        on(0);
+        const long long g = members[0]->read_state().gens_done;
+        std::vector<DevRecord> out = members[0]->all_records(g);
+        for (size_t k = 1; k < members.size(); ++k) {
+            on(k);
+            std::vector<DevRecord> r = members[k]->all_records(g);
+            for (size_t i = 0; i < out.size(); ++i) {
+                out[i].feasible += r[i].feasible;
+                out[i].replaced += r[i].replaced;
+            }
+        }
+        on(0);
+        return out;
+    }
+
+    // slots whose records the history counts (all N when the shards are summed)
+    long long counted_slots() const { return (comm || is_group()) ? N : own1 - own0; }
+
     // one generation in two phases (sharded runs; no graph, plain launches)
     void phase(int ph) {
+        if (is_group() || comm) throw std::invalid_argument("phase: this run exchanges inside the engine");
         if (ph == 1) {
             if (gen_limit >= 0 && gens_enqueued >= gen_limit)
                 throw std::invalid_argument("phase: generation limit reached");
@@ -883,11 +1087,16 @@ struct gmpea_engine {
         if (!time_mode) {
             if (gen_limit < 0) throw std::invalid_argument("run: unbounded run without a budget");
             step(gen_limit - gens_enqueued);
-            CK(cudaStreamSynchronize(s));
+            sync_all();
         } else {
             // time budget: keep at most two chunks in flight and stop launching
-            // once the device reports the deadline (gmpea.cpp:458, :481-486)
-            const long long chunk = n >= 100000 ? 2 : 16;
+            // once the device reports the deadline (gmpea.cpp:458, :481-486).
+            // Shards watch the agreed flag (rank 0's decision, follow_kernel)
+            // and launch identical chunk sequences, so their collectives match.
+            gmpea_engine& lead_e = is_group() ? *members[0] : *this;
+            volatile int* flag = lead_e.exchange ? lead_e.lead_flag : lead_e.host_flag;
+            const long long chunk = N / world >= 100000 ? 2 : 16;
+            if (is_group()) on(0);
             cudaEvent_t ev[2];
             CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
@@ -897,7 +1106,7 @@ struct gmpea_engine {
                 if (pending[k]) {
                     CK(cudaEventSynchronize(ev[k]));
                     pending[k] = false;
-                    if (*(volatile int*)host_flag) break;
+                    if (*flag) break;
                 }
                 long long launched = step(chunk);
                 if (launched == 0) break;
@@ -905,12 +1114,24 @@ struct gmpea_engine {
                 pending[k] = true;
                 k ^= 1;
             }
-            CK(cudaStreamSynchronize(s));
+            sync_all();
             cudaEventDestroy(ev[0]);
             cudaEventDestroy(ev[1]);
         }
         finished = true;
         check_errors(-1);
+    }
+
+    void sync_all() {
+        if (!is_group()) {
+            CK(cudaStreamSynchronize(s));
+            return;
+        }
+        for (size_t k = 0; k < members.size(); ++k) {
+            on(k);
+            CK(cudaStreamSynchronize(members[k]->s));
+        }
+        on(0);
     }
 
     DevState read_state() {
@@ -921,6 +1142,14 @@ struct gmpea_engine {
     }
 
     void check_errors(int phase) {
+        if (is_group()) {
+            for (size_t k = 0; k < members.size(); ++k) {
+                on(k);
+                members[k]->check_errors(phase);
+            }
+            on(0);
+            return;
+        }
         DevState h = read_state();
         if (!h.err) return;
         std::string where = phase == 0 ? std::string("") :
@@ -942,9 +1171,8 @@ struct gmpea_engine {
     }
 
     std::vector<gmpea_gen_record> history() {
-        DevState h = read_state();
-        const long long g = h.gens_done;
-        std::vector<DevRecord> r = all_records(g);
+        std::vector<DevRecord> r = run_records();
+        const long long g = (long long)r.size() - 1;
         std::vector<gmpea_gen_record> out(g + 1);
         for (long long k = 0; k <= g; ++k) {
             gmpea_gen_record& o = out[k];
@@ -952,7 +1180,7 @@ struct gmpea_engine {
             o.gen = k;
             o.evals = 2ll * N * (k + 1);
             o.wall_ms = cfg.record_walltime ? (k == 0 ? 0.0 : (double)r[k].loop_ns * 1e-6) : 0.0;
-            o.feasible_ratio = (double)r[k].feasible / (double)(own1 - own0);
+            o.feasible_ratio = (double)r[k].feasible / (double)counted_slots();
             o.igd = std::numeric_limits<double>::quiet_NaN();
             o.hv = std::numeric_limits<double>::quiet_NaN();
         }
@@ -961,9 +1189,8 @@ struct gmpea_engine {
 
 
     std::vector<int64_t> replacements() {
-        DevState h = read_state();
-        const long long g = h.gens_done;
-        std::vector<DevRecord> r = all_records(g);
+        std::vector<DevRecord> r = run_records();
+        const long long g = (long long)r.size() - 1;
         std::vector<int64_t> out(g + 1);
         for (long long k = 0; k <= g; ++k) out[k] = k == 0 ? 0 : (int64_t)r[k].replaced;
         return out;
@@ -971,6 +1198,12 @@ struct gmpea_engine {
 
     void record_async(void* dst) {
         static_assert(sizeof(DevRecord) == sizeof(gmpea_raw_record), "raw record layout");
+        if (is_group()) {  // shard 0's record (its own slots' counts), in its stream order
+            on(0);
+            members[0]->gens_enqueued = gens_enqueued;
+            members[0]->record_async(dst);
+            return;
+        }
         const long long k = gens_enqueued - rec_base;
         if (k < 0 || k >= rec_cap) throw std::invalid_argument("record_async: record outside the device window");
         CK(cudaMemcpyAsync(dst, rec.p + k, sizeof(DevRecord), cudaMemcpyDeviceToHost, s));
@@ -978,6 +1211,7 @@ struct gmpea_engine {
 
     // the newest generation record only (one small D2H; the per-step result)
     gmpea_gen_record last_record() {
+        if (is_group()) return history().back();
         struct {
             int gens_done;
         } g{};
@@ -995,7 +1229,7 @@ struct gmpea_engine {
         o.gen = k;
         o.evals = 2ll * N * (k + 1);
         o.wall_ms = cfg.record_walltime && k ? (double)r.loop_ns * 1e-6 : 0.0;
-        o.feasible_ratio = (double)r.feasible / (double)(own1 - own0);
+        o.feasible_ratio = (double)r.feasible / (double)(own1 - own0);  // this rank's slots
         o.igd = o.hv = std::numeric_limits<double>::quiet_NaN();
         return o;
     }
@@ -1007,6 +1241,17 @@ struct gmpea_engine {
     void get_population(int which, double* X, double* F, double* C, double* cv, bool offspring = false) {
         if (which != 1 && which != 2) throw std::invalid_argument("get_population: which must be 1 or 2");
         check_errors(-1);  // never hand out a population a failed generation left behind
+        if (is_group()) {  // the shards' owned rows in slot order
+            for (size_t k = 0; k < members.size(); ++k) {
+                on(k);
+                gmpea_engine& e = *members[k];
+                const long long o = e.own0;
+                e.get_population(which, X ? X + o * d : nullptr, F ? F + o * m : nullptr, C ? C + o * nc : nullptr,
+                                 cv ? cv + o : nullptr, offspring);
+            }
+            on(0);
+            return;
+        }
         const int q = which - 1;
         const long long o0 = own0 - e0, on = own1 - own0;
         const PopBuf& src = offspring ? off[q] : pop[q];
@@ -1034,43 +1279,300 @@ struct gmpea_engine {
         CK(cudaStreamSynchronize(s));
     }
 
+    // per-phase device times of `gens` generations (events on the launching
+    // stream; a multi-device handle: shard 0's stream): ms = [vary_eval, op1,
+    // select (+ end_gen), exchange + restore, total]
     void profile(long long gens, double* ms) {
         if (gen_limit >= 0) gens = std::min(gens, gen_limit - gens_enqueued);
         if (gens <= 0) throw std::invalid_argument("profile: no generations left");
-        start_loop_clock();
-        std::vector<cudaEvent_t> ev(5 * gens);
+        if (is_group()) {
+            sync_all();
+            on(0);
+        } else {
+            start_loop_clock();
+        }
+        std::vector<cudaEvent_t> ev(6 * gens);
         for (auto& e : ev) CK(cudaEventCreate(&e));
         for (long long g = 0; g < gens; ++g) {
-            cudaEvent_t* e = &ev[5 * g];
+            cudaEvent_t* e = &ev[6 * g];
+            if (is_group()) {
+                group_generation(g == 0, e);
+                continue;
+            }
             CK(cudaEventRecord(e[0], s));
-            launch_vary(vary, vp, 2, s);
+            enqueue_phase1();
             CK(cudaEventRecord(e[1], s));
-            launch_op1();
+            exchange_z();
             CK(cudaEventRecord(e[2], s));
-            launch_select();  // + end_gen
+            launch_op1();
             CK(cudaEventRecord(e[3], s));
-            if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
+            launch_select();  // + end_gen
             CK(cudaEventRecord(e[4], s));
+            exchange_lead(nullptr);
+            launch_restore();
+            exchange_halo();
+            CK(cudaEventRecord(e[5], s));
         }
         CK(cudaGetLastError());
-        CK(cudaStreamSynchronize(s));
+        sync_all();
         gens_enqueued += gens;
         double acc[5] = {0, 0, 0, 0, 0};
-        for (long long g = 0; g < gens; ++g) {
-            cudaEvent_t* e = &ev[5 * g];
-            for (int k = 0; k < 4; ++k) {
-                float t = 0.0f;
-                CK(cudaEventElapsedTime(&t, e[k], e[k + 1]));
-                acc[k] += t;
-            }
+        auto dt = [&](cudaEvent_t a, cudaEvent_t b) {
             float t = 0.0f;
-            CK(cudaEventElapsedTime(&t, e[0], e[4]));
-            acc[4] += t;
+            CK(cudaEventElapsedTime(&t, a, b));
+            return (double)t;
+        };
+        for (long long g = 0; g < gens; ++g) {
+            cudaEvent_t* e = &ev[6 * g];
+            acc[0] += dt(e[0], e[1]);
+            acc[1] += dt(e[2], e[3]);
+            acc[2] += dt(e[3], e[4]);
+            acc[3] += dt(e[1], e[2]) + dt(e[4], e[5]);
+            acc[4] += dt(e[0], e[5]);
         }
         for (auto& e : ev) cudaEventDestroy(e);
         for (int k = 0; k < 5; ++k) ms[k] = acc[k] / (double)gens;
         check_errors(-1);
     }
+
+    // ================================================= multi-device handle
+    // (gmpea_engine_create_multi): shard k runs on member_dev[k]; one
+    // generation is one multi-device CUDA graph launched on shard 0's stream.
+    std::vector<PeerStates> peers;       // per shard: every other shard's state
+    std::vector<cudaEvent_t> gev[4];     // per shard: vary / select / finished / halo done
+    cudaEvent_t gev_fork = nullptr, gev_lead = nullptr;
+
+    void on(size_t k) const { CK(cudaSetDevice(member_dev[k])); }
+
+    static std::unique_ptr<gmpea_problem> clone_problem(const gmpea_problem& p) {
+        auto q = std::make_unique<gmpea_problem>();
+        q->name = p.name;
+        q->fam = p.fam;
+        q->id = p.id;
+        q->d = p.d;
+        q->m = p.m;
+        q->nin = p.nin;
+        q->neq = p.neq;
+        q->lo = p.lo;
+        q->hi = p.hi;
+        q->wta = p.wta;
+        q->upload();  // on the current device
+        return q;
+    }
+
+    void setup_group(const gmpea_problem* p, const gmpea_run_config& c, const int32_t* devices, int ndev) {
+        if (!devices || ndev < 1 || ndev > kMaxShards)
+            throw std::invalid_argument("gmpea_engine_create_multi: 1 to 16 devices");
+        if (c.world > 1) throw std::invalid_argument("gmpea_engine_create_multi: world is for one process per GPU");
+        if (c.shard_end > c.shard_begin) throw std::invalid_argument("gmpea_engine_create_multi: no shard range");
+        prob = p;
+        cfg = c;
+        member_dev.assign(devices, devices + ndev);
+        int ndevs = 0;
+        CK(cudaGetDeviceCount(&ndevs));
+        for (int dv : member_dev)
+            if (dv < 0 || dv >= ndevs) throw std::invalid_argument("gmpea_engine_create_multi: no such device");
+        // peer access between the distinct devices (z and the boundary rows)
+        for (int a : member_dev)
+            for (int b : member_dev) {
+                if (a == b) continue;
+                int ok = 0;
+                CK(cudaDeviceCanAccessPeer(&ok, a, b));
+                if (!ok) throw cuda_error("gmpea_engine_create_multi: no peer access between devices");
+                CK(cudaSetDevice(a));
+                cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else CK(e);
+            }
+        for (int k = 0; k < ndev; ++k) {
+            on(k);
+            member_prob.push_back(clone_problem(*p));
+            gmpea_run_config ck = c;
+            ck.device = member_dev[k];
+            ck.stream = k == 0 ? c.stream : 0;
+            ck.world = 0;
+            ck.rank = 0;
+            ck.nccl_id = nullptr;
+            members.push_back(std::make_unique<gmpea_engine>());
+            members.back()->setup(member_prob.back().get(), ck, ndev, k);
+        }
+        gmpea_engine& L = *members[0];
+        N = L.N;
+        d = L.d;
+        m = L.m;
+        nc = L.nc;
+        t1 = L.t1;
+        t2 = L.t2;
+        H = L.H;
+        geo = L.geo;
+        reach = L.reach;
+        own0 = e0 = v0 = 0;
+        own1 = e1 = v1 = N;
+        n = (int)N;
+        world = ndev;
+        exchange = true;
+        sharded = ndev > 1;
+        time_mode = L.time_mode;
+        gen_limit = L.gen_limit;
+        s = L.s;
+        own_stream = false;
+        peers.assign(ndev, PeerStates{});
+        for (int k = 0; k < ndev; ++k)
+            for (int j = 0; j < ndev; ++j)
+                if (j != k) peers[k].st[peers[k].n++] = members[j]->st.p;
+        for (int q = 0; q < 4; ++q) {
+            gev[q].resize(ndev);
+            for (int k = 0; k < ndev; ++k) {
+                on(k);
+                CK(cudaEventCreateWithFlags(&gev[q][k], cudaEventDisableTiming));
+            }
+        }
+        on(0);
+        CK(cudaEventCreateWithFlags(&gev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&gev_lead, cudaEventDisableTiming));
+        exchange_z_eager();  // the initial ideal point is global (gmpea.cpp:435-437)
+        graph = capture_group(false);
+        graph_first = capture_group(true);
+        on(0);
+    }
+
+    void destroy_group_events() {
+        for (auto& v : gev)
+            for (auto e : v) cudaEventDestroy(e);
+        if (gev_fork) cudaEventDestroy(gev_fork);
+        if (gev_lead) cudaEventDestroy(gev_lead);
+    }
+
+    // outside a generation (setup, set_population): z MIN over the shards
+    void exchange_z_eager() {
+        sync_all();
+        for (size_t k = 0; k < members.size(); ++k) {
+            on(k);
+            z_peers_kernel<<<1, 32, 0, members[k]->s>>>(members[k]->st.p, peers[k]);
+            CK(cudaGetLastError());
+        }
+        sync_all();
+    }
+
+    // one generation over every shard; prof (6 events on shard 0's stream)
+    // brackets shard 0's phases for profile()
+    void group_generation(bool clock, cudaEvent_t* prof) {
+        const size_t K = members.size();
+        gmpea_engine& L = *members[0];
+        on(0);
+        if (prof) CK(cudaEventRecord(prof[0], L.s));
+        CK(cudaEventRecord(gev_fork, L.s));
+        for (size_t k = 1; k < K; ++k) {
+            on(k);
+            CK(cudaStreamWaitEvent(members[k]->s, gev_fork, 0));
+        }
+        if (clock) {
+            on(0);
+            L.start_loop_clock();
+        }
+        for (size_t k = 0; k < K; ++k) {  // vary_eval (+ local ideal point)
+            on(k);
+            members[k]->enqueue_phase1();
+            CK(cudaEventRecord(gev[0][k], members[k]->s));
+        }
+        if (prof) {
+            on(0);
+            CK(cudaEventRecord(prof[1], L.s));
+        }
+        for (size_t k = 0; k < K; ++k) {  // ideal point over the shards (peer loads)
+            on(k);
+            for (size_t j = 0; j < K; ++j)
+                if (j != k) CK(cudaStreamWaitEvent(members[k]->s, gev[0][j], 0));
+            z_peers_kernel<<<1, 32, 0, members[k]->s>>>(members[k]->st.p, peers[k]);
+            if (prof && k == 0) CK(cudaEventRecord(prof[2], L.s));
+            members[k]->launch_op1();
+            if (prof && k == 0) CK(cudaEventRecord(prof[3], L.s));
+            members[k]->launch_select();  // + end_gen (shard 0 keeps the clock)
+            if (prof && k == 0) CK(cudaEventRecord(prof[4], L.s));
+            CK(cudaEventRecord(gev[1][k], members[k]->s));
+        }
+        int fin = 1;
+        if (time_mode) {  // every shard adopts shard 0's clock and deadline decision
+            on(0);
+            lead_pack_kernel<<<1, 1, 0, L.s>>>(L.st.p, L.lead.p);
+            CK(cudaEventRecord(gev_lead, L.s));
+            for (size_t k = 0; k < K; ++k) {
+                on(k);
+                if (k) CK(cudaStreamWaitEvent(members[k]->s, gev_lead, 0));
+                follow_kernel<<<1, 1, 0, members[k]->s>>>(members[k]->st.p, L.lead.p, members[k]->lead_flag_dev);
+                members[k]->launch_restore();
+                CK(cudaEventRecord(gev[2][k], members[k]->s));
+            }
+            fin = 2;
+        }
+        for (size_t k = 0; k < K; ++k) {  // boundary parent rows from the neighbours
+            gmpea_engine& E = *members[k];
+            on(k);
+            for (const Halo& h : E.halos) {
+                gmpea_engine& P = *members[h.peer];
+                CK(cudaStreamWaitEvent(E.s, gev[fin][h.peer], 0));
+                const size_t bytes = (size_t)(h.recv1 - h.recv0) * geo.rs4 * sizeof(float4);
+                for (int q = 0; q < 2; ++q)
+                    CK(cudaMemcpyPeerAsync(E.pop[q].X.p + (h.recv0 - E.e0) * geo.rs4, member_dev[k],
+                                           P.pop[q].X.p + (h.recv0 - P.e0) * geo.rs4, member_dev[h.peer], bytes, E.s));
+            }
+            CK(cudaEventRecord(gev[3][k], E.s));
+        }
+        on(0);
+        for (size_t k = 1; k < K; ++k) CK(cudaStreamWaitEvent(L.s, gev[3][k], 0));
+        if (prof) CK(cudaEventRecord(prof[5], L.s));
+        CK(cudaGetLastError());
+    }
+
+    cudaGraphExec_t capture_group(bool clock) {
+        gmpea_engine& L = *members[0];
+        on(0);
+        cudaGraph_t g;
+        cudaGraphExec_t x;
+        CK(cudaStreamBeginCapture(L.s, cudaStreamCaptureModeThreadLocal));
+        group_generation(clock, nullptr);
+        CK(cudaStreamEndCapture(L.s, &g));
+        CK(cudaGraphInstantiate(&x, g, 0));
+        CK(cudaGraphDestroy(g));
+        return x;
+    }
+
+    long long group_step(long long k) {
+        gmpea_engine& L = *members[0];
+        on(0);
+        long long done = 0;
+        while (done < k) {
+            long long room = L.rec_cap - 2 - (gens_enqueued - L.rec_base);
+            if (room <= 0) {  // drain every shard's record window together
+                sync_all();
+                for (size_t j = 0; j < members.size(); ++j) {
+                    on(j);
+                    members[j]->drain_records();
+                }
+                on(0);
+                room = L.rec_cap - 2 - (gens_enqueued - L.rec_base);
+                if (room <= 0) break;
+            }
+            const long long part = std::min(k - done, room);
+            CK(cudaGraphLaunch(done == 0 ? graph_first : graph, L.s));
+            for (long long i = 1; i < part; ++i) CK(cudaGraphLaunch(graph, L.s));
+            gens_enqueued += part;
+            done += part;
+        }
+        return done;
+    }
+
+    void group_set_population(int which, const double* X) {
+        if (gens_enqueued) throw std::invalid_argument("set_population: the run has started");
+        sync_all();
+        for (size_t k = 0; k < members.size(); ++k) {
+            on(k);
+            members[k]->set_population(which, X);
+        }
+        exchange_z_eager();
+        on(0);
+    }
+
 };
 
 // ====================================================================== C ABI
@@ -1495,6 +1997,29 @@ int gmpea_engine_create(const gmpea_problem* p, const gmpea_run_config* cfg, gmp
     });
 }
 
+int gmpea_engine_create_multi(const gmpea_problem* p, const gmpea_run_config* cfg, const int32_t* devices,
+                              int32_t ndev, gmpea_engine** out) {
+    return guarded([&] {
+        if (!p || !cfg || !out) throw std::invalid_argument("gmpea_engine_create_multi: null argument");
+        require_device();
+        int saved = 0;
+        CK(cudaGetDevice(&saved));
+        auto e = std::make_unique<gmpea_engine>();
+        e->setup_group(p, *cfg, devices, ndev);
+        *out = e.release();
+        CK(cudaSetDevice(saved));
+    });
+}
+
+int gmpea_nccl_unique_id(void* id128) {
+    return guarded([&] {
+        if (!id128) throw std::invalid_argument("gmpea_nccl_unique_id: null argument");
+        ncclUniqueId id;
+        NK(Nccl::get().GetUniqueId(&id));
+        std::memcpy(id128, &id, sizeof(id));
+    });
+}
+
 int gmpea_engine_set_population(gmpea_engine* e, int32_t which, const double* X) {
     return guarded([&] { e->set_population(which, X); });
 }
@@ -1555,21 +2080,34 @@ int gmpea_engine_get_offspring(gmpea_engine* e, int32_t which, double* X, double
 
 int gmpea_engine_ideal(gmpea_engine* e, double* z) {
     return guarded([&] {
-        DevState h = e->read_state();
+        if (e->is_group()) {
+            e->sync_all();
+            e->on(0);
+        }
+        DevState h = (e->is_group() ? *e->members[0] : *e).read_state();
         for (int k = 0; k < e->m; ++k) z[k] = ordered_to_float(h.zbits[k]);
     });
 }
 
 int gmpea_engine_neighborhoods(gmpea_engine* e, uint32_t* B1, uint32_t* B2) {
     return guarded([&] {
-        const long long o0 = e->own0 - e->e0, on = e->own1 - e->own0;
-        uint32_t* outs[2] = {B1, B2};
-        for (int q = 0; q < 2; ++q) {
-            if (!outs[q]) continue;
-            const int t = q ? e->t2 : e->t1;
-            CK(cudaMemcpy(outs[q], e->B[q].p + o0 * t, (size_t)on * t * sizeof(int), cudaMemcpyDeviceToHost));
-            for (long long k = 0; k < on * t; ++k) outs[q][k] += (uint32_t)e->e0;  // global slots
+        auto one = [&](gmpea_engine* x, uint32_t* b1, uint32_t* b2) {
+            const long long o0 = x->own0 - x->e0, on = x->own1 - x->own0;
+            uint32_t* outs[2] = {b1, b2};
+            for (int q = 0; q < 2; ++q) {
+                if (!outs[q]) continue;
+                const int t = q ? x->t2 : x->t1;
+                CK(cudaMemcpy(outs[q], x->B[q].p + o0 * t, (size_t)on * t * sizeof(int), cudaMemcpyDeviceToHost));
+                for (long long k = 0; k < on * t; ++k) outs[q][k] += (uint32_t)x->e0;  // global slots
+            }
+        };
+        if (!e->is_group()) return one(e, B1, B2);
+        for (size_t k = 0; k < e->members.size(); ++k) {  // the shards' owned rows in slot order
+            e->on(k);
+            gmpea_engine* x = e->members[k].get();
+            one(x, B1 ? B1 + x->own0 * e->t1 : nullptr, B2 ? B2 + x->own0 * e->t2 : nullptr);
         }
+        e->on(0);
     });
 }
 
@@ -1591,6 +2129,7 @@ int gmpea_engine_phase(gmpea_engine* e, int32_t phase) {
 
 int gmpea_engine_device_buffers(gmpea_engine* e, gmpea_device_buffers* o) {
     return guarded([&] {
+        if (e->is_group()) throw std::invalid_argument("device_buffers: a multi-device handle has one set per shard");
         o->ideal_bits = e->st.p->zbits;
         for (int q = 0; q < 2; ++q) {
             o->rows[q] = e->pop[q].X.p;

@@ -35,6 +35,9 @@ extern thread_local std::string g_err;  // defined in engine.cu
 struct cuda_error : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct nccl_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 #define CK(expr)                                                                             \
     do {                                                                                     \
@@ -51,6 +54,9 @@ int guarded(Fn&& fn) {
     } catch (const cuda_error& e) {
         g_err = e.what();
         return GMPEA_ECUDA;
+    } catch (const nccl_error& e) {
+        g_err = e.what();
+        return GMPEA_ENCCL;
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return GMPEA_EINVAL;

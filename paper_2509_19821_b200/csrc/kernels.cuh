@@ -757,7 +757,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 if (k < p.bad_cap) p.bad_rows[pi][k] = p.slot_base + i;  // the population's row index
                 if (atomicCAS(&st->err, 0, ERR_EVAL_OOB) == 0) st->err_gen = (int)gen;
                 // the reference throws here (gmpea.cpp:469-471): the rest of the run is a no-op
-                if (MODE == MODE_VARY) st->stop = 1;
+                if (MODE == MODE_VARY) halt(st);
             } else {
                 Emitter em{reinterpret_cast<float*>(wr4) + d, {}, 0.0, false};
                 em.cv.init(p.P.nin);

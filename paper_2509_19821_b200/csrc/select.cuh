@@ -65,7 +65,11 @@ struct Op1Params {
 // Heaviside masks over differences, which reject non-finite inputs.
 template <int AGG>
 __device__ __forceinline__ void op1_body(const Op1Params& p, const int bx) {
-    if (p.st->stop) return;
+    // a shard's error arrives as a zero go flag with the ideal-point exchange
+    if (p.st->stop || p.st->zbits[3] == 0u) {
+        if (bx == 0 && threadIdx.x == 0) halt(p.st);
+        return;
+    }
     const int i = p.row0 + bx * blockDim.x + threadIdx.x;
     if (i >= p.row_end) return;
     const float3 z = load_z(p.st, p.m);
@@ -73,7 +77,7 @@ __device__ __forceinline__ void op1_body(const Op1Params& p, const int bx) {
     const float g1 = agg_key<AGG>(a, u, z, p.theta), g2 = agg_key<AGG>(b, u, z, p.theta);
     if (!isfinite(a.w - b.w) || !isfinite(g1 - g2)) {
         atomicCAS(&p.st->err, 0, ERR_NONFINITE);
-        p.st->stop = 1;
+        halt(p.st);
         return;
     }
     const bool s1 = b.w < a.w || (a.w == b.w && g1 > g2);
@@ -237,7 +241,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     }
     if (negcv) {
         atomicCAS(&p.st->err, 0, ERR_NEG_CV);
-        p.st->stop = 1;
+        halt(p.st);
     }
     // The reference puts the parent into the argmin at index mex(claims)
     // (gmpea.cpp:343-371), where that index decides only an exact key tie
@@ -311,7 +315,7 @@ __device__ __forceinline__ void select_body(const SelParams& p, const int bx, co
 
 // loop-time bookkeeping after a generation (gmpea.cpp:480-488)
 __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
-    if (st->stop) return;
+    if (st->stop || st->follower) return;  // a follower takes rank 0's clock (follow_kernel)
     const unsigned long long now = globaltimer();
     st->loop_ns += now - st->t_gen_start;
     if (st->budget_ns && st->loop_ns >= st->budget_ns) {
@@ -325,7 +329,7 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     st->gen += 1;
     if (rec_slot(st, st->gen) < 0) {  // the host did not drain the records: fail loudly
         atomicCAS(&st->err, 0, ERR_RECORDS);
-        st->stop = 1;
+        halt(st);
         return;
     }
     st->t_gen_start = globaltimer();
