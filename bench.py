@@ -5,20 +5,27 @@ update_ideal, environmental selection) over both populations.  The headline
 workload is BASELINE.json configs[2]: LIRCMOP13 (m = 3, D = 30, DE — the
 suite default, experiment.cpp:117-123) at N = 1,000,000 subproblems, the
 N = 1M metric "individual-generations/sec" (2N per generation, the
-reference's evals unit, gmpea.cpp:433,487).
+reference's evals unit, gmpea.cpp:433,487).  The metric's second half, "IGD
+at fixed 1 s budget", is the line's `quality_1s` (LIRCMOP13: the engine at
+N = 10^5 and the reference's own loop at N = 1000 on one core, both with
+run_gmpea's deadline semantics, gmpea.cpp:458,481-486).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-Multi-GPU (torchrun, one rank per GPU): the same N = 1M run split into
-weight-region shards — an ideal-point all-reduce and a
-boundary-row exchange over NCCL per generation; value = 2N per generation /
-max step time over ranks (strong scaling).
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun
+re-launches itself under torch.distributed.run).  The same N = 1M run is split
+into weight-region shards; the engine all-reduces the ideal
+point and exchanges the boundary rows over NCCL inside every generation's
+CUDA graph (torch.distributed only shares the NCCL id and takes the max of
+the ranks' times).  value = 2N per generation / max step time over ranks
+(strong scaling).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -67,7 +74,7 @@ def peaks():
 
 
 def alg_bytes(d, m, nc, t1, t2):
-    """Algorithmic bytes per individual (DESIGN.md "Roofline"):
+    """Algorithmic bytes per individual (DESIGN.md §4):
     vary_eval reads the parent row + its neighbour row and writes the child
     row (X, G, packed F|cv); op1 reads two packed keys + the unit weight and
     writes two keys + a byte; select reads the parent key, weight and reverse
@@ -83,7 +90,7 @@ def alg_bytes(d, m, nc, t1, t2):
 class Clocks:
     """SM clock and throttle-reason samples DURING the timed region
     (B200_PROFILING.md): an NVML poller thread (~2 ms period), so even a
-    50 ms region is sampled; falls back to nvidia-smi if NVML is missing."""
+    50 ms region is sampled."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
@@ -141,6 +148,17 @@ def dist_env():
     return world, rank, local
 
 
+def relaunch_distributed(nproc):
+    """`python bench.py --gpus N` outside torchrun: run this script under
+    torch.distributed.run with one rank per GPU (rank 0 prints the line)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def ncu_traffic(kernel, workload):
     """dram bytes per launch of `kernel` from the committed ncu --set full
     summary: the entry "kernel@workload", or the plain "kernel" entry, which
@@ -176,6 +194,51 @@ def ref_threads():
     return int(os.environ.get("GMPEA_REF_THREADS", "0")) or max(1, os.cpu_count() or 1)
 
 
+def quality_1s(g, problem="LIRCMOP13", op=1, budget=1.0, gpu_n=100_000, ref_n=1000, seed=1):
+    """The metric's second half: final IGD after a fixed 1 s loop budget with
+    run_gmpea's semantics (checked before each generation, the crossing one
+    discarded: gmpea.cpp:458,481-486), scored with metric_front + IGD against
+    the reference's own 1000-point pf_reference front (tests/golden/fronts.npz).
+    The engine runs on this GPU at N = gpu_n; the reference's own run_gmpea
+    (oracle/_ref) on one host core at N = ref_n."""
+    front = np.load(os.path.join(ROOT, "tests", "golden", "fronts.npz"))[problem]
+    p = g.make_problem(problem)
+    out = {"problem": problem, "budget_s": budget, "seed": seed, "front": "reference pf_reference, 1000 points"}
+    r = g.run_gmpea(p, g.RunConfig(n=gpu_n, time_budget_s=budget, seed=seed, op=op))
+    fr = g.metric_front(r.pop1)
+    out["engine"] = {"n": gpu_n, "generations": r.history[-1].gen, "loop_ms": r.history[-1].wall_ms,
+                     "front_points": int(len(fr)), "igd": float(g.igd(fr, front)) if len(fr) else float("inf")}
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Reference  # the reference arm (baseline only)
+
+        ref = Reference()
+        pop, hist = ref.run_gmpea(problem, ref_n, k_max=0, seed=seed, op=op, time_budget_s=budget,
+                                  record_walltime=True)
+        rfr = ref.metric_front(pop["F"], pop["cv"])
+        out["reference"] = {"n": ref_n, "cores": 1, "generations": int(hist[-1][0]), "loop_ms": float(hist[-1][2]),
+                            "front_points": int(len(rfr)),
+                            "igd": float(ref.igd(rfr, front)) if len(rfr) else float("inf")}
+    except Exception as e:  # noqa: BLE001
+        out["reference"] = {"unavailable": str(e)}
+    return out
+
+
+def throughput(g, eng, steps, warmup, stream):
+    """Device-timed generations of an engine: (ms per step, clocks)."""
+    import torch
+
+    eng.step(warmup)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    eng.step(steps)
+    end.record(stream)
+    torch.cuda.synchronize()
+    eng.sync()
+    return start.elapsed_time(end) / steps
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -184,9 +247,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="lircmop13-1m", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip quality_1s and the mw1-1m sub-line")
     ap.add_argument("--cpu-gens", type=int, default=20)
     args = ap.parse_args()
     world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
     problem, n, op = WORKLOADS[args.workload]
     config = {"workload": f"{args.workload}: {problem} ({CONFIG_OF[args.workload]}), N={n}, t1=5, t2=20, "
                           f"theta=5, op={'de' if op else 'sbx_pm'}, seed=1",
@@ -218,40 +284,50 @@ def main():
     import torch
 
     # GMPEA_DIST_BACKEND=gloo: a functional check of the sharded path with
-    # several ranks on fewer GPUs (host-staged exchange, no rank's kernel waits
-    # on another's); never a bench number.  The product path is NCCL.
+    # several ranks on fewer GPUs (caller-driven exchange, host-staged, no
+    # rank's kernel waits on another's); never a bench number.  The product
+    # path is the engine's own NCCL exchange.
     backend = os.environ.get("GMPEA_DIST_BACKEND", "nccl")
     if backend != "nccl":
         local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group(backend)
+        # plumbing only (the NCCL id, the max of the ranks' times): gloo on host
+        dist.init_process_group("gloo")
     import paper_2509_19821_b200 as g
 
     stream = torch.cuda.Stream()  # the engine's launching stream (events are recorded on it)
     torch.cuda.set_stream(stream)
     prob = g.make_problem(problem)
     budget_gens = args.warmup + 4 * args.steps + 16
-    if world == 1:
-        cfg = g.RunConfig(n=n, k_max=0, eval_budget=2 * n * budget_gens, seed=1, op=op, device=local,
-                          stream=stream.cuda_stream)
-        eng = g.Engine(prob, cfg)
-        advance = eng.step  # CUDA-graph replay, one graph per generation
-    else:
-        # weight-region shards of the same N = 1M run (strong scaling): ideal
-        # point all-reduce + boundary-row exchange over NCCL every generation
+
+    def shard_cfg(**kw):
+        """the run's config: unsharded, or this rank's NCCL shard"""
+        if world == 1:
+            return g.RunConfig(n=n, seed=kw.pop("seed", 1), op=op, device=local, stream=stream.cuda_stream, **kw)
+        if backend == "nccl":
+            ids = [g.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+            return g.RunConfig(n=n, seed=kw.pop("seed", 1), op=op, device=local, stream=stream.cuda_stream,
+                               world=world, rank=rank, nccl_id=ids[0], **kw)
+        return g.RunConfig(n=n, seed=kw.pop("seed", 1), op=op, device=local, stream=stream.cuda_stream, **kw)
+
+    legacy = world > 1 and backend != "nccl"
+    if legacy:
         from paper_2509_19821_b200.sharded import GpuShard, TorchComm
 
-        cfg = g.RunConfig(n=n, k_max=budget_gens, seed=1, op=op, device=local, stream=stream.cuda_stream)
-        shard = GpuShard(prob, cfg, world, rank, TorchComm())
-        eng = shard.eng
-        advance = shard.run
+        shard = GpuShard(prob, shard_cfg(k_max=budget_gens), world, rank, TorchComm())
+        eng, advance = shard.eng, shard.run
+    else:
+        eng = g.Engine(prob, shard_cfg(k_max=0, eval_budget=2 * n * budget_gens))
+        advance = eng.step  # one CUDA graph per generation (NCCL inside it when sharded)
     advance(args.warmup)
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    if dist:
+        dist.barrier()
 
     # ---- timed region: K generations, CUDA events on the engine's stream,
     # clocks sampled by NVML while it runs
@@ -264,19 +340,20 @@ def main():
         torch.cuda.synchronize()
     eng.sync()
     ms_total = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([ms_total], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    if dist:
+        t = torch.tensor([ms_total], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = 2 * n / (ms_step * 1e-3)  # whole job: all ranks together process the N-slot generation
     # replacement rate over the timed generations (it drifts
-    # over a run, so it is reported with the throughput)
+    # over a run, so it is reported with the throughput); all ranks together
     rr = eng.replacement_rates()
     rep_rate = float(np.mean(rr[args.warmup + 1:args.warmup + 1 + args.steps]))
-    # per-kernel device times (events around every launch) on this rank's
-    # engine; run after the timed region (the shards no longer exchange)
+    # per-kernel device times (events around every launch, this rank's
+    # engine, the exchange included), after the timed region
     kms = eng.profile(args.steps)
+    info = eng.shard_info()
 
     # ---- e2e: the public API with (pinned) host buffers
     def pinned(shape):
@@ -286,74 +363,82 @@ def main():
     X1, X2 = pinned((n, prob.d)), pinned((n, prob.d))
     X1[:] = prob.lower + (prob.upper - prob.lower) * rng.random((n, prob.d))
     X2[:] = prob.lower + (prob.upper - prob.lower) * rng.random((n, prob.d))
-    if world == 1:
-        eng2 = g.Engine(prob, g.RunConfig(n=n, k_max=args.steps, seed=11, op=op, device=local))
-        step1 = lambda: eng2.step(1)  # noqa: E731
+    if legacy:
+        sh2 = GpuShard(prob, shard_cfg(k_max=args.steps, seed=11), world, rank, TorchComm())
+        eng2, step1 = sh2.eng, sh2.step
     else:
-        sh2 = GpuShard(prob, g.RunConfig(n=n, k_max=args.steps, seed=11, op=op, device=local,
-                                         stream=stream.cuda_stream), world, rank, TorchComm())
-        eng2 = sh2.eng
-        step1 = sh2.step
+        eng2 = g.Engine(prob, shard_cfg(k_max=args.steps, seed=11))
+        step1 = lambda: eng2.step(1)  # noqa: E731
     rows = eng2.rows_owned
+    info2 = eng2.shard_info()
     out = g.Population(pinned((rows, prob.d)), pinned((rows, prob.m)), pinned((rows, prob.n_constraints)),
                        pinned(rows))
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    if dist:
+        dist.barrier()
     t0 = time.perf_counter()
-    eng2.set_population(1, X1)
+    eng2.set_population(1, X1)  # asynchronous: H2D + conversion + evaluation in stream order
     eng2.set_population(2, X2)
-    if world > 1:
+    if legacy:
         sh2._z_allreduce()
-    # each step's result (the generation record: pop1 feasible count) is
-    # copied D2H into pinned memory in stream order, without a host stall
-    # between steps; the host reads them after the final population copy
+    # each step's result (the generation record: feasible count of the rank's
+    # slots) is copied D2H into pinned memory in stream order, without a host
+    # stall between steps; the host reads them after the final population copy
     recs = torch.zeros((args.steps, 16), dtype=torch.uint8, pin_memory=True).numpy()
     for k in range(args.steps):
         step1()
         eng2.record_async(recs[k])
-    pop = eng2.population(1, out=out)  # synchronises the stream
+    pop = eng2.population(1, out=out)  # one synchronisation for the whole readback
     feas = recs.view(np.uint32)[:, 0].astype(np.float64) / rows
     t1 = time.perf_counter()
     e2e_s = t1 - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    h2d = X1.nbytes + X2.nbytes
+    # bytes this rank copied: its parent window of each population in, its
+    # owned rows of pop1 and the records out
+    h2d = 2 * (info2["window_end"] - info2["window_begin"]) * prob.d * 8
     d2h = recs.nbytes + pop.X.nbytes + pop.F.nbytes + pop.C.nbytes + pop.cv.nbytes
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+        b = torch.tensor([h2d, d2h], dtype=torch.float64)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM)
+        h2d, d2h = (int(v) for v in b.tolist())
     e2e = {"value": 2 * n * args.steps / e2e_s, "unit": "ind-gen/s",
            "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
-           "note": "pinned host buffers: set_population x2 (H2D + evaluation) + K x (step + async D2H "
-                   "of the step's generation record) + final pop1 (X, F, C, cv) D2H, host wall clock, "
-                   "max over ranks",
+           "note": "pinned host buffers: set_population x2 (f64 H2D + evaluation, asynchronous) + K x (step + "
+                   "async D2H of the step's generation record) + final pop1 (X, F, C, cv) D2H with one "
+                   "synchronisation; host wall clock, max over ranks; bytes summed over ranks",
            "feasible_ratio_last": float(feas[-1])}
     eng2.close()
 
     if rank != 0:
         eng.close()
-        if world > 1:
-            torch.distributed.destroy_process_group()
+        if dist:
+            dist.destroy_process_group()
         return
 
+    # ---- roofline of the dominant kernel, per rank (this rank's own rows)
     pk, pk_kind = peaks()
     ab = alg_bytes(prob.d, prob.m, prob.n_constraints, 5, 20)
     names = ["vary_eval", "op1", "select"]
     shares = {k: float(kms[i] / kms[4]) for i, k in enumerate(names)}
     dom = max(names, key=lambda k: kms[names.index(k)])
     di = names.index(dom)
-    units = 2 * n if dom != "op1" else n
+    vary_rows = info["vary_end"] - info["vary_begin"]
+    own_rows = info["own_end"] - info["own_begin"]
+    units = {"vary_eval": 2 * vary_rows, "op1": vary_rows, "select": 2 * own_rows}[dom]
     per_unit = ab[dom] * (2 if dom == "op1" else 1)
     achieved = per_unit * units / (kms[di] * 1e-3) / 1e9
-    traffic = ncu_traffic(dom, args.workload)
+    traffic = ncu_traffic(dom, args.workload) if world == 1 else None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
                 "alg_bytes_per_unit": per_unit, "units_per_launch": units,
+                "scope": "rank 0's kernel over its own rows" if world > 1 else "the whole run",
                 "kernel_ms": {k: float(kms[i]) for i, k in enumerate(names)},
+                "exchange_ms": float(kms[3]),
                 "kernel_share": shares,
                 "whole_step": {"alg_bytes_per_individual": ab["survey_B_alg"],
                                "achieved_GBps": ab["survey_B_alg"] * 2 * n / (ms_step * 1e-3) / 1e9}}
-
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -368,17 +453,35 @@ def main():
                    "sample": f"unavailable: {e}"}
     eng.close()
 
-    if backend != "nccl":
+    extras = {}
+    if world == 1 and not args.no_extras and args.workload == "lircmop13-1m":
+        # the north-star's MW target (>= 1e8 ind-gen/s per B200 on MW at N = 1M)
+        mp = g.make_problem("MW1")
+        me = g.Engine(mp, g.RunConfig(n=1_000_000, k_max=0, eval_budget=2_000_000 * 64, seed=1, op=0,
+                                      device=local, stream=stream.cuda_stream))
+        mms = throughput(g, me, 20, 5, stream)
+        mk = me.profile(5)
+        me.close()
+        mab = alg_bytes(mp.d, mp.m, mp.n_constraints, 5, 20)
+        extras["mw1_1m"] = {"value": 2e6 / (mms * 1e-3), "unit": "ind-gen/s", "ms_per_step": mms, "steps": 20,
+                            "warmup": 5, "vary_eval_ms": float(mk[0]),
+                            "vary_eval_roofline_frac": mab["vary_eval"] * 2e6 / (mk[0] * 1e-3) / 1e9 / pk["hbm_gbs"],
+                            "north_star_target": 1e8}
+        extras["quality_1s"] = quality_1s(g)
+
+    if legacy:
         config["functional_check"] = f"{world} ranks over {backend} on {torch.cuda.device_count()} GPU(s): not a bench number"
+    elif world > 1:
+        config["shards"] = f"{world} weight-region shards, NCCL z all-reduce + boundary-row send/recv in the generation graph"
     line = {"metric": METRIC, "value": value, "unit": "ind-gen/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong",  # N = 1M slots in total, split into weight-region shards
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (Philox-initialised populations)",
             "config": config, "replacement_rate": rep_rate, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "clocks": clocks.summary(), "gpu_launches": int(3 * args.steps + 1 if world == 1 else 4 * args.steps)}
+            "clocks": clocks.summary(), "gpu_launches": int(3 * args.steps), **extras}
     print(json.dumps(line), flush=True)
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    if dist:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

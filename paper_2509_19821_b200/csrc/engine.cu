@@ -556,8 +556,11 @@ struct gmpea_engine {
     std::vector<int> member_dev;
 
     ~gmpea_engine() {
-        if (!members.empty()) {
-            sync_all();
+        if (!members.empty()) {  // (no throwing calls in a destructor)
+            for (size_t k = 0; k < members.size(); ++k) {
+                cudaSetDevice(member_dev[k]);
+                cudaStreamSynchronize(members[k]->s);
+            }
             destroy_group_events();
         }
         members.clear();
@@ -1511,10 +1514,13 @@ struct gmpea_engine {
             for (const Halo& h : E.halos) {
                 gmpea_engine& P = *members[h.peer];
                 CK(cudaStreamWaitEvent(E.s, gev[fin][h.peer], 0));
-                const size_t bytes = (size_t)(h.recv1 - h.recv0) * geo.rs4 * sizeof(float4);
-                for (int q = 0; q < 2; ++q)
-                    CK(cudaMemcpyPeerAsync(E.pop[q].X.p + (h.recv0 - E.e0) * geo.rs4, member_dev[k],
-                                           P.pop[q].X.p + (h.recv0 - P.e0) * geo.rs4, member_dev[h.peer], bytes, E.s));
+                HaloCopy hc;
+                hc.n4 = (h.recv1 - h.recv0) * geo.rs4;
+                for (int q = 0; q < 2; ++q) {
+                    hc.dst[q] = E.pop[q].X.p + (h.recv0 - E.e0) * geo.rs4;
+                    hc.src[q] = P.pop[q].X.p + (h.recv0 - P.e0) * geo.rs4;
+                }
+                halo_pull_kernel<<<(int)std::min<long long>(blocks_for(hc.n4, 256), 4 * 148), 256, 0, E.s>>>(hc);
             }
             CK(cudaEventRecord(gev[3][k], E.s));
         }

@@ -58,4 +58,19 @@ __global__ void follow_kernel(DevState* st, const LeadState* lead, volatile int*
     if (host_flag) *host_flag = st->stop | (st->err ? 2 : 0);
 }
 
+// boundary rows of both populations from a neighbour shard (peer loads over
+// NVLink, or the same device): dst[q][i] = src[q][i], i < n4 float4
+struct HaloCopy {
+    float4* dst[2];
+    const float4* src[2];
+    long long n4;
+};
+
+__global__ void __launch_bounds__(256) halo_pull_kernel(HaloCopy h) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (int q = 0; q < 2; ++q)
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < h.n4; i += stride)
+            h.dst[q][i] = h.src[q][i];
+}
+
 }  // namespace gmpea_b200
