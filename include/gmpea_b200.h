@@ -173,7 +173,12 @@ typedef struct {
     /* engine extensions */
     int32_t device;        /* CUDA device ordinal */
     uint64_t stream;       /* cudaStream_t to run on; 0 = the engine's own stream */
-    const double* igd_reference; /* optional per-generation IGD hook: reference front */
+    /* optional per-generation IGD hook (RunConfig::igd_metric, gmpea.hpp:123,
+     * as the harness installs it, experiment.cpp:200-205): igd(metric_front(
+     * pop1), igd_reference) on the device after generation 0 and every kept
+     * generation, outside the loop clock; GenRecord.igd / has_igd carry it.
+     * igd_reference: igd_reference_rows x m, copied at create.  Unsharded runs. */
+    const double* igd_reference;
     int64_t igd_reference_rows;
     /* weight-region sharding: this engine owns the slots
      * [shard_begin, shard_end) of n; 0, 0 = all of them */

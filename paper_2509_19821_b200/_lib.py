@@ -444,6 +444,9 @@ class RunConfig:
     world: int = 0
     rank: int = 0
     nccl_id: Optional[bytes] = None
+    # the per-generation IGD hook (RunConfig::igd_metric as experiment.cpp:200-205
+    # installs it): igd(metric_front(pop1), igd_reference) on the device
+    igd_reference: Optional[np.ndarray] = None
 
     def _c(self) -> _RunConfig:
         c = _RunConfig()
@@ -464,6 +467,10 @@ class RunConfig:
             c.shard_begin, c.shard_end = int(self.shard[0]), int(self.shard[1])
         c.aggregation = int(self.aggregation)
         c.world, c.rank = int(self.world), int(self.rank)
+        if self.igd_reference is not None:
+            self._igd_ref = _f64(self.igd_reference)  # kept alive with the config (copied at create)
+            c.igd_reference = _p(self._igd_ref)
+            c.igd_reference_rows = self._igd_ref.shape[0]
         if self.nccl_id is not None:
             if len(self.nccl_id) != 128:
                 raise ValueError("nccl_id: 128 bytes expected")

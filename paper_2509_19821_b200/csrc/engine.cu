@@ -838,6 +838,14 @@ struct gmpea_engine {
             exchange_halo();
         }
         if (!sharded || comm) build_graph();
+        if (c.igd_reference && c.igd_reference_rows > 0) {
+            if (exchange || sharded) throw std::invalid_argument("igd_reference: unsharded runs only");
+            igd_rows = c.igd_reference_rows;
+            igd_ref.alloc((size_t)igd_rows * m);
+            CK(cudaMemcpyAsync(igd_ref.p, c.igd_reference, (size_t)igd_rows * m * sizeof(double),
+                               cudaMemcpyHostToDevice, s));
+            igd_hist.assign(1, igd_now());  // record(0)
+        }
         CK(cudaStreamSynchronize(s));
         check_errors(0);
     }
@@ -914,6 +922,7 @@ struct gmpea_engine {
         CK(cudaGetLastError());
         finish_init();
         exchange_z();  // NCCL shards: the ideal point of the new populations is global (all ranks call this)
+        if (igd_rows > 0) igd_hist.assign(1, igd_now());
     }
 
     void enqueue_generation() {
@@ -972,11 +981,43 @@ struct gmpea_engine {
     // (metric hooks) stays outside the loop time, as in gmpea.cpp:442-453
     void start_loop_clock() { mark_start_kernel<<<1, 1, 0, s>>>(st.p); }
 
+    // ---- the per-generation IGD hook (RunConfig::igd_metric, gmpea.cpp:442-453,
+    // which the harness sets to igd(metric_front(pop1), ref) for problems with
+    // a front, experiment.cpp:200-205): on the device, outside the loop clock
+    DevBuf<double> igd_ref;
+    long long igd_rows = 0;
+    std::vector<double> igd_hist;  // index: generation
+
+    double igd_now() {
+        const long long o0 = own0 - e0, on = own1 - own0;
+        double* tF = staging.p;
+        double* tcv = tF + (size_t)on * m;
+        fcv_to_rows_kernel<<<blocks_for(on, 256), 256, 0, s>>>(pop[0].Fcv.p + o0, on, m, tF, tcv);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));  // igd_dev works on the default stream
+        return igd_dev(tF, tcv, on, m, igd_ref.p, igd_rows);
+    }
+
     // enqueue up to k generations, respecting the generation limit
     long long step(long long k) {
         if (gen_limit >= 0) k = std::min(k, gen_limit - gens_enqueued);
         if (k <= 0) return 0;
         if (is_group()) return group_step(k);
+        if (igd_rows == 0) return launch_gens(k);
+        // with the IGD hook: one generation at a time, each its own loop-clock
+        // interval, the metric after it (a discarded generation records none)
+        long long done = 0;
+        while (done < k) {
+            if (launch_gens(1) == 0) break;
+            ++done;
+            const DevState h = read_state();
+            if ((long long)igd_hist.size() <= h.gens_done) igd_hist.push_back(igd_now());
+            if (h.stop) break;
+        }
+        return done;
+    }
+
+    long long launch_gens(long long k) {
         build_graph();
         long long done = 0;
         while (done < k) {
@@ -1186,6 +1227,10 @@ struct gmpea_engine {
             o.feasible_ratio = (double)r[k].feasible / (double)counted_slots();
             o.igd = std::numeric_limits<double>::quiet_NaN();
             o.hv = std::numeric_limits<double>::quiet_NaN();
+            if (k < (long long)igd_hist.size()) {
+                o.igd = igd_hist[k];
+                o.has_igd = 1;
+            }
         }
         return out;
     }

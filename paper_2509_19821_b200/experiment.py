@@ -157,29 +157,9 @@ def run_algorithm(algorithm: str, problem: g.Problem, cfg: g.RunConfig,
         c.t1 = c.t2 = 5
     elif algorithm == "gmpea-l":
         c.t1 = c.t2 = 20
-    if igd_front is None:
-        return g.run_gmpea(problem, c)
-    eng = g.Engine(problem, c)
-    try:
-        hist = []
-
-        def hook(rec):
-            fr = g.metric_front(eng.population(1))
-            rec.igd = g.igd(fr, igd_front) if len(fr) else math.inf
-            hist.append(rec)
-
-        hook(eng.last_record())
-        while True:
-            before = hist[-1].gen
-            eng.step(1)
-            eng.sync()
-            r = eng.last_record()
-            if r.gen == before:
-                break
-            hook(r)
-        return g.RunResult(eng.population(1), hist, eng.n)
-    finally:
-        eng.close()
+    # the IGD hook on the device (RunConfig.igd_reference), outside the loop clock
+    c.igd_reference = igd_front
+    return g.run_gmpea(problem, c)
 
 
 def _num(v) -> str:
