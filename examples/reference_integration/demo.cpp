@@ -5,12 +5,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <span>
 #include <string>
 
 #include "gmpea/baselines.hpp"
 #include "gmpea/gmpea.hpp"
 #include "gmpea/metrics.hpp"
 #include "gmpea/problems.hpp"
+#include "gmpea/wta.hpp"
 #include "gmpea_b200_adapter.hpp"
 
 using namespace gmpea;
@@ -55,6 +57,46 @@ int main(int argc, char** argv) {
     h.igd_metric = [&](const Population& pop) { return igd(metric_front(pop), ref); };
     RunResult c = run_algorithm_with_b200("gmpea-b200", p, h);
     std::printf("hook records %zu last igd %.6g\n", c.history.size(), *c.history.back().igd);
+    // the same IGD hook on the device (the harness passes its front)
+    RunResult cd = gmpea_b200::run_gmpea(p, h, &ref);
+    double hd = 0.0;
+    for (std::size_t k = 0; k < c.history.size() && k < cd.history.size(); ++k)
+        hd = std::max(hd, std::abs(*c.history[k].igd - *cd.history[k].igd));
+    std::printf("device_hook records %zu/%zu max_diff %.3g\n", cd.history.size(), c.history.size(), hd);
+    // a ProblemDef that reuses a registered name with another evaluator is refused
+    ProblemDef fake = p;
+    fake.eval_row = [&p](std::span<const double> x, std::span<double> f, std::span<double> g) {
+        p.eval_row(x, f, g);
+        f[0] += 0.5;
+    };
+    int refused = 0;
+    try {
+        gmpea_b200::run_gmpea(fake, h);
+    } catch (const std::invalid_argument&) {
+        refused = 1;
+    }
+    // a loaded WTA scenario with edited tables under a built-in name: refused by
+    // the ProblemDef path, run with its own tables through the WTAInstance path
+    WTAInstance w = wta_scenario("P3");
+    for (auto& row : w.p)
+        for (double& v : row) v = std::min(1.0, v * 0.5 + 0.4);
+    w.capacity[0] += 3;
+    int wta_refused = 0;
+    try {
+        gmpea_b200::run_gmpea(make_wta_problem(w), h);
+    } catch (const std::invalid_argument&) {
+        wta_refused = 1;
+    }
+    RunConfig wc = cfg;
+    wc.k_max = 3;
+    wc.op = VariationOp::sbx_pm;
+    RunResult wr = gmpea_b200::run_gmpea(w, wc);
+    Population we = evaluate_population(make_wta_problem(w), wr.pop1.X);  // the reference's own evaluator
+    double wd = 0.0;
+    for (std::size_t i = 0; i < we.F.data.size(); ++i)
+        wd = std::max(wd, std::abs(we.F.data[i] - wr.pop1.F.data[i]) / std::max(1.0, std::abs(we.F.data[i])));
+    std::printf("plugin refused %d wta_refused %d wta_gens %zu wta_eval_diff %.3g\n", refused, wta_refused,
+                wr.history.size() - 1, wd);
     // comparison algorithms through the same registration, with the IGD hook
     RunConfig bc = cfg;
     bc.n = 60;

@@ -2,8 +2,11 @@
 // reference's own types (proj/include/gmpea/*.hpp).  Header-only; include it
 // from the reference tree and link libgmpea_b200.so.  See INTEGRATION.md.
 //
-//   gmpea_b200::run_gmpea(const ProblemDef&, const RunConfig&)  -> RunResult
-//        replaces gmpea::run_gmpea (gmpea.hpp:144, gmpea.cpp:421-493)
+//   gmpea_b200::run_gmpea(const ProblemDef&, const RunConfig&[, const Matrix* igd_front])
+//        replaces gmpea::run_gmpea (gmpea.hpp:144, gmpea.cpp:421-493); with
+//        igd_front the IGD hook runs on the device (experiment.cpp:200-205)
+//   gmpea_b200::run_gmpea(const WTAInstance&, const RunConfig&)  -> RunResult
+//        a loaded scenario (load_wta, wta.cpp:148-192) with its own tables
 //   gmpea_b200::evaluate_population(const ProblemDef&, Matrix) -> Population
 //        replaces gmpea::evaluate_population (gmpea.hpp:33)
 //   gmpea_b200::environmental_selection(...)                   -> pair<Population>
@@ -20,6 +23,9 @@
 #pragma once
 
 #include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <span>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -27,6 +33,7 @@
 #include <vector>
 
 #include "gmpea/gmpea.hpp"
+#include "gmpea/wta.hpp"
 #include "gmpea_b200.h"
 
 namespace gmpea_b200 {
@@ -46,12 +53,57 @@ struct ProblemHandle {
         int32_t d, m, nin, neq;
         check(gmpea_problem_info(p, &d, &m, &nin, &neq));
         if ((std::size_t)d != def.d || (std::size_t)m != def.m || (std::size_t)nin != def.n_ineq ||
-            (std::size_t)neq != def.n_eq)
+            (std::size_t)neq != def.n_eq) {
+            gmpea_problem_destroy(p);
             throw std::invalid_argument("gmpea-b200: problem shape differs from " + def.name);
+        }
+        probe(def);
+    }
+    // a loaded WTA scenario with its own tables (make_wta_problem, wta.cpp:112-129)
+    explicit ProblemHandle(const gmpea::WTAInstance& w) {
+        std::vector<int32_t> strikes(w.max_strikes.begin(), w.max_strikes.end());
+        std::vector<int32_t> cap(w.capacity.begin(), w.capacity.end());
+        std::vector<double> pv;
+        for (const auto& row : w.p) pv.insert(pv.end(), row.begin(), row.end());
+        check(gmpea_problem_create_wta(w.scenario.c_str(), (int32_t)w.n_targets, (int32_t)w.n_vehicles,
+                                       strikes.data(), cap.data(), pv.data(), &p));
     }
     ~ProblemHandle() { gmpea_problem_destroy(p); }
     ProblemHandle(const ProblemHandle&) = delete;
     ProblemHandle& operator=(const ProblemHandle&) = delete;
+
+    // The reference's plugin is any ProblemDef (problems.hpp:19-37) and the
+    // engine only knows its registered evaluators: evaluate probe rows through
+    // def.eval_row and the device, and refuse a ProblemDef whose evaluation
+    // differs (e.g. a loaded WTA scenario that reuses the name "WTA-P3" with
+    // other tables; run those through the WTAInstance overloads).
+    void probe(const gmpea::ProblemDef& def) {
+        const std::size_t d = def.d, m = def.m, nc = def.n_ineq + def.n_eq, rows = 16;
+        std::vector<double> X(rows * d), F(rows * m), G(rows * nc), Fr(m), Gr(nc);
+        uint64_t state = 0x9E3779B97F4A7C15ull;
+        for (std::size_t r = 0; r < rows; ++r)
+            for (std::size_t j = 0; j < d; ++j) {
+                state = state * 6364136223846793005ull + 1442695040888963407ull;
+                const double u = (double)(uint32_t)(state >> 40) / 16777216.0;  // fp32-exact in [0, 1)
+                const double lo = def.bounds[j].first, hi = def.bounds[j].second;
+                X[r * d + j] = (double)(float)(lo + (hi - lo) * u);
+                if (!(X[r * d + j] >= lo && X[r * d + j] <= hi)) X[r * d + j] = lo;
+            }
+        check(gmpea_evaluate(p, X.data(), (int64_t)rows, F.data(), G.data(), nullptr));
+        auto close = [](double a, double b) { return std::abs(a - b) <= 1e-5 * std::max(1.0, std::abs(b)); };
+        for (std::size_t r = 0; r < rows; ++r) {
+            def.eval_row(std::span<const double>(X.data() + r * d, d), std::span<double>(Fr), std::span<double>(Gr));
+            bool same = true;
+            for (std::size_t k = 0; k < m; ++k) same = same && close(F[r * m + k], Fr[k]);
+            for (std::size_t k = 0; k < nc; ++k) same = same && close(G[r * nc + k], Gr[k]);
+            if (!same) {
+                gmpea_problem_destroy(p);
+                p = nullptr;
+                throw std::invalid_argument("gmpea-b200: " + def.name +
+                                            " evaluates differently from the engine's problem of that name");
+            }
+        }
+    }
 };
 
 inline gmpea_operator_params to_c(const gmpea::OperatorParams& o) {
@@ -79,9 +131,26 @@ inline gmpea::Population read_population(gmpea_engine* e, int which, const gmpea
 
 // run_gmpea (gmpea.cpp:421-493) on the device.  Metric hooks, when set, are
 // called on pop1 after every generation, outside the loop timer, as the
-// reference does (gmpea.cpp:442-453).
-inline gmpea::RunResult run_gmpea(const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg) {
+// reference does (gmpea.cpp:442-453).  igd_front: the IGD hook the harness
+// installs, igd(metric_front(pop1), *igd_front) (experiment.cpp:200-205), runs
+// on the device instead of copying pop1 back every generation.
+inline gmpea::RunResult run_on(gmpea_problem* prob, const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg,
+                               const gmpea::Matrix* igd_front);
+
+inline gmpea::RunResult run_gmpea(const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg,
+                                  const gmpea::Matrix* igd_front = nullptr) {
     ProblemHandle ph(def);
+    return run_on(ph.p, def, cfg, igd_front);
+}
+
+// a loaded scenario with its own tables (load_wta + make_wta_problem)
+inline gmpea::RunResult run_gmpea(const gmpea::WTAInstance& w, const gmpea::RunConfig& cfg) {
+    ProblemHandle ph(w);
+    return run_on(ph.p, gmpea::make_wta_problem(w), cfg, nullptr);
+}
+
+inline gmpea::RunResult run_on(gmpea_problem* prob, const gmpea::ProblemDef& def, const gmpea::RunConfig& cfg,
+                               const gmpea::Matrix* igd_front) {
     gmpea_run_config c;
     gmpea_run_config_default(&c);
     c.n = (int64_t)cfg.n;
@@ -95,18 +164,25 @@ inline gmpea::RunResult run_gmpea(const gmpea::ProblemDef& def, const gmpea::Run
     c.t1 = (int32_t)cfg.t1;
     c.t2 = (int32_t)cfg.t2;
     c.record_walltime = cfg.record_walltime ? 1 : 0;
+    if (igd_front) {
+        if (igd_front->cols != def.m) throw std::invalid_argument("igd: objective count mismatch");
+        c.igd_reference = igd_front->data.data();
+        c.igd_reference_rows = (int64_t)igd_front->rows;
+    }
     gmpea_engine* e = nullptr;
-    check(gmpea_engine_create(ph.p, &c, &e));
+    check(gmpea_engine_create(prob, &c, &e));
     std::unique_ptr<gmpea_engine, void (*)(gmpea_engine*)> guard(e, gmpea_engine_destroy);
     gmpea::RunResult res;
     res.effective_n = (std::size_t)gmpea_engine_effective_n(e);
-    const bool hooks = (bool)cfg.igd_metric || (bool)cfg.hv_metric;
+    // host hooks: the HV hook, and an IGD hook the device does not run
+    const bool hooks = (!igd_front && (bool)cfg.igd_metric) || (bool)cfg.hv_metric;
     auto to_rec = [](const gmpea_gen_record& r) {
         gmpea::GenRecord g;
         g.gen = (std::size_t)r.gen;
         g.evals = (std::size_t)r.evals;
         g.wall_ms = r.wall_ms;
         g.feasible_ratio = r.feasible_ratio;
+        if (r.has_igd) g.igd = r.igd;
         return g;
     };
     if (!hooks) {
@@ -120,7 +196,7 @@ inline gmpea::RunResult run_gmpea(const gmpea::ProblemDef& def, const gmpea::Run
         // generation by generation so the host hooks see every pop1
         auto hook = [&](gmpea::GenRecord g) {
             gmpea::Population p1 = read_population(e, 1, def, res.effective_n);
-            if (cfg.igd_metric) g.igd = cfg.igd_metric(p1);
+            if (cfg.igd_metric && !igd_front) g.igd = cfg.igd_metric(p1);
             if (cfg.hv_metric) g.hv = cfg.hv_metric(p1);
             res.history.push_back(g);
         };
@@ -134,6 +210,14 @@ inline gmpea::RunResult run_gmpea(const gmpea::ProblemDef& def, const gmpea::Run
             check(gmpea_engine_last_record(e, &r));
             if (r.gen == before) break;  // limit reached or deadline crossed
             hook(to_rec(r));
+        }
+        if (igd_front) {  // the device hook's values (last_record carries none)
+            int64_t n = 0;
+            check(gmpea_engine_history(e, nullptr, 0, &n));
+            std::vector<gmpea_gen_record> h((std::size_t)n);
+            check(gmpea_engine_history(e, h.data(), n, &n));
+            for (std::size_t k = 0; k < res.history.size() && k < h.size(); ++k)
+                if (h[k].has_igd) res.history[k].igd = h[k].igd;
         }
     }
     res.pop1 = read_population(e, 1, def, res.effective_n);

@@ -38,6 +38,13 @@ def test_adapter_runs_next_to_reference():
     assert "evals ref=60600 b200=60600" in out  # 2 n (k_max + 1)
     assert float(lines["evaluate"].split()[-1]) <= 1e-5
     assert lines["hook"].startswith("records 6")
+    # the device IGD hook gives the host hook's values, record for record
+    rec, diff = lines["device_hook"].split()[1], float(lines["device_hook"].split()[-1])
+    assert rec == "6/6" and diff <= 1e-12
+    # a foreign evaluator under a registered name is refused; a loaded WTA
+    # scenario runs with its own tables (evaluation checked by the reference)
+    pl = lines["plugin"].split()
+    assert pl[1] == "1" and pl[3] == "1" and pl[5] == "3" and float(pl[7]) <= 1e-5
     # comparison algorithms registered the same way: records with the hook, evals per generation
     assert lines["baselines"] == "records cnsga2 11/11 ccmo 11/11 evals 660/660 1320/1320"
     assert lines["operators"] == "ranks_equal 1 fitness_equal 1 front_rows 1000/1000"
