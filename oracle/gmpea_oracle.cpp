@@ -1218,66 +1218,104 @@ void selection(const SelIn& s, int32_t* src1, int32_t* src2, uint8_t* marks1, ui
 struct Keyed {
     uint32_t key[2];
     uint32_t slot, gen, pop;
-    // PICK stream: sequence of 64-bit draws
-    uint32_t q = 0;
-    uint64_t next_pick() {
-        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_PICK), q / 2};
-        uint32_t o[4];
-        orc_philox4x32_10(ctr, key, o);
-        uint64_t v = (q % 2 == 0) ? ((uint64_t)o[1] << 32 | o[0]) : ((uint64_t)o[3] << 32 | o[2]);
-        ++q;
-        return v;
+    uint32_t out[4];
+    void draw(uint32_t stream, uint32_t index) {
+        uint32_t ctr[4] = {slot, gen, orc_tag(pop, stream), index};
+        orc_philox4x32_10(ctr, key, out);
     }
-    // rng.hpp:23-30 rejection semantics on the PICK stream
+    // PICK stream: a sequence of 32-bit words, four per counter (the picks a,
+    // b with the b == a redraw, DE's jrand and SBX's per-child coin, in order)
+    uint32_t q = 0;
+    uint32_t pick_cache[4];
+    uint32_t pick32() {
+        if (q % 4 == 0) {
+            draw(ORC_STREAM_PICK, q / 4);
+            for (int k = 0; k < 4; ++k) pick_cache[k] = out[k];
+        }
+        return pick_cache[q++ % 4];
+    }
+    // rng.hpp:23-30 rejection semantics, on 32-bit words
     uint64_t index(uint64_t n) {
-        uint64_t limit = UINT64_MAX - UINT64_MAX % n;
+        const uint64_t limit = (1ull << 32) - (1ull << 32) % n;
         uint64_t v;
-        do { v = next_pick(); } while (v >= limit);
+        do { v = pick32(); } while (v >= limit);
         return v % n;
     }
-    double child_coin() {
-        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_CHILD), 0};
-        uint32_t o[4];
-        orc_philox4x32_10(ctr, key, o);
-        uint64_t v = (uint64_t)o[1] << 32 | o[0];
-        return static_cast<double>(v >> 11) * 0x1.0p-53;
+    // SBX per-child coin u <= pc (gmpea.cpp:117): the next PICK word w, taken
+    // iff w < ceil(pc 2^32)
+    bool child_coin(double pc) {
+        const double t = std::ceil(pc * 4294967296.0);
+        return static_cast<double>(pick32()) < t;
     }
-    // 32-bit coin of gene j: head = 16-bit half j % 8 of index j / 8 of the
-    // coin stream, tail = low 16 bits of index j of the refinement stream
+    // 32-bit coin of gene j with an exact threshold (DE's CR coin, CR < 1):
+    // head = 16-bit half j % 8 of index j / 8 of the coin stream, tail = low
+    // 16 bits of index j of the refinement stream
     double coin(uint32_t stream, uint32_t ref_stream, uint32_t j) {
-        uint32_t ctr[4] = {slot, gen, orc_tag(pop, stream), j / 8};
-        uint32_t o[4];
-        orc_philox4x32_10(ctr, key, o);
-        uint32_t word = o[(j % 8) / 2];
+        draw(stream, j / 8);
+        uint32_t word = out[(j % 8) / 2];
         uint32_t head = (j % 2) ? (word >> 16) : (word & 0xffffu);
-        uint32_t rc[4] = {slot, gen, orc_tag(pop, ref_stream), j};
-        orc_philox4x32_10(rc, key, o);
-        uint32_t tail = o[0] & 0xffffu;
+        draw(ref_stream, j);
+        uint32_t tail = out[0] & 0xffffu;
         return static_cast<double>((head << 16) | tail) * 0x1.0p-32;
+    }
+    // SBX per-gene crossover coin (gmpea.cpp:119, u <= 0.5): one bit per gene,
+    // bit j % 32 of word (j % 128) / 32 of index j / 128 of XCOIN; crosses iff 1
+    bool xbit(uint32_t j) {
+        draw(ORC_STREAM_XCOIN, j / 128);
+        return (out[(j % 128) / 32] >> (j % 32)) & 1u;
     }
     // four genes per counter: gene j is word j % 4 of index j / 4
     double word(uint32_t stream, uint32_t j) {
-        uint32_t ctr[4] = {slot, gen, orc_tag(pop, stream), j / 4};
-        uint32_t o[4];
-        orc_philox4x32_10(ctr, key, o);
-        return static_cast<double>(o[j % 4]) * 0x1.0p-32;
+        draw(stream, j / 4);
+        return static_cast<double>(out[j % 4]) * 0x1.0p-32;
     }
     double mu(uint32_t j) {
-        uint32_t ctr[4] = {slot, gen, orc_tag(pop, ORC_STREAM_MU), j};
-        uint32_t o[4];
-        orc_philox4x32_10(ctr, key, o);
-        return static_cast<double>(o[0]) * 0x1.0p-32;
+        draw(ORC_STREAM_MU, j);
+        return static_cast<double>(out[0]) * 0x1.0p-32;
     }
 };
+
+// Polynomial mutation's per-gene coin (gmpea.cpp:139: skip gene iff U > pm)
+// drawn as gaps: the genes between two mutated ones are Geometric(pm); word t
+// of MSKIP (index t / 4, word t % 4) gives gap t = the largest k in [0, d]
+// with w <= T[k], T[k] = ceil((1 - pm)^k 2^32) - 1, so P(gap >= k) =
+// (1 - pm)^k up to 2^-32 and every gene mutates independently with
+// probability pm.  The engine builds the identical table (host.cuh).
+std::vector<int64_t> pm_gap_table(double pm, int d) {
+    std::vector<int64_t> T(static_cast<size_t>(d) + 1);
+    T[0] = 0xffffffffll;
+    double v = 1.0;
+    for (int k = 1; k <= d; ++k) {
+        v *= 1.0 - pm;
+        T[k] = static_cast<int64_t>(std::ceil(v * 4294967296.0)) - 1;
+    }
+    return T;
+}
+
+std::vector<uint8_t> pm_mutated(Keyed& kd, const std::vector<int64_t>& T, int d) {
+    std::vector<uint8_t> mut(static_cast<size_t>(d), 0);
+    int64_t pos = -1;
+    for (uint32_t t = 0;; ++t) {
+        uint32_t ctr[4] = {kd.slot, kd.gen, orc_tag(kd.pop, ORC_STREAM_MSKIP), t / 4};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, kd.key, o);
+        const int64_t w = o[t % 4];
+        int gap = 0;
+        while (gap < d && w <= T[gap + 1]) ++gap;
+        pos += gap + 1;
+        if (pos >= d) break;
+        mut[pos] = 1;
+    }
+    return mut;
+}
 
 struct OpParams {
     double sbx_prob, sbx_eta, pm_eta, de_cr, de_f, pm_prob;  // pm_prob < 0: 1/d
 };
 
-// gmpea.cpp:135-160 for one gene: the skip coin comes from MCOIN, the
+// gmpea.cpp:135-160 for one gene the gap draws selected (pm_mutated); the
 // direction uniform from MU (drawn only for mutated genes)
-void pm_gene(double& x, double lo, double hi, double pm, double eta, Keyed& k, uint32_t j) {
-    if (k.coin(ORC_STREAM_MCOIN, ORC_STREAM_MREF, j) > pm) return;
+void pm_gene(double& x, double lo, double hi, double eta, Keyed& k, uint32_t j) {
     double span = hi - lo;
     if (span <= 0.0) return;
     double u = k.mu(j), dq;
@@ -1300,6 +1338,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
                int32_t* picks, uint32_t slot_base = 0) {
     const int d = p.d;
     const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / static_cast<double>(d);
+    const std::vector<int64_t> gapT = pm_gap_table(pm, d);
     for (size_t i = 0; i < n; ++i) {
         Keyed k;
         k.key[0] = static_cast<uint32_t>(seed);
@@ -1316,7 +1355,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
         size_t jrand = 0;
         bool cross = true;
         if (op == 0) {
-            cross = k.child_coin() <= prm.sbx_prob;
+            cross = k.child_coin(prm.sbx_prob);
         } else {
             jrand = k.index(static_cast<uint64_t>(d));
         }
@@ -1325,6 +1364,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
             picks[i * 3 + 1] = static_cast<int32_t>(b);
             picks[i * 3 + 2] = op == 0 ? (cross ? 1 : 0) : static_cast<int32_t>(jrand);
         }
+        const std::vector<uint8_t> mut = pm_mutated(k, gapT, d);
         const double* base = X + i * d;
         for (int j = 0; j < d; ++j) {
             const uint32_t uj = static_cast<uint32_t>(j);
@@ -1332,7 +1372,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
             if (op == 0) {
                 if (!cross) {
                     c = xa[j];
-                } else if (k.coin(ORC_STREAM_XCOIN, ORC_STREAM_XREF, uj) <= 0.5) {
+                } else if (k.xbit(uj)) {
                     double u = k.word(ORC_STREAM_XU, uj);
                     double beta = u <= 0.5 ? std::pow(2.0 * u, 1.0 / (prm.sbx_eta + 1.0))
                                            : std::pow(1.0 / (2.0 * (1.0 - u)), 1.0 / (prm.sbx_eta + 1.0));
@@ -1346,7 +1386,7 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
                             k.coin(ORC_STREAM_XCOIN, ORC_STREAM_XREF, uj) < prm.de_cr;
                 c = take ? base[j] + prm.de_f * (xa[j] - xb[j]) : base[j];
             }
-            pm_gene(c, p.lo[j], p.hi[j], pm, prm.pm_eta, k, uj);
+            if (mut[j]) pm_gene(c, p.lo[j], p.hi[j], prm.pm_eta, k, uj);
             child[j] = clamp_ref(c, p.lo[j], p.hi[j]);
         }
     }

@@ -11,15 +11,20 @@
  *   key = { (u32)seed, (u32)(seed >> 32) }
  *   ctr = { slot, gen, tag(pop, stream), index }
  *   tag(pop, stream) = (pop << 28) | (stream << 20)
- * streams: INIT (initial population, gen = 0; two 64-bit draws per counter),
- * PICK (neighbour draws and DE jrand: a sequence of 64-bit draws, two per
- * counter), CHILD (the SBX per-child coin, one 53-bit uniform), XU (SBX
- * spread uniform: gene j = word j%4 of index j/4, u = w * 2^-32), MU (PM
- * direction, index j, word 0) and the two coin streams XCOIN (SBX per-gene
- * coin / DE CR coin) and MCOIN (PM coin).  A coin is the 32-bit value
- * w = (h << 16) | l: its head h is 16-bit half j%8 of index j/8 of the coin
- * stream (word (j%8)/2, low half first), its tail l the low 16 bits of word 0
- * of index j of XREF / MREF; u = w * 2^-32 as for every other draw.
+ * streams (draw schema v2):
+ *   INIT   initial population, gen = 0; two 64-bit draws per counter
+ *   PICK   a sequence of 32-bit words, four per counter: the neighbour picks a,
+ *          b (rejection sampling, b == a redrawn), then DE's jrand or SBX's
+ *          per-child coin (taken iff w < ceil(pc 2^32))
+ *   XCOIN  SBX per-gene crossover bit: gene j is bit j%32 of word (j%128)/32 of
+ *          index j/128 (crosses iff 1); DE's CR coin when CR < 1: the 32-bit
+ *          coin w = (h << 16) | l, head h = 16-bit half j%8 of index j/8
+ *          (word (j%8)/2, low half first), tail l = low 16 bits of word 0 of
+ *          index j of XREF
+ *   XU     SBX spread uniform: gene j = word j%4 of index j/4, u = w * 2^-32
+ *   MSKIP  PM gaps: word t (index t/4, word t%4) is the t-th gap between
+ *          mutated genes, gap = max k in [0, d] with w <= ceil((1-pm)^k 2^32) - 1
+ *   MU     PM direction of a mutated gene j: index j, word 0
  */
 #ifndef GMPEA_ORACLE_PHILOX_H
 #define GMPEA_ORACLE_PHILOX_H
@@ -28,7 +33,7 @@
 enum {
     ORC_STREAM_INIT = 1, ORC_STREAM_PICK = 2, ORC_STREAM_CHILD = 3,
     ORC_STREAM_XCOIN = 5, ORC_STREAM_XU = 6, ORC_STREAM_MCOIN = 7, ORC_STREAM_MU = 8,
-    ORC_STREAM_XREF = 9, ORC_STREAM_MREF = 10
+    ORC_STREAM_XREF = 9, ORC_STREAM_MREF = 10, ORC_STREAM_MSKIP = 11  /* CHILD, MCOIN, MREF: draw schema v1 */
 };
 
 static inline uint32_t orc_tag(uint32_t pop, uint32_t stream) {

@@ -423,6 +423,7 @@ struct BaselineRun {
     DevBuf<DevState> st;
     DevBuf<int> bad[2];
     VaryParams vp{};
+    PmGaps gaps;
     VaryKernel init_k = nullptr, vary_k = nullptr;
     std::vector<gmpea_gen_record> hist;
     long long evals = 0;
@@ -465,7 +466,7 @@ struct BaselineRun {
         vp.pop_id[1] = 2;
         vp.P = p->dev;
         vp.key = make_philox_key(c.seed);
-        fill_op_params(vp, c.params, d);
+        fill_op_params(vp, c.params, d, gaps);
         vp.eval = 1;
         vp.update_z = 0;
         vp.st = st.p;

@@ -93,16 +93,15 @@ __host__ __device__ inline float ordered_to_float(unsigned u) {
 // ---- Philox4x32-10 (Salmon et al. SC'11), the counter-based generator of the
 // engine.  Key schema (shared with oracle/philox.h, the test checker):
 //   key = {(u32)seed, (u32)(seed >> 32)}, ctr = {slot, gen, tag(pop, stream), index}
+// Draw schema v2 (oracle/philox.h is the checker's copy of the contract)
 enum : unsigned {
     STREAM_INIT = 1,   // initial population, pair of 64-bit draws per counter
-    STREAM_PICK = 2,   // neighbour picks / DE jrand: 64-bit draw sequence
-    STREAM_CHILD = 3,  // SBX per-child crossover coin (53-bit uniform)
-    STREAM_XCOIN = 5,  // per-gene SBX coin / DE CR coin: 16-bit heads, 8 genes per counter
+    STREAM_PICK = 2,   // 32-bit words, four per counter: picks a, b (b == a redrawn), DE jrand / SBX child coin
+    STREAM_XCOIN = 5,  // SBX per-gene crossover bit (128 genes per counter); DE CR coin heads (CR < 1)
     STREAM_XU = 6,     // per-gene SBX spread uniform, 4 genes per counter
-    STREAM_MCOIN = 7,  // per-gene PM coin: 16-bit heads, 8 genes per counter
     STREAM_MU = 8,     // PM direction uniform, one counter per mutated gene
-    STREAM_XREF = 9,   // low 16 bits of an XCOIN coin whose head ties the threshold
-    STREAM_MREF = 10,  // low 16 bits of an MCOIN coin whose head ties the threshold
+    STREAM_XREF = 9,   // low 16 bits of a DE CR coin whose head ties the threshold
+    STREAM_MSKIP = 11, // PM gaps between mutated genes, 32-bit words, four per counter
 };
 
 __host__ __device__ inline unsigned philox_tag(unsigned pop, unsigned stream) {

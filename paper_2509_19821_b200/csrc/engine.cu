@@ -525,6 +525,7 @@ struct gmpea_engine {
     int* host_flag_dev = nullptr;
 
     VaryParams vp{};
+    PmGaps gaps;  // the PM gap table vp.pm_gap points into
     Op1Params op1p{};
     SelParams sp{};
     RestoreParams rp{};
@@ -746,7 +747,7 @@ struct gmpea_engine {
         vp.ui[0] = make_uidx((unsigned long long)t1);
         vp.ui[1] = make_uidx((unsigned long long)t2);
         vp.key = make_philox_key(c.seed);
-        fill_op_params(vp, c.params, d);
+        fill_op_params(vp, c.params, d, gaps);
         vp.eval = 1;
         vp.update_z = 1;
         vp.fixed_gen = -1;
@@ -1881,7 +1882,8 @@ int gmpea_reproduce(const gmpea_problem* p, const double* X, int64_t n, const ui
         gmpea_operator_params prm;
         gmpea_operator_params_default(&prm);
         if (params) prm = *params;
-        fill_op_params(vp, prm, d);
+        PmGaps gaps;
+        fill_op_params(vp, prm, d, gaps);
         vp.eval = 0;
         vp.fixed_gen = (int)gen;
         vp.st = st.p;

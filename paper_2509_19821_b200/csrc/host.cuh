@@ -261,15 +261,36 @@ inline void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStrea
     k<<<dim3(blocks_for(vp.row_end - vp.row0, g.bs), npops), g.bs, g.smem, s>>>(vp);
 }
 
-inline void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d) {
-    vp.sbx_prob = prm.sbx_prob;
+// the PM gap table of draw schema v2 (kernels.cuh MutCursor): T[k] =
+// ceil((1 - pm)^k 2^32) - 1, computed exactly as the oracle does
+// (oracle/gmpea_oracle.cpp pm_gap_table)
+struct PmGaps {
+    DevBuf<long long> T;
+    void build(double pm, int d) {
+        std::vector<long long> h((size_t)d + 1);
+        h[0] = 0xffffffffll;
+        double v = 1.0;
+        for (int k = 1; k <= d; ++k) {
+            v *= 1.0 - pm;
+            h[k] = (long long)std::ceil(v * 4294967296.0) - 1;
+        }
+        T.alloc(h.size());
+        CK(cudaMemcpy(T.p, h.data(), h.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    }
+};
+
+inline void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int d, PmGaps& gaps) {
+    // SBX per-child coin u <= pc: cross iff the PICK word < ceil(pc 2^32)
+    const double pc = std::ceil(prm.sbx_prob * 4294967296.0);
+    vp.sbx_T = pc <= 0.0 ? 0ull : (pc >= 4294967296.0 ? (1ull << 32) : (unsigned long long)pc);
     vp.sbx_e = (float)(1.0 / (prm.sbx_eta + 1.0));
     vp.pm_e1 = (float)(prm.pm_eta + 1.0);
     vp.pm_einv = (float)(1.0 / (prm.pm_eta + 1.0));
     const double pm = prm.pm_prob >= 0.0 ? prm.pm_prob : 1.0 / (double)d;
-    // PM: skip iff u > pm with u = w 2^-32  <=>  mutate iff w <= floor(pm 2^32)
-    const double T = pm * 4294967296.0;
-    vp.pm_T = pm < 0.0 ? -1 : (long long)std::min(std::floor(T), 4294967295.0);
+    vp.pm_T = pm > 0.0 ? 0 : -1;
+    gaps.build(pm, d);
+    vp.pm_gap = gaps.T.p;
+    vp.pm_glog = pm >= 1.0 ? 0.0f : (float)(1.0 / std::log2(1.0 - pm));
     // DE: take iff u < CR  <=>  w < ceil(CR 2^32)  <=>  w <= ceil(CR 2^32) - 1
     const double C = prm.de_cr * 4294967296.0;
     vp.de_T = prm.de_cr >= 1.0 ? 0xffffffffll : (prm.de_cr <= 0.0 ? -1ll : (long long)std::ceil(C) - 1);

@@ -31,16 +31,16 @@ namespace gmpea_b200 {
 enum : int { OP_SBX = 0, OP_DE = 1 };
 enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
 
-// a divisor of uniform_index with its rejection limit and 64-bit reciprocal
+// a divisor of uniform_index (rng.hpp:23-30) on 32-bit words: values >= lim
+// are rejected, the rest taken modulo n
 struct UIdx {
-    unsigned long long n, lim, mag;
+    unsigned n;
+    unsigned long long lim;  // 2^32 - (2^32 mod n)
 };
 __host__ inline UIdx make_uidx(unsigned long long n) {
     UIdx u;
-    u.n = n;
-    u.lim = ~0ull - (~0ull % n);
-    u.mag = ~0ull / n;  // floor((2^64 - 1) / n) == floor(2^64 / n) unless n | 2^64
-    if (n && (n & (n - 1)) == 0) u.mag = n == 1 ? ~0ull : (1ull << 63) / (n >> 1);
+    u.n = (unsigned)n;
+    u.lim = (1ull << 32) - (1ull << 32) % n;
     return u;
 }
 
@@ -59,11 +59,13 @@ struct VaryParams {
     float4* out[2];          // output rows (x | g)
     float4* outFcv[2];
     PhiloxKey key;           // Philox key (seed) with its round keys
-    double sbx_prob;         // SBX per-child coin threshold on the 53-bit uniform
+    unsigned long long sbx_T; // SBX per-child coin: cross iff the PICK word < sbx_T (= ceil(pc 2^32))
     float sbx_e;             // 1 / (eta_c + 1)
     float pm_e1;             // eta_m + 1
     float pm_einv;           // 1 / (eta_m + 1)
-    long long pm_T;          // PM: mutate iff w <= pm_T (w: 32-bit coin; -1 never)
+    long long pm_T;          // PM on (>= 0) / off (-1)
+    const long long* pm_gap; // PM gap table: gap = max k in [0, d] with w <= pm_gap[k] (host.cuh PmGaps)
+    float pm_glog;           // 1 / log2(1 - pm): the gap's first estimate
     long long de_T;          // DE: take iff w <= de_T (>= 2^32 - 1: always)
     UIdx ui[2], uid;         // uniform_index divisors: t per population, d (jrand)
     // tournament parents (comparison algorithms, baselines.cpp:347-352, 416-420):
@@ -143,32 +145,12 @@ struct Emitter {
     }
 };
 
-// ---- Philox-keyed draws
-// 16-bit coin h of a gene, refined to an exact 32-bit comparison w <= thr:
-// with w = h * 2^16 + l,  w <= thr  <=>  h < thr_hi  or  (h == thr_hi and l <= thr_lo),
-// where l (the low half) is drawn from its own counter only in the rare tie.
-__device__ __forceinline__ unsigned half16(const u32x4& w, int k8) {
-    const unsigned word = (k8 >> 1) == 0 ? w.x : ((k8 >> 1) == 1 ? w.y : ((k8 >> 1) == 2 ? w.z : w.w));
-    return (k8 & 1) ? (word >> 16) : (word & 0xffffu);
-}
-
-// Rare draws (coin tails, p = 2^-16 per gene).  The SBX kernels, which draw
-// two coin streams per gene group, take them out of line (fewer inlined Philox
-// copies: -2.7 % DAS-CMOP7, -0.9 % MW7 generation time); inlined they suit the
-// DE kernel's register allocation better (+2 % LIRCMOP13 out of line).
-static __device__ __noinline__ unsigned philox_x_rare(unsigned c0, unsigned c1, unsigned c2, unsigned c3, unsigned k0,
-                                               unsigned k1) {
-    return philox4x32_10(c0, c1, c2, c3, k0, k1).x;
-}
-
-// Eight exact 32-bit coins "w <= T" (T in [-1, 2^32 - 1]) from the 16-bit
-// heads of one counter: bit k is set when gene j0 + k wins.  A head equal to
-// T's head is refined with the tail drawn from its own counter (probability
-// 2^-16 per gene), so the result equals the full 32-bit comparison.
-// OUTLINE (the SBX kernels): tails out of line and the tie mask formed only
-// when a has-zero test finds a tie (-1.4 % DAS-CMOP7, -0.8 % MW7 vary); the
-// DE kernel keeps the one-pass form (+3 % LIRCMOP13 otherwise).
-template <bool OUTLINE = false>
+// ---- Philox-keyed draws (draw schema v2, common.cuh / oracle/philox.h)
+// DE's crossover coin when CR < 1 (gmpea.cpp:196, u < CR): eight exact 32-bit
+// coins "w <= T" (T in [-1, 2^32 - 1]) from the 16-bit heads of one counter:
+// bit k is set when gene j0 + k wins.  A head equal to T's head is refined
+// with the tail drawn from its own counter (probability 2^-16 per gene), so
+// the result equals the full 32-bit comparison.
 __device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngenes, unsigned slot, unsigned gen,
                                            unsigned tag_ref, unsigned j0, const PhiloxKey& K) {
     if (T < 0) return 0u;
@@ -176,81 +158,68 @@ __device__ __forceinline__ unsigned coins8(const u32x4& w, long long T, int ngen
     const unsigned thi = (unsigned)(T >> 16), tlo = (unsigned)(T & 0xffff);
     const unsigned words[4] = {w.x, w.y, w.z, w.w};
     const unsigned valid = (1u << ngenes) - 1u;
-    if (!OUTLINE) {  // the DE kernels: one pass (their register allocation prefers it)
-        unsigned win = 0u, tie = 0u;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const unsigned h = (k & 1) ? (words[k >> 1] >> 16) : (words[k >> 1] & 0xffffu);
-            win |= (unsigned)(h < thi) << k;
-            tie |= (unsigned)(h == thi) << k;
-        }
-        win &= valid;
-        tie &= valid;
-        while (tie) {  // rare
-            const int k = __ffs(tie) - 1;
-            tie &= tie - 1u;
-            win |= (unsigned)((philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, K).x & 0xffffu) <= tlo) << k;
-        }
-        return win;
-    }
-    unsigned win = 0u;
+    unsigned win = 0u, tie = 0u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const unsigned h = (k & 1) ? (words[k >> 1] >> 16) : (words[k >> 1] & 0xffffu);
         win |= (unsigned)(h < thi) << k;
-    }
-    win &= valid;
-    // the SBX kernels: a head equal to thi anywhere?  x = word ^ (thi, thi) has a zero 16-bit
-    // half exactly then (the classic has-zero test, two halves per word); the
-    // per-gene tie mask is formed only in that rare case
-    const unsigned t2 = thi | (thi << 16);
-    unsigned any = 0u;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const unsigned x = words[q] ^ t2;
-        any |= (x - 0x00010001u) & ~x & 0x80008000u;
-    }
-    if (!any) return win;
-    unsigned tie = 0u;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const unsigned h = (k & 1) ? (words[k >> 1] >> 16) : (words[k >> 1] & 0xffffu);
         tie |= (unsigned)(h == thi) << k;
     }
+    win &= valid;
     tie &= valid;
     while (tie) {  // rare
         const int k = __ffs(tie) - 1;
         tie &= tie - 1u;
-        const unsigned l = philox_x_rare(slot, gen, tag_ref, j0 + (unsigned)k, K.k[0], K.k[1]) & 0xffffu;
-        win |= (unsigned)(l <= tlo) << k;
+        win |= (unsigned)((philox4x32_10(slot, gen, tag_ref, j0 + (unsigned)k, K).x & 0xffffu) <= tlo) << k;
     }
     return win;
 }
 
+__device__ __forceinline__ unsigned pick_word(const u32x4& w, int k) {
+    return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
+}
+
+// the PICK stream: 32-bit words, four per counter, consumed in order
 struct PickStream {
     unsigned slot, gen, tag;
     const PhiloxKey& K;
     unsigned q;
     u32x4 cache;
-    __device__ __forceinline__ unsigned long long next() {
-        if ((q & 1) == 0) cache = philox4x32_10(slot, gen, tag, q >> 1, K);
-        unsigned long long v = (q & 1) == 0 ? (((unsigned long long)cache.y << 32) | cache.x)
-                                            : (((unsigned long long)cache.w << 32) | cache.z);
-        ++q;
-        return v;
+    __device__ __forceinline__ unsigned next() {
+        if ((q & 3) == 0) cache = philox4x32_10(slot, gen, tag, q >> 2, K);
+        return pick_word(cache, (int)(q++ & 3));
     }
-    // rng.hpp:23-30: uniform integer in [0, n) by rejection; the division is
-    // a precomputed reciprocal (UIdx): q = hi64(v * floor(2^64 / n)) is
-    // floor(v / n) or one less, so one correction makes v % n exact
+    // rng.hpp:23-30: uniform integer in [0, n) by rejection
     __device__ __forceinline__ unsigned index(const UIdx& u) {
-        unsigned long long v;
+        unsigned v;
         do {
             v = next();
-        } while (v >= u.lim);
-        const unsigned long long q = __umul64hi(v, u.mag);
-        unsigned long long r = v - q * u.n;
-        if (r >= u.n) r -= u.n;
-        return (unsigned)r;
+        } while ((unsigned long long)v >= u.lim);
+        return v % u.n;
+    }
+};
+
+// Polynomial mutation's per-gene coin (gmpea.cpp:139, skip iff U > pm) as
+// gaps between mutated genes: word t of MSKIP gives the t-th gap, the largest
+// k in [0, d] with w <= T[k], T[k] = ceil((1 - pm)^k 2^32) - 1 -- Geometric(pm)
+// gaps, i.e. every gene mutates independently with probability pm, at ~2
+// words per child instead of one coin per gene.  `next` walks the mutated
+// genes in ascending order (d or more: none left).
+struct MutCursor {
+    unsigned slot, gen, tag;
+    unsigned t;
+    u32x4 cache;
+    int next;
+    __device__ __forceinline__ void advance(const PhiloxKey& K, const long long* __restrict__ T, int d,
+                                            float glog) {
+        if ((t & 3) == 0) cache = philox4x32_10(slot, gen, tag, t >> 2, K);
+        const unsigned w = pick_word(cache, (int)(t++ & 3));
+        // first estimate from the log, then exact against the table
+        const float u = ((float)w + 0.5f) * 0x1.0p-32f;
+        int k = (int)fminf(fmaxf(__log2f(u) * glog, 0.0f), (float)d);
+        while (k > 0 && (long long)w > T[k]) --k;
+        while (k < d && (long long)w <= T[k + 1]) ++k;
+        next += k + 1;
     }
 };
 
@@ -259,10 +228,6 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
     asm("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
         : "l"(p));
-}
-
-__device__ __forceinline__ unsigned pick_word(const u32x4& w, int k) {
-    return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
 }
 
 __device__ __forceinline__ float clamp_ref(float v, float lo, float hi) {
@@ -521,8 +486,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                     ob = (unsigned)Brow[b] * (unsigned)rs4;
                 }
                 if (OP == OP_SBX) {
-                    u32x4 c = philox4x32_10(slot, gen, philox_tag(pid, STREAM_CHILD), 0u, p.key);
-                    cross = u53(c.x, c.y) <= p.sbx_prob;
+                    cross = (unsigned long long)ps.next() < p.sbx_T;  // the per-child coin (gmpea.cpp:117)
                 } else {
                     jrand = (int)ps.index(p.uid);
                 }
@@ -530,11 +494,29 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             const bool de_all = p.de_T >= 0xffffffffll;
             const bool even_rows = (rs4 & 1) == 0;  // rows 32 B aligned
             const PhiloxKey& K = p.key;
+            // the mutated genes, in ascending order (gaps, MutCursor)
+            MutCursor mc{slot, gen, philox_tag(pid, STREAM_MSKIP), 0u, {}, -1};
+            if (MODE == MODE_VARY && active && p.pm_T >= 0)
+                mc.advance(K, p.pm_gap, d, p.pm_glog);
+            else
+                mc.next = d;
             for (int w0 = 0; w0 < d; w0 += 64) {
                 const int w1 = min(d, w0 + 64);
                 // genes of this window PM selects (32 bits suffice for d <= 32)
                 using Mask = typename std::conditional<(DC > 0 && DC <= 32), unsigned, unsigned long long>::type;
                 Mask mmask = 0;
+                while (mc.next < w1) {
+                    mmask |= (Mask)1 << (mc.next - w0);
+                    mc.advance(K, p.pm_gap, d, p.pm_glog);
+                }
+                // SBX per-gene crossover bits of the window (gmpea.cpp:119): one
+                // XCOIN counter holds 128 genes' bits
+                unsigned long long xwin = 0ull;
+                if (OP == OP_SBX && MODE == MODE_VARY && active && cross) {
+                    const u32x4 xw = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), (unsigned)(w0 >> 7), K);
+                    const int wi = (w0 & 127) >> 5;
+                    xwin = (unsigned long long)pick_word(xw, wi) | ((unsigned long long)pick_word(xw, wi + 1) << 32);
+                }
                 if (MODE == MODE_INIT) {
                     for (int jb = w0; jb < (active ? w1 : w0); jb += 4) {  // 64-bit pair (j % 2) of counter j / 2
                         const u32x4 xa = philox4x32_10(slot, 0u, philox_tag(pid, STREAM_INIT), (unsigned)(jb >> 1), K);
@@ -556,24 +538,25 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         wr4[jb >> 2] = make_float4(v[0], v[1], v[2], v[3]);
                     }
                 } else {
-                    // eight genes per group: one XCOIN and one MCOIN counter (16-bit coin
-                    // heads), two XU counters (32-bit spread uniforms).  NGC > 0 makes
-                    // the group's gene count a compile-time constant (DC suites), so
-                    // the per-gene code carries no bounds tests
+                    // eight genes per group: their crossover and mutation bits from the
+                    // window masks, two XU counters (32-bit spread uniforms); DE's CR
+                    // coin (CR < 1 only) one XCOIN counter of 16-bit heads.  NGC > 0
+                    // makes the group's gene count a compile-time constant (DC suites),
+                    // so the per-gene code carries no bounds tests
                     auto group = [&](const int jb, auto ngc) {
                         constexpr int NGC = decltype(ngc)::value;
                         const int ng = NGC > 0 ? NGC : min(8, w1 - jb);
                         const bool two = NGC > 0 ? (NGC > 4) : (jb + 4 < w1);
                         const int q = jb >> 2;
-                        u32x4 xc{0, 0, 0, 0}, mc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0};
+                        u32x4 xc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0};
                         const unsigned idx8 = (unsigned)(jb >> 3);
-                        if (OP == OP_SBX && cross) {
-                            xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, K);
+                        const unsigned gmask = (2u << (ng - 1)) - 1u;
+                        const unsigned xg = (unsigned)(xwin >> (jb - w0)) & gmask;
+                        if (OP == OP_SBX && xg) {  // spread uniforms only for a group that crosses
                             xu0 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q, K);
                             if (two) xu1 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q + 1u, K);
                         }
                         if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, K);
-                        if (p.pm_T >= 0) mc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, K);
                         float4 a4[2], b4[2], c4[2];
                         if (two && even_rows) {  // one 32 B sector per parent: 256-bit loads
                             ldg256(PX + (oa + q), a4[0], a4[1]);
@@ -596,16 +579,13 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                             a4[1] = b4[1] = c4[1] = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
                         }
-                        // per-gene SBX coin u <= 0.5 <=> w <= 2^31 (gmpea.cpp:119), DE CR coin, PM coin
+                        // per-gene SBX crossover bit (gmpea.cpp:119), DE CR coin, PM gene
                         const unsigned xbits =
-                            OP == OP_SBX ? (cross ? coins8<OP == OP_SBX>(xc, 0x80000000ll, ng, slot, gen, philox_tag(pid, STREAM_XREF),
-                                                           (unsigned)jb, K)
-                                                  : 0u)
+                            OP == OP_SBX ? xg
                                          : (de_all ? (1u << ng) - 1u
-                                                   : coins8<OP == OP_SBX>(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
-                                                            (unsigned)jb, K));
-                        const unsigned mbits = coins8<OP == OP_SBX>(mc, p.pm_T, ng, slot, gen, philox_tag(pid, STREAM_MREF),
-                                                      (unsigned)jb, K);
+                                                   : coins8(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
+                                                                   (unsigned)jb, K));
+                        const unsigned mbits = (unsigned)(mmask >> (jb - w0)) & gmask;
                         float v[8];
                         auto comp = [](const float4& f, int kk) {
                             return kk == 0 ? f.x : (kk == 1 ? f.y : (kk == 2 ? f.z : f.w));
@@ -648,9 +628,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         for (int k = 0; k < 8; ++k)
                             if (k < ng && !((mbits >> k) & 1u))
                                 v[k] = fminf(fmaxf(v[k], GMPEA_LO(jb + k)), GMPEA_HI(jb + k));
-                        if constexpr (ST) {
-                            mmask |= (Mask)mbits << (jb - w0);
-                        } else {
+                        if constexpr (!ST) {
                             // inline polynomial mutation + clip, then the evaluator, as
                             // rolled loops over the group: one code copy of the PM draw
                             // and of the evaluator's gene step instead of eight (the

@@ -40,6 +40,16 @@ def _run(job):
     return seed, fp32, F[idx]
 
 
+def _run_ref(job):
+    """the reference's own run_gmpea (mt19937_64, f64), another batch of seeds"""
+    from oracle import Reference
+
+    seed, n, gens = job
+    r = Reference()
+    pop, _ = r.run_gmpea("LIRCMOP1", n, k_max=gens, seed=seed, op=1, record_walltime=False)
+    return seed, r.metric_front(pop["F"], pop["cv"])
+
+
 def main():
     from scipy.stats import mannwhitneyu
     from oracle import Oracle
@@ -47,6 +57,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--seeds", type=int, default=90)
+    ap.add_argument("--noise", action="store_true",
+                    help="also a second batch of seeds (91-180) of the reference and philox-f64 arms: how far two "
+                         "batches of the SAME arm drift apart")
     args = ap.parse_args()
     refj = json.load(open(os.path.join(ROOT, "tests", "golden", "lircmop1_90seeds_ref.json")))
     n, gens = refj["n"], refj["gens"]
@@ -72,10 +85,18 @@ def main():
                     "b200": {"igd": eng["b200_igd"], "hv": eng["b200_hv"]}}}
     for k, v in arms.items():
         res["arms"][k] = {"igd": [v[s][0] for s in sorted(v)], "hv": [v[s][1] for s in sorted(v)]}
-    res["median"] = {k: {"igd": float(np.median(a["igd"])), "hv": float(np.median(a["hv"]))}
-                     for k, a in res["arms"].items()}
     pairs = [("philox-f64", "reference"), ("philox-f32", "philox-f64"), ("b200", "philox-f32"),
              ("b200", "reference"), ("philox-f32", "reference")]
+    if args.noise:
+        s2 = range(args.seeds + 1, 2 * args.seeds + 1)
+        with ProcessPoolExecutor(args.procs) as ex:
+            ref2 = {sd: score(fr) for sd, fr in ex.map(_run_ref, [(sd, n, gens) for sd in s2])}
+            ph2 = {sd: score(fr) for sd, _, fr in ex.map(_run, [(sd, False, n, gens) for sd in s2])}
+        res["arms"]["reference-b2"] = {"igd": [ref2[k][0] for k in sorted(ref2)], "hv": [ref2[k][1] for k in sorted(ref2)]}
+        res["arms"]["philox-f64-b2"] = {"igd": [ph2[k][0] for k in sorted(ph2)], "hv": [ph2[k][1] for k in sorted(ph2)]}
+        pairs += [("reference-b2", "reference"), ("philox-f64-b2", "philox-f64"), ("philox-f64-b2", "reference-b2")]
+    res["median"] = {k: {"igd": float(np.median(a["igd"])), "hv": float(np.median(a["hv"]))}
+                     for k, a in res["arms"].items()}
     res["mann_whitney_p"] = {f"{a} vs {b}": {m: float(mannwhitneyu(res["arms"][a][m], res["arms"][b][m],
                                                                     alternative="two-sided").pvalue)
                                              for m in ("igd", "hv")} for a, b in pairs}

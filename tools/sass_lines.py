@@ -40,8 +40,9 @@ def ncu_rows(rep, kregex):
 def sass_lines(lib, mangled_hint):
     d = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=d, capture_output=True)
-    cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".cubin")][0]
-    txt = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
+    # one cubin per translation unit (csrc/*.cu): every function of every cubin
+    txt = "\n".join(subprocess.run(["nvdisasm", "-gi", "-c", os.path.join(d, f)], capture_output=True,
+                                   text=True).stdout for f in sorted(os.listdir(d)) if f.endswith(".cubin"))
     funcs = {}
     # each instruction is preceded by its inlining chain, innermost first
     # ("line A inlined at B", then "line B" ...); attribute it to the
