@@ -35,11 +35,13 @@ enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
 // are rejected, the rest taken modulo n
 struct UIdx {
     unsigned n;
+    unsigned mag;            // floor(2^32 / n) (n >= 2; 0 for n = 1)
     unsigned long long lim;  // 2^32 - (2^32 mod n)
 };
 __host__ inline UIdx make_uidx(unsigned long long n) {
     UIdx u;
     u.n = (unsigned)n;
+    u.mag = n >= 2 ? (unsigned)((1ull << 32) / n) : 0u;
     u.lim = (1ull << 32) - (1ull << 32) % n;
     return u;
 }
@@ -65,7 +67,8 @@ struct VaryParams {
     float pm_einv;           // 1 / (eta_m + 1)
     long long pm_T;          // PM on (>= 0) / off (-1)
     const long long* pm_gap; // PM gap table: gap = max k in [0, d] with w <= pm_gap[k] (host.cuh PmGaps)
-    float pm_glog;           // 1 / log2(1 - pm): the gap's first estimate
+    double pm_glog;          // 1 / log(1 - pm) (the gap, MutCursor; 0: pm >= 1)
+    double pm_gdelta;        // the fp64 gap's error margin
     long long de_T;          // DE: take iff w <= de_T (>= 2^32 - 1: always)
     UIdx ui[2], uid;         // uniform_index divisors: t per population, d (jrand)
     // tournament parents (comparison algorithms, baselines.cpp:347-352, 416-420):
@@ -189,13 +192,16 @@ struct PickStream {
         if ((q & 3) == 0) cache = philox4x32_10(slot, gen, tag, q >> 2, K);
         return pick_word(cache, (int)(q++ & 3));
     }
-    // rng.hpp:23-30: uniform integer in [0, n) by rejection
+    // rng.hpp:23-30: uniform integer in [0, n) by rejection; v mod n by the
+    // reciprocal: q = hi32(v floor(2^32 / n)) is floor(v / n) or one less
     __device__ __forceinline__ unsigned index(const UIdx& u) {
         unsigned v;
         do {
             v = next();
         } while ((unsigned long long)v >= u.lim);
-        return v % u.n;
+        unsigned r = v - __umulhi(v, u.mag) * u.n;
+        if (r >= u.n) r -= u.n;
+        return r;
     }
 };
 
@@ -204,21 +210,35 @@ struct PickStream {
 // k in [0, d] with w <= T[k], T[k] = ceil((1 - pm)^k 2^32) - 1 -- Geometric(pm)
 // gaps, i.e. every gene mutates independently with probability pm, at ~2
 // words per child instead of one coin per gene.  `next` walks the mutated
-// genes in ascending order (d or more: none left).
+// genes in ascending order (d or more: none left).  u = w 2^-32 < q^k, q = 1 -
+// pm, iff k < L = log(u) / log(q), so the gap is ceil(L) - 1, found in fp64;
+// within delta of an integer (delta bounds the fp64 error of L and of the
+// table's iterated powers, ~1e-13 for d = 30) the table decides.
 struct MutCursor {
     unsigned slot, gen, tag;
     unsigned t;
     u32x4 cache;
     int next;
     __device__ __forceinline__ void advance(const PhiloxKey& K, const long long* __restrict__ T, int d,
-                                            float glog) {
+                                            double glog, double delta) {
         if ((t & 3) == 0) cache = philox4x32_10(slot, gen, tag, t >> 2, K);
         const unsigned w = pick_word(cache, (int)(t++ & 3));
-        // first estimate from the log, then exact against the table
-        const float u = ((float)w + 0.5f) * 0x1.0p-32f;
-        int k = (int)fminf(fmaxf(__log2f(u) * glog, 0.0f), (float)d);
-        while (k > 0 && (long long)w > T[k]) --k;
-        while (k < d && (long long)w <= T[k + 1]) ++k;
+        int k;
+        if (glog == 0.0) {  // pm >= 1: every gene
+            k = 0;
+        } else {
+            const double L = w ? log((double)w * 0x1.0p-32) * glog : 1e300;
+            if (L > (double)d + delta) {
+                k = d;
+            } else {
+                k = min((int)L, d);  // L >= 0
+                const double f = L - (double)k;
+                if (f < delta || f > 1.0 - delta) {  // at a boundary: the table decides
+                    while (k > 0 && (long long)w > T[k]) --k;
+                    while (k < d && (long long)w <= T[k + 1]) ++k;
+                }
+            }
+        }
         next += k + 1;
     }
 };
@@ -497,7 +517,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             // the mutated genes, in ascending order (gaps, MutCursor)
             MutCursor mc{slot, gen, philox_tag(pid, STREAM_MSKIP), 0u, {}, -1};
             if (MODE == MODE_VARY && active && p.pm_T >= 0)
-                mc.advance(K, p.pm_gap, d, p.pm_glog);
+                mc.advance(K, p.pm_gap, d, p.pm_glog, p.pm_gdelta);
             else
                 mc.next = d;
             for (int w0 = 0; w0 < d; w0 += 64) {
@@ -507,7 +527,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 Mask mmask = 0;
                 while (mc.next < w1) {
                     mmask |= (Mask)1 << (mc.next - w0);
-                    mc.advance(K, p.pm_gap, d, p.pm_glog);
+                    mc.advance(K, p.pm_gap, d, p.pm_glog, p.pm_gdelta);
                 }
                 // SBX per-gene crossover bits of the window (gmpea.cpp:119): one
                 // XCOIN counter holds 128 genes' bits
