@@ -1275,8 +1275,9 @@ struct Keyed {
     }
 };
 
-// Polynomial mutation's per-gene coin (gmpea.cpp:139: skip gene iff U > pm)
-// drawn as gaps: the genes between two mutated ones are Geometric(pm); word t
+// Polynomial mutation's per-gene coin (gmpea.cpp:139: skip gene iff U > pm).
+// The DE operator draws one 32-bit coin per gene (MCOIN head + MREF tail, as
+// Keyed::coin).  The SBX operator draws it as gaps: the genes between two mutated ones are Geometric(pm); word t
 // of MSKIP (index t / 4, word t % 4) gives gap t = the largest k in [0, d]
 // with w <= T[k], T[k] = ceil((1 - pm)^k 2^32) - 1, so P(gap >= k) =
 // (1 - pm)^k up to 2^-32 and every gene mutates independently with
@@ -1364,7 +1365,8 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
             picks[i * 3 + 1] = static_cast<int32_t>(b);
             picks[i * 3 + 2] = op == 0 ? (cross ? 1 : 0) : static_cast<int32_t>(jrand);
         }
-        const std::vector<uint8_t> mut = pm_mutated(k, gapT, d);
+        // PM genes: the SBX kernels draw gaps, the DE kernels one coin per gene
+        const std::vector<uint8_t> mut = op == 0 ? pm_mutated(k, gapT, d) : std::vector<uint8_t>();
         const double* base = X + i * d;
         for (int j = 0; j < d; ++j) {
             const uint32_t uj = static_cast<uint32_t>(j);
@@ -1386,7 +1388,9 @@ void reproduce(const Problem& p, const double* X, size_t n, const uint32_t* nb, 
                             k.coin(ORC_STREAM_XCOIN, ORC_STREAM_XREF, uj) < prm.de_cr;
                 c = take ? base[j] + prm.de_f * (xa[j] - xb[j]) : base[j];
             }
-            if (mut[j]) pm_gene(c, p.lo[j], p.hi[j], prm.pm_eta, k, uj);
+            const bool mutate = op == 0 ? mut[j] != 0
+                                        : pm > 0.0 && k.coin(ORC_STREAM_MCOIN, ORC_STREAM_MREF, uj) <= pm;
+            if (mutate) pm_gene(c, p.lo[j], p.hi[j], prm.pm_eta, k, uj);
             child[j] = clamp_ref(c, p.lo[j], p.hi[j]);
         }
     }

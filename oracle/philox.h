@@ -22,8 +22,11 @@
  *          (word (j%8)/2, low half first), tail l = low 16 bits of word 0 of
  *          index j of XREF
  *   XU     SBX spread uniform: gene j = word j%4 of index j/4, u = w * 2^-32
- *   MSKIP  PM gaps: word t (index t/4, word t%4) is the t-th gap between
- *          mutated genes, gap = max k in [0, d] with w <= ceil((1-pm)^k 2^32) - 1
+ *   MSKIP  SBX operator's PM gaps: word t (index t/4, word t%4) is the t-th gap
+ *          between mutated genes, gap = max k in [0, d] with
+ *          w <= ceil((1-pm)^k 2^32) - 1
+ *   MCOIN  DE operator's PM coin of gene j: the 32-bit coin (as XCOIN's for CR,
+ *          tail from MREF); mutates iff pm > 0 and w 2^-32 <= pm
  *   MU     PM direction of a mutated gene j: index j, word 0
  */
 #ifndef GMPEA_ORACLE_PHILOX_H
@@ -33,7 +36,7 @@
 enum {
     ORC_STREAM_INIT = 1, ORC_STREAM_PICK = 2, ORC_STREAM_CHILD = 3,
     ORC_STREAM_XCOIN = 5, ORC_STREAM_XU = 6, ORC_STREAM_MCOIN = 7, ORC_STREAM_MU = 8,
-    ORC_STREAM_XREF = 9, ORC_STREAM_MREF = 10, ORC_STREAM_MSKIP = 11  /* CHILD, MCOIN, MREF: draw schema v1 */
+    ORC_STREAM_XREF = 9, ORC_STREAM_MREF = 10, ORC_STREAM_MSKIP = 11  /* CHILD: draw schema v1 */
 };
 
 static inline uint32_t orc_tag(uint32_t pop, uint32_t stream) {

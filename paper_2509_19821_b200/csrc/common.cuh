@@ -99,9 +99,11 @@ enum : unsigned {
     STREAM_PICK = 2,   // 32-bit words, four per counter: picks a, b (b == a redrawn), DE jrand / SBX child coin
     STREAM_XCOIN = 5,  // SBX per-gene crossover bit (128 genes per counter); DE CR coin heads (CR < 1)
     STREAM_XU = 6,     // per-gene SBX spread uniform, 4 genes per counter
+    STREAM_MCOIN = 7,  // DE kernels' per-gene PM coin: 16-bit heads, 8 genes per counter
     STREAM_MU = 8,     // PM direction uniform, one counter per mutated gene
     STREAM_XREF = 9,   // low 16 bits of a DE CR coin whose head ties the threshold
-    STREAM_MSKIP = 11, // PM gaps between mutated genes, 32-bit words, four per counter
+    STREAM_MREF = 10,  // low 16 bits of a PM coin whose head ties the threshold
+    STREAM_MSKIP = 11, // SBX kernels' PM gaps between mutated genes, 32-bit words, four per counter
 };
 
 __host__ __device__ inline unsigned philox_tag(unsigned pop, unsigned stream) {

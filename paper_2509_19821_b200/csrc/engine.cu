@@ -705,6 +705,7 @@ struct gmpea_engine {
         maxdeg[1] = device_reverse(s, n, t2, B[1].p, ld, Rdeg[1], R[1], (int)(v0 - e0), (int)(v1 - e0));
         rpack = device_pack_reverse(s, n, maxdeg[0], R[0], ld, Rdeg[0], Rp[0]) &&
                 device_pack_reverse(s, n, maxdeg[1], R[1], ld, Rdeg[1], Rp[1]);
+        pack_static();
 
         for (int q = 0; q < 2; ++q) {
             pop[q].alloc(n, geo.rs4, ld);
@@ -779,7 +780,7 @@ struct gmpea_engine {
         vary = vary_kernel_for(p->dev, MODE_VARY, c.op);
         vp.row0 = (int)(v0 - e0);
         vp.row_end = (int)(v1 - e0);
-        op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, U.p, {off[0].Fcv.p, off[1].Fcv.p},
+        op1p = Op1Params{(int)(v0 - e0), (int)(v1 - e0), m, (float)c.theta, sU ? sU : U.p, {off[0].Fcv.p, off[1].Fcv.p},
                          {eff[0].p, eff[1].p}, srcbits.p, st.p};
         sp = SelParams{};
         sp.n = n;
@@ -789,16 +790,17 @@ struct gmpea_engine {
         sp.ldr = ld;
         sp.m = m;
         sp.theta = (float)c.theta;
-        sp.U = U.p;
+        sp.U = sU ? sU : U.p;
         for (int q = 0; q < 2; ++q) {
             sp.X[q] = pop[q].X.p;
             sp.Fcv[q] = pop[q].Fcv.p;
             sp.oX[q] = off[q].X.p;
             sp.oFcv[q] = off[q].Fcv.p;
             sp.eff[q] = eff[q].p;
-            sp.R[q] = R[q].p;
-            sp.Rp[q] = rpack ? Rp[q].p : nullptr;
-            sp.Rdeg[q] = Rdeg[q].p;
+            // the static tables from the L2-resident arena (pack_static), if any
+            sp.R[q] = sRev[q] && !rpack ? (const int*)sRev[q] : R[q].p;
+            sp.Rp[q] = rpack ? (sRev[q] ? (const uint2*)sRev[q] : Rp[q].p) : nullptr;
+            sp.Rdeg[q] = sRdeg[q] ? sRdeg[q] : Rdeg[q].p;
             sp.winner[q] = nullptr;
             if (time_mode) {
                 sp.uX[q] = undo[q].X.p;
@@ -951,6 +953,74 @@ struct gmpea_engine {
         if (time_mode) restore_kernel<<<dim3(blocks_for(own1 - own0, 256), 2), 256, 0, s>>>(rp);
     }
 
+    // ---- the selection's static tables (unit weights, reverse neighbourhood
+    // in-degrees and rows) in one arena, so one L2 access-policy window can
+    // keep them resident: select re-reads them every generation while
+    // vary_eval streams ~600 MB through L2 in between (GMPEA_L2_PERSIST=0: off)
+    DevBuf<char> sarena;
+    const float4* sU = nullptr;
+    const int* sRdeg[2] = {nullptr, nullptr};
+    const void* sRev[2] = {nullptr, nullptr};
+    size_t persist_bytes = 0;
+
+    void pack_static() {
+        const char* env = getenv("GMPEA_L2_PERSIST");
+        if (env && *env == '0') return;
+        int dev = 0, maxwin = 0, maxpersist = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+        CK(cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        if (maxwin <= 0 || maxpersist <= 0) return;
+        auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+        const size_t bU = (size_t)n * sizeof(float4), bd = (size_t)n * sizeof(int);
+        size_t br[2];
+        for (int q = 0; q < 2; ++q) br[q] = rpack ? Rp[q].n * sizeof(uint2) : R[q].n * sizeof(int);
+        const size_t total = al(bU) + 2 * al(bd) + al(br[0]) + al(br[1]);
+        sarena.alloc(total);
+        size_t o = 0;
+        auto put = [&](const void* src, size_t b) {
+            char* dst = sarena.p + o;
+            CK(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToDevice, s));
+            o += al(b);
+            return (const void*)dst;
+        };
+        // the hottest first: the window may not cover everything
+        for (int q = 1; q >= 0; --q) sRev[q] = put(rpack ? (const void*)Rp[q].p : (const void*)R[q].p, br[q]);
+        for (int q = 1; q >= 0; --q) sRdeg[q] = (const int*)put(Rdeg[q].p, bd);
+        sU = (const float4*)put(U.p, bU);
+        persist_bytes = std::min<size_t>({total, (size_t)maxwin, (size_t)maxpersist});
+        size_t cur = 0;
+        CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+        if (cur < persist_bytes) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist_bytes));
+    }
+
+    // the access-policy window on the captured op1 / select nodes (not on
+    // vary_eval, whose traffic streams)
+    void set_l2_window(cudaGraph_t g) {
+        if (!persist_bytes) return;
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        size_t lim = 0;
+        CK(cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize));
+        cudaKernelNodeAttrValue v{};
+        v.accessPolicyWindow.base_ptr = sarena.p;
+        v.accessPolicyWindow.num_bytes = persist_bytes;
+        v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)lim / (double)persist_bytes);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType t;
+            CK(cudaGraphNodeGetType(nd, &t));
+            if (t != cudaGraphNodeTypeKernel) continue;
+            cudaKernelNodeParams kp{};
+            CK(cudaGraphKernelNodeGetParams(nd, &kp));
+            if (kp.func == (void*)vary) continue;
+            CK(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v));
+        }
+    }
+
     // two graphs of one generation: graph_first also restarts the loop clock
     // (the first generation of a step() call), so step(1) is one launch
     cudaGraphExec_t capture_generation(bool clock) {
@@ -966,6 +1036,7 @@ struct gmpea_engine {
         enqueue_generation();
         s = saved;
         CK(cudaStreamEndCapture(cs, &g));
+        set_l2_window(g);
         CK(cudaGraphInstantiate(&x, g, 0));
         CK(cudaGraphDestroy(g));
         CK(cudaStreamDestroy(cs));

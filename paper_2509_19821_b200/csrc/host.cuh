@@ -290,11 +290,9 @@ inline void fill_op_params(VaryParams& vp, const gmpea_operator_params& prm, int
     vp.pm_T = pm > 0.0 ? 0 : -1;
     gaps.build(pm, d);
     vp.pm_gap = gaps.T.p;
-    vp.pm_glog = pm >= 1.0 ? 0.0 : 1.0 / std::log(1.0 - pm);
-    // |error| of L: the table's k-fold product (k <= d roundings) and fp64 log,
-    // over |log q|; with a 16x safety factor and a 1e-12 floor
-    vp.pm_gdelta = pm >= 1.0 || pm <= 0.0 ? 1e-12
-                                          : std::max(1e-12, 16.0 * (d + 4) * 0x1.0p-52 / std::fabs(std::log(1.0 - pm)));
+    vp.pm_glog = pm >= 1.0 ? 0.0f : (float)(1.0 / std::log2(1.0 - pm));
+    // the DE kernels' per-gene PM coin: skip iff u > pm <=> mutate iff w <= floor(pm 2^32)
+    vp.pm_coinT = pm <= 0.0 ? -1 : (long long)std::min(std::floor(pm * 4294967296.0), 4294967295.0);
     // DE: take iff u < CR  <=>  w < ceil(CR 2^32)  <=>  w <= ceil(CR 2^32) - 1
     const double C = prm.de_cr * 4294967296.0;
     vp.de_T = prm.de_cr >= 1.0 ? 0xffffffffll : (prm.de_cr <= 0.0 ? -1ll : (long long)std::ceil(C) - 1);

@@ -32,7 +32,7 @@ enum : int { OP_SBX = 0, OP_DE = 1 };
 enum : int { MODE_VARY = 0, MODE_EVAL = 1, MODE_INIT = 2 };
 
 // a divisor of uniform_index (rng.hpp:23-30) on 32-bit words: values >= lim
-// are rejected, the rest taken modulo n
+// are rejected, the rest taken modulo n through a reciprocal
 struct UIdx {
     unsigned n;
     unsigned mag;            // floor(2^32 / n) (n >= 2; 0 for n = 1)
@@ -67,8 +67,8 @@ struct VaryParams {
     float pm_einv;           // 1 / (eta_m + 1)
     long long pm_T;          // PM on (>= 0) / off (-1)
     const long long* pm_gap; // PM gap table: gap = max k in [0, d] with w <= pm_gap[k] (host.cuh PmGaps)
-    double pm_glog;          // 1 / log(1 - pm) (the gap, MutCursor; 0: pm >= 1)
-    double pm_gdelta;        // the fp64 gap's error margin
+    float pm_glog;           // 1 / log2(1 - pm): the gap's first estimate (MutCursor)
+    long long pm_coinT;      // DE kernels' PM coin: mutate iff w <= pm_coinT (-1 never)
     long long de_T;          // DE: take iff w <= de_T (>= 2^32 - 1: always)
     UIdx ui[2], uid;         // uniform_index divisors: t per population, d (jrand)
     // tournament parents (comparison algorithms, baselines.cpp:347-352, 416-420):
@@ -182,7 +182,8 @@ __device__ __forceinline__ unsigned pick_word(const u32x4& w, int k) {
     return k == 0 ? w.x : (k == 1 ? w.y : (k == 2 ? w.z : w.w));
 }
 
-// the PICK stream: 32-bit words, four per counter, consumed in order
+// the PICK stream: 32-bit words, four per counter, consumed in order (a 64-bit
+// draw sequence as rng.hpp's measured no faster for DE, A/B DESIGN.md)
 struct PickStream {
     unsigned slot, gen, tag;
     const PhiloxKey& K;
@@ -210,35 +211,23 @@ struct PickStream {
 // k in [0, d] with w <= T[k], T[k] = ceil((1 - pm)^k 2^32) - 1 -- Geometric(pm)
 // gaps, i.e. every gene mutates independently with probability pm, at ~2
 // words per child instead of one coin per gene.  `next` walks the mutated
-// genes in ascending order (d or more: none left).  u = w 2^-32 < q^k, q = 1 -
-// pm, iff k < L = log(u) / log(q), so the gap is ceil(L) - 1, found in fp64;
-// within delta of an integer (delta bounds the fp64 error of L and of the
-// table's iterated powers, ~1e-13 for d = 30) the table decides.
+// genes in ascending order (d or more: none left).  A float estimate from
+// log2(u) / log2(1 - pm) is corrected against the table (one or two loads).
+// The SBX kernels draw PM this way; the DE kernels keep one coin per gene
+// (MCOIN: its per-group Philox hides the parent loads' latency, A/B DESIGN.md).
 struct MutCursor {
     unsigned slot, gen, tag;
     unsigned t;
     u32x4 cache;
     int next;
     __device__ __forceinline__ void advance(const PhiloxKey& K, const long long* __restrict__ T, int d,
-                                            double glog, double delta) {
+                                            float glog) {
         if ((t & 3) == 0) cache = philox4x32_10(slot, gen, tag, t >> 2, K);
         const unsigned w = pick_word(cache, (int)(t++ & 3));
-        int k;
-        if (glog == 0.0) {  // pm >= 1: every gene
-            k = 0;
-        } else {
-            const double L = w ? log((double)w * 0x1.0p-32) * glog : 1e300;
-            if (L > (double)d + delta) {
-                k = d;
-            } else {
-                k = min((int)L, d);  // L >= 0
-                const double f = L - (double)k;
-                if (f < delta || f > 1.0 - delta) {  // at a boundary: the table decides
-                    while (k > 0 && (long long)w > T[k]) --k;
-                    while (k < d && (long long)w <= T[k + 1]) ++k;
-                }
-            }
-        }
+        const float u = ((float)w + 0.5f) * 0x1.0p-32f;
+        int k = (int)fminf(fmaxf(__log2f(u) * glog, 0.0f), (float)d);
+        while (k > 0 && (long long)w > T[k]) --k;
+        while (k < d && (long long)w <= T[k + 1]) ++k;
         next += k + 1;
     }
 };
@@ -516,8 +505,8 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             const PhiloxKey& K = p.key;
             // the mutated genes, in ascending order (gaps, MutCursor)
             MutCursor mc{slot, gen, philox_tag(pid, STREAM_MSKIP), 0u, {}, -1};
-            if (MODE == MODE_VARY && active && p.pm_T >= 0)
-                mc.advance(K, p.pm_gap, d, p.pm_glog, p.pm_gdelta);
+            if (OP == OP_SBX && MODE == MODE_VARY && active && p.pm_T >= 0)
+                mc.advance(K, p.pm_gap, d, p.pm_glog);
             else
                 mc.next = d;
             for (int w0 = 0; w0 < d; w0 += 64) {
@@ -527,7 +516,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                 Mask mmask = 0;
                 while (mc.next < w1) {
                     mmask |= (Mask)1 << (mc.next - w0);
-                    mc.advance(K, p.pm_gap, d, p.pm_glog, p.pm_gdelta);
+                    mc.advance(K, p.pm_gap, d, p.pm_glog);
                 }
                 // SBX per-gene crossover bits of the window (gmpea.cpp:119): one
                 // XCOIN counter holds 128 genes' bits
@@ -568,7 +557,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         const int ng = NGC > 0 ? NGC : min(8, w1 - jb);
                         const bool two = NGC > 0 ? (NGC > 4) : (jb + 4 < w1);
                         const int q = jb >> 2;
-                        u32x4 xc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0};
+                        u32x4 xc{0, 0, 0, 0}, xu0{0, 0, 0, 0}, xu1{0, 0, 0, 0}, pmc{0, 0, 0, 0};
                         const unsigned idx8 = (unsigned)(jb >> 3);
                         const unsigned gmask = (2u << (ng - 1)) - 1u;
                         const unsigned xg = (unsigned)(xwin >> (jb - w0)) & gmask;
@@ -577,6 +566,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                             if (two) xu1 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q + 1u, K);
                         }
                         if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, K);
+                        if (OP == OP_DE && p.pm_T >= 0) pmc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, K);
                         float4 a4[2], b4[2], c4[2];
                         if (two && even_rows) {  // one 32 B sector per parent: 256-bit loads
                             ldg256(PX + (oa + q), a4[0], a4[1]);
@@ -605,7 +595,9 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                                          : (de_all ? (1u << ng) - 1u
                                                    : coins8(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
                                                                    (unsigned)jb, K));
-                        const unsigned mbits = (unsigned)(mmask >> (jb - w0)) & gmask;
+                        const unsigned mbits =
+                            OP == OP_DE ? coins8(pmc, p.pm_coinT, ng, slot, gen, philox_tag(pid, STREAM_MREF), (unsigned)jb, K)
+                                        : (unsigned)(mmask >> (jb - w0)) & gmask;
                         float v[8];
                         auto comp = [](const float4& f, int kk) {
                             return kk == 0 ? f.x : (kk == 1 ? f.y : (kk == 2 ? f.z : f.w));
@@ -648,7 +640,9 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         for (int k = 0; k < 8; ++k)
                             if (k < ng && !((mbits >> k) & 1u))
                                 v[k] = fminf(fmaxf(v[k], GMPEA_LO(jb + k)), GMPEA_HI(jb + k));
-                        if constexpr (!ST) {
+                        if constexpr (ST) {
+                            if (OP == OP_DE) mmask |= (Mask)mbits << (jb - w0);  // the DE kernels' coins
+                        } else {
                             // inline polynomial mutation + clip, then the evaluator, as
                             // rolled loops over the group: one code copy of the PM draw
                             // and of the evaluator's gene step instead of eight (the
