@@ -58,8 +58,10 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     # every header may feed every TU: a header change rebuilds all objects
     todo = [s for s in SOURCES if force or _stale(_obj(s), [s] + HEADERS)]
 
+    extra = os.environ.get("GMPEA_NVCC_EXTRA", "").split()  # A/B variants (-DGMPEA_...)
+
     def compile_one(src):
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", _obj(src) + ".tmp", src]
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", _obj(src) + ".tmp", src]
         if verbose:
             print(" ".join(cmd), file=sys.stderr, flush=True)
         subprocess.run(cmd, check=True)

@@ -956,7 +956,11 @@ struct gmpea_engine {
     // ---- the selection's static tables (unit weights, reverse neighbourhood
     // in-degrees and rows) in one arena, so one L2 access-policy window can
     // keep them resident: select re-reads them every generation while
-    // vary_eval streams ~600 MB through L2 in between (GMPEA_L2_PERSIST=0: off)
+    // vary_eval streams ~600 MB through L2 in between.  Opt-in
+    // (GMPEA_L2_PERSIST=1): measured, the persisting carve-out costs vary_eval
+    // and op1 more L2 than it saves select (LIRCMOP13 N = 10^6: select
+    // 0.0951 -> 0.0931 ms, vary_eval 0.208 -> 0.281, op1 0.017 -> 0.032;
+    // profiles/r02/ab_l2_persist.txt)
     DevBuf<char> sarena;
     const float4* sU = nullptr;
     const int* sRdeg[2] = {nullptr, nullptr};
@@ -965,7 +969,7 @@ struct gmpea_engine {
 
     void pack_static() {
         const char* env = getenv("GMPEA_L2_PERSIST");
-        if (env && *env == '0') return;
+        if (!env || *env != '1') return;
         int dev = 0, maxwin = 0, maxpersist = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev));

@@ -407,6 +407,9 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #ifndef GMPEA_VARY_MINBLOCKS
 #define GMPEA_VARY_MINBLOCKS 8
 #endif
+#ifndef GMPEA_TMA_STORE
+#define GMPEA_TMA_STORE 1
+#endif
 // DC > 0 compiles the kernel for a fixed decision dimension (the registered
 // suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
 // TOUR: tournament parent picks (the comparison algorithms' instantiation;
@@ -763,8 +766,25 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             }
         }
     }
-    // phase 4: rows [i0, i0 + rows) leave as one contiguous, coalesced copy
-    if (ST) {
+    // phase 4: the block's rows leave shared memory.  Rows of whole 128 B lines
+    // (rs4 % 8 == 0, LIRCMOP1-13: 30 + 2 floats): every thread's staged row
+    // through the bulk-copy engine (cp.async.bulk, UBLKCP) after a proxy fence
+    // and one barrier (PM tasks wrote other threads' rows): LIRCMOP13 vary
+    // -1.9 %.  Other rows as one contiguous, coalesced copy of rows [i0, i0 +
+    // rows) (the bulk copies of 32-160 B rows that straddle lines cost MW7
+    // +6 %, DAS-CMOP9 +2 %, C1-DTLZ1 +13 %; A/B in DESIGN.md)
+    if (ST && GMPEA_TMA_STORE && (rs4 & 7) == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (active) {
+            const unsigned saddr = (unsigned)__cvta_generic_to_shared(my4);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(grow), "r"(saddr),
+                         "r"(rs4 * 16)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+    } else if (ST) {
         __syncthreads();
         const int rows = min((int)blockDim.x, p.row_end - i0);
         const int total = rows * rs4;
