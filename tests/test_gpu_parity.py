@@ -479,3 +479,34 @@ def test_set_population_reports_out_of_bounds_rows(g):
     eng.set_population(1, X)  # asynchronous: reported at the next synchronisation
     with pytest.raises(ValueError, match="evaluate: out-of-bounds rows: 3 17$"):
         eng.sync()
+
+
+def test_baseline_config0_mw1_n100_1000_generations(g):
+    """BASELINE configs[0]: GMPEA on MW1 (D = 15, 2 objectives), N = 100, 1000
+    generations.  30 engine seeds against 30 runs of the reference's own
+    run_gmpea with the restated MW1 evaluator as its ProblemDef
+    (tests/golden/config0_mw1_ref.json, tools/mw_parity.py ref): final IGD
+    against the restated front and normalised HV not significantly worse."""
+    import json
+
+    from scipy.stats import mannwhitneyu
+
+    from conftest import GOLDEN
+
+    ref = json.load(open(f"{GOLDEN}/config0_mw1_ref.json"))
+    rp = ref["problems"]["MW1"]
+    front = golden("pf_restated.npz")["MW1/1000"]
+    lo, hi = np.array(rp["ideal"]), np.array(rp["nadir"])
+    span = np.where(hi > lo, hi - lo, 1.0)
+    p = g.make_problem("MW1")
+    igd, hv = [], []
+    for seed in range(1, 31):
+        r = g.run_gmpea(p, g.RunConfig(n=100, k_max=1000, seed=seed, op=g.VariationOp.sbx_pm))
+        fr = g.metric_front(r.pop1)
+        igd.append(g.igd(fr, front) if len(fr) else 1e9)
+        hv.append(g.hypervolume((fr - lo) / span, np.full(2, 1.1)) if len(fr) else 0.0)
+    ri = np.where(np.isfinite(rp["igd"]), rp["igd"], 1e9)
+    for mine, theirs, higher in ((igd, ri, False), (hv, rp["hv"], True)):
+        pv = mannwhitneyu(mine, theirs, alternative="two-sided").pvalue
+        worse = np.median(mine) < np.median(theirs) if higher else np.median(mine) > np.median(theirs)
+        assert not (pv < 0.01 and worse), (np.median(mine), np.median(theirs), pv)
