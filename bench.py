@@ -204,10 +204,16 @@ def quality_1s(g, problem="LIRCMOP13", op=1, budget=1.0, gpu_n=100_000, ref_n=10
     front = np.load(os.path.join(ROOT, "tests", "golden", "fronts.npz"))[problem]
     p = g.make_problem(problem)
     out = {"problem": problem, "budget_s": budget, "seed": seed, "front": "reference pf_reference, 1000 points"}
-    r = g.run_gmpea(p, g.RunConfig(n=gpu_n, time_budget_s=budget, seed=seed, op=op))
+    # tens of thousands of generations at N = 10^5 can meet the reference's PM
+    # hazard (its own evaluation error, which the engine raises as it does)
+    r, retries = retry_hazard(lambda sd: g.run_gmpea(p, g.RunConfig(n=gpu_n, time_budget_s=budget, seed=sd, op=op)),
+                              first_seed=seed)
     fr = g.metric_front(r.pop1)
-    out["engine"] = {"n": gpu_n, "generations": r.history[-1].gen, "loop_ms": r.history[-1].wall_ms,
-                     "front_points": int(len(fr)), "igd": float(g.igd(fr, front)) if len(fr) else float("inf")}
+    out["engine"] = {"n": gpu_n, "seed": seed + retries, "generations": r.history[-1].gen,
+                     "loop_ms": r.history[-1].wall_ms, "front_points": int(len(fr)),
+                     "igd": float(g.igd(fr, front)) if len(fr) else float("inf")}
+    if retries:
+        out["engine"]["hazard_retries"] = retries
     try:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from oracle import Reference  # the reference arm (baseline only)

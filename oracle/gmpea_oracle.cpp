@@ -40,8 +40,6 @@
 #include <map>
 #include <mutex>
 #include <utility>
-#include <map>
-#include <mutex>
 #include <vector>
 
 #include "philox.h"
@@ -1497,7 +1495,31 @@ double hypervolume(const double* P, size_t n, int m, const double* ref) {
         }
         return vol;
     }
-    throw std::invalid_argument("hypervolume: oracle covers m = 2, 3 only");
+    // m > 3: Monte-Carlo estimate, metrics.cpp:95-121 — 10^6 samples of
+    // mt19937_64(0x48563D), uniform(lo, ref) = lo + (ref - lo) * (e() >> 11) * 2^-53
+    std::vector<double> lo(m, std::numeric_limits<double>::infinity());
+    for (size_t i : keep)
+        for (int c = 0; c < m; ++c) lo[c] = std::min(lo[c], P[i * m + c]);
+    double box = 1.0;
+    for (int c = 0; c < m; ++c) box *= ref[c] - lo[c];
+    if (box <= 0.0) return 0.0;
+    std::mt19937_64 e(0x48563D);
+    const size_t samples = 1000000;
+    size_t hits = 0;
+    std::vector<double> x(m);
+    for (size_t s = 0; s < samples; ++s) {
+        for (int c = 0; c < m; ++c) x[c] = lo[c] + (ref[c] - lo[c]) * ((double)(e() >> 11) * 0x1.0p-53);
+        for (size_t i : keep) {
+            bool dom = true;
+            for (int c = 0; c < m && dom; ++c)
+                if (P[i * m + c] > x[c]) dom = false;
+            if (dom) {
+                ++hits;
+                break;
+            }
+        }
+    }
+    return box * (double)hits / (double)samples;
 }
 
 template <class Fn>

@@ -413,7 +413,7 @@ void device_knn(cudaStream_t s, int n, int m, int t1, int t2, const double* dW, 
         int* Bbig = t2 >= t1 ? B2 : B1;
         int* Bsmall = t2 >= t1 ? B1 : B2;
         int tsmall = std::min(t1, t2);
-        if (lattice && n > 4096) {
+        if (lattice && m <= 3 && n > 4096) {  // the window search knows the m <= 3 lattices
             DevBuf<int> retry(1);
             for (int R = 6;; R *= 2) {
                 retry.zero(s);
@@ -1865,11 +1865,14 @@ int gmpea_evaluate(const gmpea_problem* p, const double* X, int64_t n, double* F
 int gmpea_reference_vectors(int32_t m, int64_t n, double* W) {
     return guarded([&] {
         if (n <= 0) throw std::invalid_argument("reference_vectors: target_n must be positive");
-        if (m < 2 || m > 3) throw std::invalid_argument("reference_vectors: m must be 2 or 3");
+        if (m < 2 || m > kMaxLatM) throw std::invalid_argument("reference_vectors: m must be 2 to 16");
         require_device();
         DevBuf<double> w((size_t)n * m);
         DevBuf<float4> u(n);
-        lattice_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, lattice_H(m, n), w.p, u.p);
+        if (m <= 3)
+            lattice_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, lattice_H(m, n), w.p, u.p);
+        else
+            lattice_m_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, lattice_H(m, n), w.p);
         CK(cudaGetLastError());
         CK(cudaMemcpy(W, w.p, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToHost));
     });
@@ -1878,15 +1881,17 @@ int gmpea_reference_vectors(int32_t m, int64_t n, double* W) {
 static void knn_api(const double* Wh, int64_t n, int32_t m, int32_t t1, int32_t t2, uint32_t* B1,
                     uint32_t* B2, bool lattice) {
     if (n <= 0) throw std::invalid_argument("build_neighborhoods: empty population");
-    if (m < 2 || m > 3) throw std::invalid_argument("build_neighborhoods: m must be 2 or 3");
+    if (m < 2 || m > kMaxLatM) throw std::invalid_argument("build_neighborhoods: m must be 2 to 16");
     if (t1 > n || t2 > n) throw std::invalid_argument("build_neighborhoods: neighborhood exceeds population");
     require_device();
     cudaStream_t s = 0;
     DevBuf<double> w((size_t)n * m);
     DevBuf<float4> u(n);
     long long H = lattice_H(m, n);
-    if (lattice)
+    if (lattice && m <= 3)
         lattice_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, H, w.p, u.p);
+    else if (lattice)
+        lattice_m_kernel<<<blocks_for(n, 256), 256>>>((int)n, m, H, w.p);
     else
         CK(cudaMemcpy(w.p, Wh, (size_t)n * m * sizeof(double), cudaMemcpyHostToDevice));
     DevBuf<int> b1((size_t)n * std::max(t1, 1)), b2((size_t)n * std::max(t2, 1));

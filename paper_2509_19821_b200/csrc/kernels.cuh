@@ -410,6 +410,12 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #ifndef GMPEA_TMA_STORE
 #define GMPEA_TMA_STORE 1
 #endif
+#ifndef GMPEA_DE_GAPS
+#define GMPEA_DE_GAPS 0  // DE kernels: PM by gaps instead of per-gene coins (A/B switch)
+#endif
+#ifndef GMPEA_VARY_MINBLOCKS_DE
+#define GMPEA_VARY_MINBLOCKS_DE GMPEA_VARY_MINBLOCKS
+#endif
 // DC > 0 compiles the kernel for a fixed decision dimension (the registered
 // suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
 // TOUR: tournament parent picks (the comparison algorithms' instantiation;
@@ -508,7 +514,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             const PhiloxKey& K = p.key;
             // the mutated genes, in ascending order (gaps, MutCursor)
             MutCursor mc{slot, gen, philox_tag(pid, STREAM_MSKIP), 0u, {}, -1};
-            if (OP == OP_SBX && MODE == MODE_VARY && active && p.pm_T >= 0)
+            if ((OP == OP_SBX || GMPEA_DE_GAPS) && MODE == MODE_VARY && active && p.pm_T >= 0)
                 mc.advance(K, p.pm_gap, d, p.pm_glog);
             else
                 mc.next = d;
@@ -569,7 +575,8 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                             if (two) xu1 = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XU), (unsigned)q + 1u, K);
                         }
                         if (OP == OP_DE && !de_all) xc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_XCOIN), idx8, K);
-                        if (OP == OP_DE && p.pm_T >= 0) pmc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, K);
+                        if (OP == OP_DE && !GMPEA_DE_GAPS && p.pm_T >= 0)
+                            pmc = philox4x32_10(slot, gen, philox_tag(pid, STREAM_MCOIN), idx8, K);
                         float4 a4[2], b4[2], c4[2];
                         if (two && even_rows) {  // one 32 B sector per parent: 256-bit loads
                             ldg256(PX + (oa + q), a4[0], a4[1]);
@@ -599,7 +606,8 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                                                    : coins8(xc, p.de_T, ng, slot, gen, philox_tag(pid, STREAM_XREF),
                                                                    (unsigned)jb, K));
                         const unsigned mbits =
-                            OP == OP_DE ? coins8(pmc, p.pm_coinT, ng, slot, gen, philox_tag(pid, STREAM_MREF), (unsigned)jb, K)
+                            OP == OP_DE && !GMPEA_DE_GAPS
+                                ? coins8(pmc, p.pm_coinT, ng, slot, gen, philox_tag(pid, STREAM_MREF), (unsigned)jb, K)
                                         : (unsigned)(mmask >> (jb - w0)) & gmask;
                         float v[8];
                         auto comp = [](const float4& f, int kk) {
@@ -644,7 +652,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                             if (k < ng && !((mbits >> k) & 1u))
                                 v[k] = fminf(fmaxf(v[k], GMPEA_LO(jb + k)), GMPEA_HI(jb + k));
                         if constexpr (ST) {
-                            if (OP == OP_DE) mmask |= (Mask)mbits << (jb - w0);  // the DE kernels' coins
+                            if (OP == OP_DE && !GMPEA_DE_GAPS) mmask |= (Mask)mbits << (jb - w0);  // the DE kernels' coins
                         } else {
                             // inline polynomial mutation + clip, then the evaluator, as
                             // rolled loops over the group: one code copy of the PM draw
@@ -831,13 +839,13 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 // blocks per SM: 8 (63 registers); the MW kernel (d = 15, smaller rows and
 // evaluator state) runs faster at 10 (48 registers) despite a small spill,
 // LIRCMOP13 slower (A/B)
-template <class Ev, int DC>
+template <class Ev, int OP, int DC>
 constexpr int vary_minblocks() {
-    return DC == 15 && std::is_same<Ev, EvalMw>::value ? 10 : GMPEA_VARY_MINBLOCKS;
+    return DC == 15 && std::is_same<Ev, EvalMw>::value ? 10 : (OP == OP_DE ? GMPEA_VARY_MINBLOCKS_DE : GMPEA_VARY_MINBLOCKS);
 }
 
 template <class Ev, int MODE, int OP, int DC = 0, bool UB = false, bool TOUR = false>
-__global__ void __launch_bounds__(128, (vary_minblocks<Ev, DC>())) vary_eval_kernel(VaryParams p) {
+__global__ void __launch_bounds__(128, (vary_minblocks<Ev, OP, DC>())) vary_eval_kernel(VaryParams p) {
     vary_body<Ev, MODE, OP, DC, UB, TOUR>(p, blockIdx.x, blockIdx.y);
 }
 

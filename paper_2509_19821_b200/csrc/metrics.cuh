@@ -147,10 +147,64 @@ __global__ void nd3_kernel(const double* F, const long long* order, const long l
 }
 
 // IGD partial: best squared distance of reference point r over a chunk of A
+// objectives the metrics take on the device (any m up to this)
+constexpr int kMaxObj = 16;
+
+// nondominated (+ deduplicated, the earlier of equal rows kept) subset of the
+// candidate rows, any m, O(k^2): metrics.cpp:155-175 (metric_front) and
+// :42-61 (hv_relevant) as the reference writes them; cand in row order
+__global__ void nd_any_kernel(const double* F, const long long* cand, long long k, int m, int dedup,
+                              unsigned char* keep) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= k) return;
+    const long long i = cand[p];
+    bool ok = true;
+    for (long long q = 0; q < k && ok; ++q) {
+        if (q == p) continue;
+        const long long j = cand[q];
+        bool le = true, lt = false, eq = true;
+        for (int c = 0; c < m; ++c) {
+            const double a = F[j * m + c], b = F[i * m + c];
+            if (a > b) le = false;
+            if (a < b) lt = true;
+            if (a != b) eq = false;
+        }
+        if (le && lt) ok = false;  // pareto_dominates(row j, row i)
+        if (dedup && eq && q < p) ok = false;
+    }
+    keep[p] = ok ? 1 : 0;
+}
+
+// hv_mc (metrics.cpp:95-121): the number of samples (host-drawn from the
+// reference's fixed-seed stream, s-major, m coordinates each) dominated by
+// some relevant point; the count is an integer, so the estimate is exact
+__global__ void hv_mc_kernel(const double* P, const long long* keep, long long nk, int m, const double* X,
+                             long long samples, unsigned long long* hits) {
+    __shared__ unsigned cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < samples) {
+        const double* x = X + s * m;
+        for (long long t = 0; t < nk; ++t) {
+            const double* pi = P + keep[t] * m;
+            bool dom = true;
+            for (int c = 0; c < m && dom; ++c)
+                if (pi[c] > x[c]) dom = false;
+            if (dom) {
+                atomicAdd(&cnt, 1u);
+                break;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && cnt) atomicAdd(hits, (unsigned long long)cnt);
+}
+
 __global__ void igd_min_kernel(const double* A, long long na, const double* Rf, long long nr, int m,
                                unsigned long long* best) {
     const long long r = blockIdx.y;
-    double rr[3];
+    double rr[kMaxObj];
     for (int c = 0; c < m; ++c) rr[c] = Rf[r * m + c];
     double b = 1.0 / 0.0;
     for (long long a = (long long)blockIdx.x * blockDim.x + threadIdx.x; a < na;

@@ -22,6 +22,16 @@ thrust::device_vector<long long> front_filter(const double* dF, int m, thrust::d
     const long long k = (long long)cand.size();
     thrust::device_vector<long long> kept;
     if (k == 0) return kept;
+    if (m > 3) {  // any m: the reference's pairwise form; kept rows in row order
+        thrust::device_vector<unsigned char> keep(k);
+        nd_any_kernel<<<blocks_for(k, 128), 128>>>(dF, thrust::raw_pointer_cast(cand.data()), k, m, dedup,
+                                                   thrust::raw_pointer_cast(keep.data()));
+        CK(cudaGetLastError());
+        kept.resize(k);
+        auto end = thrust::copy_if(thrust::device, cand.begin(), cand.end(), keep.begin(), kept.begin(), NonZero{});
+        kept.resize(end - kept.begin());
+        return kept;
+    }
     thrust::sort(thrust::device, cand.begin(), cand.end(), LexLess{dF, m});
     thrust::device_vector<long long> gs(k);
     const long long* order = thrust::raw_pointer_cast(cand.data());
@@ -185,7 +195,7 @@ int gmpea_pf_reference(const gmpea_problem* p, int64_t n_points, double* out, in
 
 int gmpea_metric_front(const double* F, const double* cv, int64_t n, int32_t m, int64_t* idx, int64_t* count) {
     return guarded([&] {
-        if (m < 2 || m > 3) throw std::invalid_argument("metric_front: m must be 2 or 3");
+        if (m < 2 || m > kMaxObj) throw std::invalid_argument("metric_front: m must be 2 to 16");
         *count = 0;
         if (n <= 0) return;
         require_device();
@@ -211,7 +221,7 @@ int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t 
             *out = std::numeric_limits<double>::infinity();
             return;
         }
-        if (m < 1 || m > 3) throw std::invalid_argument("igd: objective count mismatch");
+        if (m < 1 || m > kMaxObj) throw std::invalid_argument("igd: objective count mismatch");
         require_device();
         thrust::device_vector<double> dA(A, A + na * m), dR(R, R + nr * m), res(1);
         thrust::device_vector<unsigned long long> best(nr, 0x7ff0000000000000ull);  // +inf
@@ -227,7 +237,7 @@ int gmpea_igd(const double* A, int64_t na, const double* R, int64_t nr, int32_t 
 
 int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, double* out) {
     return guarded([&] {
-        if (m < 2 || m > 3) throw std::invalid_argument("hypervolume: m must be 2 or 3 on device");
+        if (m < 2 || m > kMaxObj) throw std::invalid_argument("hypervolume: m must be 2 to 16");
         *out = 0.0;
         if (n <= 0) return;
         require_device();
@@ -241,6 +251,31 @@ int gmpea_hypervolume(const double* P, int64_t n, int32_t m, const double* ref, 
         auto xy = front_filter(pP, m, cand);  // hv_relevant, sorted by (x, y[, z])
         const long long cnt = (long long)xy.size();
         if (cnt == 0) return;
+        if (m > 3) {  // hv_mc (metrics.cpp:95-121)
+            std::vector<long long> keep(cnt);
+            thrust::copy(xy.begin(), xy.end(), keep.begin());
+            std::vector<double> lo(m, std::numeric_limits<double>::infinity());
+            for (long long i : keep)
+                for (int c = 0; c < m; ++c) lo[c] = std::min(lo[c], P[i * m + c]);
+            double box = 1.0;
+            for (int c = 0; c < m; ++c) box *= ref[c] - lo[c];
+            if (box <= 0.0) return;
+            // the reference's sample stream: Rng(0x48563D) = mt19937_64, uniform(lo, hi)
+            std::mt19937_64 e(0x48563D);
+            const long long samples = 1000000;
+            std::vector<double> X((size_t)samples * m);
+            for (long long s2 = 0; s2 < samples; ++s2)
+                for (int c = 0; c < m; ++c)
+                    X[(size_t)s2 * m + c] = lo[c] + (ref[c] - lo[c]) * ((double)(e() >> 11) * 0x1.0p-53);
+            thrust::device_vector<double> dX(X.begin(), X.end());
+            thrust::device_vector<unsigned long long> hits(1, 0ull);
+            hv_mc_kernel<<<blocks_for(samples, 256), 256>>>(pP, thrust::raw_pointer_cast(xy.data()), cnt, m,
+                                                            thrust::raw_pointer_cast(dX.data()), samples,
+                                                            thrust::raw_pointer_cast(hits.data()));
+            CK(cudaGetLastError());
+            *out = box * (double)(unsigned long long)hits[0] / (double)samples;
+            return;
+        }
         thrust::device_vector<double> slab(m == 2 ? 1 : cnt), res(1);
         thrust::device_vector<long long> zorder, zrank;
         if (m == 3) {

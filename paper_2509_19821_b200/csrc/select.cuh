@@ -119,13 +119,66 @@ struct SelParams {
     volatile int* host_flag;
 };
 
+// L1 policy of the select kernel (GMPEA_SELECT_L1HINTS): the claimants' keys
+// are gathered many times by neighbouring slots and should stay in L1; the
+// per-slot streams (parent key, weight, in-degree, reverse rows) and the
+// winner rows are touched once, so they bypass / leave L1 first
+#ifndef GMPEA_SELECT_L1HINTS
+#define GMPEA_SELECT_L1HINTS 1
+#endif
+// GMPEA_SELECT_L1HINTS 1: ld.global.cs (evict first in L1 and L2); 2: only
+// L1::no_allocate (L2 policy untouched)
+__device__ __forceinline__ float4 ld_once(const float4* p) {
+#if GMPEA_SELECT_L1HINTS == 2
+    float4 v;
+    asm("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+#elif GMPEA_SELECT_L1HINTS == 1
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+__device__ __forceinline__ int ld_once(const int* p) {
+#if GMPEA_SELECT_L1HINTS == 2
+    int v;
+    asm("ld.global.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+#elif GMPEA_SELECT_L1HINTS == 1
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+__device__ __forceinline__ uint2 ld_once(const uint2* p) {
+#if GMPEA_SELECT_L1HINTS == 2
+    uint2 v;
+    asm("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+#elif GMPEA_SELECT_L1HINTS == 1
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+// 256-bit load that does not allocate in L1 (winner rows)
+__device__ __forceinline__ void ldg256_na(const float4* p, float4& a, float4& b) {
+#if GMPEA_SELECT_L1HINTS
+    asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+#else
+    ldg256(p, a, b);
+#endif
+}
+
 __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4* __restrict__ src, int rs4) {
     if ((rs4 & 1) == 0) {  // rows 32 B aligned: 256-bit loads and stores
         for (int q0 = 0; q0 < rs4; q0 += 8) {
             float4 v[8];
 #pragma unroll
             for (int u = 0; u < 8; u += 2)
-                if (q0 + u < rs4) ldg256(src + q0 + u, v[u], v[u + 1]);
+                if (q0 + u < rs4) ldg256_na(src + q0 + u, v[u], v[u + 1]);
 #pragma unroll
             for (int u = 0; u < 8; u += 2)
                 if (q0 + u < rs4)
@@ -163,11 +216,11 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     constexpr int NW = NB / 4;
     // only the parent's cv and PBI stay live (the full keys are re-read at the
     // end), which keeps select at 48 registers (5 blocks of 256 per SM)
-    const float4 par4 = p.Fcv[POP][j];
-    const float4 u4 = p.U[j];
+    const float4 par4 = ld_once(&p.Fcv[POP][j]);
+    const float4 u4 = ld_once(&p.U[j]);
     const float gp = agg_key<AGG>(par4, u4, z, p.theta);
     const float pw = par4.w;
-    const int deg = p.Rdeg[POP][j];
+    const int deg = ld_once(&p.Rdeg[POP][j]);
     const int* __restrict__ R = p.R[POP];
     const uint2* __restrict__ Rp = p.Rp[POP] + j;
     const float4* __restrict__ eff = p.eff[POP];
@@ -182,7 +235,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     uint2 wn[NW];
     if (PACK) {
 #pragma unroll
-        for (int h = 0; h < NW; ++h) wn[h] = 4 * h < deg ? Rp[(long long)h * p.ldr] : make_uint2(0u, 0u);
+        for (int h = 0; h < NW; ++h) wn[h] = 4 * h < deg ? ld_once(&Rp[(long long)h * p.ldr]) : make_uint2(0u, 0u);
 #pragma unroll
         for (int h = 0; h < NW; ++h) unpack_claims(wn[h], j, deg - 4 * h, cc + 4 * h);
     } else {
@@ -198,7 +251,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
         if (PACK) {
 #pragma unroll
             for (int h = 0; h < NW; ++h)
-                if (k0 + NB + 4 * h < deg) wn[h] = Rp[(long long)((k0 + NB) / 4 + h) * p.ldr];
+                if (k0 + NB + 4 * h < deg) wn[h] = ld_once(&Rp[(long long)((k0 + NB) / 4 + h) * p.ldr]);
         } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u) cn[u] = k0 + 4 + u < deg ? R[(long long)(k0 + 4 + u) * p.ldr + j] : -1;

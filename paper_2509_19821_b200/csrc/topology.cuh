@@ -20,6 +20,7 @@
 namespace gmpea_b200 {
 
 constexpr int kMaxT = 64;  // insertion-list length for t <= kMaxT
+constexpr int kMaxLatM = 16;  // objectives of the operator API's lattices / KNN / metrics (the engine: m <= 3)
 
 __device__ __forceinline__ double d2_exact(const double* a, const double* b, int m) {
     double s = 0.0;
@@ -64,6 +65,35 @@ __device__ __forceinline__ void lat_weights(int m, long long H, long long a, lon
         w[1] = (double)b / h;
         w[2] = (double)(H - a - b) / h;
     }
+}
+
+// compositions of `total` into `parts` non-negative parts: C(total + parts - 1, parts - 1)
+__host__ __device__ inline long long lat_count(long long total, int parts) {
+    long long c = 1;
+    for (int i = 1; i < parts; ++i) c = c * (total + i) / i;
+    return c;
+}
+
+// reference_vectors for any m (gmpea.cpp:27-71): row i is the i-th composition
+// (a_0, .., a_{m-2}, H - sum) in the reference's recursion order (lexicographic,
+// a_0 outermost), unranked by counting the compositions of each prefix;
+// w_c = a_c / H exactly as the reference divides
+__global__ void lattice_m_kernel(int n, int m, long long H, double* W) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    long long r = i, rem = H;
+    const double h = (double)H;
+    for (int p = 0; p < m - 1; ++p) {
+        long long v = 0;
+        for (;; ++v) {
+            const long long c = lat_count(rem - v, m - 1 - p);
+            if (r < c) break;
+            r -= c;
+        }
+        W[(long long)i * m + p] = (double)v / h;
+        rem -= v;
+    }
+    W[(long long)i * m + m - 1] = (double)rem / h;
 }
 
 __global__ void lattice_kernel(int n, int m, long long H, double* W, float4* U) {
@@ -128,7 +158,7 @@ __global__ void knn_lattice_kernel(int n, int m, long long H, int t1, int t2, in
                                    int* B1, int* B2, int* needs_retry) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double wi[3];
+    double wi[kMaxLatM];
     for (int c = 0; c < m; ++c) wi[c] = W[(long long)i * m + c];
     TopK tk;
     tk.init(t2);
@@ -170,7 +200,7 @@ __global__ void knn_lattice_kernel(int n, int m, long long H, int t1, int t2, in
 __global__ void knn_brute_kernel(int n, int m, int t1, int t2, const double* W, int* B1, int* B2) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double wi[3];
+    double wi[kMaxLatM];
     for (int c = 0; c < m; ++c) wi[c] = W[(long long)i * m + c];
     TopK tk;
     tk.init(t2);
@@ -183,7 +213,7 @@ __global__ void knn_brute_kernel(int n, int m, int t1, int t2, const double* W, 
 __global__ void knn_select_kernel(int n, int m, int t, const double* W, int* B) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    double wi[3];
+    double wi[kMaxLatM];
     for (int c = 0; c < m; ++c) wi[c] = W[(long long)i * m + c];
     double pd = -1.0;
     int pj = -1;

@@ -298,12 +298,44 @@ def wta_large_fixture(ref):
     np.savez_compressed(os.path.join(HERE, "wta_large.npz"), **out)
 
 
+def many_obj_fixture(ref):
+    """m > 3 operators: the reference's own
+    reference_vectors + build_neighborhoods on m = 4..6 lattices, and
+    metric_front / igd / hypervolume (the Monte-Carlo hv_mc branch,
+    metrics.cpp:95-121) on random m = 4, 5 sets."""
+    rng = np.random.default_rng(4567)
+    out = {}
+    for (m, n, t1, t2) in ((4, 120, 5, 20), (4, 300, 8, 30), (5, 210, 5, 20), (6, 462, 5, 20), (6, 100, 3, 10)):
+        W = ref.reference_vectors(m, n)
+        B1, B2 = ref.build_neighborhoods(W, t1, t2)
+        key = f"lat_{m}_{n}_{t1}_{t2}"
+        out[key + "/W"], out[key + "/B1"], out[key + "/B2"] = W, B1, B2
+    for k in range(6):
+        m = 4 + k % 2
+        n = int(rng.integers(20, 300))
+        F = f32(rng.random((n, m)))
+        F[rng.random(n) < 0.1] = F[0]
+        cv = np.where(rng.random(n) < 0.3, rng.random(n), 0.0)
+        R = rng.random((40, m))
+        key = f"met_{k}/"
+        out[key + "F"], out[key + "cv"], out[key + "R"] = F, cv, R
+        out[key + "front"] = ref.metric_front(F, cv)
+        out[key + "igd"] = np.array(ref.igd(F, R))
+        P = f32(rng.random((min(n, 60), m)) * 1.2)
+        out[key + "P"] = P
+        out[key + "hv"] = np.array(ref.hypervolume(P, np.full(m, 1.1)))
+    np.savez_compressed(os.path.join(HERE, "many_obj.npz"), **out)
+
+
 def main():
     if not build_ref():
         raise SystemExit("reference sources not available")
     ref, orc = Reference(), Oracle()
     if "--restated-fronts" in sys.argv:  # only the MW / DAS-CMOP front fixture
         restated_fronts_fixture(ref, orc)
+        return
+    if "--many-obj" in sys.argv:  # only the m > 3 operator fixture
+        many_obj_fixture(ref)
         return
     if "--wta-large" in sys.argv:  # only the large WTA scenario fixture
         wta_large_fixture(ref)
@@ -319,6 +351,7 @@ def main():
     runs_fixture(ref)
     baseline_runs_fixture(ref)
     wta_large_fixture(ref)
+    many_obj_fixture(ref)
     print("golden fixtures written to", HERE)
 
 

@@ -248,6 +248,40 @@ def test_metrics_match_reference_golden(g):
         assert g.hypervolume(gd[pre + "P"], np.full(m, 1.1)) == float(gd[pre + "hv"]), k
 
 
+def test_many_objective_operators_match_reference_golden(g):
+    """m > 3: the any-m lattice, brute-force KNN, metric_front, IGD and the
+    Monte-Carlo hypervolume (metrics.cpp:95-121, same mt19937_64 samples)
+    reproduce the reference's outputs exactly."""
+    gd = golden("many_obj.npz")
+    for key in sorted({k.split("/")[0] for k in gd.files}):
+        if key.startswith("lat_"):
+            _, m, n, t1, t2 = key.split("_")
+            W, B1, B2 = gd[key + "/W"], gd[key + "/B1"], gd[key + "/B2"]
+            assert np.array_equal(g.reference_vectors(int(m), int(n)), W), key
+            t = g.build_neighborhoods(W, int(t1), int(t2))
+            assert np.array_equal(t.b1, B1) and np.array_equal(t.b2, B2), key
+            lt = g.lattice_neighborhoods(int(m), int(n), int(t1), int(t2))
+            assert np.array_equal(lt.b1, B1) and np.array_equal(lt.b2, B2), key
+        else:
+            pre = key + "/"
+            F, cv = gd[pre + "F"], gd[pre + "cv"]
+            fr = g.metric_front(g.Population(np.zeros((len(F), 1)), F, np.zeros((len(F), 1)), cv))
+            assert np.array_equal(fr, gd[pre + "front"]), key
+            assert g.igd(F, gd[pre + "R"]) == float(gd[pre + "igd"]), key
+            m = F.shape[1]
+            assert g.hypervolume(gd[pre + "P"], np.full(m, 1.1)) == float(gd[pre + "hv"]), key
+
+
+def test_many_objective_large_vs_oracle(g, orc):
+    rng = np.random.default_rng(11)
+    F = f32(rng.random((2000, 5)))
+    cv = np.where(rng.random(2000) < 0.2, 1.0, 0.0)
+    fr = g.metric_front(g.Population(np.zeros((2000, 1)), F, np.zeros((2000, 1)), cv))
+    assert np.array_equal(fr, F[orc.metric_front(F, cv)])
+    W = g.reference_vectors(4, 5000)
+    assert np.array_equal(W, orc.reference_vectors(4, 5000))
+
+
 def test_metric_known_answers(g):
     assert g.igd(np.array([[0.0, 0.0]]), np.array([[3.0, 4.0], [0.0, 0.0]])) == 2.5
     assert g.igd(np.zeros((0, 2)), np.ones((3, 2))) == np.inf

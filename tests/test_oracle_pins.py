@@ -81,6 +81,26 @@ def test_metrics_match_golden(orc):
         assert orc.hypervolume(gd[pre + "P"], np.full(m, 1.1)) == float(gd[pre + "hv"])
 
 
+def test_many_objective_operators_match_golden(orc):
+    """m > 3 (lattice, KNN, metric_front, IGD, Monte-Carlo HV) against the
+    reference's own outputs (make_golden.py many_obj_fixture)."""
+    gd = golden("many_obj.npz")
+    for key in sorted({k.split("/")[0] for k in gd.files}):
+        if key.startswith("lat_"):
+            _, m, n, t1, t2 = key.split("_")
+            W = gd[key + "/W"]
+            assert np.array_equal(orc.reference_vectors(int(m), int(n)), W), key
+            assert np.array_equal(orc.knn(W, int(t1)), gd[key + "/B1"]), key
+            assert np.array_equal(orc.knn(W, int(t2)), gd[key + "/B2"]), key
+        else:
+            pre = key + "/"
+            F, cv = gd[pre + "F"], gd[pre + "cv"]
+            assert np.array_equal(F[orc.metric_front(F, cv)], gd[pre + "front"]), key
+            assert orc.igd(F, gd[pre + "R"]) == float(gd[pre + "igd"]), key
+            m = F.shape[1]
+            assert orc.hypervolume(gd[pre + "P"], np.full(m, 1.1)) == float(gd[pre + "hv"]), key
+
+
 def test_wta_scenarios_match_reference(orc, ref):
     for num in range(1, 11):
         a, b = orc.wta_scenario(num), ref.wta_scenario(num)
