@@ -81,6 +81,22 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 0) -> str:
     return LIB
 
 
+def build_variant(out: str, extra: str, only) -> str:
+    """A/B helper: the library with the TUs `only` (basenames, e.g. engine.cu)
+    recompiled with the extra flags and every other object as built."""
+    build()
+    objs = []
+    for src in SOURCES:
+        if os.path.basename(src) in only:
+            o = os.path.join(OBJ, "variant_" + os.path.basename(src)[:-3] + ".o")
+            subprocess.run([nvcc(), *NVCC_FLAGS, *extra.split(), "-c", "-o", o, src], check=True)
+            objs.append(o)
+        else:
+            objs.append(_obj(src))
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", *LINK_FLAGS, "-o", out, *objs], check=True)
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
     print(LIB)

@@ -206,6 +206,19 @@ struct PickStream {
     }
 };
 
+// the MUFU log2 / exp2 without the denormal fix-ups of __log2f / exp2f (for
+// operands known to be normal or zero)
+__device__ __forceinline__ float lg2_ftz(float x) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Polynomial mutation's per-gene coin (gmpea.cpp:139, skip iff U > pm) as
 // gaps between mutated genes: word t of MSKIP gives the t-th gap, the largest
 // k in [0, d] with w <= T[k], T[k] = ceil((1 - pm)^k 2^32) - 1 -- Geometric(pm)
@@ -225,7 +238,7 @@ struct MutCursor {
         if ((t & 3) == 0) cache = philox4x32_10(slot, gen, tag, t >> 2, K);
         const unsigned w = pick_word(cache, (int)(t++ & 3));
         const float u = ((float)w + 0.5f) * 0x1.0p-32f;
-        int k = (int)fminf(fmaxf(__log2f(u) * glog, 0.0f), (float)d);
+        int k = (int)fminf(fmaxf(lg2_ftz(u) * glog, 0.0f), (float)d);  // u >= 2^-33: normal
         while (k > 0 && (long long)w > T[k]) --k;
         while (k < d && (long long)w <= T[k + 1]) ++k;
         next += k + 1;
@@ -283,11 +296,24 @@ __device__ __forceinline__ float pm_apply(float x, float lo, float hi, unsigned 
 // lies in (0, 2] and e = 1/(eta+1) is small, so exp2(e log2 b) through the
 // MUFU pair is accurate to ~2 ulp here (the child differs from the f64 oracle
 // by < 1e-6 of the parents' spread) at a fraction of powf's cost.
+#ifndef GMPEA_SBX_BRANCHY
+#define GMPEA_SBX_BRANCHY 0  // the per-gene branch around the SBX spread (A/B switch)
+#endif
+// The MUFU pair is issued directly (.ftz: b >= 2^-31 or 0 and the exponent
+// lies in [-1.5, 1.5], so the denormal fix-ups exp2f / __log2f wrap around
+// it never apply); b = 0 gives lg2 = -inf, ex2(-inf) = +0 = beta.  No branch,
+// so a warp computes the spread of a group's genes in one pass.
 __device__ __forceinline__ float sbx_beta(unsigned w, float e) {
+#if GMPEA_SBX_BRANCHY
     const bool low = w <= 0x80000000u;
     const float b = low ? (float)w * 0x1.0p-31f : (float)(0u - w) * 0x1.0p-31f;  // 2^32 - w (w > 2^31)
     if (b == 0.0f) return 0.0f;  // u = 0: beta = 0
     return exp2f((low ? e : -e) * __log2f(b));
+#else
+    const bool low = w <= 0x80000000u;
+    const float b = (float)(low ? w : 0u - w) * 0x1.0p-31f;  // 2u, or 2(1-u) = (2^32 - w) 2^-31
+    return ex2_ftz((low ? e : -e) * lg2_ftz(b));
+#endif
 }
 
 template <class T>
@@ -412,6 +438,9 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #endif
 #ifndef GMPEA_DE_GAPS
 #define GMPEA_DE_GAPS 0  // DE kernels: PM by gaps instead of per-gene coins (A/B switch)
+#endif
+#ifndef GMPEA_SBX_FULLGROUPS
+#define GMPEA_SBX_FULLGROUPS 1  // streaming kernels: compile-time full groups + tail (A/B switch)
 #endif
 #ifndef GMPEA_VARY_MINBLOCKS_DE
 #define GMPEA_VARY_MINBLOCKS_DE GMPEA_VARY_MINBLOCKS
@@ -623,12 +652,21 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                             const float av = comp(a4[k >> 2], kk);
                             const float bv = comp(b4[k >> 2], kk);
                             if (OP == OP_SBX) {
+#if GMPEA_SBX_BRANCHY
                                 if ((xbits >> k) & 1u) {
                                     const float beta = sbx_beta(pick_word(k < 4 ? xu0 : xu1, kk), p.sbx_e);
                                     v[k] = 0.5f * ((1.0f + beta) * av + (1.0f - beta) * bv);
                                 } else {
                                     v[k] = av;
                                 }
+#else
+                                // every gene of a crossing group through the branch-free
+                                // spread, the crossover bit selects (a warp's lanes cross
+                                // some gene k almost surely: a branch costs all of them)
+                                const float beta = sbx_beta(pick_word(k < 4 ? xu0 : xu1, kk), p.sbx_e);
+                                const float cv = 0.5f * ((1.0f + beta) * av + (1.0f - beta) * bv);
+                                v[k] = ((xbits >> k) & 1u) ? cv : av;
+#endif
                             } else {
                                 v[k] = comp(c4[k >> 2], kk) + p.de_f * (av - bv);
                             }
@@ -704,6 +742,12 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 #pragma unroll 1
                             for (int jb = 0; jb + 8 <= DC; jb += 8) group(jb, std::integral_constant<int, 8>{});
                             if (DC % 8) group(DC / 8 * 8, std::integral_constant<int, (DC % 8)>{});
+                        } else if (GMPEA_SBX_FULLGROUPS && DC == 0 && !ST) {
+                            // streaming evaluators (WTA, d in the hundreds): full groups
+                            // with a compile-time count, then the run-time tail
+#pragma unroll 1
+                            for (int jb = w0; jb + 8 <= w1; jb += 8) group(jb, std::integral_constant<int, 8>{});
+                            if ((w1 - w0) & 7) group(w1 - ((w1 - w0) & 7), std::integral_constant<int, 0>{});
                         } else {
 #pragma unroll 1
                             for (int jb = w0; jb < w1; jb += 8) group(jb, std::integral_constant<int, 0>{});

@@ -1,6 +1,7 @@
 """Attributes an ncu SASS-page capture to CUDA source lines.
 
     python tools/sass_lines.py <report.ncu-rep> <kernel-regex> <lib.so> [top]
+    (SASS_FUNC=<regex on the mangled name> picks among same-sized functions)
 
 Joins `ncu --page source --csv` (per-instruction executed counts and stall
 samples, addressed absolutely) with `nvdisasm -gi` of the same cubin (per
@@ -76,7 +77,8 @@ def main():
     base = data[0][0]
     ninstr = len(data)
     # pick the function whose instruction count matches
-    cands = [f for f, m in funcs.items() if re.search(kregex.replace("|", ".*|.*"), f) and len(m) == ninstr]
+    fre = os.environ.get("SASS_FUNC", kregex.replace("|", ".*|.*"))  # regex on the mangled name
+    cands = [f for f, m in funcs.items() if re.search(fre, f) and len(m) == ninstr]
     if not cands:
         cands = [f for f, m in funcs.items() if len(m) == ninstr]
     fmap = funcs[cands[0]] if cands else {}
