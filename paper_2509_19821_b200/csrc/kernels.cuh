@@ -439,6 +439,9 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #ifndef GMPEA_DE_GAPS
 #define GMPEA_DE_GAPS 0  // DE kernels: PM by gaps instead of per-gene coins (A/B switch)
 #endif
+#ifndef GMPEA_PREFETCH
+#define GMPEA_PREFETCH 1  // bit 0: neighbourhood row to L1 before the picks; bit 1: parent lines to L2 (A/B)
+#endif
 #ifndef GMPEA_SBX_FULLGROUPS
 #define GMPEA_SBX_FULLGROUPS 1  // streaming kernels: compile-time full groups + tail (A/B switch)
 #endif
@@ -506,6 +509,10 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             int jrand = -1;
             bool cross = true;
             if (MODE == MODE_VARY && active) {
+#if GMPEA_PREFETCH & 1
+                // the neighbourhood row arrives while the picks are drawn
+                if (!GMPEA_TOUR_COND) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.B[pi] + (long long)i * p.t[pi]));
+#endif
                 PickStream ps{slot, gen, philox_tag(pid, STREAM_PICK), p.key, 0u, {}};
                 if (GMPEA_TOUR_COND) {
                     auto tournament = [&]() {
@@ -538,6 +545,15 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                     jrand = (int)ps.index(p.uid);
                 }
             }
+#if GMPEA_PREFETCH & 2
+            // the parents' lines, all at once, before the first group needs them
+            if (MODE == MODE_VARY && active) {
+                for (int q = 0; q < rs4; q += 8) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(PX + oa + q));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(PX + ob + q));
+                }
+            }
+#endif
             const bool de_all = p.de_T >= 0xffffffffll;
             const bool even_rows = (rs4 & 1) == 0;  // rows 32 B aligned
             const PhiloxKey& K = p.key;
