@@ -215,7 +215,7 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
     constexpr int NB = PACK ? NBP : 4;
     constexpr int NW = NB / 4;
     // only the parent's cv and PBI stay live (the full keys are re-read at the
-    // end), which keeps select at 48 registers (5 blocks of 256 per SM)
+    // end), which keeps select small: 40 registers at 6 blocks of 256 per SM
     const float4 par4 = ld_once(&p.Fcv[POP][j]);
     const float4 u4 = ld_once(&p.U[j]);
     const float gp = agg_key<AGG>(par4, u4, z, p.theta);
@@ -325,7 +325,10 @@ __device__ __forceinline__ bool select_slot(const SelParams& p, int j, const flo
 }
 
 #ifndef GMPEA_SELECT_MINBLOCKS
-#define GMPEA_SELECT_MINBLOCKS 5
+#define GMPEA_SELECT_MINBLOCKS 6  // 40 registers (a small spill): select -3 % against 5 blocks (48)
+#endif
+#ifndef GMPEA_SELECT_NBP
+#define GMPEA_SELECT_NBP 4  // packed claimants gathered per batch (4 or 8)
 #endif
 template <bool PACK = false, int NBP = 4, int AGG = AGG_PBI>
 __device__ __forceinline__ void select_body(const SelParams& p, const int bx, const int by) {
@@ -390,7 +393,7 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
 
 template <bool PACK = false, int AGG = AGG_PBI>
 __global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
-    select_body<PACK, 4, AGG>(p, blockIdx.x, blockIdx.y);
+    select_body<PACK, GMPEA_SELECT_NBP, AGG>(p, blockIdx.x, blockIdx.y);
     if (p.done == nullptr) return;
     __syncthreads();
     if (threadIdx.x == 0) {
