@@ -1,1 +1,1 @@
-for W in lircmop13-1m lircmop14-1m; do W=$W REPS="1 2" bash ab/run.sh base.so de6.so de7.so de9.so; done
+for W in mw7-1m mw1-1m dascmop9-1m c1dtlz1-1m; do W=$W REPS="1 2" bash ab/run.sh base.so eu2.so eu3.so eu5.so; done
