@@ -1,8 +1,10 @@
 """Summarises ncu captures for profiles/.
 
-    python tools/ncu_summary.py <report.ncu-rep> <out-prefix>
+    python tools/ncu_summary.py <report.ncu-rep> <out-prefix> [workload]
         writes <out-prefix>.txt (human) and merges per-kernel DRAM bytes per
         launch into profiles/ncu_summary.json (read by bench.py for `traffic`)
+        under "<kernel>@<workload>" (and the plain "<kernel>" for the
+        headline workload lircmop13-1m)
     python tools/ncu_summary.py --launches <launches.csv> <out.txt>
         condenses a `--metrics gpu__time_duration.sum` launch list into
         per-kernel counts, mean time and share of the profiled span
@@ -49,7 +51,7 @@ def units_of(raw_hdr, raw_units):
     return dict(zip(raw_hdr, raw_units))
 
 
-def summarize(rep, prefix):
+def summarize(rep, prefix, workload="lircmop13-1m"):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
@@ -77,8 +79,11 @@ def summarize(rep, prefix):
         lines.append(f"{short(name)}: " + ", ".join(f"{k}={v}" for k, v in rec.items()))
         k = kernel_key(name)
         if "dram_read_MB" in rec and "dram_write_MB" in rec:
-            js[k] = {"dram_bytes_per_launch": (rec["dram_read_MB"] + rec["dram_write_MB"]) * 1e6,
-                     "source": os.path.basename(rep), **rec}
+            e = {"dram_bytes_per_launch": (rec["dram_read_MB"] + rec["dram_write_MB"]) * 1e6,
+                 "source": os.path.basename(rep), **rec}
+            js[f"{k}@{workload}"] = e
+            if workload == "lircmop13-1m":
+                js[k] = e
     with open(prefix + ".txt", "w") as f:
         f.write(f"ncu --set full capture: {os.path.basename(rep)}\n" + "\n".join(lines) + "\n")
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -119,4 +124,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2], sys.argv[3])
     else:
-        summarize(sys.argv[1], sys.argv[2])
+        summarize(sys.argv[1], sys.argv[2], *sys.argv[3:4])
