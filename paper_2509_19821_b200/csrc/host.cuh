@@ -258,6 +258,20 @@ inline void launch_vary(VaryKernel k, const VaryParams& vp, int npops, cudaStrea
     }();
     if (g.smem > 48 * 1024)
         CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    // the streaming (WTA) kernels gather parent rows through L1: a carveout
+    // for ~6 resident blocks leaves L1 the rest (A/B: WTA-P10 vary -4.8 %
+    // against the occupancy-driven default; the staged kernels keep theirs)
+    static const int carve_env = [] {
+        const char* e = getenv("GMPEA_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    int carve = carve_env;
+    if (carve < 0 && vp.scratch8 > 0) {
+        const size_t per_sm = 228 * 1024;
+        carve = (int)((6 * (g.smem + 1024) * 100 + per_sm - 1) / per_sm);
+        if (carve >= 100) carve = -1;
+    }
+    if (carve >= 0) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     k<<<dim3(blocks_for(vp.row_end - vp.row0, g.bs), npops), g.bs, g.smem, s>>>(vp);
 }
 
