@@ -763,7 +763,7 @@ struct EvalWtaT {
     __device__ __forceinline__ void begin(const ProbDev& P) {
         v = 0;
         slot = 0;
-        for (int k = counts_at(P); k < P.wta_n32; ++k) at(k) = 0u;
+        for (int k = counts_at(P); k < mask_at(P); ++k) at(k) = 0u;  // counts, minima (finish clears the mask)
     }
     // A vehicle's candidates are ranked by (value desc, slot asc), i.e. the
     // reference's stable order restricted to one vehicle (its genes are
@@ -841,6 +841,7 @@ struct EvalWtaT {
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
         const int V = P.wta_vehicles, T = P.wta_targets;
         const int k0 = mask_at(P);  // mask words
+        for (int w = 0, nw = (P.d + 31) / 32; w < nw; ++w) at(k0 + w) = 0u;
         for (int u = 0; u < V; ++u) {
             const int c = (int)at(counts_at(P) + u);
             for (int e = 0; e < c; ++e) {
