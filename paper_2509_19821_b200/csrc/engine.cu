@@ -473,17 +473,19 @@ static void launch_op1_kernel(int blocks, int agg, const Op1Params& p, cudaStrea
         op1_kernel<AGG_PBI><<<blocks, 256, 0, s>>>(p);
 }
 
-static void launch_select_kernel(dim3 grid, bool pack, int agg, const SelParams& p, cudaStream_t s) {
+// select over parent slots [row0, row0 + rows) of both populations (grid y)
+static void launch_select_kernel(int rows, bool pack, int agg, const SelParams& p, cudaStream_t s) {
+    const dim3 grid(blocks_for(rows, kSelectBS), 2);
     if (agg == AGG_TCH) {
         if (pack)
-            select_kernel<true, AGG_TCH><<<grid, 256, 0, s>>>(p);
+            select_kernel<true, AGG_TCH><<<grid, kSelectBS, 0, s>>>(p);
         else
-            select_kernel<false, AGG_TCH><<<grid, 256, 0, s>>>(p);
+            select_kernel<false, AGG_TCH><<<grid, kSelectBS, 0, s>>>(p);
     } else {
         if (pack)
-            select_kernel<true, AGG_PBI><<<grid, 256, 0, s>>>(p);
+            select_kernel<true, AGG_PBI><<<grid, kSelectBS, 0, s>>>(p);
         else
-            select_kernel<false, AGG_PBI><<<grid, 256, 0, s>>>(p);
+            select_kernel<false, AGG_PBI><<<grid, kSelectBS, 0, s>>>(p);
     }
 }
 
@@ -935,7 +937,7 @@ struct gmpea_engine {
     }
 
     void launch_select() {
-        launch_select_kernel(dim3(blocks_for(own1 - own0, 256), 2), rpack, cfg.aggregation, sp, s);
+        launch_select_kernel((int)(own1 - own0), rpack, cfg.aggregation, sp, s);
     }
     void launch_op1() { launch_op1_kernel(blocks_for(v1 - v0, 256), cfg.aggregation, op1p, s); }
 
@@ -2068,7 +2070,7 @@ int gmpea_environmental_selection_ex(int64_t n, int32_t d, int32_t m, int32_t nc
         sp.srcbits = sb.p;
         sp.apply = 0;
         sp.st = st.p;
-        launch_select_kernel(dim3(blocks_for(n, 256), 2), pack, aggregation, sp, 0);
+        launch_select_kernel((int)n, pack, aggregation, sp, 0);
         CK(cudaGetLastError());
         std::vector<int> w1(n), w2(n);
         CK(cudaMemcpy(w1.data(), win[0].p, n * sizeof(int), cudaMemcpyDeviceToHost));

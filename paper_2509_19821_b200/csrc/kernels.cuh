@@ -436,6 +436,9 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #ifndef GMPEA_TMA_STORE
 #define GMPEA_TMA_STORE 1
 #endif
+#ifndef GMPEA_MUT_ONLY_CHECK
+#define GMPEA_MUT_ONLY_CHECK 0  // phase 3 bounds test on the mutated genes only (A/B switch)
+#endif
 #ifndef GMPEA_DE_GAPS
 #define GMPEA_DE_GAPS 0  // DE kernels: PM by gaps instead of per-gene coins (A/B switch)
 #endif
@@ -492,6 +495,13 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 
     double f[kMaxM] = {0.0, 0.0, 0.0};
     bool bad = false;
+    // a child's genes outside [lo, hi] can only be mutated ones: crossover /
+    // DE children of in-bounds parents are finite and clipped, so only the
+    // reference's PM hazard (a NaN, gmpea.cpp:146-150) fails the bounds test
+    // of evaluate (problems.cpp:554-561).  With the whole mutation mask in one
+    // window (d <= 64, compile-time d) phase 3 tests the mutated genes only.
+    constexpr bool kMutOnly = GMPEA_MUT_ONLY_CHECK && MODE == MODE_VARY && DC > 0 && DC <= 64 && !Ev::kStream;
+    unsigned long long mut_all = 0ull;
     {
         if (MODE == MODE_EVAL) {
             if (ST && active) {
@@ -779,6 +789,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                     else
                         pm_tasks(p, (unsigned long long)mmask, w0, sm4, gen, pid, i0);
                 }
+                if (kMutOnly) mut_all = (unsigned long long)mmask;
             }
         }
         if (p.eval && active) {
@@ -800,7 +811,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 #pragma unroll EU
                 for (int j = 0; j < d; ++j) {
                     const float x = rd[j];
-                    if (!(x >= GMPEA_LO(j) && x <= GMPEA_HI(j))) bad = true;
+                    if (!kMutOnly && !(x >= GMPEA_LO(j) && x <= GMPEA_HI(j))) bad = true;
                     ev.gene(p.P, j, x);
                 }
             } else if (!stream_eval) {
@@ -813,9 +824,16 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                     for (int k = 0; k < 4; ++k) {
                         const int j = jb + k;
                         if (j >= d) break;
-                        if (!(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
+                        if (!kMutOnly && !(v[k] >= GMPEA_LO(j) && v[k] <= GMPEA_HI(j))) bad = true;
                         ev.gene(p.P, j, v[k]);
                     }
+                }
+            }
+            if (kMutOnly) {
+                const float* rd = reinterpret_cast<const float*>(my4);
+                for (unsigned long long mm = mut_all; mm; mm &= mm - 1ull) {
+                    const int j = __ffsll((long long)mm) - 1;
+                    if (!(rd[j] >= GMPEA_LO(j) && rd[j] <= GMPEA_HI(j))) bad = true;
                 }
             }
             if (bad) {

@@ -505,9 +505,15 @@ struct EvalMw {
                 f[0] = g * xs[0];
                 double r = f[0] / g;
                 f[1] = g * sqrt(1.0 - r * r);
-                double l = atan(f[1] / f[0]);
                 double q = f[0] * f[0] + f[1] * f[1];
-                double sn = sin(4.0 * l);
+                double sn;
+                if (ref) {  // front candidates: the reference's own rounding
+                    sn = sin(4.0 * atan(f[1] / f[0]));
+                } else {
+                    // sin(4 atan(y / x)) = 4 x y (x^2 - y^2) / (x^2 + y^2)^2 for x, y >= 0
+                    // (double-angle identities; no fp64 atan / sin on the generation path)
+                    sn = 4.0 * f[0] * f[1] * (f[0] * f[0] - f[1] * f[1]) / (q * q);
+                }
                 double a = 1.2 + 0.4 * ipow(sn, 16);
                 double b = 1.15 - 0.2 * ipow(sn, 8);
                 emit(0, q - a * a);

@@ -391,8 +391,12 @@ __device__ __forceinline__ void end_gen_body(DevState* st, DevRecord* rec) {
     st->t_gen_start = globaltimer();
 }
 
+#ifndef GMPEA_SELECT_BS
+#define GMPEA_SELECT_BS 128  // threads per select block (A/B: 128 select -2..-4 % against 256, 64 slower)
+#endif
+constexpr int kSelectBS = GMPEA_SELECT_BS;
 template <bool PACK = false, int AGG = AGG_PBI>
-__global__ void __launch_bounds__(256, GMPEA_SELECT_MINBLOCKS) select_kernel(SelParams p) {
+__global__ void __launch_bounds__(kSelectBS, GMPEA_SELECT_MINBLOCKS * 256 / kSelectBS) select_kernel(SelParams p) {
     select_body<PACK, GMPEA_SELECT_NBP, AGG>(p, blockIdx.x, blockIdx.y);
     if (p.done == nullptr) return;
     __syncthreads();
