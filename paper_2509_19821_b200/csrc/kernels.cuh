@@ -439,6 +439,9 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #ifndef GMPEA_MUT_ONLY_CHECK
 #define GMPEA_MUT_ONLY_CHECK 0  // phase 3 bounds test on the mutated genes only (A/B switch)
 #endif
+#ifndef GMPEA_DE_ONECOPY
+#define GMPEA_DE_ONECOPY 1  // DE kernels: every gene group through one run-time-count copy (A/B: vary LIRCMOP13 -0.9 %, LIRCMOP14 -0.4 %; 2896 -> 2544 SASS)
+#endif
 #ifndef GMPEA_DE_GAPS
 #define GMPEA_DE_GAPS 0  // DE kernels: PM by gaps instead of per-gene coins (A/B switch)
 #endif
@@ -763,8 +766,9 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
                         // SBX kernels run every group, the tail included, through one
                         // run-time-count copy: their second (tail) copy cost more in
                         // instruction fetch than the bounds tests it saves (A/B:
-                        // DAS-CMOP9 vary -4.2 %, DAS-CMOP7 -3.3 %, MW1 -0.9 %, MW7 +0.3 %)
-                        if (DC > 0 && DC <= 64 && OP != OP_SBX) {  // one window, full groups then the tail
+                        // DAS-CMOP9 vary -4.2 %, DAS-CMOP7 -3.3 %, MW1 -0.9 %, MW7 +0.3 %);
+                        // so do the DE kernels (GMPEA_DE_ONECOPY)
+                        if (DC > 0 && DC <= 64 && OP != OP_SBX && !GMPEA_DE_ONECOPY) {  // one window, full groups then the tail
 #pragma unroll 1
                             for (int jb = 0; jb + 8 <= DC; jb += 8) group(jb, std::integral_constant<int, 8>{});
                             if (DC % 8) group(DC / 8 * 8, std::integral_constant<int, (DC % 8)>{});
