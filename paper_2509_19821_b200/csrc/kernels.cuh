@@ -458,10 +458,11 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 // suites: LIRCMOP 30, MW 15, DTLZ 7/12) so the gene loops unroll completely.
 // TOUR: tournament parent picks (the comparison algorithms' instantiation;
 // the GMPEA kernels carry no tournament code)
-// (the DE kernels keep the run-time branch: its absence costs LIRCMOP13 13 %
-// through a worse register allocation, A/B in DESIGN.md)
+// (the DE kernels used to keep a dead run-time tournament branch, which once
+// bought a better register allocation; with one gene-group copy its removal
+// is -0.8 % LIRCMOP13 vary and 2544 -> 2136 SASS instructions, A/B in DESIGN.md)
 #ifndef GMPEA_TOUR_COND
-#define GMPEA_TOUR_COND (TOUR || (OP == OP_DE && p.tour))
+#define GMPEA_TOUR_COND (TOUR)
 #endif
 template <class Ev, int MODE, int OP, int DC = 0, bool UB = false, bool TOUR = false>
 __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, const int by) {
