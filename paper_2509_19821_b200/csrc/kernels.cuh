@@ -805,14 +805,13 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             // A/B vary: MW1 -4.6 %, MW7 -2.6 %, DAS-CMOP7 -1.4 %, DAS-CMOP9 -4.3 %,
             // C1-DTLZ1 -1.1 %;
             // the LIRCMOP kernels lose 8-11 % rolled and keep the unrolled loop)
-            constexpr bool ROLL_EVAL = ST && (std::is_same<Ev, EvalMw>::value || std::is_same<Ev, EvalDas>::value ||
-                                              std::is_same<Ev, EvalDtlz>::value);
+            constexpr bool ROLL_EVAL = ST && (is_mw<Ev>::value || is_das<Ev>::value || is_dtlz<Ev>::value);
             if constexpr (ROLL_EVAL) {
                 ev.begin(p.P);
                 const float* rd = reinterpret_cast<const float*>(my4);
                 // MW: two genes per trip (A/B: vary MW1 -2.2 %, MW7 -0.9 %;
                 // DAS-CMOP9 +0.8 % and C1-DTLZ1 +0.2 % keep one)
-                constexpr int EU = std::is_same<Ev, EvalMw>::value ? 2 : 1;
+                constexpr int EU = is_mw<Ev>::value ? 2 : 1;
 #pragma unroll EU
                 for (int j = 0; j < d; ++j) {
                     const float x = rd[j];
@@ -927,7 +926,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 // LIRCMOP13 slower (A/B)
 template <class Ev, int OP, int DC>
 constexpr int vary_minblocks() {
-    return DC == 15 && std::is_same<Ev, EvalMw>::value ? 10 : (OP == OP_DE ? GMPEA_VARY_MINBLOCKS_DE : GMPEA_VARY_MINBLOCKS);
+    return DC == 15 && is_mw<Ev>::value ? 10 : (OP == OP_DE ? GMPEA_VARY_MINBLOCKS_DE : GMPEA_VARY_MINBLOCKS);
 }
 
 template <class Ev, int MODE, int OP, int DC = 0, bool UB = false, bool TOUR = false>

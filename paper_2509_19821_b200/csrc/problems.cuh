@@ -208,7 +208,9 @@ struct EvalLirT {
 using EvalLir = EvalLirT<0>;
 
 // ---------------------------------------------------------------- C/DC-DTLZ
-struct EvalDtlz {
+// ID > 0 fixes the C/DC-DTLZ problem at compile time (per-problem generation kernels)
+template <int ID = 0>
+struct EvalDtlzT {
     static constexpr bool kStream = false;
     __device__ __forceinline__ void bind(void*, int, int) {}
     double pos[2];
@@ -257,7 +259,7 @@ struct EvalDtlz {
     }
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
-        const int k = P.id;
+        const int k = (ID ? ID : P.id);
         const int m = P.m;
         const double gr = 100.0 * ((double)(P.d - m + 1) + rast);
         switch (k) {
@@ -316,6 +318,11 @@ struct EvalDtlz {
         }
     }
 };
+using EvalDtlz = EvalDtlzT<0>;
+template <class Ev>
+struct is_dtlz : std::false_type {};
+template <int ID>
+struct is_dtlz<EvalDtlzT<ID>> : std::true_type {};
 
 // ---------------------------------------------------------------- MW (unpinned)
 __device__ __forceinline__ double ipow(double x, int e) {
@@ -336,7 +343,10 @@ __device__ __forceinline__ double ipow(double x, int e) {
     return r;
 }
 
-struct EvalMw {
+// ID > 0 fixes the MW problem at compile time (the generation kernels at
+// d = 15: one kernel per problem, no problem dispatch in the hot code)
+template <int ID = 0>
+struct EvalMwT {
     static constexpr bool kStream = false;
     __device__ __forceinline__ void bind(void*, int, int) {}
     double xs[2];
@@ -346,7 +356,7 @@ struct EvalMw {
     bool ref;  // fp64 front candidates: reference-rounded trigonometry (trig_sin)
     __device__ __forceinline__ void begin(const ProbDev& P) {
         gs = 0.0;
-        kd = kind(P.id);
+        kd = kind(ID ? ID : P.id);
         ref = false;
     }
     __device__ __forceinline__ static int kind(int id) {
@@ -418,7 +428,7 @@ struct EvalMw {
     }
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
-        const int id = P.id, n = P.d;
+        const int id = ID ? ID : P.id, n = P.d;
         const double r2 = sqrt(2.0);
         switch (id) {
             case 1: case 2: {
@@ -602,6 +612,11 @@ struct EvalMw {
         }
     }
 };
+using EvalMw = EvalMwT<0>;
+template <class Ev>
+struct is_mw : std::false_type {};
+template <int ID>
+struct is_mw<EvalMwT<ID>> : std::true_type {};
 
 // ---------------------------------------------------------------- DAS-CMOP (unpinned)
 // DAS-CMOP1-9 (Fan et al., Evol. Comput. 28(3), 2020; D = 30, x in [0,1]^D),
@@ -623,7 +638,9 @@ struct DasConst {
     static constexpr double ea = 0.3, eb = 1.2;     // ellipse semi-axes (DAS1-6)
 };
 
-struct EvalDas {
+// ID > 0 fixes the DAS-CMOP problem at compile time (per-problem generation kernels)
+template <int ID = 0>
+struct EvalDasT {
     static constexpr bool kStream = false;
     __device__ __forceinline__ void bind(void*, int, int) {}
     double xs[2];
@@ -634,7 +651,7 @@ struct EvalDas {
     __device__ __forceinline__ void begin(const ProbDev& P) {
         gs = 0.0;
         sh = 0.5;
-        rast = P.id == 4 || P.id == 5 || P.id == 6 || P.id == 9;
+        rast = (ID ? ID : P.id) == 4 || (ID ? ID : P.id) == 5 || (ID ? ID : P.id) == 6 || (ID ? ID : P.id) == 9;
         ref = false;
     }
     // front candidates (pf_reference): g itself
@@ -664,7 +681,7 @@ struct EvalDas {
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
         using K = DasConst;
-        const int id = P.id;
+        const int id = (ID ? ID : P.id);
         const double g = rast ? (double)(P.d - P.m + 1) + gs : gs;
         const double x1 = xs[0];
         emit(0, K::b - trig_sin(ref, K::a, x1));
@@ -717,6 +734,11 @@ struct EvalDas {
         }
     }
 };
+using EvalDas = EvalDasT<0>;
+template <class Ev>
+struct is_das : std::false_type {};
+template <int ID>
+struct is_das<EvalDasT<ID>> : std::true_type {};
 
 // ---------------------------------------------------------------- WTA
 // decode_wta (wta.cpp:51-72): genes >= 0.5 are candidates, taken in
