@@ -434,7 +434,7 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #define GMPEA_VARY_MINBLOCKS 8
 #endif
 #ifndef GMPEA_TMA_STORE
-#define GMPEA_TMA_STORE 1
+#define GMPEA_TMA_STORE 0  // whole-line rows by per-thread cp.async.bulk (A/B switch; phase 4)
 #endif
 #ifndef GMPEA_MUT_ONLY_CHECK
 #define GMPEA_MUT_ONLY_CHECK 0  // phase 3 bounds test on the mutated genes only (A/B switch)
@@ -859,13 +859,15 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
             }
         }
     }
-    // phase 4: the block's rows leave shared memory.  Rows of whole 128 B lines
-    // (rs4 % 8 == 0, LIRCMOP1-13: 30 + 2 floats): every thread's staged row
-    // through the bulk-copy engine (cp.async.bulk, UBLKCP) after a proxy fence
-    // and one barrier (PM tasks wrote other threads' rows): LIRCMOP13 vary
-    // -1.9 %.  Other rows as one contiguous, coalesced copy of rows [i0, i0 +
-    // rows) (the bulk copies of 32-160 B rows that straddle lines cost MW7
-    // +6 %, DAS-CMOP9 +2 %, C1-DTLZ1 +13 %; A/B in DESIGN.md)
+    // phase 4: the block's rows leave shared memory as one contiguous,
+    // coalesced copy of rows [i0, i0 + rows).  GMPEA_TMA_STORE sends rows of
+    // whole 128 B lines (rs4 % 8 == 0, LIRCMOP1-13) through the bulk-copy
+    // engine instead (per-thread cp.async.bulk, UBLKCP, after a proxy fence
+    // and one barrier): LIRCMOP13 vary -1.9 % when it was measured, +2.2 %
+    // since the kernel's hot code shrank (one group copy, no tournament
+    // branch: its operand loop over the lanes now costs more than it saves);
+    // rows that straddle lines cost MW7 +6 %, DAS-CMOP9 +2 %, C1-DTLZ1 +13 %
+    // (A/B in DESIGN.md)
     if (ST && GMPEA_TMA_STORE && (rs4 & 7) == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
