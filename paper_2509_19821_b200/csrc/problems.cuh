@@ -232,6 +232,8 @@ struct EvalDtlzT {
             return;
         }
         double t = x - 0.5;  // problems.cpp:144-147, 153-155
+        // (fp64 cosine: DC2/DC3-DTLZ feed 100 g into cos(3 pi .), which turns
+        // an fp32 cosine's 1e-7 per term into 1e-4 in the constraints)
         rast += t * t - trig_cos(ref, 20.0, t);
         sph += t * t;
     }
@@ -630,6 +632,12 @@ struct is_mw<EvalMwT<ID>> : std::true_type {};
 //                            r^2 - |f - P_k|^2 (DAS7-9, 4 spheres)
 // The per-gene distance terms are fp64 (the DAS4-6/9 Rastrigin cosine has a
 // 20 pi argument: fp32 would lose 1e-5 relative in g).
+// DAS-CMOP4-6/9 distance terms on generation rows: cos(20 pi y) in fp32 on an
+// exactly reduced argument (A/B switch)
+#ifndef GMPEA_DAS_COS32
+#define GMPEA_DAS_COS32 1
+#endif
+
 struct DasConst {
     static constexpr double a = 20.0, b = 0.0;      // b = 2*0.5 - 1
     static constexpr double d = 0.5;
@@ -676,7 +684,18 @@ struct EvalDasT {
             return;
         }
         const double y = x - sh;
-        gs += rast ? y * y - trig_cos(ref, 20.0, y) : y * y;
+        if (!rast) {
+            gs += y * y;
+        } else if (std::is_same<T, double>::value || !GMPEA_DAS_COS32) {
+            gs += y * y - trig_cos(ref, 20.0, y);
+        } else {
+            // generation rows: the cosine in fp32 on an exactly reduced argument
+            // (20 y - 2 round(10 y) in [-1, 1], exact in fp64; < 1.2e-7 off per
+            // term), the sum in fp64 -- as the MW terms (EvalMwT::gene)
+            const double t = 20.0 * y;
+            const double r = fma(-2.0, rint(0.5 * t), t);
+            gs += y * y - (double)cospif((float)r);
+        }
     }
     template <class G>
     __device__ __forceinline__ void finish(const ProbDev& P, double* f, G&& emit) {
