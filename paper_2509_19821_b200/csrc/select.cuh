@@ -172,6 +172,16 @@ __device__ __forceinline__ void ldg256_na(const float4* p, float4& a, float4& b)
 #endif
 }
 
+// 128-bit load that does not allocate in L1 (winner rows of odd-float4 strides)
+#ifndef GMPEA_COPY_NA
+#define GMPEA_COPY_NA 1  // (A/B switch)
+#endif
+__device__ __forceinline__ float4 ldg128_na(const float4* p) {
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4* __restrict__ src, int rs4) {
     if ((rs4 & 1) == 0) {  // rows 32 B aligned: 256-bit loads and stores
         for (int q0 = 0; q0 < rs4; q0 += 8) {
@@ -193,7 +203,7 @@ __device__ __forceinline__ void copy_row(float4* __restrict__ dst, const float4*
         float4 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            if (q0 + u < rs4) v[u] = src[q0 + u];
+            if (q0 + u < rs4) v[u] = GMPEA_COPY_NA ? ldg128_na(src + q0 + u) : src[q0 + u];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
             if (q0 + u < rs4) dst[q0 + u] = v[u];
