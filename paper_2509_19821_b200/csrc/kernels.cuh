@@ -442,6 +442,9 @@ __device__ __forceinline__ void pm_tasks_warp(const VP& p, unsigned mask, int w0
 #ifndef GMPEA_DE_ONECOPY
 #define GMPEA_DE_ONECOPY 1  // DE kernels: every gene group through one run-time-count copy (A/B: vary LIRCMOP13 -0.9 %, LIRCMOP14 -0.4 %; 2896 -> 2544 SASS)
 #endif
+#ifndef GMPEA_VARY_MINBLOCKS_MW
+#define GMPEA_VARY_MINBLOCKS_MW 10  // MW kernels (d = 15): 48 registers
+#endif
 #ifndef GMPEA_DE_GAPS
 #define GMPEA_DE_GAPS 0  // DE kernels: PM by gaps instead of per-gene coins (A/B switch)
 #endif
@@ -928,7 +931,7 @@ __device__ __forceinline__ void vary_body(const VaryParams& p, const int bx, con
 // LIRCMOP13 slower (A/B)
 template <class Ev, int OP, int DC>
 constexpr int vary_minblocks() {
-    return DC == 15 && is_mw<Ev>::value ? 10 : (OP == OP_DE ? GMPEA_VARY_MINBLOCKS_DE : GMPEA_VARY_MINBLOCKS);
+    return DC == 15 && is_mw<Ev>::value ? GMPEA_VARY_MINBLOCKS_MW : (OP == OP_DE ? GMPEA_VARY_MINBLOCKS_DE : GMPEA_VARY_MINBLOCKS);
 }
 
 template <class Ev, int MODE, int OP, int DC = 0, bool UB = false, bool TOUR = false>
